@@ -1,0 +1,178 @@
+"""CPU oracle for the radix-tree-forest sampler (arXiv 1901.05423).
+
+TEST INFRASTRUCTURE ONLY: only ``tests/``, ``__graft_entry__.smoke()`` and the
+``cpu_baseline`` / ``--impl reference`` legs of ``bench.py`` may import this
+package.  The product package ``paper_1901_05423_b200`` never imports it and
+shares no code with it (the oracle is plain serial C in ``rtf_oracle.c``, built
+with gcc; this module is argument marshalling only).
+
+Every function follows the paper step by step; see the header of
+``rtf_oracle.c`` for the step list (O1..O12) with PAPER.md line citations, and
+DESIGN.md section 3 for the readings (R1..R17) and the pin of each function.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import subprocess
+from dataclasses import dataclass
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_SRC = os.path.join(_HERE, "rtf_oracle.c")
+_LIB = os.path.join(_HERE, "liboracle.so")
+
+OK, EINVAL, EALLZERO, ETOOLARGE = 0, 1, 2, 3
+ONE = 1 << 63  # fixed-point 1.0 (reading R4)
+
+
+def build_oracle(force: bool = False) -> str:
+    """Compile rtf_oracle.c with gcc (plain C, -O2, single thread)."""
+    if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < os.path.getmtime(_SRC):
+        tmp = _LIB + f".tmp{os.getpid()}"
+        subprocess.check_call(["gcc", "-O2", "-std=c11", "-Wall", "-Wextra", "-shared",
+                               "-fPIC", "-o", tmp, _SRC])
+        os.replace(tmp, _LIB)
+    return _LIB
+
+
+_lib = None
+
+
+def _load():
+    global _lib
+    if _lib is None:
+        lib = ctypes.CDLL(build_oracle())
+        P = ctypes.c_void_p
+        u32, u64, i32 = ctypes.c_uint32, ctypes.c_uint64, ctypes.c_int32
+        lib.orc_quantize.argtypes = [P, u32, P, P, P]
+        lib.orc_cdf_all.argtypes = [P, u32, P, P]
+        lib.orc_build.argtypes = [P, u32, u32, P, P, P, P, P, P, P, P, P]
+        lib.orc_sample.argtypes = [P, P, P, P, u32, P, u64, P, P]
+        lib.orc_sample.restype = None
+        lib.orc_sample_bsearch.argtypes = [P, u32, P, u64, P]
+        lib.orc_sample_bsearch.restype = None
+        lib.orc_build_rows.argtypes = [P, u32, u32, u32, P, P, P, P, P, P, P, P, P, P]
+        for f in (lib.orc_quantize, lib.orc_cdf_all, lib.orc_build, lib.orc_build_rows):
+            f.restype = i32
+        _lib = lib
+    return _lib
+
+
+def _ptr(a: np.ndarray):
+    return ctypes.c_void_p(a.ctypes.data)
+
+
+class OracleError(ValueError):
+    def __init__(self, status: int):
+        super().__init__({EINVAL: "EINVAL", EALLZERO: "EALLZERO",
+                          ETOOLARGE: "ETOOLARGE"}.get(status, str(status)))
+        self.status = status
+
+
+def _f32(p) -> np.ndarray:
+    return np.ascontiguousarray(np.asarray(p, dtype=np.float32))
+
+
+def quantize(p):
+    """O1-O3: returns (w uint64[n], E, B)."""
+    p = _f32(p)
+    w = np.zeros(max(p.size, 1), dtype=np.uint64)
+    E, B = ctypes.c_int(0), ctypes.c_int(0)
+    st = _load().orc_quantize(_ptr(p), p.size, _ptr(w), ctypes.byref(E), ctypes.byref(B))
+    if st:
+        raise OracleError(st)
+    return w[: p.size], E.value, B.value
+
+
+def cdf_all(p):
+    """Fixed-point CDF over all n entries (zeros included): (K uint64[n], T)."""
+    p = _f32(p)
+    K = np.zeros(max(p.size, 1), dtype=np.uint64)
+    T = ctypes.c_uint64(0)
+    st = _load().orc_cdf_all(_ptr(p), p.size, _ptr(K), ctypes.byref(T))
+    if st:
+        raise OracleError(st)
+    return K[: p.size], T.value
+
+
+@dataclass
+class Forest:
+    """Oracle forest.  Arrays are indexed by the compacted leaf / node index j."""
+    n: int
+    m: int
+    n_pos: int
+    T: int
+    key: np.ndarray      # uint64[n_pos]
+    orig: np.ndarray     # int32[n_pos]
+    cell: np.ndarray     # uint32[n_pos]
+    lam: np.ndarray      # uint8[n_pos]   split levels (64 = boundary)
+    child0: np.ndarray   # int32[n_pos]
+    child1: np.ndarray   # int32[n_pos]
+    table: np.ndarray    # int32[m]
+
+    def records(self) -> np.ndarray:
+        """The 16-byte node records {u64 key; i32 child0; i32 child1} as a
+        structured array (the layout of Sec.3.2 P:1082-1083 interleaving)."""
+        r = np.zeros(self.n_pos, dtype=[("key", "<u8"), ("c0", "<i4"), ("c1", "<i4")])
+        r["key"], r["c0"], r["c1"] = self.key, self.child0, self.child1
+        return r
+
+    def sample(self, xi, with_loads: bool = False):
+        xi = np.ascontiguousarray(np.asarray(xi, dtype=np.uint32))
+        out = np.empty(xi.size, dtype=np.int32)
+        loads = np.empty(xi.size, dtype=np.uint32) if with_loads else None
+        _load().orc_sample(_ptr(self.key), _ptr(self.child0), _ptr(self.child1),
+                           _ptr(self.table), self.m, _ptr(xi), xi.size, _ptr(out),
+                           _ptr(loads) if with_loads else None)
+        return (out, loads) if with_loads else out
+
+
+def build(p, m: int) -> Forest:
+    """O1-O11 for one distribution."""
+    p = _f32(p)
+    n = p.size
+    nn = max(n, 1)
+    key = np.zeros(nn, np.uint64)
+    orig = np.zeros(nn, np.int32)
+    cell = np.zeros(nn, np.uint32)
+    lam = np.zeros(nn, np.uint8)
+    c0 = np.zeros(nn, np.int32)
+    c1 = np.zeros(nn, np.int32)
+    table = np.zeros(max(m, 1), np.int32)
+    T = ctypes.c_uint64(0)
+    npos = ctypes.c_uint32(0)
+    st = _load().orc_build(_ptr(p), n, m, _ptr(key), _ptr(orig), _ptr(cell), _ptr(lam),
+                           _ptr(c0), _ptr(c1), _ptr(table), ctypes.byref(T), ctypes.byref(npos))
+    if st:
+        raise OracleError(st)
+    k = npos.value
+    return Forest(n, m, k, T.value, key[:k], orig[:k], cell[:k], lam[:k], c0[:k], c1[:k],
+                  table[:m])
+
+
+def sample_bsearch(K: np.ndarray, xi) -> np.ndarray:
+    """Binary search on the full fixed-point CDF (Sec.2.2): independent of the forest."""
+    K = np.ascontiguousarray(K, dtype=np.uint64)
+    xi = np.ascontiguousarray(np.asarray(xi, dtype=np.uint32))
+    out = np.empty(xi.size, dtype=np.int32)
+    _load().orc_sample_bsearch(_ptr(K), K.size, _ptr(xi), xi.size, _ptr(out))
+    return out
+
+
+def build_rows(p, rows: int, n_row: int, m_row: int):
+    """Batched independent rows (Sec.5).  Returns dict of arrays laid
+    out row-major with per-row stride n_row (nodes) / m_row (table), plus the
+    per-row T, n_pos and status."""
+    p = _f32(p).reshape(-1)
+    assert p.size == rows * n_row
+    N = rows * n_row
+    out = dict(key=np.zeros(N, np.uint64), orig=np.zeros(N, np.int32),
+               cell=np.zeros(N, np.uint32), lam=np.zeros(N, np.uint8),
+               child0=np.zeros(N, np.int32), child1=np.zeros(N, np.int32),
+               table=np.zeros(rows * m_row, np.int32), T=np.zeros(rows, np.uint64),
+               n_pos=np.zeros(rows, np.uint32), status=np.zeros(rows, np.int32))
+    _load().orc_build_rows(_ptr(p), rows, n_row, m_row, *(_ptr(out[k]) for k in (
+        "key", "orig", "cell", "lam", "child0", "child1", "table", "T", "n_pos", "status")))
+    return out
