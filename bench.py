@@ -1,0 +1,415 @@
+#!/usr/bin/env python
+"""Benchmark of the radix-tree-forest hot path on B200.
+
+One step = one pass of the whole hot path over one batch of synthetic input:
+  build (rtf_build: p resident in HBM -> guide table + forest, 4 kernels) and
+  sample (rtf_sample: 2^30 xi resident in HBM -> 2^30 original indices).
+Default workload: config 3 (power law p_i ~ ((i+1)/n)^20, n = 2^24, m = 2^22,
+2^30 Philox4x32-10 xi per GPU).  L2 is flushed (512 MiB write) between steps.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--workload c3|c2]
+  python bench.py --impl reference ...    # the CPU oracle arm
+
+`value` = forest build throughput (G entries/s, whole job); the sampling
+throughput, its binary-search baseline, roofline fractions, the CPU oracle
+baseline, end-to-end (host buffer) numbers and clocks are extra keys.
+Multi-GPU (torchrun): every rank builds and samples its own problem (weak
+scaling, no collective on the data path); times are max over ranks.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "forest build G entries/s; sampling G samples/s (vs binary search) at 1/2/4/8 B200"
+L2_FLUSH_BYTES = 512 << 20
+
+WORKLOADS = {
+    "c3": dict(name="c3_powerlaw", n=1 << 24, m=1 << 22, samples=1 << 30,
+               desc="config 3: power law p_i ~ ((i+1)/n)^20 (family A), n=2^24, m=2^22, "
+                    "2^30 Philox4x32-10 xi per GPU"),
+    "c2": dict(name="c2_envmap", n=2048 * 1024, m=2048 * 1024, samples=1 << 26,
+               desc="config 2: 2048x1024 synthetic env-map luminance, m=n, 2^26 Sobol xi per GPU"),
+}
+
+
+def make_p(wl):
+    from workloads import env_map, power_law
+    if wl["name"] == "c3_powerlaw":
+        return power_law(wl["n"], "A")
+    return env_map()
+
+
+def peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(path):
+        d = json.load(open(path))
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+def ncu_traffic(kernel: str, workload: str):
+    """dram bytes per launch of `kernel` from the committed ncu --set full summary."""
+    path = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if not os.path.exists(path):
+        return None
+    d = json.load(open(path))
+    return d.get(workload, {}).get(kernel)
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.idx = gpu_index
+        self.rows = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", f"--id={self.idx}", f"--query-gpu={self.Q}",
+                                      "--format=csv,noheader,nounits"], capture_output=True,
+                                     text=True, timeout=5).stdout.strip()
+                if out:
+                    self.rows.append([x.strip() for x in out.split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._t = threading.Thread(target=self._run, daemon=True)
+        self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        self._t.join(timeout=10)
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[k] for r in self.rows for k in range(4)
+                          if len(r) > 3 + k and r[3 + k].lower().startswith("active")})
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+                "samples": len(self.rows)}
+
+
+# ============================================================================ GPU arm
+
+def run_gpu(args):
+    import torch
+    import torch.distributed as dist
+
+    import paper_1901_05423_b200 as rtf
+    from workloads import sobol0_xi
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus:
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+
+    wl = WORKLOADS[args.workload]
+    n, m, S = wl["n"], wl["m"], wl["samples"]
+    if args.samples:
+        S = args.samples
+    p_host = make_p(wl)
+    p = torch.from_numpy(p_host).to(dev)
+    forest = rtf.Forest(n, m)
+    if wl["name"] == "c2_envmap":  # Sobol dim 0, this rank's slice of the sequence
+        xi = torch.from_numpy(sobol0_xi(S, start=rank * S).view(np.int32)).to(dev)
+    else:  # Philox, this rank's counter range
+        xi = rtf.philox(S, seed=0x5EED, start=rank * S, device=dev)
+    out = torch.empty(S, dtype=torch.int32, device=dev)
+    flush = torch.empty(L2_FLUSH_BYTES, dtype=torch.uint8, device=dev)
+    stream = torch.cuda.current_stream()
+
+    def step(ev=None):
+        if ev:
+            ev[0].record(stream)
+        forest.build(p)
+        if ev:
+            ev[1].record(stream)
+        forest.sample(xi, out)
+        if ev:
+            ev[2].record(stream)
+
+    for _ in range(args.warmup):
+        step()
+        flush.zero_()
+    torch.cuda.synchronize()
+    assert forest.status() == 0
+
+    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(args.steps)]
+    sampler = ClockSampler(local)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    l0 = rtf.launch_count()
+    with sampler:
+        for k in range(args.steps):
+            step(evs[k])
+            flush.zero_()  # L2 flush between timed steps (not inside the events)
+        torch.cuda.synchronize()
+    launches = rtf.launch_count() - l0
+    if world > 1:
+        dist.barrier()
+    build_ms = [e[0].elapsed_time(e[1]) for e in evs]
+    sample_ms = [e[1].elapsed_time(e[2]) for e in evs]
+    tb, ts = sum(build_ms), sum(sample_ms)
+    if world > 1:  # max over ranks
+        t = torch.tensor([tb, ts], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        tb, ts = t.tolist()
+    K = args.steps
+    build_gs = world * n * K / (tb * 1e-3) / 1e9
+    sample_gs = world * S * K / (ts * 1e-3) / 1e9
+
+    # ------------------------------------------------ baseline: binary search on the same CDF
+    cdf = rtf.build_cdf(p)
+    bs_out = torch.empty_like(out)
+    cdf.sample(xi, bs_out)
+    torch.cuda.synchronize()
+    eq = bool(torch.equal(bs_out, out))
+    bs_ms = []
+    for _ in range(max(2, min(3, K))):
+        flush.zero_()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        cdf.sample(xi, bs_out)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        bs_ms.append(e0.elapsed_time(e1))
+    tbs = statistics.median(bs_ms)
+    if world > 1:
+        t = torch.tensor([tbs], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        tbs = t.item()
+    bsearch_gs = world * S / (tbs * 1e-3) / 1e9
+
+    # ------------------------------------------------ load statistics (E[visits], avg_32)
+    loads = forest.sample_loads(xi[: 1 << 20]).double()
+    e_loads = loads.mean().item()
+    avg32 = loads.view(-1, 32).max(dim=1).values.mean().item()
+    max_loads = int(loads.max().item())
+
+    # ------------------------------------------------ roofline
+    peak, peak_src = peaks()
+    n_pos = forest.n_pos()
+    bytes_sample = 4 + 4 + 4 + 16 * (e_loads - 1.0)   # xi, out, table entry, visited records
+    t_sample_launch = ts / K * 1e-3
+    ach_s = S * bytes_sample / t_sample_launch / 1e9
+    bytes_build = 4 * n + 16 * n_pos + 4 * m          # read p, write records, write table
+    t_build = tb / K * 1e-3
+    ach_b = bytes_build / t_build / 1e9
+
+    # ------------------------------------------------ end to end through host buffers
+    e2e = None
+    if not args.no_e2e:
+        import torch as T
+        p_pin = T.from_numpy(p_host).pin_memory()
+        p_stage = T.empty(n, dtype=T.float32, device=dev)
+        f2 = rtf.Forest(n, m)
+        rtf.build_host(f2, p_pin, p_stage)
+        ts_e = []
+        for _ in range(K):
+            flush.zero_()
+            T.cuda.synchronize()
+            t0 = time.perf_counter()
+            st = rtf.build_host(f2, p_pin, p_stage)
+            ts_e.append(time.perf_counter() - t0)
+            assert st == 0
+        te = sum(ts_e)
+        S_e = min(S, 1 << 28)
+        xi_h = T.empty(S_e, dtype=T.int32).pin_memory()
+        xi_h.copy_(xi[:S_e].cpu())
+        out_h = T.empty(S_e, dtype=T.int32).pin_memory()
+        chunk = 1 << 24
+        xs = T.empty(2 * chunk, dtype=T.int32, device=dev)
+        os_ = T.empty(2 * chunk, dtype=T.int32, device=dev)
+        rtf.sample_host(f2, xi_h, out_h, xs, os_)
+        ts_s = []
+        for _ in range(max(2, min(3, K))):
+            t0 = time.perf_counter()
+            rtf.sample_host(f2, xi_h, out_h, xs, os_)
+            ts_s.append(time.perf_counter() - t0)
+        tss = statistics.median(ts_s)
+        if world > 1:
+            t = T.tensor([te, tss], dtype=T.float64, device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            te, tss = t.tolist()
+        e2e = {"value": round(world * n * K / te / 1e9, 4), "unit": "G entries/s",
+               "h2d_bytes_per_step": 4 * n, "d2h_bytes_per_step": 40,
+               "path": "rtf_build_host: pinned host p -> device copy -> build -> header read back",
+               "sampling": {"value": round(world * S_e / tss / 1e9, 4), "unit": "G samples/s",
+                            "samples": S_e, "h2d_bytes_per_step": 4 * S_e,
+                            "d2h_bytes_per_step": 4 * S_e,
+                            "path": "rtf_sample_host: pinned host xi -> 3-stream pipeline -> "
+                                    "pinned host out"}}
+
+    result = {
+        "metric": METRIC,
+        "value": round(build_gs, 4),
+        "unit": "G entries/s",
+        "n_gpus": world,
+        "steps": K,
+        "warmup": args.warmup,
+        "ms_per_step": round((tb + ts) / K, 4),
+        "higher_is_better": True,
+        "scaling": "weak",
+        "vs_baseline": None,
+        "dtype": "u64",
+        "data": "synthetic",
+        "config": {"workload": wl["desc"], "n": n, "m": m, "samples_per_gpu": S,
+                   "n_pos": n_pos,
+                   "l2": f"flushed between steps ({L2_FLUSH_BYTES >> 20} MiB write, untimed)",
+                   "parallelism": f"replicas x{world}: each GPU builds and samples its own "
+                                  "problem, no collective on the data path",
+                   "value_is": "build entries per second: n * n_gpus * steps / sum of build "
+                               "times (max over ranks)"},
+        "build": {"value": round(build_gs, 4), "unit": "G entries/s",
+                  "ms_per_build": round(tb / K, 5)},
+        "sampling": {"value": round(sample_gs, 4), "unit": "G samples/s",
+                     "ms_per_batch": round(ts / K, 4),
+                     "bsearch": {"value": round(bsearch_gs, 4), "unit": "G samples/s",
+                                 "ms_per_batch": round(tbs, 4), "identical_indices": eq},
+                     "speedup_vs_bsearch": round(sample_gs / bsearch_gs, 3),
+                     "loads_per_sample": {"avg": round(e_loads, 4), "avg32": round(avg32, 4),
+                                          "max": max_loads, "of": 1 << 20}},
+        "roofline": {"kernel": "k_sample (Alg. 2)", "bound": "hbm",
+                     "achieved": round(ach_s, 2), "peak": peak, "unit": "GB/s",
+                     "frac": round(ach_s / peak, 4),
+                     "traffic": ncu_traffic("k_sample", wl["name"]),
+                     "algorithmic_bytes_per_unit": round(bytes_sample, 3),
+                     "unit_of_work": "sample", "peak_source": peak_src},
+        "roofline_build": {"kernel": "build pipeline (k_scale, k_tile_totals, k_scan_build, "
+                                     "k_cross_tile)", "bound": "hbm",
+                           "achieved": round(ach_b, 2), "peak": peak, "unit": "GB/s",
+                           "frac": round(ach_b / peak, 4),
+                           "traffic": ncu_traffic("build", wl["name"]),
+                           "algorithmic_bytes_per_launch": bytes_build,
+                           "peak_source": peak_src},
+        "gpu_launches": launches,
+        "clocks": sampler.summary(),
+    }
+    if e2e:
+        result["e2e"] = e2e
+    if rank == 0 and not args.no_cpu_baseline:
+        result["cpu_baseline"] = cpu_baseline(p_host, m, xi[: 1 << 22].cpu().numpy().view(np.uint32))
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+    if rank == 0:
+        print(json.dumps(result), flush=True)
+
+
+def cpu_baseline(p_host, m, xi_sample):
+    """The CPU oracle as it stands (single thread), on a bounded sample."""
+    import oracle
+    n = p_host.size
+    reps, tb = 0, 0.0
+    while tb < 8.0 and reps < 6:
+        t0 = time.perf_counter()
+        f = oracle.build(p_host, m)
+        tb += time.perf_counter() - t0
+        reps += 1
+    t0 = time.perf_counter()
+    f.sample(xi_sample)
+    tsm = time.perf_counter() - t0
+    return {"value": round(n * reps / tb / 1e9, 6), "unit": "G entries/s", "cores": 1,
+            "kind": "oracle",
+            "sample": f"{reps} full oracle builds of the same n={n} input; sampling "
+                      f"{xi_sample.size} of the same xi",
+            "sampling": {"value": round(xi_sample.size / tsm / 1e9, 6), "unit": "G samples/s"}}
+
+
+# ============================================================================ reference arm
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    import oracle
+    from workloads import philox_xi, sobol0_xi
+    wl = WORKLOADS[args.workload]
+    n, m = wl["n"], wl["m"]
+    p = make_p(wl)
+    S_ref = 1 << 20
+    xi = philox_xi(S_ref, seed=0x5EED) if wl["name"] == "c3_powerlaw" else sobol0_xi(S_ref)
+    for _ in range(args.warmup if args.warmup < 2 else 1):
+        oracle.build(p, m)
+    tb, ts = 0.0, 0.0
+    for _ in range(args.steps):
+        t0 = time.perf_counter()
+        f = oracle.build(p, m)
+        t1 = time.perf_counter()
+        f.sample(xi)
+        t2 = time.perf_counter()
+        tb += t1 - t0
+        ts += t2 - t1
+    value = n * args.steps / tb / 1e9
+    result = {
+        "metric": METRIC, "value": round(value, 6), "unit": "G entries/s", "impl": "reference",
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": round((tb + ts) / args.steps * 1e3, 3), "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "u64", "data": "synthetic",
+        "config": {"workload": wl["desc"], "n": n, "m": m,
+                   "samples_per_step": S_ref,
+                   "note": "CPU oracle (oracle/rtf_oracle.c, serial, 1 thread): each step = one "
+                           "full build of the same input + a bounded sample of 2^20 xi"},
+        "cpu_baseline": {"value": round(value, 6), "unit": "G entries/s", "cores": 1,
+                         "kind": "oracle",
+                         "sample": f"full n={n} build per step; sampling {S_ref} xi per step",
+                         "sampling": {"value": round(S_ref * args.steps / ts / 1e9, 6),
+                                      "unit": "G samples/s"}},
+        "e2e": {"value": round(value, 6), "unit": "G entries/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(result), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="rtf", choices=["rtf", "reference"])
+    ap.add_argument("--workload", default="c3", choices=sorted(WORKLOADS))
+    ap.add_argument("--samples", type=int, default=0, help="override samples per GPU")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3 and args.impl != "reference":
+        print("warning: fewer than 3 warm-up steps", file=sys.stderr)
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_gpu(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,219 @@
+/*
+ * rtf.h -- C ABI of librtf.so, the B200 (sm_100a) radix-tree-forest sampler.
+ *
+ * Implements the data-parallel hot path of Binder & Keller, arXiv 1901.05423:
+ *   rtf_build:  p  ->  fixed-point CDF, guide table and radix-tree forest
+ *               (prefix sum Sec.1, Alg. 1, guide-table
+ *               encoding Sec.3.2);
+ *   rtf_sample: xi -> i with P_{i-1} <= xi < P_i (Alg. 2).
+ * "P:<line>" cites /root/reference/PAPER.md (not needed at run time).
+ *
+ * Conventions for every call
+ *   - Pointers are DEVICE pointers unless the parameter name ends in _host.
+ *   - The library never allocates device memory: the caller owns p, xi, out,
+ *     the forest buffer and the workspace (sizes from the *_bytes calls).
+ *   - `stream` is a cudaStream_t passed as void* (NULL = legacy default
+ *     stream).  All device work is enqueued on it; calls return after
+ *     enqueueing unless documented as synchronous.
+ *   - Argument errors are detected on the host BEFORE any launch and returned
+ *     as an rtf_status; nothing is enqueued then.
+ *   - Data errors (NaN, +-Inf, negative or all-zero weights) are detected on
+ *     the device: they set rtf_header.status, every later kernel of the build
+ *     becomes a no-op and every rtf_sample output is INT32_MAX.  Read them
+ *     with rtf_forest_status (synchronous).
+ *   - Indices are 0-based (reading R1).  Sampled indices are ORIGINAL input
+ *     indices; entries with p_i == 0 are never returned (reading R8).
+ *   - Limits: 1 <= n < 2^31, 1 <= m < 2^31 (leaf references use the sign bit,
+ *     P:1334 / reading R3).
+ *   - Fixed point (reading R4, R7): weights are quantised to integers
+ *     w_i = max(1, floor(p_i 2^(B-E))) for p_i > 0 (E = floor(log2 max p),
+ *     B = 62 - ceil(log2 n)), T = sum w < 2^63, and the CDF boundaries are
+ *     key_j = floor(W_j 2^63 / T) over the compacted positive entries; the
+ *     implicit key_{n'} = 2^63 is "1".  xi is u32 fixed point xi/2^32 (R11).
+ */
+#ifndef RTF_H
+#define RTF_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ------------------------------------------------------------------ types */
+
+typedef enum rtf_status {
+    RTF_OK = 0,
+    RTF_EINVAL = 1,    /* null pointer, n == 0, m == 0, bad flags, misaligned buffer */
+    RTF_EALLZERO = 2,  /* (data) no strictly positive weight                          */
+    RTF_ETOOLARGE = 3, /* n or m >= 2^31, or a batched row larger than supported      */
+    RTF_ENOSPACE = 4,  /* caller buffer smaller than the *_bytes() requirement        */
+    RTF_ECUDA = 5,     /* a CUDA runtime call failed (launch error, bad stream ...)   */
+    RTF_EDATA = 6      /* (data) NaN / Inf / negative weight (see rtf_header.status)  */
+} rtf_status;
+
+/* rtf_header.status bits (device-side data errors) */
+#define RTF_DATA_NAN 1u
+#define RTF_DATA_INF 2u
+#define RTF_DATA_NEG 4u
+#define RTF_DATA_ALLZERO 8u
+
+/* One node record, 16 bytes: the CDF boundary of node j interleaved with its
+ * two children (Sec.3.2).  child >= 0: node index; child < 0:
+ * leaf reference ~i of ORIGINAL interval i (Alg.2). */
+typedef struct rtf_node {
+    uint64_t key;      /* key_j = floor(W_j 2^63 / T), strictly increasing in j */
+    int32_t child[2];  /* [0]: taken if xi 2^31 < key, [1]: otherwise          */
+} rtf_node;
+
+/* Device-resident build summary (one per row for batched forests). */
+typedef struct rtf_header {
+    uint64_t total;      /* T = sum of quantised weights, 0 < T < 2^63            */
+    uint64_t recip;      /* internal: reciprocal of T << norm_shift                */
+    uint32_t n_pos;      /* n' = number of strictly positive weights = #nodes     */
+    int32_t exponent;    /* E = floor(log2(max p))                                 */
+    int32_t scale_bits;  /* B = 62 - ceil(log2 n)                                  */
+    uint32_t status;     /* 0 or RTF_DATA_* bits                                   */
+    uint32_t norm_shift; /* internal                                               */
+    uint32_t reserved;
+} rtf_header; /* 40 bytes */
+
+/* Host-side view of a forest living in a caller-owned device buffer. */
+typedef struct rtf_forest {
+    uint32_t n;      /* entries per row                                   */
+    uint32_t m;      /* guide-table cells per row                         */
+    uint32_t rows;   /* 1, or the number of independent rows (batched)    */
+    uint32_t flags;  /* build flags                                       */
+    rtf_node *nodes; /* rows * n records (the first n_pos of each row valid) */
+    int32_t *table;  /* rows * m references: >= 0 anchor node, < 0 leaf ~i */
+    rtf_header *header; /* rows headers                                  */
+} rtf_forest;
+
+/* rtf_build flags */
+#define RTF_BUILD_DEFAULT 0u
+#define RTF_BUILD_SMALL_TILES 1u /* 128-entry tiles: a test/debug schedule that moves most
+                                    merges into the cross-tile phase; same result bytes */
+
+/* ------------------------------------------------------------- sizing */
+
+/* Bytes of the forest buffer for `rows` rows of n entries and m cells
+ * (header + nodes + table, 256-byte aligned sections).  Host only. */
+size_t rtf_forest_bytes(uint32_t n, uint32_t m, uint32_t rows);
+
+/* Bytes of scratch workspace rtf_build needs for (n, m, flags).  Host only. */
+size_t rtf_workspace_bytes(uint32_t n, uint32_t m, uint32_t flags);
+
+/* Byte offset of Alg. 1's synchronisation array otherBounds (int32[n])
+ * inside the workspace; all -1 whenever no build is running.  For tests and
+ * debugging only.  Host only. */
+size_t rtf_workspace_sync_offset(uint32_t n, uint32_t m, uint32_t flags);
+
+/* Initialise a workspace once after allocating it (enqueues memsets).  Every
+ * rtf_build leaves the workspace initialised again (reset-on-consume of the
+ * Alg. 1 synchronisation array), so this is needed only once. */
+int rtf_workspace_init(void *ws, size_t ws_bytes, uint32_t n, uint32_t m, uint32_t flags,
+                       void *stream);
+
+/* --------------------------------------------------------------- build */
+
+/* Build the guide table and radix-tree forest of p[0..n) with m cells.
+ *   p:      n float32 weights (device), >= 0, finite, not all zero; need not
+ *           be normalised.  16-byte alignment gives vectorised loads.
+ *   forest_buf / forest_bytes: >= rtf_forest_bytes(n, m, 1), 256-B aligned.
+ *   ws / ws_bytes: >= rtf_workspace_bytes(n, m, flags), initialised once.
+ *   out (host): receives the view of the forest.
+ * Asynchronous: 4 kernels on `stream` (scale, tile totals with decoupled
+ * look-back, scan+normalise+in-tile Alg. 1, cross-tile Alg. 1 + table).
+ * The result bytes are independent of the schedule and of `flags`. */
+int rtf_build(const float *p, uint32_t n, uint32_t m, uint32_t flags, void *forest_buf,
+              size_t forest_bytes, void *ws, size_t ws_bytes, void *stream, rtf_forest *out);
+
+/* Batched build of `rows` independent distributions of n_row entries each
+ * (p is row-major rows x n_row), m_row cells per row, one CTA per row entirely
+ * in shared memory (Sec.5: the row boundary is one more partition
+ * criterion).  Each row is normalised independently (reading R15).
+ * Requires n_row <= 4096 and m_row <= 4096 (else RTF_ETOOLARGE).  No workspace. */
+int rtf_build_rows(const float *p, uint32_t rows, uint32_t n_row, uint32_t m_row,
+                   void *forest_buf, size_t forest_bytes, void *stream, rtf_forest *out);
+
+/* Re-create a view of an existing forest buffer (no device work). */
+int rtf_forest_view(void *forest_buf, size_t forest_bytes, uint32_t n, uint32_t m,
+                    uint32_t rows, rtf_forest *out);
+
+/* Synchronous: waits for `stream`, copies the f->rows device headers into
+ * headers_host (may be NULL) and returns RTF_OK, RTF_EALLZERO or RTF_EDATA
+ * (the worst row for batched forests). */
+int rtf_forest_status(const rtf_forest *f, void *stream, rtf_header *headers_host);
+
+/* ------------------------------------------------------------ sampling */
+
+/* Alg. 2 for count samples: out[k] = the ORIGINAL index i with
+ * key_i <= xi[k] 2^31 < key_next (guide-table lookup g = floor(xi m / 2^32),
+ * then descent while the reference is a node).  Read-only on the forest, so
+ * concurrent calls on one forest are safe.  xi / out need 4-byte alignment
+ * (16-byte alignment enables vector access). */
+int rtf_sample(const rtf_forest *f, const uint32_t *xi, uint64_t count, int32_t *out,
+               void *stream);
+
+/* Measurement aid: loads[k] = number of memory loads Alg. 2 performs for
+ * xi[k] (1 guide-table entry + 1 per node visited), the load-count convention
+ * of Table 1.  Gives E[visits], the maximum and average_32. */
+int rtf_sample_loads(const rtf_forest *f, const uint32_t *xi, uint64_t count, int32_t *loads,
+                     void *stream);
+
+/* Batched: sample k uses row[k] (< f->rows); out is row-local. */
+int rtf_sample_rows(const rtf_forest *f, const uint32_t *row, const uint32_t *xi,
+                    uint64_t count, int32_t *out, void *stream);
+
+/* ----------------------------------------------- baselines (same CDF) */
+
+/* The full fixed-point CDF over all n entries, zeros included:
+ * cdf[i] = floor(W_i 2^63 / T), W_i = sum_{k<i} w_k (u64[n], device), and a
+ * device header.  This is the array a plain binary search (Sec.2.2
+ * P:114-127) searches.  Uses the same workspace as rtf_build. */
+int rtf_build_cdf(const float *p, uint32_t n, uint64_t *cdf, rtf_header *header, void *ws,
+                  size_t ws_bytes, void *stream);
+
+/* Binary search baseline: out[k] = last i with cdf[i] <= xi[k] 2^31
+ * (identical results to rtf_sample on the same p). */
+int rtf_sample_bsearch(const uint64_t *cdf, uint32_t n, const rtf_header *header,
+                       const uint32_t *xi, uint64_t count, int32_t *out, void *stream);
+
+/* ------------------------------------------- host-buffer entry points */
+
+/* End-to-end build from HOST weights: copies p_host (pinned for full speed)
+ * into p_dev (n floats, device scratch), builds, and reads the header back.
+ * Synchronous; returns the build status (data errors included). */
+int rtf_build_host(const float *p_host, uint32_t n, uint32_t m, uint32_t flags, float *p_dev,
+                   void *forest_buf, size_t forest_bytes, void *ws, size_t ws_bytes,
+                   void *stream, rtf_forest *out, rtf_header *header_host);
+
+/* End-to-end sampling from HOST xi to HOST out: chunks of `chunk` samples
+ * are copied in, sampled and copied out on three internal streams so copies
+ * overlap the kernel.  xi_dev / out_dev: device staging of 2*chunk entries
+ * each.  Synchronous. */
+int rtf_sample_host(const rtf_forest *f, const uint32_t *xi_host, uint64_t count,
+                    int32_t *out_host, uint32_t *xi_dev, int32_t *out_dev, uint64_t chunk,
+                    void *stream);
+
+/* ---------------------------------------------------------- utilities */
+
+/* Input generator (not part of the method): Philox4x32-10 u32 stream,
+ * out[k] = word (start+k) mod 4 of philox(counter = ((start+k)/4 lo, hi, 0, 0),
+ * key = seed).  Identical to workloads.philox_xi. */
+int rtf_philox_u32(uint64_t seed, uint64_t start, uint64_t count, uint32_t *out, void *stream);
+
+/* Number of kernels this process has launched through librtf (monotonic). */
+uint64_t rtf_launch_count(void);
+
+/* Human-readable status name. */
+const char *rtf_status_string(int status);
+
+/* Library version string. */
+const char *rtf_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* RTF_H */

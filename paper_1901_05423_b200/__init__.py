@@ -1,0 +1,284 @@
+"""paper_1901_05423_b200 -- radix-tree-forest sampling (Binder & Keller,
+arXiv 1901.05423) on NVIDIA B200.
+
+A thin binding over librtf.so (C ABI, include/rtf.h).  This module only
+marshals arguments: device memory and streams come from PyTorch, every step of
+the build and of sampling runs in the library's sm_100a kernels.  If the
+library is missing, importing the ops raises -- there is no CPU fallback.
+
+    import torch, paper_1901_05423_b200 as rtf
+    f = rtf.build(p_cuda_float32, m)            # guide table + radix forest
+    idx = rtf.sample(f, xi_cuda_uint32)         # Alg. 2, original indices
+"""
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import _lib
+from ._lib import (RTF_BUILD_DEFAULT, RTF_BUILD_SMALL_TILES, RTF_DATA_ALLZERO,  # noqa: F401
+                   RTF_DATA_INF, RTF_DATA_NAN, RTF_DATA_NEG, RtfError, check, rtf_forest,
+                   rtf_header)
+
+__all__ = ["Forest", "RowsForest", "build", "build_rows", "sample", "sample_rows",
+           "build_cdf", "sample_bsearch", "philox", "build_host", "sample_host",
+           "launch_count", "RtfError", "lib"]
+
+NODE_DTYPE = np.dtype([("key", "<u8"), ("c0", "<i4"), ("c1", "<i4")])
+
+
+def lib():
+    return _lib.load()
+
+
+def _stream(stream=None) -> ctypes.c_void_p:
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return ctypes.c_void_p(s.cuda_stream)
+
+
+def _ptr(t: torch.Tensor) -> ctypes.c_void_p:
+    return ctypes.c_void_p(t.data_ptr())
+
+
+def _u32_view(t: torch.Tensor) -> torch.Tensor:
+    if t.dtype not in (torch.int32, torch.uint32):
+        raise TypeError(f"expected a 32-bit integer tensor of fixed-point xi/2^32, got {t.dtype}")
+    if not t.is_cuda or not t.is_contiguous():
+        raise ValueError("xi must be a contiguous CUDA tensor")
+    return t
+
+
+def _bytes_tensor(nbytes: int, device) -> torch.Tensor:
+    return torch.empty(max(int(nbytes), 1), dtype=torch.uint8, device=device)
+
+
+@dataclass
+class _Buffers:
+    forest: torch.Tensor
+    ws: torch.Tensor | None
+
+
+class Forest:
+    """A guide table + radix forest over n weights with m cells, in device memory
+    owned by this object (forest buffer + build workspace)."""
+
+    def __init__(self, n: int, m: int, flags: int = RTF_BUILD_DEFAULT, device="cuda"):
+        L = lib()
+        self.n, self.m, self.flags = int(n), int(m), int(flags)
+        self.device = torch.device(device)
+        fb = L.rtf_forest_bytes(self.n, self.m, 1)
+        wb = L.rtf_workspace_bytes(self.n, self.m, self.flags)
+        self._buf = _Buffers(_bytes_tensor(fb, self.device), _bytes_tensor(wb, self.device))
+        self.view = rtf_forest()
+        check(L.rtf_forest_view(_ptr(self._buf.forest), fb, self.n, self.m, 1,
+                                ctypes.byref(self.view)), "rtf_forest_view")
+        check(L.rtf_workspace_init(_ptr(self._buf.ws), wb, self.n, self.m, self.flags,
+                                   _stream()), "rtf_workspace_init")
+
+    # ---------------------------------------------------------------- build
+    def build(self, p: torch.Tensor, stream=None) -> "Forest":
+        if p.dtype != torch.float32 or not p.is_cuda or not p.is_contiguous():
+            raise TypeError("p must be a contiguous float32 CUDA tensor")
+        if p.numel() != self.n:
+            raise ValueError(f"p has {p.numel()} entries, forest was sized for {self.n}")
+        self._p = p  # keep alive while kernels run
+        check(lib().rtf_build(_ptr(p), self.n, self.m, self.flags, _ptr(self._buf.forest),
+                              self._buf.forest.numel(), _ptr(self._buf.ws),
+                              self._buf.ws.numel(), _stream(stream), ctypes.byref(self.view)),
+              "rtf_build")
+        return self
+
+    # ---------------------------------------------------------------- sampling
+    def sample(self, xi: torch.Tensor, out: torch.Tensor | None = None, stream=None):
+        xi = _u32_view(xi)
+        if out is None:
+            out = torch.empty(xi.numel(), dtype=torch.int32, device=xi.device)
+        check(lib().rtf_sample(ctypes.byref(self.view), _ptr(xi), xi.numel(), _ptr(out),
+                               _stream(stream)), "rtf_sample")
+        return out
+
+    def sample_loads(self, xi: torch.Tensor, stream=None) -> torch.Tensor:
+        """Per-sample memory loads of Alg. 2 (1 table entry + nodes visited)."""
+        xi = _u32_view(xi)
+        out = torch.empty(xi.numel(), dtype=torch.int32, device=xi.device)
+        check(lib().rtf_sample_loads(ctypes.byref(self.view), _ptr(xi), xi.numel(), _ptr(out),
+                                     _stream(stream)), "rtf_sample_loads")
+        return out
+
+    # ---------------------------------------------------------------- inspection
+    def header(self, stream=None) -> rtf_header:
+        h = rtf_header()
+        self.last_status = lib().rtf_forest_status(ctypes.byref(self.view), _stream(stream),
+                                                   ctypes.byref(h))
+        return h
+
+    def status(self, stream=None) -> int:
+        self.header(stream)
+        return self.last_status
+
+    def n_pos(self) -> int:
+        return int(self.header().n_pos)
+
+    def _section(self, ptr, nbytes) -> torch.Tensor:
+        base = self._buf.forest.data_ptr()
+        off = ptr - base
+        return self._buf.forest[off: off + nbytes]
+
+    def nodes_numpy(self) -> np.ndarray:
+        k = self.n_pos()
+        raw = self._section(self.view.nodes, 16 * k).cpu().numpy()
+        return raw.view(NODE_DTYPE)
+
+    def table_numpy(self) -> np.ndarray:
+        return self._section(self.view.table, 4 * self.m).cpu().numpy().view(np.int32)
+
+    def other_bounds_numpy(self) -> np.ndarray:
+        """Alg. 1's otherBounds array in the workspace; all -1 between
+        builds (reset-on-consume)."""
+        off = lib().rtf_workspace_sync_offset(self.n, self.m, self.flags)
+        return self._buf.ws[off: off + 4 * self.n].cpu().numpy().view(np.int32)
+
+
+class RowsForest:
+    """`rows` independent forests of n_row entries / m_row cells (config 5)."""
+
+    def __init__(self, rows: int, n_row: int, m_row: int, device="cuda"):
+        L = lib()
+        self.rows, self.n, self.m = int(rows), int(n_row), int(m_row)
+        fb = L.rtf_forest_bytes(self.n, self.m, self.rows)
+        self._forest = _bytes_tensor(fb, torch.device(device))
+        self.view = rtf_forest()
+        check(L.rtf_forest_view(_ptr(self._forest), fb, self.n, self.m, self.rows,
+                                ctypes.byref(self.view)), "rtf_forest_view")
+
+    def build(self, p: torch.Tensor, stream=None) -> "RowsForest":
+        if p.dtype != torch.float32 or not p.is_cuda or not p.is_contiguous():
+            raise TypeError("p must be a contiguous float32 CUDA tensor")
+        if p.numel() != self.rows * self.n:
+            raise ValueError("p must hold rows * n_row weights")
+        self._p = p
+        check(lib().rtf_build_rows(_ptr(p), self.rows, self.n, self.m, _ptr(self._forest),
+                                   self._forest.numel(), _stream(stream),
+                                   ctypes.byref(self.view)), "rtf_build_rows")
+        return self
+
+    def sample(self, row: torch.Tensor, xi: torch.Tensor, out=None, stream=None):
+        xi = _u32_view(xi)
+        row = _u32_view(row)
+        if out is None:
+            out = torch.empty(xi.numel(), dtype=torch.int32, device=xi.device)
+        check(lib().rtf_sample_rows(ctypes.byref(self.view), _ptr(row), _ptr(xi), xi.numel(),
+                                    _ptr(out), _stream(stream)), "rtf_sample_rows")
+        return out
+
+    def headers(self, stream=None) -> np.ndarray:
+        arr = (rtf_header * self.rows)()
+        self.last_status = lib().rtf_forest_status(ctypes.byref(self.view), _stream(stream),
+                                                   ctypes.cast(arr, ctypes.POINTER(rtf_header)))
+        return np.ctypeslib.as_array(arr)
+
+    def _section(self, ptr, nbytes):
+        off = ptr - self._forest.data_ptr()
+        return self._forest[off: off + nbytes]
+
+    def nodes_numpy(self) -> np.ndarray:
+        return self._section(self.view.nodes, 16 * self.rows * self.n).cpu().numpy().view(NODE_DTYPE)
+
+    def table_numpy(self) -> np.ndarray:
+        return self._section(self.view.table, 4 * self.rows * self.m).cpu().numpy().view(np.int32)
+
+
+# -------------------------------------------------------------------- functional API
+
+def build(p: torch.Tensor, m: int, flags: int = RTF_BUILD_DEFAULT, stream=None) -> Forest:
+    return Forest(p.numel(), m, flags, device=p.device).build(p, stream)
+
+
+def sample(forest: Forest, xi: torch.Tensor, out=None, stream=None) -> torch.Tensor:
+    return forest.sample(xi, out, stream)
+
+
+def build_rows(p: torch.Tensor, m_row: int, stream=None) -> RowsForest:
+    rows, n_row = p.shape
+    return RowsForest(rows, n_row, m_row, device=p.device).build(p.contiguous().view(-1), stream)
+
+
+def sample_rows(forest: RowsForest, row, xi, out=None, stream=None):
+    return forest.sample(row, xi, out, stream)
+
+
+class Cdf:
+    """The full fixed-point CDF (zeros included) for the binary-search baseline."""
+
+    def __init__(self, n: int, device="cuda"):
+        self.n = int(n)
+        self.cdf = torch.empty(self.n, dtype=torch.int64, device=device)
+        self.header = torch.zeros(48, dtype=torch.uint8, device=device)
+        wb = lib().rtf_workspace_bytes(self.n, 1, 0)
+        self.ws = _bytes_tensor(wb, torch.device(device))
+        check(lib().rtf_workspace_init(_ptr(self.ws), self.ws.numel(), self.n, 1, 0, _stream()),
+              "rtf_workspace_init")
+
+    def build(self, p: torch.Tensor, stream=None) -> "Cdf":
+        self._p = p
+        check(lib().rtf_build_cdf(_ptr(p), self.n, _ptr(self.cdf), _ptr(self.header),
+                                  _ptr(self.ws), self.ws.numel(), _stream(stream)),
+              "rtf_build_cdf")
+        return self
+
+    def sample(self, xi: torch.Tensor, out=None, stream=None) -> torch.Tensor:
+        xi = _u32_view(xi)
+        if out is None:
+            out = torch.empty(xi.numel(), dtype=torch.int32, device=xi.device)
+        check(lib().rtf_sample_bsearch(_ptr(self.cdf), self.n, _ptr(self.header), _ptr(xi),
+                                       xi.numel(), _ptr(out), _stream(stream)),
+              "rtf_sample_bsearch")
+        return out
+
+
+def build_cdf(p: torch.Tensor, stream=None) -> Cdf:
+    return Cdf(p.numel(), p.device).build(p, stream)
+
+
+def sample_bsearch(cdf: Cdf, xi: torch.Tensor, out=None, stream=None) -> torch.Tensor:
+    return cdf.sample(xi, out, stream)
+
+
+def philox(count: int, seed: int = 0x5EED, start: int = 0, out=None, device="cuda",
+           stream=None) -> torch.Tensor:
+    if out is None:
+        out = torch.empty(int(count), dtype=torch.int32, device=device)
+    check(lib().rtf_philox_u32(seed, start, int(count), _ptr(out), _stream(stream)),
+          "rtf_philox_u32")
+    return out
+
+
+def build_host(forest: Forest, p_host: torch.Tensor, p_dev: torch.Tensor, stream=None) -> int:
+    """End-to-end build from a (pinned) host float32 tensor; synchronous."""
+    h = rtf_header()
+    st = lib().rtf_build_host(ctypes.c_void_p(p_host.data_ptr()), forest.n, forest.m,
+                              forest.flags, _ptr(p_dev), _ptr(forest._buf.forest),
+                              forest._buf.forest.numel(), _ptr(forest._buf.ws),
+                              forest._buf.ws.numel(), _stream(stream),
+                              ctypes.byref(forest.view), ctypes.byref(h))
+    if st not in (_lib.RTF_OK, _lib.RTF_EALLZERO, _lib.RTF_EDATA):
+        check(st, "rtf_build_host")
+    return st
+
+
+def sample_host(forest: Forest, xi_host: torch.Tensor, out_host: torch.Tensor,
+                xi_dev: torch.Tensor, out_dev: torch.Tensor, stream=None) -> None:
+    """End-to-end sampling host -> host through pipelined staging buffers
+    (xi_dev / out_dev hold 2 chunks each); synchronous."""
+    chunk = xi_dev.numel() // 2
+    check(lib().rtf_sample_host(ctypes.byref(forest.view), ctypes.c_void_p(xi_host.data_ptr()),
+                                xi_host.numel(), ctypes.c_void_p(out_host.data_ptr()),
+                                _ptr(xi_dev), _ptr(out_dev), chunk, _stream(stream)),
+          "rtf_sample_host")
+
+
+def launch_count() -> int:
+    return int(lib().rtf_launch_count())

@@ -1,0 +1,316 @@
+// rtf_api.cu -- the C ABI of librtf (include/rtf.h): argument checks, buffer
+// carve-up and launches on the caller's stream.  No device allocation, no CPU
+// fallback: every result is computed by the kernels in rtf_build.cu,
+// rtf_rows.cu and rtf_sample.cu.
+#include <atomic>
+#include <cstring>
+
+#include "rtf_internal.h"
+
+namespace {
+
+std::atomic<uint64_t> g_launches{0};
+
+constexpr size_t kAlign = 256;
+
+inline size_t align_up(size_t x) { return (x + kAlign - 1) & ~(kAlign - 1); }
+
+struct ForestLayout {
+    size_t header, nodes, table, total;
+};
+
+ForestLayout forest_layout(uint32_t n, uint32_t m, uint32_t rows) {
+    ForestLayout L;
+    size_t off = 0;
+    L.header = off;
+    off += align_up(sizeof(rtf_header) * (size_t)rows);
+    L.nodes = off;
+    off += align_up(sizeof(rtf_node) * (size_t)n * rows);
+    L.table = off;
+    off += align_up(sizeof(int32_t) * (size_t)m * rows);
+    L.total = off;
+    return L;
+}
+
+inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
+
+inline int check_nm(uint32_t n, uint32_t m) {
+    if (n == 0 || m == 0) return RTF_EINVAL;
+    if (n >= 0x80000000u || m >= 0x80000000u) return RTF_ETOOLARGE;
+    return RTF_OK;
+}
+
+inline int finish(cudaError_t e, int launches) {
+    g_launches.fetch_add((uint64_t)launches, std::memory_order_relaxed);
+    return e == cudaSuccess ? RTF_OK : RTF_ECUDA;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* rtf_version(void) { return "rtf-b200 0.1 (sm_100a)"; }
+
+const char* rtf_status_string(int s) {
+    switch (s) {
+        case RTF_OK: return "RTF_OK";
+        case RTF_EINVAL: return "RTF_EINVAL";
+        case RTF_EALLZERO: return "RTF_EALLZERO";
+        case RTF_ETOOLARGE: return "RTF_ETOOLARGE";
+        case RTF_ENOSPACE: return "RTF_ENOSPACE";
+        case RTF_ECUDA: return "RTF_ECUDA";
+        case RTF_EDATA: return "RTF_EDATA";
+        default: return "RTF_UNKNOWN";
+    }
+}
+
+uint64_t rtf_launch_count(void) { return g_launches.load(); }
+
+size_t rtf_forest_bytes(uint32_t n, uint32_t m, uint32_t rows) {
+    if (rows == 0) rows = 1;
+    return forest_layout(n, m, rows).total;
+}
+
+size_t rtf_workspace_bytes(uint32_t n, uint32_t m, uint32_t flags) {
+    rtf::WsLayout L;
+    return rtf::build_workspace_layout(n ? n : 1, m ? m : 1, flags, &L);
+}
+
+size_t rtf_workspace_sync_offset(uint32_t n, uint32_t m, uint32_t flags) {
+    rtf::WsLayout L;
+    rtf::build_workspace_layout(n ? n : 1, m ? m : 1, flags, &L);
+    return L.ob;
+}
+
+int rtf_workspace_init(void* ws, size_t ws_bytes, uint32_t n, uint32_t m, uint32_t flags,
+                       void* stream) {
+    if (!ws) return RTF_EINVAL;
+    if (int s = check_nm(n, m)) return s;
+    rtf::WsLayout L;
+    if (ws_bytes < rtf::build_workspace_layout(n, m, flags, &L)) return RTF_ENOSPACE;
+    cudaStream_t st = as_stream(stream);
+    unsigned char* w = static_cast<unsigned char*>(ws);
+    cudaError_t e = cudaMemsetAsync(w, 0, L.ob, st);  // partials, counters, flags, prefixes
+    if (e == cudaSuccess) e = cudaMemsetAsync(w + L.ob, 0xFF, sizeof(int32_t) * (size_t)n, st);
+    return e == cudaSuccess ? RTF_OK : RTF_ECUDA;
+}
+
+int rtf_forest_view(void* buf, size_t bytes, uint32_t n, uint32_t m, uint32_t rows,
+                    rtf_forest* out) {
+    if (!buf || !out || rows == 0) return RTF_EINVAL;
+    if (int s = check_nm(n, m)) return s;
+    if (((uintptr_t)buf & (kAlign - 1)) != 0) return RTF_EINVAL;
+    const ForestLayout L = forest_layout(n, m, rows);
+    if (bytes < L.total) return RTF_ENOSPACE;
+    unsigned char* b = static_cast<unsigned char*>(buf);
+    out->n = n;
+    out->m = m;
+    out->rows = rows;
+    out->flags = 0;
+    out->header = reinterpret_cast<rtf_header*>(b + L.header);
+    out->nodes = reinterpret_cast<rtf_node*>(b + L.nodes);
+    out->table = reinterpret_cast<int32_t*>(b + L.table);
+    return RTF_OK;
+}
+
+int rtf_build(const float* p, uint32_t n, uint32_t m, uint32_t flags, void* forest_buf,
+              size_t forest_bytes, void* ws, size_t ws_bytes, void* stream, rtf_forest* out) {
+    if (!p || !ws || !out) return RTF_EINVAL;
+    if (flags & ~RTF_BUILD_SMALL_TILES) return RTF_EINVAL;
+    if (((uintptr_t)p & 3u) != 0) return RTF_EINVAL;
+    if (int s = rtf_forest_view(forest_buf, forest_bytes, n, m, 1, out)) return s;
+    out->flags = flags;
+    rtf::WsLayout L;
+    if (ws_bytes < rtf::build_workspace_layout(n, m, flags, &L)) return RTF_ENOSPACE;
+    if (((uintptr_t)ws & (kAlign - 1)) != 0) return RTF_EINVAL;
+    int launches = 0;
+    cudaError_t e = rtf::launch_build(p, n, m, flags, out->header, out->nodes, out->table,
+                                      nullptr, ws, L, as_stream(stream), &launches);
+    return finish(e, launches);
+}
+
+int rtf_build_rows(const float* p, uint32_t rows, uint32_t n_row, uint32_t m_row,
+                   void* forest_buf, size_t forest_bytes, void* stream, rtf_forest* out) {
+    if (!p || !out || rows == 0) return RTF_EINVAL;
+    if (((uintptr_t)p & 3u) != 0) return RTF_EINVAL;
+    if (int s = check_nm(n_row, m_row)) return s;
+    if (n_row > rtf::kRowsMax || m_row > rtf::kRowsMax) return RTF_ETOOLARGE;
+    if (int s = rtf_forest_view(forest_buf, forest_bytes, n_row, m_row, rows, out)) return s;
+    int launches = 0;
+    cudaError_t e = rtf::launch_build_rows(p, rows, n_row, m_row, out->header, out->nodes,
+                                           out->table, as_stream(stream), &launches);
+    return finish(e, launches);
+}
+
+int rtf_forest_status(const rtf_forest* f, void* stream, rtf_header* headers_host) {
+    if (!f || !f->header || f->rows == 0) return RTF_EINVAL;
+    cudaStream_t st = as_stream(stream);
+    rtf_header one;
+    rtf_header* dst = headers_host ? headers_host : nullptr;
+    int worst = RTF_OK;
+    const size_t bytes = sizeof(rtf_header) * (size_t)f->rows;
+    rtf_header* tmp = dst;
+    bool owned = false;
+    if (!tmp) {
+        if (f->rows == 1) tmp = &one;
+        else {
+            tmp = new rtf_header[f->rows];
+            owned = true;
+        }
+    }
+    cudaError_t e = cudaMemcpyAsync(tmp, f->header, bytes, cudaMemcpyDeviceToHost, st);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+    if (e != cudaSuccess) worst = RTF_ECUDA;
+    else
+        for (uint32_t r = 0; r < f->rows; ++r) {
+            const uint32_t s = tmp[r].status;
+            if (s & (RTF_DATA_NAN | RTF_DATA_INF | RTF_DATA_NEG)) worst = RTF_EDATA;
+            else if ((s & RTF_DATA_ALLZERO) && worst == RTF_OK) worst = RTF_EALLZERO;
+        }
+    if (owned) delete[] tmp;
+    return worst;
+}
+
+int rtf_sample(const rtf_forest* f, const uint32_t* xi, uint64_t count, int32_t* out,
+               void* stream) {
+    if (!f || !f->nodes || !f->table || !f->header || f->rows != 1) return RTF_EINVAL;
+    if (count && (!xi || !out)) return RTF_EINVAL;
+    if ((((uintptr_t)xi | (uintptr_t)out) & 3u) != 0) return RTF_EINVAL;
+    int launches = 0;
+    cudaError_t e = rtf::launch_sample(*f, nullptr, xi, count, out, as_stream(stream), &launches);
+    return finish(e, launches);
+}
+
+int rtf_sample_loads(const rtf_forest* f, const uint32_t* xi, uint64_t count, int32_t* loads,
+                     void* stream) {
+    if (!f || !f->nodes || !f->table || !f->header || f->rows != 1) return RTF_EINVAL;
+    if (count && (!xi || !loads)) return RTF_EINVAL;
+    if ((((uintptr_t)xi | (uintptr_t)loads) & 3u) != 0) return RTF_EINVAL;
+    int launches = 0;
+    cudaError_t e = rtf::launch_sample_loads(*f, xi, count, loads, as_stream(stream), &launches);
+    return finish(e, launches);
+}
+
+int rtf_sample_rows(const rtf_forest* f, const uint32_t* row, const uint32_t* xi, uint64_t count,
+                    int32_t* out, void* stream) {
+    if (!f || !f->nodes || !f->table || !f->header || f->rows == 0) return RTF_EINVAL;
+    if (count && (!xi || !out || !row)) return RTF_EINVAL;
+    if ((((uintptr_t)xi | (uintptr_t)out | (uintptr_t)row) & 3u) != 0) return RTF_EINVAL;
+    int launches = 0;
+    cudaError_t e = rtf::launch_sample(*f, row, xi, count, out, as_stream(stream), &launches);
+    return finish(e, launches);
+}
+
+int rtf_build_cdf(const float* p, uint32_t n, uint64_t* cdf, rtf_header* header, void* ws,
+                  size_t ws_bytes, void* stream) {
+    if (!p || !cdf || !header || !ws) return RTF_EINVAL;
+    if (int s = check_nm(n, 1)) return s;
+    if ((((uintptr_t)p & 3u) | ((uintptr_t)cdf & 7u) | ((uintptr_t)header & 7u)) != 0)
+        return RTF_EINVAL;
+    rtf::WsLayout L;
+    if (ws_bytes < rtf::build_workspace_layout(n, 1, 0, &L)) return RTF_ENOSPACE;
+    int launches = 0;
+    cudaError_t e = rtf::launch_build(p, n, 1, 0, header, nullptr, nullptr, cdf, ws, L,
+                                      as_stream(stream), &launches);
+    return finish(e, launches);
+}
+
+int rtf_sample_bsearch(const uint64_t* cdf, uint32_t n, const rtf_header* header,
+                       const uint32_t* xi, uint64_t count, int32_t* out, void* stream) {
+    if (!cdf || !header) return RTF_EINVAL;
+    if (int s = check_nm(n, 1)) return s;
+    if (count && (!xi || !out)) return RTF_EINVAL;
+    if ((((uintptr_t)xi | (uintptr_t)out) & 3u) != 0) return RTF_EINVAL;
+    int launches = 0;
+    cudaError_t e = rtf::launch_bsearch(cdf, n, header, xi, count, out, as_stream(stream),
+                                        &launches);
+    return finish(e, launches);
+}
+
+int rtf_build_host(const float* p_host, uint32_t n, uint32_t m, uint32_t flags, float* p_dev,
+                   void* forest_buf, size_t forest_bytes, void* ws, size_t ws_bytes, void* stream,
+                   rtf_forest* out, rtf_header* header_host) {
+    if (!p_host || !p_dev) return RTF_EINVAL;
+    if (int s = check_nm(n, m)) return s;
+    cudaStream_t st = as_stream(stream);
+    if (cudaMemcpyAsync(p_dev, p_host, sizeof(float) * (size_t)n, cudaMemcpyHostToDevice, st) !=
+        cudaSuccess)
+        return RTF_ECUDA;
+    int s = rtf_build(p_dev, n, m, flags, forest_buf, forest_bytes, ws, ws_bytes, stream, out);
+    if (s != RTF_OK) return s;
+    return rtf_forest_status(out, stream, header_host);
+}
+
+int rtf_sample_host(const rtf_forest* f, const uint32_t* xi_host, uint64_t count, int32_t* out_host,
+                    uint32_t* xi_dev, int32_t* out_dev, uint64_t chunk, void* stream) {
+    if (!f || f->rows != 1 || (count && (!xi_host || !out_host || !xi_dev || !out_dev)))
+        return RTF_EINVAL;
+    if (count == 0) return RTF_OK;
+    if (chunk == 0) return RTF_EINVAL;
+    chunk = (chunk + 3) & ~3ull;
+    cudaStream_t user = as_stream(stream);
+    // three stages on three streams: H2D, sample, D2H; double-buffered staging
+    cudaStream_t s_in, s_run, s_out;
+    cudaEvent_t ev_ready[2], ev_in[2], ev_run[2], ev_out[2];
+    cudaError_t e = cudaSuccess;
+    bool ok = cudaStreamCreateWithFlags(&s_in, cudaStreamNonBlocking) == cudaSuccess;
+    ok = ok && cudaStreamCreateWithFlags(&s_run, cudaStreamNonBlocking) == cudaSuccess;
+    ok = ok && cudaStreamCreateWithFlags(&s_out, cudaStreamNonBlocking) == cudaSuccess;
+    for (int b = 0; b < 2 && ok; ++b) {
+        ok = ok && cudaEventCreateWithFlags(&ev_ready[b], cudaEventDisableTiming) == cudaSuccess;
+        ok = ok && cudaEventCreateWithFlags(&ev_in[b], cudaEventDisableTiming) == cudaSuccess;
+        ok = ok && cudaEventCreateWithFlags(&ev_run[b], cudaEventDisableTiming) == cudaSuccess;
+        ok = ok && cudaEventCreateWithFlags(&ev_out[b], cudaEventDisableTiming) == cudaSuccess;
+    }
+    if (!ok) return RTF_ECUDA;
+    // order after everything already enqueued on the caller's stream (the build)
+    cudaEvent_t ev_user;
+    cudaEventCreateWithFlags(&ev_user, cudaEventDisableTiming);
+    cudaEventRecord(ev_user, user);
+    cudaStreamWaitEvent(s_in, ev_user, 0);
+    cudaStreamWaitEvent(s_run, ev_user, 0);
+    int launches = 0;
+    uint64_t k = 0;
+    for (uint64_t c = 0; k < count && e == cudaSuccess; ++c) {
+        const int b = (int)(c & 1);
+        const uint64_t len = std::min<uint64_t>(chunk, count - k);
+        uint32_t* xd = xi_dev + (size_t)b * chunk;
+        int32_t* od = out_dev + (size_t)b * chunk;
+        if (c >= 2) cudaStreamWaitEvent(s_in, ev_run[b], 0);  // xi buffer b free
+        e = cudaMemcpyAsync(xd, xi_host + k, len * 4, cudaMemcpyHostToDevice, s_in);
+        cudaEventRecord(ev_in[b], s_in);
+        cudaStreamWaitEvent(s_run, ev_in[b], 0);
+        if (c >= 2) cudaStreamWaitEvent(s_run, ev_out[b], 0);  // out buffer b drained
+        if (e == cudaSuccess) e = rtf::launch_sample(*f, nullptr, xd, len, od, s_run, &launches);
+        cudaEventRecord(ev_run[b], s_run);
+        cudaStreamWaitEvent(s_out, ev_run[b], 0);
+        if (e == cudaSuccess)
+            e = cudaMemcpyAsync(out_host + k, od, len * 4, cudaMemcpyDeviceToHost, s_out);
+        cudaEventRecord(ev_out[b], s_out);
+        k += len;
+    }
+    cudaError_t e2 = cudaStreamSynchronize(s_out);
+    if (e == cudaSuccess) e = e2;
+    cudaStreamSynchronize(s_run);
+    cudaStreamSynchronize(s_in);
+    for (int b = 0; b < 2; ++b) {
+        cudaEventDestroy(ev_ready[b]);
+        cudaEventDestroy(ev_in[b]);
+        cudaEventDestroy(ev_run[b]);
+        cudaEventDestroy(ev_out[b]);
+    }
+    cudaEventDestroy(ev_user);
+    cudaStreamDestroy(s_in);
+    cudaStreamDestroy(s_run);
+    cudaStreamDestroy(s_out);
+    return finish(e, launches);
+}
+
+int rtf_philox_u32(uint64_t seed, uint64_t start, uint64_t count, uint32_t* out, void* stream) {
+    if (count && !out) return RTF_EINVAL;
+    int launches = 0;
+    cudaError_t e = rtf::launch_philox(seed, start, count, out, as_stream(stream), &launches);
+    return finish(e, launches);
+}
+
+}  // extern "C"

@@ -1,0 +1,203 @@
+// rtf_device.cuh -- device helpers of librtf (product path; shares nothing with oracle/).
+//
+// Fixed-point conventions (readings R4/R7/R11):
+//   w_i   = max(1, floor(p_i 2^(B-E))) for p_i > 0, else 0
+//   key_j = floor(W_j 2^63 / T)       (63 fractional bits, "1" = 2^63)
+//   cell  = floor(key m / 2^63)       (Alg. 1, curCell = floor(data m))
+//   lambda_j = 64 at a cell boundary / array end, else msb(key_j ^ key_{j+1})
+//              (XOR distance P:1049-1055, "distance set to the maximum" P:1078-1079)
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "../../include/rtf.h"
+
+namespace rtf {
+
+constexpr uint64_t kOne63 = 1ull << 63;
+constexpr uint32_t kLamBoundary = 64;
+
+// ------------------------------------------------------------ memory-model helpers
+
+__device__ __forceinline__ uint32_t ld_acquire_u32(const uint32_t* p) {
+    uint32_t v;
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+
+__device__ __forceinline__ void st_release_u32(uint32_t* p, uint32_t v) {
+    asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+// streaming 16-byte load that does not allocate in L1 (read-once data)
+__device__ __forceinline__ uint4 ld_stream_u4(const void* p) {
+    uint4 r;
+    asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+                 : "l"(p));
+    return r;
+}
+
+__device__ __forceinline__ float4 ld_stream_f4(const float* p) {
+    uint4 r = ld_stream_u4(p);
+    return make_float4(__uint_as_float(r.x), __uint_as_float(r.y), __uint_as_float(r.z),
+                       __uint_as_float(r.w));
+}
+
+// ------------------------------------------------------------ quantisation
+
+// floor(log2(x)) of a positive finite float given its bits
+__device__ __forceinline__ int floor_log2_bits(uint32_t b) {
+    uint32_t be = b >> 23;
+    if (be) return (int)be - 127;
+    return (31 - __clz((int)b)) - 149;  // subnormal: frac * 2^-149
+}
+
+// w = max(1, floor(x 2^shift)) for x > 0 (exact on the mantissa), 0 otherwise
+__device__ __forceinline__ uint64_t quantize(float x, int shift) {
+    if (!(x > 0.0f)) return 0;
+    uint32_t b = __float_as_uint(x);
+    uint32_t be = b >> 23, fr = b & 0x7fffffu;
+    uint64_t mant = be ? (uint64_t)(fr | 0x800000u) : (uint64_t)fr;
+    int sh = (be ? (int)be - 150 : -149) + shift;
+    uint64_t v = sh >= 0 ? (mant << sh) : (sh <= -64 ? 0ull : (mant >> (-sh)));
+    return v ? v : 1ull;
+}
+
+// ------------------------------------------------------------ exact normalisation
+//
+// key = floor(W 2^63 / T) for 0 <= W < T < 2^63 by division with a precomputed
+// reciprocal of the normalised divisor d = T << s (Moller & Granlund 2011,
+// "Improved division by invariant integers", Alg. 4): the numerator is
+// (u1, u0) = (W << (s-1), 0) since W 2^63 2^s = (W 2^(s-1)) 2^64.
+
+struct Norm {
+    uint64_t d;  // T << s, msb set
+    uint64_t v;  // floor((2^128 - 1) / d) - 2^64
+    uint32_t s;  // clz(T) >= 1
+};
+
+// v for a normalised d: the 128/64 quotient of (~d, ~0) by d, bit by bit.
+__device__ __forceinline__ uint64_t reciprocal_of(uint64_t d) {
+    uint64_t rem = ~d, lo = ~0ull, q = 0;
+    for (int i = 63; i >= 0; --i) {
+        uint64_t carry = rem >> 63;
+        rem = (rem << 1) | ((lo >> i) & 1ull);
+        q <<= 1;
+        if (carry || rem >= d) {
+            rem -= d;
+            q |= 1ull;
+        }
+    }
+    return q;
+}
+
+__device__ __forceinline__ uint64_t fixed_point(uint64_t W, const Norm& nm) {
+    uint64_t u1 = W << (nm.s - 1);
+    uint64_t q0 = nm.v * u1;
+    uint64_t q1 = __umul64hi(nm.v, u1) + u1 + 1ull;
+    uint64_t r = 0ull - q1 * nm.d;  // u0 - q1 d (mod 2^64), u0 = 0
+    if (r > q0) {
+        q1 -= 1ull;
+        r += nm.d;
+    }
+    if (r >= nm.d) q1 += 1ull;
+    return q1;
+}
+
+__device__ __forceinline__ uint32_t cell_of(uint64_t key, uint32_t m) {
+    return (uint32_t)__umul64hi(key << 1, (uint64_t)m);  // floor(key m / 2^63)
+}
+
+__device__ __forceinline__ uint32_t split_level(uint64_t a, uint64_t b) {
+    return 63u - (uint32_t)__clzll((long long)(a ^ b));  // msb(a ^ b)
+}
+
+// ------------------------------------------------------------ scan prefix payload
+
+// Aggregate of a run of entries: sum of quantised weights, number of positive
+// entries, original index of the last positive entry (-1 if none).
+struct __align__(16) Pfx {
+    uint64_t W;
+    uint32_t cnt;
+    int32_t last;
+};
+
+__device__ __forceinline__ Pfx combine(const Pfx& a, const Pfx& b) {  // a precedes b
+    Pfx r;
+    r.W = a.W + b.W;
+    r.cnt = a.cnt + b.cnt;
+    r.last = b.last >= 0 ? b.last : a.last;
+    return r;
+}
+
+__device__ __forceinline__ Pfx ld_pfx_cg(const Pfx* p) {
+    uint4 u = __ldcg(reinterpret_cast<const uint4*>(p));
+    Pfx r;
+    r.W = (uint64_t)u.x | ((uint64_t)u.y << 32);
+    r.cnt = u.z;
+    r.last = (int32_t)u.w;
+    return r;
+}
+
+__device__ __forceinline__ void st_pfx(Pfx* p, const Pfx& v) {
+    uint4 u = make_uint4((uint32_t)v.W, (uint32_t)(v.W >> 32), v.cnt, (uint32_t)v.last);
+    *reinterpret_cast<uint4*>(p) = u;
+}
+
+// ------------------------------------------------------------ warp / block scans
+
+__device__ __forceinline__ uint64_t shfl_up_u64(uint64_t v, int d) {
+    return __shfl_up_sync(0xffffffffu, v, d);
+}
+
+// Block-wide exclusive scan of (u64, u32) pairs.  scratch: 2 * (THREADS/32) words of each.
+template <int THREADS>
+__device__ __forceinline__ void block_scan_excl(uint64_t w, uint32_t c, uint64_t& w_ex,
+                                                uint32_t& c_ex, uint64_t& w_tot, uint32_t& c_tot,
+                                                uint64_t* s_w, uint32_t* s_c) {
+    constexpr int NW = THREADS / 32;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    uint64_t wi = w;
+    uint32_t ci = c;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+        uint64_t tw = shfl_up_u64(wi, d);
+        uint32_t tc = __shfl_up_sync(0xffffffffu, ci, d);
+        if (lane >= d) {
+            wi += tw;
+            ci += tc;
+        }
+    }
+    if (lane == 31) {
+        s_w[warp] = wi;
+        s_c[warp] = ci;
+    }
+    __syncthreads();
+    if (warp == 0) {
+        uint64_t ww = lane < NW ? s_w[lane] : 0ull;
+        uint32_t cc = lane < NW ? s_c[lane] : 0u;
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {
+            uint64_t tw = shfl_up_u64(ww, d);
+            uint32_t tc = __shfl_up_sync(0xffffffffu, cc, d);
+            if (lane >= d) {
+                ww += tw;
+                cc += tc;
+            }
+        }
+        if (lane < NW) {
+            s_w[NW + lane] = ww;  // inclusive warp prefixes
+            s_c[NW + lane] = cc;
+        }
+    }
+    __syncthreads();
+    uint64_t wbase = warp ? s_w[NW + warp - 1] : 0ull;
+    uint32_t cbase = warp ? s_c[NW + warp - 1] : 0u;
+    w_ex = wbase + wi - w;
+    c_ex = cbase + ci - c;
+    w_tot = s_w[2 * NW - 1];
+    c_tot = s_c[2 * NW - 1];
+}
+
+}  // namespace rtf

@@ -1,0 +1,259 @@
+// rtf_rows.cu -- batched build of many small independent distributions (config 5:
+// per-pixel / per-light tables; Sec.5 P:1531-1533 "adding yet another criterion
+// to the extended check ... the index boundary of a row").
+//
+// One CTA per row; the whole pipeline of rtf_build (validate, quantise, scan,
+// normalise, cells, split levels, guide table, Alg. 1) runs in shared memory and
+// the row's records and table are written once, coalesced.  Each row has its
+// own scale E, B and total T (reading R15).
+#include "rtf_device.cuh"
+#include "rtf_internal.h"
+
+namespace rtf {
+
+struct RowsArgs {
+    const float* p;
+    uint32_t rows, n_row, m_row;
+    rtf_header* hdr;
+    rtf_node* nodes;
+    int32_t* table;
+    bool vec;
+};
+
+template <int THREADS, int VPT>
+__global__ void __launch_bounds__(THREADS) k_build_rows(RowsArgs A) {
+    constexpr int NMAX = THREADS * VPT;
+    extern __shared__ __align__(16) unsigned char smem[];
+    struct __align__(16) SRec {
+        uint64_t key;
+        int32_t c0, c1;
+    };
+    SRec* s_rec = reinterpret_cast<SRec*>(smem);
+    int32_t* s_orig = reinterpret_cast<int32_t*>(s_rec + NMAX);
+    int32_t* s_ob = s_orig + NMAX;
+    int32_t* s_anc = s_ob + NMAX;     // [m_row] first leaf of the cell, -1 if empty
+    int32_t* s_lst = s_anc + NMAX;    // [m_row] last leaf of the cell, -1 if empty
+    uint8_t* s_lam = reinterpret_cast<uint8_t*>(s_lst + NMAX);
+    __shared__ uint64_t s_w[2 * (THREADS / 32)];
+    __shared__ uint32_t s_c[2 * (THREADS / 32)];
+    __shared__ uint32_t s_red[2 * (THREADS / 32)];
+    __shared__ uint64_t s_recip;
+
+    const uint32_t r = blockIdx.x;
+    const uint32_t n = A.n_row, m = A.m_row;
+    const float* p = A.p + (size_t)r * n;
+    const uint32_t first = threadIdx.x * VPT;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+
+    float x[VPT];
+    if (A.vec && first + VPT <= n) {
+#pragma unroll
+        for (int k = 0; k < VPT; k += 4) {
+            const float4 v = ld_stream_f4(p + first + k);
+            x[k] = v.x;
+            x[k + 1] = v.y;
+            x[k + 2] = v.z;
+            x[k + 3] = v.w;
+        }
+    } else {
+#pragma unroll
+        for (int k = 0; k < VPT; ++k) x[k] = first + k < n ? p[first + k] : 0.0f;
+    }
+    // validate + max (K1 of the single-distribution pipeline)
+    uint32_t mx = 0, fl = 0;
+#pragma unroll
+    for (int k = 0; k < VPT; ++k) {
+        const float v = x[k];
+        if (v != v) fl |= RTF_DATA_NAN;
+        else if (fabsf(v) == __int_as_float(0x7f800000)) fl |= RTF_DATA_INF;
+        else if (v < 0.0f) fl |= RTF_DATA_NEG;
+        else if (v > 0.0f) mx = max(mx, __float_as_uint(v));
+    }
+    for (int d = 16; d; d >>= 1) {
+        mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, d));
+        fl |= __shfl_xor_sync(0xffffffffu, fl, d);
+    }
+    if (lane == 0) {
+        s_red[2 * warp] = mx;
+        s_red[2 * warp + 1] = fl;
+    }
+    for (uint32_t g = threadIdx.x; g < m; g += THREADS) {
+        s_anc[g] = -1;
+        s_lst[g] = -1;
+    }
+    __syncthreads();
+    mx = 0;
+    fl = 0;
+    for (int w = 0; w < THREADS / 32; ++w) {
+        mx = max(mx, s_red[2 * w]);
+        fl |= s_red[2 * w + 1];
+    }
+    const uint32_t status = fl | (mx == 0 ? RTF_DATA_ALLZERO : 0u);
+    if (status) {
+        if (threadIdx.x == 0) {
+            rtf_header h{};
+            h.status = status;
+            A.hdr[r] = h;
+        }
+        return;
+    }
+    const int E = floor_log2_bits(mx);
+    const int B = 62 - (n > 1 ? 32 - __clz((int)(n - 1)) : 0);
+    uint64_t w[VPT];
+    uint64_t tw = 0;
+    uint32_t tc = 0;
+#pragma unroll
+    for (int k = 0; k < VPT; ++k) {
+        w[k] = quantize(x[k], B - E);
+        tw += w[k];
+        tc += w[k] != 0;
+    }
+    uint64_t W, T;
+    uint32_t jl, cnt;
+    block_scan_excl<THREADS>(tw, tc, W, jl, T, cnt, s_w, s_c);
+    Norm nm;
+    nm.s = (uint32_t)__clzll((long long)T);
+    nm.d = T << nm.s;
+    if (threadIdx.x == 0) s_recip = reciprocal_of(nm.d);
+    __syncthreads();
+    nm.v = s_recip;
+
+#pragma unroll
+    for (int k = 0; k < VPT; ++k) {
+        if (!w[k]) continue;
+        const uint64_t key = fixed_point(W, nm);
+        const uint64_t Wn = W + w[k];
+        const bool last = Wn == T;
+        const uint64_t kn = last ? kOne63 : fixed_point(Wn, nm);
+        const uint32_t cell = cell_of(key, m);
+        const uint32_t cn = last ? m : cell_of(kn, m);
+        const uint32_t lam = cn != cell ? kLamBoundary : split_level(key, kn);
+        s_rec[jl].key = key;
+        s_lam[jl] = (uint8_t)lam;
+        s_orig[jl] = (int32_t)(first + k);
+        if (jl == 0) s_anc[0] = 0;
+        if (lam == kLamBoundary) {
+            s_lst[cell] = (int32_t)jl;
+            if (cn < m) s_anc[cn] = (int32_t)(jl + 1);
+        }
+        W = Wn;
+        ++jl;
+    }
+    __syncthreads();
+    for (uint32_t l = threadIdx.x; l < cnt; l += THREADS) {
+        s_rec[l].c0 = ~s_orig[l ? l - 1 : 0];
+        s_rec[l].c1 = INT32_MIN;
+        s_ob[l] = -1;
+    }
+    // guide table: exclusive max-scan of the last leaf per cell (cells blocked per thread)
+    {
+        constexpr int MPT = NMAX / THREADS;
+        const uint32_t g0 = threadIdx.x * MPT;
+        int32_t loc = -1;
+#pragma unroll
+        for (int k = 0; k < MPT; ++k)
+            if (g0 + k < m) loc = max(loc, s_lst[g0 + k]);
+        int32_t inc = loc;
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {
+            const int32_t t = __shfl_up_sync(0xffffffffu, inc, d);
+            if (lane >= d) inc = max(inc, t);
+        }
+        __syncthreads();
+        int32_t* s_wmax = reinterpret_cast<int32_t*>(s_c);  // reuse scan scratch
+        if (lane == 31) s_wmax[warp] = inc;
+        __syncthreads();
+        int32_t before = -1;
+        for (int w2 = 0; w2 < warp; ++w2) before = max(before, s_wmax[w2]);
+        int32_t run = max(before, __shfl_up_sync(0xffffffffu, inc, 1));
+        if (lane == 0) run = before;
+        int32_t* tab = A.table + (size_t)r * m;
+#pragma unroll
+        for (int k = 0; k < MPT; ++k) {
+            const uint32_t g = g0 + k;
+            if (g < m) {
+                const int32_t a = s_anc[g];
+                tab[g] = a >= 0 ? a : ~s_orig[run];
+                run = max(run, s_lst[g]);
+            }
+        }
+    }
+    __syncthreads();
+    // Alg. 1 over all leaves of the row (the row boundary is lambda = 64 at both ends)
+    for (uint32_t l = threadIdx.x; l < cnt; l += THREADS) {
+        int32_t lo = (int32_t)l, hi = (int32_t)l;
+        int32_t node = ~s_orig[l];
+        while (true) {
+            const uint32_t lamL = lo ? s_lam[lo - 1] : kLamBoundary;
+            const uint32_t lamR = s_lam[hi];
+            if (lamL == kLamBoundary && lamR == kLamBoundary) {
+                s_rec[lo].c1 = node;
+                break;
+            }
+            const int c = lamL > lamR ? 0 : 1;
+            const int32_t parent = c ? lo : hi + 1;
+            if (c) s_rec[parent].c1 = node;
+            else s_rec[parent].c0 = node;
+            const int32_t other = atomicExch(&s_ob[parent], c ? hi : lo);
+            if (other < 0) break;
+            s_ob[parent] = -1;
+            if (c) lo = other;
+            else hi = other;
+            node = parent;
+        }
+    }
+    __syncthreads();
+    uint4* gnode = reinterpret_cast<uint4*>(A.nodes + (size_t)r * n);
+    const uint4* snode = reinterpret_cast<const uint4*>(s_rec);
+    for (uint32_t l = threadIdx.x; l < cnt; l += THREADS) gnode[l] = snode[l];
+    if (threadIdx.x == 0) {
+        rtf_header h;
+        h.total = T;
+        h.recip = nm.v;
+        h.n_pos = cnt;
+        h.exponent = E;
+        h.scale_bits = B;
+        h.status = 0;
+        h.norm_shift = nm.s;
+        h.reserved = 0;
+        A.hdr[r] = h;
+    }
+}
+
+template <int THREADS, int VPT>
+static cudaError_t launch_rows_t(const RowsArgs& A, cudaStream_t st) {
+    constexpr int NMAX = THREADS * VPT;
+    const size_t smem = (size_t)NMAX * (16 + 4 + 4 + 4 + 4 + 1);
+    static bool attr = false;
+    if (!attr) {
+        cudaError_t e = cudaFuncSetAttribute(k_build_rows<THREADS, VPT>,
+                                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e != cudaSuccess) return e;
+        attr = true;
+    }
+    k_build_rows<THREADS, VPT><<<A.rows, THREADS, smem, st>>>(A);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_build_rows(const float* p, uint32_t rows, uint32_t n_row, uint32_t m_row,
+                              rtf_header* hdr, rtf_node* nodes, int32_t* table, cudaStream_t st,
+                              int* launches) {
+    RowsArgs A;
+    A.p = p;
+    A.rows = rows;
+    A.n_row = n_row;
+    A.m_row = m_row;
+    A.hdr = hdr;
+    A.nodes = nodes;
+    A.table = table;
+    A.vec = (((uintptr_t)p & 15u) == 0) && (n_row % 4 == 0);
+    const uint32_t need = std::max(n_row, m_row);
+    cudaError_t e;
+    if (need <= 256) e = launch_rows_t<64, 4>(A, st);
+    else if (need <= 1024) e = launch_rows_t<256, 4>(A, st);
+    else e = launch_rows_t<512, 8>(A, st);
+    ++*launches;
+    return e;
+}
+
+}  // namespace rtf

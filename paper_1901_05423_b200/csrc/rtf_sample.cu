@@ -1,0 +1,249 @@
+// rtf_sample.cu -- Alg. 2 sampler, the binary-search baseline and
+// the Philox input generator.
+//
+// k_sample: every thread owns 4 samples (one 16-B load of xi, one 16-B store of
+// out) and advances their 4 descents in lock-step so up to 4 independent node
+// loads are in flight per thread.  Per visit one 16-B record (key + both
+// children, the interleaving of P:1082-1083) is read through the read-only path.
+#include "rtf_device.cuh"
+#include "rtf_internal.h"
+
+namespace rtf {
+
+constexpr int kSampleThreads = 256;
+
+__device__ __forceinline__ int32_t descend_step(const rtf_node* __restrict__ nodes, int32_t j,
+                                                uint64_t x63) {
+    const ulonglong2 r = __ldg(reinterpret_cast<const ulonglong2*>(nodes + j));
+    return (int32_t)(x63 < r.x ? (uint32_t)r.y : (uint32_t)(r.y >> 32));
+}
+
+template <bool ROWS>
+__device__ __forceinline__ int32_t sample_one(const rtf_node* __restrict__ nodes,
+                                              const int32_t* __restrict__ table,
+                                              const rtf_header* __restrict__ hdr, uint32_t n,
+                                              uint32_t m, uint32_t r, uint32_t x) {
+    if (ROWS) {
+        if (hdr[r].status) return INT32_MAX;
+        nodes += (size_t)r * n;
+        table += (size_t)r * m;
+    }
+    int32_t j = __ldg(table + (uint32_t)(((uint64_t)x * m) >> 32));
+    const uint64_t x63 = (uint64_t)x << 31;
+    while (j >= 0) j = descend_step(nodes, j, x63);
+    return ~j;
+}
+
+// COUNT: write the number of memory loads per sample (1 table entry + 1 per
+// node visited; the load-count convention of Table 1) instead of
+// the index -- a measurement aid for E[visits], max and average_32.
+template <bool ROWS, bool COUNT = false>
+__global__ void __launch_bounds__(kSampleThreads)
+    k_sample(const rtf_node* __restrict__ nodes, const int32_t* __restrict__ table,
+             const rtf_header* __restrict__ hdr, uint32_t n, uint32_t m,
+             const uint32_t* __restrict__ row, const uint32_t* __restrict__ xi, uint64_t count,
+             int32_t* __restrict__ out, bool vec) {
+    const uint64_t gt = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const uint64_t gs = (uint64_t)gridDim.x * blockDim.x;
+    const bool bad = !ROWS && hdr->status != 0;
+    uint64_t done = 0;
+    if (vec) {
+        const uint64_t nq = count >> 2;
+        for (uint64_t q = gt; q < nq; q += gs) {
+            const uint4 xv = ld_stream_u4(xi + 4 * q);
+            const uint32_t x[4] = {xv.x, xv.y, xv.z, xv.w};
+            int32_t j[4];
+            const rtf_node* nb[4];
+            uint64_t x63[4];
+            bool dead[4];
+            uint4 rv = make_uint4(0, 0, 0, 0);
+            if (ROWS) rv = ld_stream_u4(row + 4 * q);
+            const uint32_t rr[4] = {rv.x, rv.y, rv.z, rv.w};
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                const rtf_node* nk = nodes;
+                const int32_t* tk = table;
+                dead[k] = bad;
+                if (ROWS) {
+                    dead[k] = hdr[rr[k]].status != 0;
+                    nk += (size_t)rr[k] * n;
+                    tk += (size_t)rr[k] * m;
+                }
+                nb[k] = nk;
+                x63[k] = (uint64_t)x[k] << 31;
+                j[k] = dead[k] ? -1 : __ldg(tk + (uint32_t)(((uint64_t)x[k] * m) >> 32));
+            }
+            int32_t loads[4] = {1, 1, 1, 1};
+            while ((j[0] & j[1] & j[2] & j[3]) >= 0) {
+#pragma unroll
+                for (int k = 0; k < 4; ++k)
+                    if (j[k] >= 0) {
+                        j[k] = descend_step(nb[k], j[k], x63[k]);
+                        if (COUNT) ++loads[k];
+                    }
+            }
+            if (COUNT) {
+                __stcs(reinterpret_cast<int4*>(out + 4 * q),
+                       make_int4(loads[0], loads[1], loads[2], loads[3]));
+                continue;
+            }
+            int4 o;
+            o.x = dead[0] ? INT32_MAX : ~j[0];
+            o.y = dead[1] ? INT32_MAX : ~j[1];
+            o.z = dead[2] ? INT32_MAX : ~j[2];
+            o.w = dead[3] ? INT32_MAX : ~j[3];
+            __stcs(reinterpret_cast<int4*>(out + 4 * q), o);
+        }
+        done = nq << 2;
+    }
+    for (uint64_t k = done + gt; k < count; k += gs) {
+        const uint32_t r = ROWS ? row[k] : 0u;
+        if (COUNT) {
+            const rtf_node* nk = nodes + (ROWS ? (size_t)r * n : 0);
+            int32_t j = __ldg(table + (ROWS ? (size_t)r * m : 0) +
+                              (uint32_t)(((uint64_t)xi[k] * m) >> 32));
+            int32_t l = 1;
+            for (; j >= 0; ++l) j = descend_step(nk, j, (uint64_t)xi[k] << 31);
+            out[k] = l;
+            continue;
+        }
+        out[k] = bad ? INT32_MAX : sample_one<ROWS>(nodes, table, hdr, n, m, r, xi[k]);
+    }
+}
+
+// ------------------------------------------------------------ binary-search baseline
+
+__global__ void __launch_bounds__(kSampleThreads)
+    k_bsearch(const uint64_t* __restrict__ cdf, uint32_t n, const rtf_header* __restrict__ hdr,
+              const uint32_t* __restrict__ xi, uint64_t count, int32_t* __restrict__ out,
+              bool vec) {
+    const uint64_t gt = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const uint64_t gs = (uint64_t)gridDim.x * blockDim.x;
+    const bool bad = hdr->status != 0;
+    uint64_t done = 0;
+    if (vec) {
+        const uint64_t nq = count >> 2;
+        for (uint64_t q = gt; q < nq; q += gs) {
+            const uint4 xv = ld_stream_u4(xi + 4 * q);
+            const uint64_t x63[4] = {(uint64_t)xv.x << 31, (uint64_t)xv.y << 31,
+                                     (uint64_t)xv.z << 31, (uint64_t)xv.w << 31};
+            uint32_t base[4] = {0, 0, 0, 0};
+            uint32_t len = n;
+            while (len > 1) {  // last index with cdf <= x (cdf[0] = 0)
+                const uint32_t half = len >> 1;
+#pragma unroll
+                for (int k = 0; k < 4; ++k)
+                    if (__ldg(cdf + base[k] + half) <= x63[k]) base[k] += half;
+                len -= half;
+            }
+            int4 o;
+            o.x = bad ? INT32_MAX : (int32_t)base[0];
+            o.y = bad ? INT32_MAX : (int32_t)base[1];
+            o.z = bad ? INT32_MAX : (int32_t)base[2];
+            o.w = bad ? INT32_MAX : (int32_t)base[3];
+            __stcs(reinterpret_cast<int4*>(out + 4 * q), o);
+        }
+        done = nq << 2;
+    }
+    for (uint64_t k = done + gt; k < count; k += gs) {
+        const uint64_t x63 = (uint64_t)xi[k] << 31;
+        uint32_t base = 0, len = n;
+        while (len > 1) {
+            const uint32_t half = len >> 1;
+            if (__ldg(cdf + base + half) <= x63) base += half;
+            len -= half;
+        }
+        out[k] = bad ? INT32_MAX : (int32_t)base;
+    }
+}
+
+// ------------------------------------------------------------ Philox4x32-10 input generator
+
+__device__ __forceinline__ uint4 philox4x32_10(uint4 c, uint32_t k0, uint32_t k1) {
+#pragma unroll
+    for (int r = 0; r < 10; ++r) {
+        if (r) {
+            k0 += 0x9E3779B9u;
+            k1 += 0xBB67AE85u;
+        }
+        const uint32_t hi0 = __umulhi(0xD2511F53u, c.x), lo0 = 0xD2511F53u * c.x;
+        const uint32_t hi1 = __umulhi(0xCD9E8D57u, c.z), lo1 = 0xCD9E8D57u * c.z;
+        c = make_uint4(hi1 ^ c.y ^ k0, lo1, hi0 ^ c.w ^ k1, lo0);
+    }
+    return c;
+}
+
+__global__ void k_philox(uint64_t seed, uint64_t start, uint64_t count, uint32_t* __restrict__ out) {
+    const uint64_t b0 = start >> 2, b1 = (start + count + 3) >> 2;
+    const uint64_t gs = (uint64_t)gridDim.x * blockDim.x;
+    for (uint64_t b = b0 + (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; b < b1; b += gs) {
+        const uint4 r = philox4x32_10(make_uint4((uint32_t)b, (uint32_t)(b >> 32), 0u, 0u),
+                                      (uint32_t)seed, (uint32_t)(seed >> 32));
+        const uint32_t v[4] = {r.x, r.y, r.z, r.w};
+        const uint64_t k0 = b << 2;
+        if (k0 >= start && k0 + 4 <= start + count && ((k0 - start) & 3) == 0 &&
+            (((uintptr_t)(out + (k0 - start))) & 15) == 0) {
+            *reinterpret_cast<uint4*>(out + (k0 - start)) = r;
+        } else {
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+                const uint64_t k = k0 + i;
+                if (k >= start && k < start + count) out[k - start] = v[i];
+            }
+        }
+    }
+}
+
+// ------------------------------------------------------------ launchers
+
+static inline uint32_t grid_for(uint64_t work_items) {
+    const uint64_t want = (work_items + kSampleThreads - 1) / kSampleThreads;
+    return (uint32_t)std::max<uint64_t>(1, std::min<uint64_t>(want, 148ull * 64ull));
+}
+
+cudaError_t launch_sample(const rtf_forest& f, const uint32_t* row, const uint32_t* xi,
+                          uint64_t count, int32_t* out, cudaStream_t st, int* launches) {
+    if (count == 0) return cudaSuccess;
+    bool vec = (((uintptr_t)xi | (uintptr_t)out) & 15u) == 0;
+    if (row) vec = vec && (((uintptr_t)row & 15u) == 0);
+    const uint32_t grid = grid_for(vec ? (count + 3) / 4 : count);
+    if (row)
+        k_sample<true><<<grid, kSampleThreads, 0, st>>>(f.nodes, f.table, f.header, f.n, f.m, row,
+                                                        xi, count, out, vec);
+    else
+        k_sample<false><<<grid, kSampleThreads, 0, st>>>(f.nodes, f.table, f.header, f.n, f.m,
+                                                         nullptr, xi, count, out, vec);
+    ++*launches;
+    return cudaGetLastError();
+}
+
+cudaError_t launch_sample_loads(const rtf_forest& f, const uint32_t* xi, uint64_t count,
+                                int32_t* loads, cudaStream_t st, int* launches) {
+    if (count == 0) return cudaSuccess;
+    const bool vec = (((uintptr_t)xi | (uintptr_t)loads) & 15u) == 0;
+    k_sample<false, true><<<grid_for(vec ? (count + 3) / 4 : count), kSampleThreads, 0, st>>>(
+        f.nodes, f.table, f.header, f.n, f.m, nullptr, xi, count, loads, vec);
+    ++*launches;
+    return cudaGetLastError();
+}
+
+cudaError_t launch_bsearch(const uint64_t* cdf, uint32_t n, const rtf_header* hdr,
+                           const uint32_t* xi, uint64_t count, int32_t* out, cudaStream_t st,
+                           int* launches) {
+    if (count == 0) return cudaSuccess;
+    const bool vec = (((uintptr_t)xi | (uintptr_t)out) & 15u) == 0;
+    k_bsearch<<<grid_for(vec ? (count + 3) / 4 : count), kSampleThreads, 0, st>>>(cdf, n, hdr, xi,
+                                                                                  count, out, vec);
+    ++*launches;
+    return cudaGetLastError();
+}
+
+cudaError_t launch_philox(uint64_t seed, uint64_t start, uint64_t count, uint32_t* out,
+                          cudaStream_t st, int* launches) {
+    if (count == 0) return cudaSuccess;
+    k_philox<<<grid_for((count + 3) / 4 + 1), kSampleThreads, 0, st>>>(seed, start, count, out);
+    ++*launches;
+    return cudaGetLastError();
+}
+
+}  // namespace rtf

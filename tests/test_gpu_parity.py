@@ -1,0 +1,320 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle, element
+by element on the same seeded inputs.  Everything here is integer / index work,
+so the bar is bit-exact."""
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+
+import oracle  # noqa: E402
+from workloads import (FIG6_WEIGHTS, SPEC_WEIGHTS, TEASER_WEIGHTS, env_map,  # noqa: E402
+                       hammersley_xi, philox_xi, power_law, random_small, rows_lognormal,
+                       sine64, sobol0_xi, spikes, stratified_xi)
+
+pytestmark = pytest.mark.gpu
+
+DEV = "cuda"
+
+
+@pytest.fixture(scope="module")
+def rtf():
+    if not torch.cuda.is_available():
+        pytest.fail("CUDA device required for -m gpu tests")
+    import paper_1901_05423_b200 as rtf
+    rtf.lib()
+    return rtf
+
+
+def dev_f32(p):
+    return torch.from_numpy(np.ascontiguousarray(p, dtype=np.float32)).to(DEV)
+
+
+def dev_u32(x):
+    return torch.from_numpy(np.ascontiguousarray(x, dtype=np.uint32).view(np.int32)).to(DEV)
+
+
+def assert_forest_equal(f, ref, what=""):
+    assert f.status() == 0, what
+    h = f.header()
+    assert h.n_pos == ref.n_pos and h.total == ref.T, what
+    nodes = f.nodes_numpy()
+    assert np.array_equal(nodes["key"], ref.key), f"{what}: keys"
+    bad = np.flatnonzero((nodes["c0"] != ref.child0) | (nodes["c1"] != ref.child1))
+    assert bad.size == 0, f"{what}: {bad.size} node records differ, first at {bad[:5]}"
+    tab = f.table_numpy()
+    badt = np.flatnonzero(tab != ref.table)
+    assert badt.size == 0, f"{what}: {badt.size} table cells differ, first at {badt[:5]}"
+
+
+def boundary_xi(ref, rng, extra=4096):
+    ks = ref.key.astype(np.uint64)
+    b = ((ks + np.uint64((1 << 31) - 1)) >> np.uint64(31)).astype(np.int64)  # ceil(k / 2^31)
+    xs = np.concatenate([b - 1, b, b + 1, rng.integers(0, 2**32, extra),
+                         (np.arange(ref.m, dtype=np.int64) << 32) // ref.m, [0, 2**32 - 1]])
+    xs = xs[(xs >= 0) & (xs < 2**32)]
+    return xs.astype(np.uint32)
+
+
+def check_sampling(f, ref, xi):
+    got = f.sample(dev_u32(xi)).cpu().numpy()
+    want = ref.sample(xi)
+    bad = np.flatnonzero(got != want)
+    assert bad.size == 0, f"{bad.size} samples differ; first xi={xi[bad[:3]]} got={got[bad[:3]]} want={want[bad[:3]]}"
+
+
+# ---------------------------------------------------------------- paper examples
+
+@pytest.mark.parametrize("flags", [0, 1])
+def test_paper_examples(rtf, flags):
+    rng = np.random.default_rng(0)
+    for w, m in ((FIG6_WEIGHTS, 12), (SPEC_WEIGHTS, 4), (TEASER_WEIGHTS, 8), (sine64(), 64)):
+        p = np.asarray(w, np.float32)
+        f = rtf.build(dev_f32(p), m, flags)
+        ref = oracle.build(p, m)
+        assert_forest_equal(f, ref, f"m={m}")
+        check_sampling(f, ref, boundary_xi(ref, rng))
+    # teaser: the 1024-point Hammersley set (config 1) splits exactly 16 w
+    f = rtf.build(dev_f32(TEASER_WEIGHTS), 8, flags)
+    x, _ = hammersley_xi(1024)
+    got = f.sample(dev_u32(x)).cpu().numpy()
+    assert np.bincount(got, minlength=16).tolist() == [16 * v for v in TEASER_WEIGHTS]
+
+
+# ---------------------------------------------------------------- random / edge cases
+
+@pytest.mark.parametrize("flags", [0, 1])
+def test_random_small(rtf, flags):
+    rng = np.random.default_rng(1 + flags)
+    for t in range(120):
+        n = int(rng.choice([1, 2, 3, 5, 17, 127, 128, 129, 1000, 4095, 4096, 4097, 9000, 20000]))
+        m = int(max(1, rng.choice([1, n // 7, n // 2, n, 2 * n + 3, 5])))
+        p = random_small(rng, n, zero_frac=float(rng.choice([0, 0.2, 0.9])),
+                         dyn=float(rng.choice([0.3, 4, 16, 40])))
+        ref = oracle.build(p, m)
+        f = rtf.build(dev_f32(p), m, flags)
+        assert_forest_equal(f, ref, f"case {t} n={n} m={m}")
+        check_sampling(f, ref, boundary_xi(ref, rng, 512))
+
+
+def test_edge_cases(rtf):
+    rng = np.random.default_rng(3)
+    cases = []
+    cases.append((np.array([3.0], np.float32), 1))                     # n = 1
+    cases.append((np.array([0, 0, 5, 0, 0], np.float32), 3))           # single positive
+    z = np.zeros(20000, np.float32); z[[0, 19999]] = 1; cases.append((z, 64))   # sparse ends
+    z = np.zeros(20000, np.float32); z[9000:9010] = 2; cases.append((z, 7))     # zero tiles
+    cases.append((np.full(10000, 1e-45, np.float32), 100))             # all subnormal
+    g = np.exp2(-np.arange(200, dtype=np.float64)).astype(np.float32)  # geometric: deep chain
+    cases.append((g, 4))
+    cases.append((np.ones(70000, np.float32), 1))                      # m = 1: one radix tree
+    cases.append((random_small(rng, 5000), 40000))                     # m >> n
+    big = np.ones(6000, np.float32); big[::3] = 3e38; cases.append((big, 999))  # huge values
+    for k, (p, m) in enumerate(cases):
+        ref = oracle.build(p, m)
+        f = rtf.build(dev_f32(p), m)
+        assert_forest_equal(f, ref, f"edge {k}")
+        check_sampling(f, ref, boundary_xi(ref, rng, 256))
+
+
+def test_data_errors_poison(rtf):
+    xi = dev_u32(np.arange(0, 2**32, 2**24, dtype=np.uint64).astype(np.uint32))
+    for bad, code in (([1.0, float("nan")], rtf._lib.RTF_EDATA),
+                      ([1.0, -2.0], rtf._lib.RTF_EDATA),
+                      ([float("inf"), 1.0], rtf._lib.RTF_EDATA),
+                      ([0.0, 0.0, -0.0], rtf._lib.RTF_EALLZERO)):
+        p = np.zeros(5000, np.float32)
+        p[:len(bad)] = bad
+        f = rtf.build(dev_f32(p), 16)
+        assert f.status() == code
+        out = f.sample(xi).cpu().numpy()
+        assert np.all(out == np.iinfo(np.int32).max)
+        # a later valid build on the same buffers recovers
+        good = random_small(np.random.default_rng(0), 5000)
+        f.build(dev_f32(good))
+        assert_forest_equal(f, oracle.build(good, 16), "recovery")
+
+
+def test_argument_errors(rtf):
+    import ctypes
+    L = rtf.lib()
+    view = rtf.rtf_forest()
+    assert L.rtf_build(None, 10, 4, 0, None, 0, None, 0, None, ctypes.byref(view)) == rtf._lib.RTF_EINVAL
+    f = rtf.Forest(100, 10)
+    p = dev_f32(np.ones(100))
+    assert L.rtf_build(ctypes.c_void_p(p.data_ptr()), 100, 0, 0, ctypes.c_void_p(f._buf.forest.data_ptr()),
+                       f._buf.forest.numel(), ctypes.c_void_p(f._buf.ws.data_ptr()), f._buf.ws.numel(),
+                       None, ctypes.byref(view)) == rtf._lib.RTF_EINVAL
+    assert L.rtf_build(ctypes.c_void_p(p.data_ptr()), 100, 10, 0, ctypes.c_void_p(f._buf.forest.data_ptr()),
+                       16, ctypes.c_void_p(f._buf.ws.data_ptr()), f._buf.ws.numel(),
+                       None, ctypes.byref(view)) == rtf._lib.RTF_ENOSPACE
+
+
+# ---------------------------------------------------------------- schedule independence
+
+def test_repeat_builds_byte_identical_and_sync_array_idle(rtf):
+    p = power_law(1 << 20, "A")
+    m = 1 << 18
+    ref = oracle.build(p, m)
+    for flags in (0, 1):
+        f = rtf.Forest(p.size, m, flags)
+        pd = dev_f32(p)
+        first = None
+        for rep in range(20 if flags == 0 else 5):
+            f.build(pd)
+            nodes = f.nodes_numpy().tobytes() + f.table_numpy().tobytes()
+            if first is None:
+                first = nodes
+                assert_forest_equal(f, ref, f"flags={flags}")
+            assert nodes == first, f"rep {rep} differs"
+            assert np.all(f.other_bounds_numpy() == -1), "otherBounds not reset"
+
+
+# ---------------------------------------------------------------- workloads at scale
+
+@pytest.mark.parametrize("fam", ["A", "B", "C", "D"])
+def test_power_law_families_2_20(rtf, fam):
+    p = power_law(1 << 20, fam)
+    m = 1 << 18
+    ref = oracle.build(p, m)
+    f = rtf.build(dev_f32(p), m)
+    assert_forest_equal(f, ref, fam)
+    rng = np.random.default_rng(5)
+    check_sampling(f, ref, np.concatenate([philox_xi(1 << 20, seed=11), boundary_xi(ref, rng, 0)[:1 << 20]]))
+
+
+def test_config2_envmap_full(rtf):
+    """Config 2 at full size: 2048x1024 env map, m = n, 2^26 Sobol samples."""
+    p = env_map()
+    m = p.size
+    ref = oracle.build(p, m)
+    f = rtf.build(dev_f32(p), m)
+    assert_forest_equal(f, ref, "envmap")
+    xi = sobol0_xi(1 << 26)
+    got = f.sample(dev_u32(xi)).cpu().numpy()
+    assert np.array_equal(got, ref.sample(xi))
+
+
+def test_config3_full_size(rtf):
+    """Config 3 at full size (n = 2^24, m = 2^22) in the bench's launch
+    configuration: every node record and table cell vs the oracle; 2^22 of the
+    bench's Philox samples vs the oracle one by one; all 2^30 bench samples vs
+    the binary-search baseline (an independent search over the CDF, itself
+    checked against the oracle's CDF)."""
+    p = power_law(1 << 24, "A")
+    m = 1 << 22
+    ref = oracle.build(p, m)
+    pd = dev_f32(p)
+    f = rtf.build(pd, m)
+    assert_forest_equal(f, ref, "C3")
+    xi_d = rtf.philox(1 << 30, seed=0x5EED)
+    head = xi_d[: 1 << 22].cpu().numpy().view(np.uint32)
+    assert np.array_equal(head, philox_xi(1 << 22, seed=0x5EED))
+    got = f.sample(xi_d)
+    assert np.array_equal(got[: 1 << 22].cpu().numpy(), ref.sample(head))
+    cdf = rtf.build_cdf(pd)
+    K, T = oracle.cdf_all(p)
+    assert np.array_equal(cdf.cdf.cpu().numpy().view(np.uint64), K)
+    bs = cdf.sample(xi_d)
+    assert torch.equal(bs, got)
+
+
+def test_config5_rows_full(rtf):
+    """Config 5: 65536 independent rows of 1024 entries (m_row = 1024)."""
+    rows, n_row, m_row = 65536, 1024, 1024
+    p = rows_lognormal(rows, n_row)
+    ref = oracle.build_rows(p, rows, n_row, m_row)
+    f = rtf.build_rows(dev_f32(p), m_row)
+    hd = f.headers()
+    assert f.last_status == 0
+    assert np.array_equal(hd["n_pos"], ref["n_pos"]) and np.array_equal(hd["total"], ref["T"])
+    nodes = f.nodes_numpy()
+    valid = (np.arange(n_row)[None, :] < ref["n_pos"][:, None]).reshape(-1)
+    assert np.array_equal(nodes["key"][valid], ref["key"][valid])
+    assert np.array_equal(nodes["c0"][valid], ref["child0"][valid])
+    assert np.array_equal(nodes["c1"][valid], ref["child1"][valid])
+    assert np.array_equal(f.table_numpy(), ref["table"])
+    # sampling (row, xi) pairs against per-row oracle forests
+    rng = np.random.default_rng(2)
+    r = rng.integers(0, rows, 1 << 16).astype(np.uint32)
+    xi = philox_xi(1 << 16, seed=3)
+    got = f.sample(dev_u32(r), dev_u32(xi)).cpu().numpy()
+    for k in np.unique(r)[:300]:
+        sel = r == k
+        fr = oracle.build(p[k], m_row)
+        assert np.array_equal(got[sel], fr.sample(xi[sel]))
+
+
+def test_rows_random_shapes(rtf):
+    rng = np.random.default_rng(9)
+    for n_row, m_row in ((1, 1), (3, 7), (64, 16), (255, 256), (1000, 333), (1024, 4096),
+                         (4096, 4096), (2500, 100)):
+        rows = 37
+        p = np.stack([random_small(rng, n_row, zero_frac=0.3) for _ in range(rows)])
+        p[5] = 0.0          # an all-zero row
+        ref = oracle.build_rows(p, rows, n_row, m_row)
+        f = rtf.build_rows(dev_f32(p), m_row)
+        hd = f.headers()
+        assert hd["status"][5] == rtf.RTF_DATA_ALLZERO and f.last_status == rtf._lib.RTF_EALLZERO
+        ok = ref["status"] == 0
+        assert np.array_equal(hd["n_pos"][ok], ref["n_pos"][ok])
+        nodes = f.nodes_numpy()
+        valid = ((np.arange(n_row)[None, :] < ref["n_pos"][:, None]) & ok[:, None]).reshape(-1)
+        assert np.array_equal(nodes["key"][valid], ref["key"][valid])
+        assert np.array_equal(nodes["c0"][valid], ref["child0"][valid])
+        assert np.array_equal(nodes["c1"][valid], ref["child1"][valid])
+        tab = f.table_numpy().reshape(rows, m_row)
+        assert np.array_equal(tab[ok], ref["table"].reshape(rows, m_row)[ok])
+        r = np.repeat(np.arange(rows, dtype=np.uint32), 64)
+        xi = philox_xi(r.size, seed=n_row)
+        got = f.sample(dev_u32(r), dev_u32(xi)).cpu().numpy()
+        assert np.all(got[r == 5] == np.iinfo(np.int32).max)
+
+
+def test_spikes_2_22(rtf):
+    p = spikes(1 << 22)
+    m = 1 << 20
+    ref = oracle.build(p, m)
+    f = rtf.build(dev_f32(p), m)
+    assert_forest_equal(f, ref, "spikes")
+    check_sampling(f, ref, philox_xi(1 << 20, seed=4))
+
+
+# ---------------------------------------------------------------- host entry points, generator
+
+def test_philox_generator(rtf):
+    for start, count in ((0, 1000), (3, 17), (1 << 33, 4099)):
+        got = rtf.philox(count, seed=99, start=start).cpu().numpy().view(np.uint32)
+        assert np.array_equal(got, philox_xi(count, seed=99, start=start))
+
+
+def test_host_entry_points(rtf):
+    p = env_map(512, 256, seed=5)
+    m = p.size // 3
+    ref = oracle.build(p, m)
+    f = rtf.Forest(p.size, m)
+    p_host = torch.from_numpy(p).pin_memory()
+    p_dev = torch.empty(p.size, dtype=torch.float32, device=DEV)
+    assert rtf.build_host(f, p_host, p_dev) == 0
+    assert_forest_equal(f, ref, "host build")
+    xi = philox_xi(1_000_003, seed=5)
+    xi_host = torch.from_numpy(xi.view(np.int32)).pin_memory()
+    out_host = torch.empty(xi.size, dtype=torch.int32).pin_memory()
+    chunk = 1 << 17
+    xi_dev = torch.empty(2 * chunk, dtype=torch.int32, device=DEV)
+    out_dev = torch.empty(2 * chunk, dtype=torch.int32, device=DEV)
+    rtf.sample_host(f, xi_host, out_host, xi_dev, out_dev)
+    assert np.array_equal(out_host.numpy(), ref.sample(xi))
+
+
+def test_stratified_histogram_closed_form_gpu(rtf):
+    p = env_map(1024, 512, seed=2)
+    f = rtf.build(dev_f32(p), 4096)
+    ref = oracle.build(p, 4096)
+    N = 1 << 24
+    got = f.sample(dev_u32(stratified_xi(N)))
+    c = torch.bincount(got.long(), minlength=p.size).cpu().numpy()
+    ks = [int(k) for k in ref.key] + [1 << 63]
+    exp = np.zeros(p.size, np.int64)
+    for j in range(ref.n_pos):
+        exp[ref.orig[j]] = -(-N * ks[j + 1] >> 63) - -(-N * ks[j] >> 63)
+    assert np.array_equal(c, exp)

@@ -97,7 +97,8 @@ def rows_lognormal(rows: int, n_row: int, seed: int = 7) -> np.ndarray:
 def random_small(rng: np.random.Generator, n: int, zero_frac: float = 0.2,
                  dyn: float = 8.0) -> np.ndarray:
     """Random small test vectors with a high dynamic range and exact zeros."""
-    p = np.exp(dyn * rng.standard_normal(n))
+    # clip keeps every value finite and representable in float32 (tiny ones subnormal)
+    p = np.exp(np.clip(dyn * rng.standard_normal(n), -100.0, 80.0))
     p[rng.random(n) < zero_frac] = 0.0
     if not np.any(p > 0):
         p[rng.integers(n)] = 1.0
