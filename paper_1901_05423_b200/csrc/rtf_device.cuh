@@ -44,6 +44,48 @@ __device__ __forceinline__ float4 ld_stream_f4(const float* p) {
                        __uint_as_float(r.w));
 }
 
+// ------------------------------------------------------------ TMA bulk copies + mbarrier
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return (uint32_t)__cvta_generic_to_shared(p);
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count)
+                 : "memory");
+}
+
+// order generic-proxy shared-memory accesses before later async-proxy (TMA) ones
+__device__ __forceinline__ void fence_proxy_async_smem() {
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+                 "r"(bytes)
+                 : "memory");
+}
+
+// 1-D bulk copy global -> shared (UBLKCP), completion counted on `bar`
+__device__ __forceinline__ void tma_load_1d(void* dst, const void* src, uint32_t bytes,
+                                            uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::
+            "r"(smem_u32(dst)),
+        "l"(src), "r"(bytes), "r"(smem_u32(bar))
+        : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+    asm volatile(
+        "{\n\t.reg .pred P1;\n"
+        "WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+        "@!P1 bra WAIT_%=;\n}" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
+
 // ------------------------------------------------------------ quantisation
 
 // floor(log2(x)) of a positive finite float given its bits
@@ -196,6 +238,68 @@ __device__ __forceinline__ void block_scan_excl(uint64_t w, uint32_t c, uint64_t
     uint32_t cbase = warp ? s_c[NW + warp - 1] : 0u;
     w_ex = wbase + wi - w;
     c_ex = cbase + ci - c;
+    w_tot = s_w[2 * NW - 1];
+    c_tot = s_c[2 * NW - 1];
+}
+
+// Block-wide exclusive scan of (sum u64, count u32) plus an exclusive max of an
+// i32 (the last positive index before each thread).  Scratch: 2*NW entries each.
+template <int THREADS>
+__device__ __forceinline__ void block_scan3_excl(uint64_t w, uint32_t c, int32_t l, uint64_t& w_ex,
+                                                 uint32_t& c_ex, int32_t& l_ex, uint64_t& w_tot,
+                                                 uint32_t& c_tot, uint64_t* s_w, uint32_t* s_c,
+                                                 int32_t* s_l) {
+    constexpr int NW = THREADS / 32;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    uint64_t wi = w;
+    uint32_t ci = c;
+    int32_t li = l;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+        const uint64_t tw = shfl_up_u64(wi, d);
+        const uint32_t tc = __shfl_up_sync(0xffffffffu, ci, d);
+        const int32_t tl = __shfl_up_sync(0xffffffffu, li, d);
+        if (lane >= d) {
+            wi += tw;
+            ci += tc;
+            li = max(li, tl);
+        }
+    }
+    if (lane == 31) {
+        s_w[warp] = wi;
+        s_c[warp] = ci;
+        s_l[warp] = li;
+    }
+    __syncthreads();
+    if (warp == 0) {
+        uint64_t ww = lane < NW ? s_w[lane] : 0ull;
+        uint32_t cc = lane < NW ? s_c[lane] : 0u;
+        int32_t ll = lane < NW ? s_l[lane] : -1;
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {
+            const uint64_t tw = shfl_up_u64(ww, d);
+            const uint32_t tc = __shfl_up_sync(0xffffffffu, cc, d);
+            const int32_t tl = __shfl_up_sync(0xffffffffu, ll, d);
+            if (lane >= d) {
+                ww += tw;
+                cc += tc;
+                ll = max(ll, tl);
+            }
+        }
+        if (lane < NW) {
+            s_w[NW + lane] = ww;
+            s_c[NW + lane] = cc;
+            s_l[NW + lane] = ll;
+        }
+    }
+    __syncthreads();
+    const uint64_t wbase = warp ? s_w[NW + warp - 1] : 0ull;
+    const uint32_t cbase = warp ? s_c[NW + warp - 1] : 0u;
+    const int32_t lbase = warp ? s_l[NW + warp - 1] : -1;
+    const int32_t lprev = __shfl_up_sync(0xffffffffu, li, 1);
+    w_ex = wbase + wi - w;
+    c_ex = cbase + ci - c;
+    l_ex = max(lbase, lane ? lprev : -1);
     w_tot = s_w[2 * NW - 1];
     c_tot = s_c[2 * NW - 1];
 }

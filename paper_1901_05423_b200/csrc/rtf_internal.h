@@ -21,7 +21,7 @@ inline int ceil_log2_u32(uint32_t n) {
 struct WsLayout {
     uint32_t nt;  // tiles
     uint32_t qcap;
-    size_t maxpart, counters, tile_flags, agg, inc, pend, ob, lam, queue, total;
+    size_t maxpart, counters, excl, pend, ob, lam, queue, total;
 };
 
 uint32_t build_tile_size(uint32_t flags);

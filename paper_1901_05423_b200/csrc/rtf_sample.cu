@@ -11,6 +11,12 @@
 namespace rtf {
 
 constexpr int kSampleThreads = 256;
+// A valid forest needs at most 64 node visits (<= 63 internal levels, since the
+// split level strictly decreases from a cell root to a leaf, plus the anchor).
+// The descent is bounded so a corrupted buffer cannot hang the GPU; such
+// samples return kCorrupt.
+constexpr int kMaxVisits = 64;
+constexpr int32_t kCorrupt = INT32_MIN;
 
 __device__ __forceinline__ int32_t descend_step(const rtf_node* __restrict__ nodes, int32_t j,
                                                 uint64_t x63) {
@@ -30,8 +36,8 @@ __device__ __forceinline__ int32_t sample_one(const rtf_node* __restrict__ nodes
     }
     int32_t j = __ldg(table + (uint32_t)(((uint64_t)x * m) >> 32));
     const uint64_t x63 = (uint64_t)x << 31;
-    while (j >= 0) j = descend_step(nodes, j, x63);
-    return ~j;
+    for (int d = 0; j >= 0 && d < kMaxVisits; ++d) j = descend_step(nodes, j, x63);
+    return j >= 0 ? kCorrupt : ~j;
 }
 
 // COUNT: write the number of memory loads per sample (1 table entry + 1 per
@@ -74,7 +80,7 @@ __global__ void __launch_bounds__(kSampleThreads)
                 j[k] = dead[k] ? -1 : __ldg(tk + (uint32_t)(((uint64_t)x[k] * m) >> 32));
             }
             int32_t loads[4] = {1, 1, 1, 1};
-            while ((j[0] & j[1] & j[2] & j[3]) >= 0) {
+            for (int it = 0; (j[0] & j[1] & j[2] & j[3]) >= 0 && it < kMaxVisits; ++it) {
 #pragma unroll
                 for (int k = 0; k < 4; ++k)
                     if (j[k] >= 0) {
@@ -88,10 +94,10 @@ __global__ void __launch_bounds__(kSampleThreads)
                 continue;
             }
             int4 o;
-            o.x = dead[0] ? INT32_MAX : ~j[0];
-            o.y = dead[1] ? INT32_MAX : ~j[1];
-            o.z = dead[2] ? INT32_MAX : ~j[2];
-            o.w = dead[3] ? INT32_MAX : ~j[3];
+            o.x = dead[0] ? INT32_MAX : (j[0] >= 0 ? kCorrupt : ~j[0]);
+            o.y = dead[1] ? INT32_MAX : (j[1] >= 0 ? kCorrupt : ~j[1]);
+            o.z = dead[2] ? INT32_MAX : (j[2] >= 0 ? kCorrupt : ~j[2]);
+            o.w = dead[3] ? INT32_MAX : (j[3] >= 0 ? kCorrupt : ~j[3]);
             __stcs(reinterpret_cast<int4*>(out + 4 * q), o);
         }
         done = nq << 2;
@@ -103,7 +109,7 @@ __global__ void __launch_bounds__(kSampleThreads)
             int32_t j = __ldg(table + (ROWS ? (size_t)r * m : 0) +
                               (uint32_t)(((uint64_t)xi[k] * m) >> 32));
             int32_t l = 1;
-            for (; j >= 0; ++l) j = descend_step(nk, j, (uint64_t)xi[k] << 31);
+            for (; j >= 0 && l <= kMaxVisits; ++l) j = descend_step(nk, j, (uint64_t)xi[k] << 31);
             out[k] = l;
             continue;
         }

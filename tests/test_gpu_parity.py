@@ -318,3 +318,20 @@ def test_stratified_histogram_closed_form_gpu(rtf):
     for j in range(ref.n_pos):
         exp[ref.orig[j]] = -(-N * ks[j + 1] >> 63) - -(-N * ks[j] >> 63)
     assert np.array_equal(c, exp)
+
+
+def test_corrupted_forest_terminates(rtf):
+    """Fault injection (SPEC S:274-275 idea): a child pointer rewritten into a
+    cycle must not hang Alg. 2; affected samples report INT32_MIN."""
+    p = np.ones(1000, np.float32)
+    f = rtf.build(dev_f32(p), 1)  # one radix tree: every sample descends ~10 levels
+    ref = oracle.build(p, 1)
+    root = int(ref.child1[0])
+    assert root >= 0
+    off = f.view.nodes - f._buf.forest.data_ptr()
+    rec = f._buf.forest[off: off + 16 * f.n].view(torch.int32).view(-1, 4)
+    rec[root, 2] = root  # child0 of the root points back to itself
+    rec[root, 3] = root
+    xi = dev_u32(np.arange(0, 2**32, 2**22, dtype=np.uint64).astype(np.uint32))
+    out = f.sample(xi).cpu().numpy()
+    assert np.all(out == np.iinfo(np.int32).min)
