@@ -104,9 +104,10 @@ size_t rtf_forest_bytes(uint32_t n, uint32_t m, uint32_t rows);
 /* Bytes of scratch workspace rtf_build needs for (n, m, flags).  Host only. */
 size_t rtf_workspace_bytes(uint32_t n, uint32_t m, uint32_t flags);
 
-/* Byte offset of Alg. 1's synchronisation array otherBounds (int32[n])
- * inside the workspace; all -1 whenever no build is running.  For tests and
- * debugging only.  Host only. */
+/* Byte offset of Alg. 1's synchronisation array otherBounds inside the
+ * workspace: uint64[n], each a deposit {bound (low 32 bits), split level beyond
+ * it (high 32 bits)}, all ones (= -1) whenever no build is running.  For tests
+ * and debugging only.  Host only. */
 size_t rtf_workspace_sync_offset(uint32_t n, uint32_t m, uint32_t flags);
 
 /* Initialise a workspace once after allocating it (enqueues memsets).  Every

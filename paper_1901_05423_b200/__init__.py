@@ -139,7 +139,8 @@ class Forest:
         """Alg. 1's otherBounds array in the workspace; all -1 between
         builds (reset-on-consume)."""
         off = lib().rtf_workspace_sync_offset(self.n, self.m, self.flags)
-        return self._buf.ws[off: off + 4 * self.n].cpu().numpy().view(np.int32)
+        # 64-bit deposits {bound, split level}; all ones (-1) when empty
+        return self._buf.ws[off: off + 8 * self.n].cpu().numpy().view(np.int64)
 
 
 class RowsForest:

@@ -90,8 +90,10 @@ int rtf_workspace_init(void* ws, size_t ws_bytes, uint32_t n, uint32_t m, uint32
     if (ws_bytes < rtf::build_workspace_layout(n, m, flags, &L)) return RTF_ENOSPACE;
     cudaStream_t st = as_stream(stream);
     unsigned char* w = static_cast<unsigned char*>(ws);
-    cudaError_t e = cudaMemsetAsync(w, 0, L.ob, st);  // partials, counters, flags, prefixes
-    if (e == cudaSuccess) e = cudaMemsetAsync(w + L.ob, 0xFF, sizeof(int32_t) * (size_t)n, st);
+    // partials, counters (grid barrier word, queue length), prefixes, pending leaves
+    cudaError_t e = cudaMemsetAsync(w, 0, L.ob, st);
+    // otherBounds: 64-bit {bound, split level} deposits, all ones = empty
+    if (e == cudaSuccess) e = cudaMemsetAsync(w + L.ob, 0xFF, sizeof(uint64_t) * (size_t)n, st);
     return e == cudaSuccess ? RTF_OK : RTF_ECUDA;
 }
 

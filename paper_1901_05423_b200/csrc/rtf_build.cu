@@ -1,22 +1,23 @@
-// rtf_build.cu -- the forest build: 4 kernels on the caller's stream.
+// rtf_build.cu -- the forest build: ONE persistent cooperative kernel (one CTA
+// pair per SM) whose phases are separated by grid-wide barriers:
 //
-//   K1 k_scale        read p once: max weight bits (for E), NaN/Inf/negative flags;
-//                     the last block folds the partials into one scale word and
-//                     resets the per-build counters.
-//   K2 k_tile_totals  per super-tile (kSubs K3 tiles): quantise (w), sum W, count
-//                     positives, last positive index; single-pass reduce-then-scan:
-//                     the last CTA to finish scans the super-tile aggregates and
-//                     writes every K3 tile's exclusive prefix (the parallel prefix
-//                     sum of P:239), T, n' and the reciprocal of T.
-//   K3 k_scan_build   persistent, TMA-fed tiles: block scan + tile prefix -> W_j,
-//                     compaction, one exact division per leaf (key_j); per owned
-//                     leaf: cell, split level lambda_j, guide-table anchors and
-//                     short runs; Alg. 1 for every leaf
-//                     of the tile except its first and last ("phase 1",
-//                     shared-memory atomicExch); coalesced flush of 16-B records.
-//   K4 k_cross_tile   "phase 2": the <= 2 pending edge leaves per tile continue
-//                     Alg. 1 with global atomicExch, consuming the deposits the
-//                     tiles flushed; plus the long empty-cell runs of the table.
+//   A  scale      read p once: max weight bits (for E), NaN/Inf/negative flags.
+//   B  totals     per 4096-entry tile: quantise (w), sum W, count positives,
+//                 last positive index (aggregates of the prefix sum).
+//   C  spine      CTA 0 turns the tile aggregates into exclusive prefixes and
+//                 publishes T, n' and the reciprocal of T (header).
+//   D  tiles      per tile (TMA-fed): block scan + tile prefix -> W_j,
+//                 compaction, one exact division per leaf (key_j); per owned
+//                 leaf: cell, split level lambda_j, guide-table anchors and
+//                 short runs; Alg. 1 for every leaf
+//                 of the tile except its first and last ("phase 1", shared-
+//                 memory atomicExch); coalesced flush of the 16-B records.
+//   E  cross      "phase 2": the <= 2 pending edge leaves per tile continue
+//                 Alg. 1 with global atomicExch, consuming the deposits the
+//                 tiles flushed; then the long empty-cell runs of the table.
+//
+// A deposit in otherBounds carries the depositor's far bound AND the split
+// level beyond it, so the sibling that continues never re-reads lambda.
 // The result bytes do not depend on the schedule.
 
 #include "rtf_device.cuh"
@@ -26,10 +27,10 @@ namespace rtf {
 
 constexpr uint32_t kShortRun = 32;  // empty-cell runs up to this length: written in place
 constexpr uint32_t kChunk = 2048;   // longer runs: queued in chunks of this many cells
-constexpr int kSubs = 2;            // K3 tiles per K2 super-tile
+constexpr uint32_t kMaxGrid = 8192; // partials capacity (CTAs of the cooperative grid)
 
 // workspace counters
-enum : int { kCtrDoneK2 = 0, kCtrQueue = 1, kCtrDoneK1 = 3 };
+enum : int { kCtrGridBar = 0, kCtrQueue = 1 };
 
 struct RunChunk {
     uint32_t start, len;
@@ -42,99 +43,74 @@ struct PendingLeaf {
     int32_t ref;  // ~orig(j)
 };
 
-// ============================================================== K1: scale and validate
+struct BuildArgs {
+    const float* p;
+    uint32_t n, m, nt;
+    int B;              // 62 - ceil(log2 n)
+    uint32_t* maxpart;  // 2 per CTA
+    uint32_t* counters;
+    Pfx* excl;          // per tile: aggregate (phase B), then exclusive prefix (phase C)
+    rtf_header* hdr;
+    rtf_node* nodes;
+    int32_t* table;
+    uint8_t* lam;                 // global split levels (phase E)
+    unsigned long long* ob;       // global otherBounds: {bound, lambda} or ~0
+    PendingLeaf* pend;            // 2 per tile
+    RunChunk* queue;
+    uint32_t qcap;
+    uint64_t* cdf;                // CDF mode only
+    bool vec;
+};
 
-__global__ void __launch_bounds__(256) k_scale(const float* __restrict__ p, uint32_t n,
-                                               uint32_t* __restrict__ maxpart,
-                                               uint32_t* __restrict__ counters,
-                                               uint32_t* __restrict__ scale_word, bool vec) {
-    const uint32_t gt = blockIdx.x * blockDim.x + threadIdx.x;
-    const uint32_t gs = gridDim.x * blockDim.x;
-    if (gt == 0) counters[kCtrQueue] = 0;
-    uint32_t mx = 0, fl = 0;
-    auto visit = [&](float x) {
-        const uint32_t b = __float_as_uint(x);
-        if (x != x) fl |= RTF_DATA_NAN;
-        else if (fabsf(x) == __int_as_float(0x7f800000)) fl |= RTF_DATA_INF;
-        else if (x < 0.0f) fl |= RTF_DATA_NEG;
-        else if (x > 0.0f) mx = max(mx, b);
-    };
-    if (vec) {
-        const uint32_t n4 = n >> 2;
-        uint32_t q = gt;
-        for (; q + 3 * gs < n4; q += 4 * gs) {  // 4 independent 16-B loads in flight
-            float4 v[4];
-#pragma unroll
-            for (int u = 0; u < 4; ++u) v[u] = ld_stream_f4(p + 4ull * (q + u * gs));
-#pragma unroll
-            for (int u = 0; u < 4; ++u) {
-                visit(v[u].x);
-                visit(v[u].y);
-                visit(v[u].z);
-                visit(v[u].w);
-            }
-        }
-        for (; q < n4; q += gs) {
-            const float4 v = ld_stream_f4(p + 4ull * q);
-            visit(v.x);
-            visit(v.y);
-            visit(v.z);
-            visit(v.w);
-        }
-        for (uint32_t i = 4 * n4 + gt; i < n; i += gs) visit(p[i]);
-    } else {
-        for (uint32_t i = gt; i < n; i += gs) visit(p[i]);
+// ------------------------------------------------------------ grid barrier
+// Sense-reversing (the cooperative-groups scheme): CTA 0 adds 2^31 - (G-1),
+// the others add 1, so the top bit flips exactly when all G arrived and the
+// word returns to its old low bits -- reusable across phases and launches.
+__device__ __forceinline__ void grid_barrier(uint32_t* bar) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        const uint32_t nb = blockIdx.x == 0 ? 0x80000000u - (gridDim.x - 1) : 1u;
+        uint32_t old;
+        asm volatile("atom.add.release.gpu.global.u32 %0, [%1], %2;"
+                     : "=r"(old)
+                     : "l"(bar), "r"(nb)
+                     : "memory");
+        while (((ld_acquire_u32(bar) ^ old) & 0x80000000u) == 0) __nanosleep(20);
+        __threadfence();  // also drops stale L1 lines of this SM
     }
+    __syncthreads();
+}
+
+// ------------------------------------------------------------ block reductions
+
+template <int THREADS>
+__device__ __forceinline__ void block_max_or(uint32_t& mx, uint32_t& fl, uint32_t* s2) {
     for (int d = 16; d; d >>= 1) {
         mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, d));
         fl |= __shfl_xor_sync(0xffffffffu, fl, d);
     }
-    __shared__ uint32_t s_mx[8], s_fl[8];
-    __shared__ bool s_last;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    __syncthreads();
     if (lane == 0) {
-        s_mx[warp] = mx;
-        s_fl[warp] = fl;
+        s2[2 * warp] = mx;
+        s2[2 * warp + 1] = fl;
     }
     __syncthreads();
-    if (threadIdx.x == 0) {
-        for (int w = 1; w < (int)(blockDim.x >> 5); ++w) {
-            mx = max(mx, s_mx[w]);
-            fl |= s_fl[w];
-        }
-        maxpart[2 * blockIdx.x] = mx;
-        maxpart[2 * blockIdx.x + 1] = fl;
-        __threadfence();
-        s_last = atomicAdd(&counters[kCtrDoneK1], 1u) == gridDim.x - 1;
-    }
-    __syncthreads();
-    if (!s_last) return;
-    // last block: fold all partials into the scale word
-    __threadfence();
     mx = 0;
     fl = 0;
-    for (uint32_t b = threadIdx.x; b < gridDim.x; b += blockDim.x) {
-        mx = max(mx, __ldcg(&maxpart[2 * b]));
-        fl |= __ldcg(&maxpart[2 * b + 1]);
+    for (int w = 0; w < THREADS / 32; ++w) {
+        mx = max(mx, s2[2 * w]);
+        fl |= s2[2 * w + 1];
     }
+}
+
+// Pfx of consecutive runs combines as (sum, sum, max): the last positive index
+// only grows along the array (-1 = none).
+__device__ __forceinline__ void warp_sum_pfx(Pfx& a) {
     for (int d = 16; d; d >>= 1) {
-        mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, d));
-        fl |= __shfl_xor_sync(0xffffffffu, fl, d);
-    }
-    __syncthreads();
-    if (lane == 0) {
-        s_mx[warp] = mx;
-        s_fl[warp] = fl;
-    }
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        for (int w = 1; w < (int)(blockDim.x >> 5); ++w) {
-            mx = max(mx, s_mx[w]);
-            fl |= s_fl[w];
-        }
-        scale_word[0] = mx;
-        scale_word[1] = fl;
-        counters[kCtrDoneK1] = 0;  // reset-on-consume for the next build
+        a.W += __shfl_xor_sync(0xffffffffu, a.W, d);
+        a.cnt += __shfl_xor_sync(0xffffffffu, a.cnt, d);
+        a.last = max(a.last, __shfl_xor_sync(0xffffffffu, a.last, d));
     }
 }
 
@@ -157,195 +133,21 @@ __device__ __forceinline__ void load_tile(const float* __restrict__ p, uint32_t 
     }
 }
 
-// ============================================================== K2: tile totals + scan
-
-// Pfx combine of consecutive runs is (sum, sum, max): the last positive index
-// only grows along the array (-1 = none).
-__device__ __forceinline__ Pfx shfl_xor_pfx(const Pfx& v, int d) {
-    Pfx r;
-    r.W = __shfl_xor_sync(0xffffffffu, v.W, d);
-    r.cnt = __shfl_xor_sync(0xffffffffu, v.cnt, d);
-    r.last = __shfl_xor_sync(0xffffffffu, v.last, d);
-    return r;
-}
-
-// K2 works on super-tiles of kSubs K3 tiles (SUB = THREADS * VPT entries each):
-// every thread keeps kSubs*VPT/4 float4 loads in flight (striped, coalesced).
-// Each CTA writes its K3 tiles' aggregates; the last CTA to finish (completion
-// counter) turns them into exclusive prefixes with one block scan.
-template <int THREADS, int VPT>
-__global__ void __launch_bounds__(THREADS)
-    k_tile_totals(const float* __restrict__ p, uint32_t n, int B, const uint32_t* scale_word,
-                  uint32_t* counters, Pfx* excl, rtf_header* hdr, uint32_t nst, uint32_t nt,
-                  bool vec) {
-    constexpr int NW = THREADS / 32;
-    constexpr int SUB = THREADS * VPT;
-    constexpr int SUPER = kSubs * SUB;
-    constexpr int NF4 = SUPER / (4 * THREADS);
-    constexpr int F4_PER_SUB = NF4 / kSubs;  // float4 k of every thread lies in sub-tile k / F4_PER_SUB
-    static_assert(F4_PER_SUB >= 1 && VPT % 4 == 0, "bad tile shape");
-    __shared__ uint64_t s_w[2 * NW];
-    __shared__ uint32_t s_c[2 * NW];
-    __shared__ int32_t s_l[2 * NW];
-    __shared__ bool s_last;
-    const uint32_t mx = scale_word[0], fl = scale_word[1];
-    const uint32_t status = fl | (mx == 0 ? RTF_DATA_ALLZERO : 0u);
-    if (status) {
-        if (blockIdx.x == 0 && threadIdx.x == 0) hdr->status = status;
-        return;
-    }
-    const int E = floor_log2_bits(mx);
-    const int shift = B - E;
-    const uint32_t st = blockIdx.x;
-    const uint32_t base = st * SUPER;
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    Pfx acc[kSubs];
-#pragma unroll
-    for (int q = 0; q < kSubs; ++q) acc[q] = Pfx{0ull, 0u, -1};
-    if (vec && (uint64_t)base + SUPER <= n) {
-        float4 v[NF4];
-#pragma unroll
-        for (int k = 0; k < NF4; ++k) v[k] = ld_stream_f4(p + base + 4 * (k * THREADS + threadIdx.x));
-#pragma unroll
-        for (int k = 0; k < NF4; ++k) {
-            const int q = k / F4_PER_SUB;
-            const int32_t e = (int32_t)(base + 4 * (k * THREADS + threadIdx.x));
-            const float xs[4] = {v[k].x, v[k].y, v[k].z, v[k].w};
-#pragma unroll
-            for (int u = 0; u < 4; ++u) {
-                const uint64_t w = quantize(xs[u], shift);
-                acc[q].W += w;
-                acc[q].cnt += w != 0;
-                if (w) acc[q].last = e + u;
-            }
-        }
-    } else {
-#pragma unroll
-        for (int k = 0; k < NF4; ++k) {
-            const int q = k / F4_PER_SUB;
-#pragma unroll
-            for (int u = 0; u < 4; ++u) {
-                const uint64_t e = (uint64_t)base + 4 * (k * THREADS + threadIdx.x) + u;
-                if (e < n) {
-                    const uint64_t w = quantize(p[e], shift);
-                    acc[q].W += w;
-                    acc[q].cnt += w != 0;
-                    if (w) acc[q].last = (int32_t)e;
-                }
-            }
-        }
-    }
-#pragma unroll
-    for (int q = 0; q < kSubs; ++q) {
-#pragma unroll
-        for (int d = 16; d; d >>= 1) {
-            const Pfx o = shfl_xor_pfx(acc[q], d);
-            acc[q].W += o.W;
-            acc[q].cnt += o.cnt;
-            acc[q].last = max(acc[q].last, o.last);
-        }
-    }
-    if (lane == 0) {
-#pragma unroll
-        for (int q = 0; q < kSubs; ++q) {
-            s_w[q * NW + warp] = acc[q].W;
-            s_c[q * NW + warp] = acc[q].cnt;
-            s_l[q * NW + warp] = acc[q].last;
-        }
-    }
-    __syncthreads();
-    if (threadIdx.x < kSubs) {  // aggregate of K3 tile kSubs*st + q (a prefix after the scan)
-        const int q = threadIdx.x;
-        Pfx s{0ull, 0u, -1};
-        for (int w = 0; w < NW; ++w) {
-            s.W += s_w[q * NW + w];
-            s.cnt += s_c[q * NW + w];
-            s.last = max(s.last, s_l[q * NW + w]);
-        }
-        const uint32_t t3 = kSubs * st + q;
-        if (t3 < nt) st_pfx(&excl[t3], s);
-        __threadfence();
-    }
-    __syncthreads();
-    if (threadIdx.x == 0) s_last = atomicAdd(&counters[kCtrDoneK2], 1u) == gridDim.x - 1;
-    __syncthreads();
-    if (!s_last) return;
-
-    // ---- the last CTA: exclusive scan over all nt tile aggregates (in place)
-    __threadfence();
-    const uint32_t per = (nt + THREADS - 1) / THREADS;  // contiguous chunk per thread
-    const uint32_t t0 = min(nt, threadIdx.x * per), t1 = min(nt, t0 + per);
-    Pfx own{0ull, 0u, -1};
-    for (uint32_t t = t0; t < t1; ++t) {
-        const Pfx a = ld_pfx_cg(&excl[t]);
-        own.W += a.W;
-        own.cnt += a.cnt;
-        own.last = max(own.last, a.last);
-    }
-    uint64_t w_ex, w_tot;
-    uint32_t c_ex, c_tot;
-    int32_t l_ex;
-    block_scan3_excl<THREADS>(own.W, own.cnt, own.last, w_ex, c_ex, l_ex, w_tot, c_tot, s_w, s_c,
-                              s_l);
-    Pfx run{w_ex, c_ex, l_ex};
-    for (uint32_t t = t0; t < t1; ++t) {
-        const Pfx a = ld_pfx_cg(&excl[t]);
-        st_pfx(&excl[t], run);
-        run.W += a.W;
-        run.cnt += a.cnt;
-        run.last = max(run.last, a.last);
-    }
-    if (threadIdx.x == THREADS - 1) {  // whole-array totals -> header
-        const uint64_t T = w_tot;
-        rtf_header h;
-        h.total = T;
-        h.n_pos = c_tot;
-        h.exponent = E;
-        h.scale_bits = B;
-        h.status = 0;
-        h.reserved = 0;
-        const uint32_t s = (uint32_t)__clzll((long long)T);  // T >= 1
-        h.norm_shift = s;
-        h.recip = reciprocal_of(T << s);
-        *hdr = h;
-        counters[kCtrDoneK2] = 0;  // reset-on-consume for the next build
-    }
-}
-
-// ============================================================== K3: scan, normalise, phase-1 Alg. 1
-
-struct BuildArgs {
-    const float* p;
-    uint32_t n, m;
-    const Pfx* excl;    // exclusive prefix of every K3 tile (from K2)
-    const rtf_header* hdr;
-    rtf_node* nodes;
-    int32_t* table;
-    uint8_t* lam;       // global split levels (read by phase 2)
-    int32_t* ob;        // global otherBounds, -1 when idle
-    PendingLeaf* pend;  // 2 per tile
-    RunChunk* queue;
-    uint32_t* counters;
-    uint32_t qcap;
-    uint64_t* cdf;      // CDF mode only
-    bool vec;
-};
-
 // Shared-memory arrays indexed by the local leaf index are padded with one slot
 // every 8 entries: with blocked ownership (lane L works on leaves ~8L + r) and
 // with strided access (consecutive leaves) both hit distinct banks.
 __device__ __forceinline__ uint32_t pad8(uint32_t j) { return j + (j >> 3); }
 
 template <int THREADS, int VPT>
-__host__ __device__ constexpr size_t scan_build_padded() {
+__host__ __device__ constexpr size_t tile_padded() {
     return (size_t)THREADS * VPT + (size_t)THREADS * VPT / 8;
 }
 
 template <int THREADS, int VPT>
-constexpr size_t scan_build_smem() {
+constexpr size_t build_smem_bytes() {
     // p tile / otherBounds (i32), keys (u64), child0, child1 (i32), split levels (u8)
-    return scan_build_padded<THREADS, VPT>() * (4 + 8 + 4 + 4) +
-           ((scan_build_padded<THREADS, VPT>() + 15) & ~(size_t)15);
+    return tile_padded<THREADS, VPT>() * (4 + 8 + 4 + 4) +
+           ((tile_padded<THREADS, VPT>() + 15) & ~(size_t)15);
 }
 
 // Guide-table entries owed by leaf j (orig i) whose split level is a boundary:
@@ -373,16 +175,13 @@ __device__ __noinline__ void table_runs(int32_t* __restrict__ table, uint32_t m,
     }
 }
 
-// Persistent: each CTA walks tiles t = blockIdx.x, +gridDim.x, ...  The weights
-// of a tile arrive in shared memory by a 1-D TMA bulk copy (issued as soon as
-// the previous tile's otherBounds are flushed); two CTAs per SM overlap each
-// other's copies and compute.  Each thread owns the compacted leaves of its VPT
-// consecutive entries (blocked), so leaf references come from registers.
-template <int THREADS, int VPT>
-__global__ void __launch_bounds__(THREADS, 2) k_scan_build(BuildArgs A, uint32_t nt) {
+// ============================================================== the build kernel
+
+template <int THREADS, int VPT, bool CDF>
+__global__ void __launch_bounds__(THREADS, 2) k_build(BuildArgs A) {
     constexpr int TILE = THREADS * VPT;
     constexpr int NW = THREADS / 32;
-    constexpr int P = (int)scan_build_padded<THREADS, VPT>();
+    constexpr int P = (int)tile_padded<THREADS, VPT>();
     extern __shared__ __align__(128) unsigned char smem[];
     float* s_p = reinterpret_cast<float*>(smem);       // tile weights (TMA target)
     int32_t* s_ob = reinterpret_cast<int32_t*>(smem);  // ... then otherBounds
@@ -395,37 +194,237 @@ __global__ void __launch_bounds__(THREADS, 2) k_scan_build(BuildArgs A, uint32_t
     __shared__ uint32_t s_c[2 * NW];
     __shared__ int32_t s_l[2 * NW];
     __shared__ uint64_t s_key_after;
+    __shared__ uint32_t s_red[2 * NW];
 
-    const rtf_header* hdr = A.hdr;
-    if (hdr->status) return;  // poisoned build: no-op
-    const uint64_t T = hdr->total;
-    Norm nm;
-    nm.s = hdr->norm_shift;
-    nm.d = T << nm.s;
-    nm.v = hdr->recip;
-    const int shift = hdr->scale_bits - hdr->exponent;
-    const uint32_t m = A.m, n = A.n;
-    const bool tma = A.vec;
-    const uint32_t tid = threadIdx.x;
-    auto tma_tile = [&](uint32_t t) { return tma && t < nt && (uint64_t)(t + 1) * TILE <= n; };
-    if (tid == 0) {
-        mbar_init(&s_bar, 1);
-        fence_proxy_async_smem();
-        if (tma_tile(blockIdx.x)) {
-            mbar_arrive_expect_tx(&s_bar, TILE * 4);
-            tma_load_1d(s_p, A.p + (size_t)blockIdx.x * TILE, TILE * 4, &s_bar);
+    const uint32_t G = gridDim.x, b = blockIdx.x, tid = threadIdx.x;
+    const uint32_t n = A.n, m = A.m, nt = A.nt;
+    const int lane = tid & 31, warp = tid >> 5;
+    uint32_t* gbar = &A.counters[kCtrGridBar];
+
+    // ---------------------------------------------------------- A: scale
+    if (b == 0 && tid == 0) A.counters[kCtrQueue] = 0;
+    {
+        uint32_t mx = 0, fl = 0;
+        auto visit = [&](float x) {
+            const uint32_t bits = __float_as_uint(x);
+            if (x != x) fl |= RTF_DATA_NAN;
+            else if (fabsf(x) == __int_as_float(0x7f800000)) fl |= RTF_DATA_INF;
+            else if (x < 0.0f) fl |= RTF_DATA_NEG;
+            else if (x > 0.0f) mx = max(mx, bits);
+        };
+        const uint32_t gs = G * THREADS, gt = b * THREADS + tid;
+        if (A.vec) {
+            const uint32_t n4 = n >> 2;
+            uint32_t q = gt;
+            for (; q + 7 * gs < n4; q += 8 * gs) {  // 8 independent 16-B loads in flight
+                float4 v[8];
+#pragma unroll
+                for (int u = 0; u < 8; ++u) v[u] = ld_stream_f4(A.p + 4ull * (q + u * gs));
+#pragma unroll
+                for (int u = 0; u < 8; ++u) {
+                    visit(v[u].x);
+                    visit(v[u].y);
+                    visit(v[u].z);
+                    visit(v[u].w);
+                }
+            }
+            for (; q < n4; q += gs) {
+                const float4 v = ld_stream_f4(A.p + 4ull * q);
+                visit(v.x);
+                visit(v.y);
+                visit(v.z);
+                visit(v.w);
+            }
+            for (uint32_t i = 4 * n4 + gt; i < n; i += gs) visit(A.p[i]);
+        } else {
+            for (uint32_t i = gt; i < n; i += gs) visit(A.p[i]);
+        }
+        block_max_or<THREADS>(mx, fl, s_red);
+        if (tid == 0) {
+            A.maxpart[2 * b] = mx;
+            A.maxpart[2 * b + 1] = fl;
         }
     }
-    __syncthreads();
+    grid_barrier(gbar);
+    uint32_t mx = 0, fl = 0;
+    for (uint32_t i = tid; i < G; i += THREADS) {
+        mx = max(mx, __ldcg(&A.maxpart[2 * i]));
+        fl |= __ldcg(&A.maxpart[2 * i + 1]);
+    }
+    block_max_or<THREADS>(mx, fl, s_red);
+    const uint32_t status = fl | (mx == 0 ? RTF_DATA_ALLZERO : 0u);
+    if (status) {  // poisoned build: report and stop (uniform across the grid)
+        if (b == 0 && tid == 0) A.hdr->status = status;
+        return;
+    }
+    const int E = floor_log2_bits(mx);
+    const double scale = pow2_f64(A.B - E);
 
-    Pfx pre_next = A.excl[blockIdx.x < nt ? blockIdx.x : 0];
+    // ---------------------------------------------------------- B: tile totals
+    // two tiles per step so each thread has 2*VPT/4 float4 loads in flight
+    for (uint32_t t0 = b; t0 < nt; t0 += 2 * G) {
+        Pfx acc[2];
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            acc[h] = Pfx{0ull, 0u, -1};
+            const uint32_t t = t0 + h * G;
+            if (t >= nt) continue;
+            const uint32_t base = t * TILE;
+            constexpr int NF4 = VPT / 4;  // striped float4 loads of the tile
+            if (A.vec && base + TILE <= n) {
+                float4 v[NF4];
+#pragma unroll
+                for (int k = 0; k < NF4; ++k) v[k] = ld_stream_f4(A.p + base + 4 * (k * THREADS + tid));
+#pragma unroll
+                for (int k = 0; k < NF4; ++k) {
+                    const int32_t e = (int32_t)(base + 4 * (k * THREADS + tid));
+                    const float xs[4] = {v[k].x, v[k].y, v[k].z, v[k].w};
+#pragma unroll
+                    for (int u = 0; u < 4; ++u) {
+                        const uint64_t w = quantize(xs[u], scale);
+                        acc[h].W += w;
+                        acc[h].cnt += w != 0;
+                        if (w) acc[h].last = e + u;
+                    }
+                }
+            } else {
+                for (uint32_t e = base + tid; e < min(n, base + TILE); e += THREADS) {
+                    const uint64_t w = quantize(A.p[e], scale);
+                    acc[h].W += w;
+                    acc[h].cnt += w != 0;
+                    if (w) acc[h].last = (int32_t)e;
+                }
+            }
+        }
+        warp_sum_pfx(acc[0]);
+        warp_sum_pfx(acc[1]);
+        __syncthreads();
+        if (lane == 0) {
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                s_w[h * NW + warp] = acc[h].W;
+                s_c[h * NW + warp] = acc[h].cnt;
+                s_l[h * NW + warp] = acc[h].last;
+            }
+        }
+        __syncthreads();
+        if (tid < 2 && t0 + tid * G < nt) {
+            Pfx s{0ull, 0u, -1};
+            for (int w = 0; w < NW; ++w) {
+                s.W += s_w[tid * NW + w];
+                s.cnt += s_c[tid * NW + w];
+                s.last = max(s.last, s_l[tid * NW + w]);
+            }
+            st_pfx(&A.excl[t0 + tid * G], s);
+        }
+    }
+    // the tile weights of phase D can stream in while the spine scan runs
+    const bool tma = !CDF && A.vec;
+    auto tma_tile = [&](uint32_t t) { return tma && t < nt && (t + 1) * TILE <= n; };
+    if (!CDF && tid == 0) {
+        mbar_init(&s_bar, 1);
+        fence_proxy_async_smem();
+        if (tma_tile(b)) {
+            mbar_arrive_expect_tx(&s_bar, TILE * 4);
+            tma_load_1d(s_p, A.p + (size_t)b * TILE, TILE * 4, &s_bar);
+        }
+    }
+    grid_barrier(gbar);
+
+    // ---------------------------------------------------------- C: spine scan (CTA 0)
+    if (b == 0) {
+        constexpr int BATCH = 4;
+        const uint32_t per = (nt + THREADS - 1) / THREADS;  // contiguous chunk per thread
+        const uint32_t u0 = min(nt, tid * per), u1 = min(nt, u0 + per);
+        Pfx own{0ull, 0u, -1};
+        for (uint32_t tb = u0; tb < u1; tb += BATCH) {
+            Pfx a[BATCH];
+#pragma unroll
+            for (int u = 0; u < BATCH; ++u)
+                a[u] = (tb + u < u1) ? ld_pfx_cg(&A.excl[tb + u]) : Pfx{0ull, 0u, -1};
+#pragma unroll
+            for (int u = 0; u < BATCH; ++u) {
+                own.W += a[u].W;
+                own.cnt += a[u].cnt;
+                own.last = max(own.last, a[u].last);
+            }
+        }
+        uint64_t w_ex, w_tot;
+        uint32_t c_ex, c_tot;
+        int32_t l_ex;
+        block_scan3_excl<THREADS>(own.W, own.cnt, own.last, w_ex, c_ex, l_ex, w_tot, c_tot, s_w,
+                                  s_c, s_l);
+        Pfx run{w_ex, c_ex, l_ex};
+        for (uint32_t tb = u0; tb < u1; tb += BATCH) {
+            Pfx a[BATCH];
+#pragma unroll
+            for (int u = 0; u < BATCH; ++u)
+                a[u] = (tb + u < u1) ? ld_pfx_cg(&A.excl[tb + u]) : Pfx{0ull, 0u, -1};
+#pragma unroll
+            for (int u = 0; u < BATCH; ++u) {
+                if (tb + u < u1) st_pfx(&A.excl[tb + u], run);
+                run.W += a[u].W;
+                run.cnt += a[u].cnt;
+                run.last = max(run.last, a[u].last);
+            }
+        }
+        if (tid == THREADS - 1) {  // whole-array totals -> header
+            rtf_header h;
+            h.total = w_tot;
+            h.n_pos = c_tot;
+            h.exponent = E;
+            h.scale_bits = A.B;
+            h.status = 0;
+            h.reserved = 0;
+            const uint32_t s = (uint32_t)__clzll((long long)w_tot);  // T >= 1
+            h.norm_shift = s;
+            h.recip = reciprocal_of(w_tot << s);
+            *A.hdr = h;
+        }
+    }
+    grid_barrier(gbar);
+
+    const rtf_header* hdr = A.hdr;
+    const uint64_t T = __ldcg(&hdr->total);
+    Norm nm;
+    nm.s = __ldcg(&hdr->norm_shift);
+    nm.d = T << nm.s;
+    nm.v = __ldcg(&hdr->recip);
+
+    if (CDF) {  // baseline: K[i] = floor(W_i 2^63 / T) for every entry, zeros included
+        for (uint32_t t = b; t < nt; t += G) {
+            const Pfx pre = ld_pfx_cg(&A.excl[t]);
+            const uint32_t first = t * TILE + tid * VPT;
+            float x[VPT];
+            load_tile<VPT>(A.p, first, n, A.vec, x);
+            uint64_t w[VPT];
+            uint64_t tw = 0;
+#pragma unroll
+            for (int k = 0; k < VPT; ++k) {
+                w[k] = quantize(x[k], scale);
+                tw += w[k];
+            }
+            uint64_t w_ex, w_tot;
+            uint32_t c_ex, cnt;
+            block_scan_excl<THREADS>(tw, 0u, w_ex, c_ex, w_tot, cnt, s_w, s_c);
+            uint64_t W = pre.W + w_ex;
+#pragma unroll
+            for (int k = 0; k < VPT; ++k) {
+                if (first + k < n) A.cdf[first + k] = (W == T) ? kOne63 : fixed_point(W, nm);
+                W += w[k];
+            }
+            __syncthreads();
+        }
+        return;
+    }
+
+    // ---------------------------------------------------------- D: tiles
     uint32_t phase = 0;
-    for (uint32_t t = blockIdx.x; t < nt; t += gridDim.x) {
-        const Pfx pre = pre_next;
-        if (t + gridDim.x < nt) pre_next = A.excl[t + gridDim.x];
+    for (uint32_t t = b; t < nt; t += G) {
+        const Pfx pre = ld_pfx_cg(&A.excl[t]);
         const uint32_t first = t * TILE + tid * VPT;
 
-        // ---- (0) weights of this thread's VPT consecutive entries
+        // (0) weights of this thread's VPT consecutive entries
         float x[VPT];
         if (tma_tile(t)) {
             mbar_wait(&s_bar, phase);
@@ -447,7 +446,7 @@ __global__ void __launch_bounds__(THREADS, 2) k_scan_build(BuildArgs A, uint32_t
         int32_t tl = -1;
 #pragma unroll
         for (int k = 0; k < VPT; ++k) {
-            w[k] = quantize(x[k], shift);
+            w[k] = quantize(x[k], scale);
             tw += w[k];
             if (w[k]) {
                 ++tc;
@@ -455,16 +454,23 @@ __global__ void __launch_bounds__(THREADS, 2) k_scan_build(BuildArgs A, uint32_t
                 tl = (int32_t)(first + k);
             }
         }
-        // ---- (1) block scan (its barriers also retire every read of s_p);
+        // (1) block scan (its barriers also retire every read of s_p);
         // one exact division per positive entry
         uint64_t w_ex, w_tot;
         uint32_t c_ex, cnt;
         int32_t l_ex;
         block_scan3_excl<THREADS>(tw, tc, tl, w_ex, c_ex, l_ex, w_tot, cnt, s_w, s_c, s_l);
         const uint32_t j0 = pre.cnt;  // global index of the tile's first leaf
+        {  // otherBounds start empty; the consumed weight tile becomes the array
+            int4* ob4 = reinterpret_cast<int4*>(s_ob);
+            for (uint32_t u = tid; u < (uint32_t)P / 4; u += THREADS)
+                ob4[u] = make_int4(-1, -1, -1, -1);
+        }
         {
             // Node records start as anchors: child0 = ~orig(j-1) (Fig. 6 caption
-            // P:1276-1277; j = 0 -> ~orig(0)); internal nodes overwrite it in Alg. 1.
+            // P:1276-1277; j = 0 -> ~orig(0)); internal nodes overwrite it in
+            // Alg. 1.  child1 needs no initial value: every slot's right child
+            // is set by phase 1 here or by phase 2 afterwards.
             int32_t prevo = l_ex >= 0 ? l_ex : (j0 ? pre.last : -1);
             uint64_t W = pre.W + w_ex;
             uint32_t jl = c_ex;
@@ -475,15 +481,13 @@ __global__ void __launch_bounds__(THREADS, 2) k_scan_build(BuildArgs A, uint32_t
                     const uint32_t q = pad8(jl);
                     s_key[q] = fixed_point(W, nm);
                     s_c0[q] = ~(prevo >= 0 ? prevo : i);
-                    s_c1[q] = INT32_MIN;
-                    s_ob[q] = -1;
                     prevo = i;
                     ++jl;
                 }
                 W += w[k];
             }
         }
-        // the tile's first and last leaf stay pending for phase 2 (K4)
+        // the tile's first and last leaf stay pending for phase 2 (E)
         if (tc && c_ex == 0)
             A.pend[2 * t] = PendingLeaf{(int32_t)j0, ~(int32_t)(first + __ffs(posmask) - 1)};
         if (tc && c_ex + tc == cnt)
@@ -496,7 +500,7 @@ __global__ void __launch_bounds__(THREADS, 2) k_scan_build(BuildArgs A, uint32_t
         }
         __syncthreads();
 
-        // ---- (2) own leaves: cell, split level, guide table
+        // (2) own leaves: cell, split level, guide table
         {
             const uint64_t key_after = s_key_after;
             uint32_t jl = c_ex;
@@ -517,52 +521,54 @@ __global__ void __launch_bounds__(THREADS, 2) k_scan_build(BuildArgs A, uint32_t
         }
         __syncthreads();
 
-        // ---- (3) phase 1: Alg. 1 for the tile's interior leaves 1..cnt-2 with
+        // (3) phase 1: Alg. 1 for the tile's interior leaves 1..cnt-2 with
         // shared-memory atomicExch.  A range that would contain the pending
         // first/last leaf can never complete here, so every range stays in
         // [1, cnt-2] and every parent slot in [1, cnt-1] -- inside the tile.
-        // Each lane walks its own leaves back to back; a merge re-reads only the
-        // split level on the side that moved.  A cell root (both neighbours out
-        // of cell, lambda = 64 on both sides) is the right child of its anchor
-        // lo and needs no exchange.
+        // Each lane walks its own leaves back to back.  A cell root (lambda =
+        // 64 on both sides) is the right child of its anchor lo and needs no
+        // exchange.  A deposit is (lambda beyond the bound) << 16 | bound.
         {
-            uint32_t mask = posmask;
-            uint32_t l = c_ex;
+            // own interior leaves [l, le): the tile's leaf 0 is this thread's
+            // lowest set bit if c_ex == 0, leaf cnt-1 its highest if it owns it
+            uint32_t mask = (c_ex == 0 && tc) ? posmask & (posmask - 1) : posmask;
+            uint32_t l = c_ex == 0 ? 1u : c_ex;
+            const uint32_t le = min(c_ex + tc, cnt >= 1 ? cnt - 1 : 0u);
+            const uint32_t a_c0 = smem_u32(s_c0), a_c1 = smem_u32(s_c1);
+            const uint32_t a_ob = smem_u32(s_ob), a_lam = smem_u32(s_lam);
             bool active = false;
             int32_t lo = 0, hi = 0, node = 0;
             uint32_t lamL = 0, lamR = 0;
             while (true) {
-                while (!active && mask) {
+                if (!active && l < le) {
                     const uint32_t k = __ffs(mask) - 1;
                     mask &= mask - 1;
-                    const uint32_t ll = l++;
-                    if (ll >= 1 && ll + 1 < cnt) {
-                        active = true;
-                        lo = hi = (int32_t)ll;
-                        node = ~(int32_t)(first + k);
-                        lamL = s_lam[pad8(ll - 1)];
-                        lamR = s_lam[pad8(ll)];
-                    }
+                    active = true;
+                    lo = hi = (int32_t)l;
+                    node = ~(int32_t)(first + k);
+                    lamL = lds_u8(a_lam + pad8(l - 1));
+                    lamR = lds_u8(a_lam + pad8(l));
+                    ++l;
                 }
                 if (!__any_sync(0xffffffffu, active)) break;
                 if (active) {
                     const bool right = lamL <= lamR;  // Alg. 1: child 1 unless left is farther
                     const bool root = (lamL & lamR & kLamBoundary) != 0;
                     const int32_t parent = right ? lo : hi + 1;
-                    const uint32_t q = pad8((uint32_t)parent);
-                    (right ? s_c1 : s_c0)[q] = node;
-                    const int32_t other = root ? -1 : atomicExch(&s_ob[q], right ? hi : lo);
+                    const uint32_t q4 = 4 * pad8((uint32_t)parent);
+                    sts_u32((right ? a_c1 : a_c0) + q4, (uint32_t)node);
+                    const int32_t dep = right ? (int32_t)(lamR << 16 | (uint32_t)hi)
+                                              : (int32_t)(lamL << 16 | (uint32_t)lo);
+                    const int32_t other = root ? -1 : atoms_exch(a_ob + q4, dep);
                     active = other >= 0;  // first to arrive (or a root): stop
                     if (active) {
-                        s_ob[q] = -1;  // reset-on-consume
-                        const uint32_t lv = s_lam[pad8(right ? other - 1 : other)];
-                        if (right) {
-                            lo = other;
-                            lamL = lv;
-                        } else {
-                            hi = other;
-                            lamR = lv;
-                        }
+                        sts_u32(a_ob + q4, 0xffffffffu);  // reset-on-consume
+                        const int32_t bound = other & 0xffff;
+                        const uint32_t lv = (uint32_t)other >> 16;
+                        lo = right ? bound : lo;
+                        hi = right ? hi : bound;
+                        lamL = right ? lv : lamL;
+                        lamR = right ? lamR : lv;
                         node = (int32_t)(j0 + parent);
                     }
                 }
@@ -570,17 +576,19 @@ __global__ void __launch_bounds__(THREADS, 2) k_scan_build(BuildArgs A, uint32_t
         }
         __syncthreads();
 
-        // ---- (4) flush: leftover deposits first, then the next tile's TMA copy
-        // can reuse the buffer while records (coalesced 16 B) and split levels go out
+        // (4) flush: leftover deposits first, then the next tile's TMA copy can
+        // reuse the buffer while records (coalesced 16 B) and split levels go out
         for (uint32_t l = 1 + tid; l < cnt; l += THREADS) {
             const int32_t o = s_ob[pad8(l)];
-            if (o >= 0) A.ob[j0 + l] = (int32_t)j0 + o;
+            if (o >= 0)
+                A.ob[j0 + l] = ((unsigned long long)((uint32_t)o >> 16) << 32) |
+                               (uint32_t)(j0 + (o & 0xffff));
         }
         __syncthreads();
-        if (tid == 0 && tma_tile(t + gridDim.x)) {
+        if (tid == 0 && tma_tile(t + G)) {
             fence_proxy_async_smem();
             mbar_arrive_expect_tx(&s_bar, TILE * 4);
-            tma_load_1d(s_p, A.p + (size_t)(t + gridDim.x) * TILE, TILE * 4, &s_bar);
+            tma_load_1d(s_p, A.p + (size_t)(t + G) * TILE, TILE * 4, &s_bar);
         }
         {
             uint4* gnode = reinterpret_cast<uint4*>(A.nodes + j0);
@@ -594,86 +602,43 @@ __global__ void __launch_bounds__(THREADS, 2) k_scan_build(BuildArgs A, uint32_t
         }
         __syncthreads();  // keys, children and split levels are free for the next tile
     }
-}
+    grid_barrier(gbar);
 
-// Baseline CDF over all entries: K[i] = floor(W_i 2^63 / T) (zeros included).
-template <int THREADS, int VPT>
-__global__ void __launch_bounds__(THREADS) k_cdf(BuildArgs A) {
-    __shared__ uint64_t s_w[2 * (THREADS / 32)];
-    __shared__ uint32_t s_c[2 * (THREADS / 32)];
-    const rtf_header* hdr = A.hdr;
-    if (hdr->status) return;
-    const uint64_t T = hdr->total;
-    Norm nm;
-    nm.s = hdr->norm_shift;
-    nm.d = T << nm.s;
-    nm.v = hdr->recip;
-    const int shift = hdr->scale_bits - hdr->exponent;
-    const uint32_t tile = blockIdx.x;
-    const Pfx pre = A.excl[tile];
-    const uint32_t first = tile * THREADS * VPT + threadIdx.x * VPT;
-    float x[VPT];
-    load_tile<VPT>(A.p, first, A.n, A.vec, x);
-    uint64_t w[VPT];
-    uint64_t tw = 0;
-#pragma unroll
-    for (int k = 0; k < VPT; ++k) {
-        w[k] = quantize(x[k], shift);
-        tw += w[k];
-    }
-    uint64_t w_ex, w_tot;
-    uint32_t c_ex, cnt;
-    block_scan_excl<THREADS>(tw, 0u, w_ex, c_ex, w_tot, cnt, s_w, s_c);
-    uint64_t W = pre.W + w_ex;
-#pragma unroll
-    for (int k = 0; k < VPT; ++k) {
-        if (first + k < A.n) A.cdf[first + k] = (W == T) ? kOne63 : fixed_point(W, nm);
-        W += w[k];
-    }
-}
-
-// ============================================================== K4: cross-tile Alg. 1 + long table runs
-
-__global__ void __launch_bounds__(256) k_cross_tile(BuildArgs A, uint32_t npend,
-                                                    uint32_t walker_blocks) {
-    if (A.hdr->status) return;
-    if (blockIdx.x < walker_blocks) {
-        const uint32_t t = blockIdx.x * blockDim.x + threadIdx.x;
-        if (t >= npend) return;
-        const PendingLeaf pl = A.pend[t];
-        if (pl.j < 0) return;
+    // ---------------------------------------------------------- E: cross-tile Alg. 1
+    for (uint32_t pi = b * THREADS + tid; pi < 2 * nt; pi += G * THREADS) {
+        const PendingLeaf pl = A.pend[pi];
+        if (pl.j < 0) continue;
         int32_t lo = pl.j, hi = pl.j, node = pl.ref;
-        const uint8_t* __restrict__ lam = A.lam;  // read-only in this kernel
-        uint32_t lamL = lo ? __ldg(lam + lo - 1) : kLamBoundary;
-        uint32_t lamR = __ldg(lam + hi);
+        uint32_t lamL = lo ? __ldcg(A.lam + lo - 1) : kLamBoundary;
+        uint32_t lamR = __ldcg(A.lam + hi);
         while (true) {
             const bool right = lamL <= lamR;
             const int32_t parent = right ? lo : hi + 1;
             A.nodes[parent].child[right ? 1 : 0] = node;
             if (lamL & lamR & kLamBoundary) break;  // cell root: right child of its anchor
-            const int32_t other = atomicExch(&A.ob[parent], right ? hi : lo);
-            if (other < 0) break;
-            A.ob[parent] = -1;
+            const unsigned long long dep =
+                right ? ((unsigned long long)lamR << 32 | (uint32_t)hi)
+                      : ((unsigned long long)lamL << 32 | (uint32_t)lo);
+            const unsigned long long o = atomicExch(&A.ob[parent], dep);
+            if (o == ~0ull) break;  // first to arrive
+            A.ob[parent] = ~0ull;   // reset-on-consume
+            const int32_t bound = (int32_t)(uint32_t)o;
             // a sibling's bound always extends the range; anything else means an
             // uninitialised workspace -- stop instead of wandering
-            if (right ? other >= lo : other <= hi) break;
+            if (right ? bound >= lo : bound <= hi) break;
             if (right) {
-                lo = other;
-                lamL = lo ? __ldg(lam + lo - 1) : kLamBoundary;
+                lo = bound;
+                lamL = (uint32_t)(o >> 32);
             } else {
-                hi = other;
-                lamR = __ldg(lam + hi);
+                hi = bound;
+                lamR = (uint32_t)(o >> 32);
             }
             node = parent;
         }
-        return;
     }
     // long empty-cell runs of the guide table: one warp per chunk
-    const uint32_t lane = threadIdx.x & 31;
-    const uint32_t warp = (blockIdx.x - walker_blocks) * (blockDim.x >> 5) + (threadIdx.x >> 5);
-    const uint32_t nwarps = (gridDim.x - walker_blocks) * (blockDim.x >> 5);
-    const uint32_t nq = min(A.counters[kCtrQueue], A.qcap);
-    for (uint32_t q = warp; q < nq; q += nwarps) {
+    const uint32_t nq = min(__ldcg(&A.counters[kCtrQueue]), A.qcap);
+    for (uint32_t q = b * NW + warp; q < nq; q += G * NW) {
         const RunChunk rc = A.queue[q];
         for (uint32_t g = lane; g < rc.len; g += 32) A.table[rc.start + g] = rc.value;
     }
@@ -706,11 +671,11 @@ size_t build_workspace_layout(uint32_t n, uint32_t m, uint32_t flags, WsLayout* 
         return o;
     };
     L->nt = nt;
-    L->maxpart = take(sizeof(uint32_t) * 2 * kMaxScaleBlocks + 16);
+    L->maxpart = take(sizeof(uint32_t) * 2 * kMaxGrid);
     L->counters = take(64);
     L->excl = take(sizeof(Pfx) * (size_t)nt);
     L->pend = take(sizeof(PendingLeaf) * 2 * (size_t)nt);
-    L->ob = take(sizeof(int32_t) * (size_t)n);
+    L->ob = take(sizeof(unsigned long long) * (size_t)n);
     L->lam = take((size_t)n);
     L->qcap = build_queue_capacity(m);
     L->queue = take(sizeof(RunChunk) * (size_t)L->qcap);
@@ -730,79 +695,59 @@ static int num_sms() {
     return sms;
 }
 
-template <int THREADS, int VPT>
-static cudaError_t launch_pipeline(const float* p, uint32_t n, uint32_t m, rtf_header* hdr,
-                                   rtf_node* nodes, int32_t* table, uint64_t* cdf,
-                                   unsigned char* ws, const WsLayout& L, cudaStream_t st,
-                                   int* launches) {
-    const bool vec = ((uintptr_t)p & 15u) == 0;
-    const int B = 62 - ceil_log2_u32(n);
-    const uint32_t nt = L.nt, nst = (nt + kSubs - 1) / kSubs;
-    uint32_t* maxpart = reinterpret_cast<uint32_t*>(ws + L.maxpart);
-    uint32_t* scale_word = maxpart + 2 * kMaxScaleBlocks;
-    uint32_t* counters = reinterpret_cast<uint32_t*>(ws + L.counters);
-    Pfx* excl = reinterpret_cast<Pfx*>(ws + L.excl);
-
-    // K1: 256-thread blocks, ~32 float4 per thread, at most 8 blocks per SM
-    const uint32_t nb1 = (uint32_t)std::max<uint64_t>(
-        1, std::min<uint64_t>(kMaxScaleBlocks, ((uint64_t)n + 32767) / 32768));
-    k_scale<<<nb1, 256, 0, st>>>(p, n, maxpart, counters, scale_word, vec);
-    ++*launches;
-    // K2: super-tiles of kSubs K3 tiles
-    k_tile_totals<THREADS, VPT><<<nst, THREADS, 0, st>>>(p, n, B, scale_word, counters, excl,
-                                                         hdr, nst, nt, vec);
-    ++*launches;
-    BuildArgs A;
-    A.p = p;
-    A.n = n;
-    A.m = m;
-    A.excl = excl;
-    A.hdr = hdr;
-    A.nodes = nodes;
-    A.table = table;
-    A.lam = reinterpret_cast<uint8_t*>(ws + L.lam);
-    A.ob = reinterpret_cast<int32_t*>(ws + L.ob);
-    A.pend = reinterpret_cast<PendingLeaf*>(ws + L.pend);
-    A.queue = reinterpret_cast<RunChunk*>(ws + L.queue);
-    A.counters = counters;
-    A.qcap = L.qcap;
-    A.cdf = cdf;
-    A.vec = vec;
-    if (cdf) {
-        k_cdf<THREADS, VPT><<<nt, THREADS, 0, st>>>(A);
-        ++*launches;
-        return cudaGetLastError();
-    }
-    // K3: persistent, 2 CTAs per SM
-    const size_t smem = scan_build_smem<THREADS, VPT>();
-    static bool attr_set = false;  // per instantiation
-    if (!attr_set) {
-        const cudaError_t e = cudaFuncSetAttribute(k_scan_build<THREADS, VPT>,
-                                                   cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                                   (int)smem);
+template <int THREADS, int VPT, bool CDF>
+static cudaError_t launch_fused(BuildArgs& A, cudaStream_t st, int* launches) {
+    auto kern = k_build<THREADS, VPT, CDF>;
+    const size_t smem = CDF ? 0 : build_smem_bytes<THREADS, VPT>();
+    static int max_grid = 0;  // per instantiation: co-resident CTAs
+    if (!max_grid) {
+        cudaError_t e = cudaSuccess;
+        if (smem)
+            e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (e != cudaSuccess) return e;
-        attr_set = true;
+        int per_sm = 0;
+        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, THREADS, smem);
+        if (e != cudaSuccess) return e;
+        if (per_sm < 1) return cudaErrorCooperativeLaunchTooLarge;
+        max_grid = std::min<int>(per_sm * num_sms(), (int)kMaxGrid);
     }
-    const uint32_t grid3 = std::min<uint32_t>(nt, 2u * (uint32_t)num_sms());
-    k_scan_build<THREADS, VPT><<<grid3, THREADS, smem, st>>>(A, nt);
+    const uint32_t grid = std::max<uint32_t>(1u, std::min<uint32_t>(A.nt, (uint32_t)max_grid));
+    void* args[] = {&A};
+    const cudaError_t e =
+        cudaLaunchCooperativeKernel((const void*)kern, dim3(grid), dim3(THREADS), args, smem, st);
     ++*launches;
-    // K4
-    const uint32_t npend = 2 * nt;
-    const uint32_t walker_blocks = (npend + 255) / 256;
-    const uint32_t fill_blocks =
-        std::max<uint32_t>(1u, std::min<uint32_t>(148u * 4u, m / 8192u + 1u));
-    k_cross_tile<<<walker_blocks + fill_blocks, 256, 0, st>>>(A, npend, walker_blocks);
-    ++*launches;
-    return cudaGetLastError();
+    return e;
 }
 
 cudaError_t launch_build(const float* p, uint32_t n, uint32_t m, uint32_t flags, rtf_header* hdr,
                          rtf_node* nodes, int32_t* table, uint64_t* cdf, void* ws,
                          const WsLayout& L, cudaStream_t st, int* launches) {
     unsigned char* w = reinterpret_cast<unsigned char*>(ws);
-    if (flags & RTF_BUILD_SMALL_TILES)
-        return launch_pipeline<64, 4>(p, n, m, hdr, nodes, table, cdf, w, L, st, launches);
-    return launch_pipeline<512, 8>(p, n, m, hdr, nodes, table, cdf, w, L, st, launches);
+    BuildArgs A;
+    A.p = p;
+    A.n = n;
+    A.m = m;
+    A.nt = L.nt;
+    A.B = 62 - ceil_log2_u32(n);
+    A.maxpart = reinterpret_cast<uint32_t*>(w + L.maxpart);
+    A.counters = reinterpret_cast<uint32_t*>(w + L.counters);
+    A.excl = reinterpret_cast<Pfx*>(w + L.excl);
+    A.hdr = hdr;
+    A.nodes = nodes;
+    A.table = table;
+    A.lam = reinterpret_cast<uint8_t*>(w + L.lam);
+    A.ob = reinterpret_cast<unsigned long long*>(w + L.ob);
+    A.pend = reinterpret_cast<PendingLeaf*>(w + L.pend);
+    A.queue = reinterpret_cast<RunChunk*>(w + L.queue);
+    A.qcap = L.qcap;
+    A.cdf = cdf;
+    A.vec = ((uintptr_t)p & 15u) == 0;
+    const bool small = flags & RTF_BUILD_SMALL_TILES;
+    if (cdf)
+        return small ? launch_fused<64, 4, true>(A, st, launches)
+                     : launch_fused<512, 8, true>(A, st, launches);
+    return small ? launch_fused<64, 4, false>(A, st, launches)
+                 : launch_fused<512, 8, false>(A, st, launches);
 }
 
 }  // namespace rtf

@@ -29,6 +29,17 @@ __device__ __forceinline__ void st_release_u32(uint32_t* p, uint32_t v) {
     asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 
+// completion counter: the release orders this CTA's prior writes (ordered before
+// the call by a barrier), the acquire lets the last arriver read everyone's
+__device__ __forceinline__ uint32_t atom_add_acq_rel_u32(uint32_t* p, uint32_t v) {
+    uint32_t old;
+    asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], %2;"
+                 : "=r"(old)
+                 : "l"(p), "r"(v)
+                 : "memory");
+    return old;
+}
+
 // streaming 16-byte load that does not allocate in L1 (read-once data)
 __device__ __forceinline__ uint4 ld_stream_u4(const void* p) {
     uint4 r;
@@ -86,6 +97,22 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
         : "memory");
 }
 
+// explicit shared-memory accesses on precomputed 32-bit addresses (keeps the
+// compiler from re-deriving generic->shared windows inside hot loops)
+__device__ __forceinline__ void sts_u32(uint32_t a, uint32_t v) {
+    asm volatile("st.shared.u32 [%0], %1;" ::"r"(a), "r"(v) : "memory");
+}
+__device__ __forceinline__ uint32_t lds_u8(uint32_t a) {
+    uint32_t v;
+    asm volatile("ld.shared.u8 %0, [%1];" : "=r"(v) : "r"(a) : "memory");
+    return v;
+}
+__device__ __forceinline__ int32_t atoms_exch(uint32_t a, int32_t v) {
+    int32_t r;
+    asm volatile("atom.shared.exch.b32 %0, [%1], %2;" : "=r"(r) : "r"(a), "r"(v) : "memory");
+    return r;
+}
+
 // ------------------------------------------------------------ quantisation
 
 // floor(log2(x)) of a positive finite float given its bits
@@ -95,14 +122,17 @@ __device__ __forceinline__ int floor_log2_bits(uint32_t b) {
     return (31 - __clz((int)b)) - 149;  // subnormal: frac * 2^-149
 }
 
-// w = max(1, floor(x 2^shift)) for x > 0 (exact on the mantissa), 0 otherwise
-__device__ __forceinline__ uint64_t quantize(float x, int shift) {
+// w = max(1, floor(x 2^shift)) for x > 0, 0 otherwise.  Exact in FP64: the
+// 24-bit mantissa of x converts exactly, scaling by 2^shift is exact (shift is
+// in [-96, 211], so the product is a normal double), x 2^shift < 2^63, and the
+// round-toward-zero conversion is the floor.
+__device__ __forceinline__ double pow2_f64(int shift) {
+    return __longlong_as_double((long long)(1023 + shift) << 52);
+}
+
+__device__ __forceinline__ uint64_t quantize(float x, double scale) {
     if (!(x > 0.0f)) return 0;
-    uint32_t b = __float_as_uint(x);
-    uint32_t be = b >> 23, fr = b & 0x7fffffu;
-    uint64_t mant = be ? (uint64_t)(fr | 0x800000u) : (uint64_t)fr;
-    int sh = (be ? (int)be - 150 : -149) + shift;
-    uint64_t v = sh >= 0 ? (mant << sh) : (sh <= -64 ? 0ull : (mant >> (-sh)));
+    const uint64_t v = __double2ull_rz((double)x * scale);
     return v ? v : 1ull;
 }
 
@@ -147,8 +177,13 @@ __device__ __forceinline__ uint64_t fixed_point(uint64_t W, const Norm& nm) {
     return q1;
 }
 
+// floor(key m / 2^63) for key < 2^63, m < 2^31: key m = hi 2^32 + lo with
+// hi = key_hi m < 2^62, lo = key_lo m < 2^63, and the fraction of lo / 2^32
+// cannot carry across a multiple of 2^31.
 __device__ __forceinline__ uint32_t cell_of(uint64_t key, uint32_t m) {
-    return (uint32_t)__umul64hi(key << 1, (uint64_t)m);  // floor(key m / 2^63)
+    const uint64_t hi = (uint64_t)(uint32_t)(key >> 32) * m;
+    const uint64_t lo = (uint64_t)(uint32_t)key * m;
+    return (uint32_t)((hi + (lo >> 32)) >> 31);
 }
 
 __device__ __forceinline__ uint32_t split_level(uint64_t a, uint64_t b) {

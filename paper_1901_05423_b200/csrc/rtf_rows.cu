@@ -104,7 +104,7 @@ __global__ void __launch_bounds__(THREADS) k_build_rows(RowsArgs A) {
     uint32_t tc = 0;
 #pragma unroll
     for (int k = 0; k < VPT; ++k) {
-        w[k] = quantize(x[k], B - E);
+        w[k] = quantize(x[k], pow2_f64(B - E));
         tw += w[k];
         tc += w[k] != 0;
     }
