@@ -52,6 +52,9 @@ __global__ void __launch_bounds__(kSampleThreads)
     const uint64_t gt = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
     const uint64_t gs = (uint64_t)gridDim.x * blockDim.x;
     const bool bad = !ROWS && hdr->status != 0;
+    // (L2 evict-first on the xi/out streams with evict-last on the forest was
+    // measured slower: 8.0 vs 7.4 ms for config 3 -- the kernel is bound by L2
+    // sector throughput of the random table/record reads, not by eviction)
     uint64_t done = 0;
     if (vec) {
         const uint64_t nq = count >> 2;
