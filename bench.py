@@ -41,13 +41,19 @@ WORKLOADS = {
                     "2^30 Philox4x32-10 xi per GPU"),
     "c2": dict(name="c2_envmap", n=2048 * 1024, m=2048 * 1024, samples=1 << 26,
                desc="config 2: 2048x1024 synthetic env-map luminance, m=n, 2^26 Sobol xi per GPU"),
+    "c4": dict(name="c4_spikes", n=1 << 28, m=1 << 26, samples=1 << 32,
+               desc="config 4: n=2^28 spiky (4 spikes x 0.24 + uniform 0.04), m=2^26; sharded "
+                    "build (cross-GPU scan of shard totals) + replication; 2^32 Philox xi split "
+                    "over the GPUs"),
 }
 
 
 def make_p(wl):
-    from workloads import env_map, power_law
+    from workloads import env_map, power_law, spikes
     if wl["name"] == "c3_powerlaw":
         return power_law(wl["n"], "A")
+    if wl["name"] == "c4_spikes":
+        return spikes(wl["n"])
     return env_map()
 
 
@@ -327,6 +333,106 @@ def run_gpu(args):
         print(json.dumps(result), flush=True)
 
 
+def run_gpu_c4(args):
+    """Config 4: strong scaling of one n = 2^28 distribution over N GPUs.  Each
+    rank holds its shard of p; the build is the sharded protocol of
+    paper_1901_05423_b200.sharded (NCCL through DistComm); every rank then
+    samples 2^32 / N xi from its replicated forest."""
+    import torch
+    import torch.distributed as dist
+
+    import paper_1901_05423_b200 as rtf
+    from paper_1901_05423_b200 import sharded
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    wl = WORKLOADS["c4"]
+    n, m = wl["n"], wl["m"]
+    S = (args.samples or wl["samples"]) // world
+    base, n_local = sharded.shard_range(n, world, rank)
+    # this rank's shard of spikes(n): uniform background + the spikes it holds
+    bg = (1.0 - 4 * 0.24) / (n - 4)
+    p_local = torch.full((n_local,), bg, dtype=torch.float32, device=dev)
+    for k in range(4):
+        pos = (2 * k + 1) * n // 8
+        if base <= pos < base + n_local:
+            p_local[pos - base] = 0.24
+    shards = sharded.make_shards_local(p_local, n, m, rank, world, base)
+    comm = sharded.DistComm() if world > 1 else sharded.LocalComm()
+    forest = rtf.Forest.from_buffer(n, m, shards[0].forest)
+    xi = rtf.philox(S, seed=0x5EED, start=rank * S, device=dev)
+    out = torch.empty(S, dtype=torch.int32, device=dev)
+    flush = torch.empty(L2_FLUSH_BYTES, dtype=torch.uint8, device=dev)
+    stream = torch.cuda.current_stream()
+
+    def step(ev=None):
+        if ev:
+            ev[0].record(stream)
+        sharded.build_sharded(shards, comm)
+        if ev:
+            ev[1].record(stream)
+        forest.sample(xi, out)
+        if ev:
+            ev[2].record(stream)
+
+    for _ in range(args.warmup):
+        step()
+        flush.zero_()
+    torch.cuda.synchronize()
+    assert forest.status() == 0
+    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(args.steps)]
+    sampler = ClockSampler(local)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    l0 = rtf.launch_count()
+    with sampler:
+        for k in range(args.steps):
+            step(evs[k])
+            flush.zero_()
+        torch.cuda.synchronize()
+    launches = rtf.launch_count() - l0
+    tb = sum(e[0].elapsed_time(e[1]) for e in evs)
+    ts = sum(e[1].elapsed_time(e[2]) for e in evs)
+    if world > 1:
+        t = torch.tensor([tb, ts], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        tb, ts = t.tolist()
+    K = args.steps
+    build_gs = n * K / (tb * 1e-3) / 1e9
+    sample_gs = S * world * K / (ts * 1e-3) / 1e9
+    peak, peak_src = peaks()
+    bytes_build = 4 * n + 16 * forest.n_pos() + 4 * m
+    result = {
+        "metric": METRIC, "value": round(build_gs, 4), "unit": "G entries/s", "n_gpus": world,
+        "steps": K, "warmup": args.warmup, "ms_per_step": round((tb + ts) / K, 4),
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "u64",
+        "data": "synthetic",
+        "config": {"workload": wl["desc"], "n": n, "m": m, "samples_total": S * world,
+                   "l2": f"flushed between steps ({L2_FLUSH_BYTES >> 20} MiB write, untimed)",
+                   "parallelism": f"sharded build over {world} GPU(s) + replicated forest; "
+                                  "sampling split across GPUs"},
+        "sampling": {"value": round(sample_gs, 4), "unit": "G samples/s",
+                     "ms_per_batch": round(ts / K, 4)},
+        "roofline_build": {"kernel": "sharded build (all calls, incl. exchanges)",
+                           "bound": "hbm", "achieved": round(bytes_build / (tb / K * 1e-3) / 1e9, 2),
+                           "peak": peak, "unit": "GB/s",
+                           "frac": round(bytes_build / (tb / K * 1e-3) / 1e9 / peak, 4),
+                           "traffic": None, "peak_source": peak_src},
+        "gpu_launches": launches, "clocks": sampler.summary(),
+    }
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+    if rank == 0:
+        print(json.dumps(result), flush=True)
+
+
 def cpu_baseline(p_host, m, xi_sample):
     """The CPU oracle as it stands (single thread), on a bounded sample."""
     import oracle
@@ -407,6 +513,8 @@ def main():
         print("warning: fewer than 3 warm-up steps", file=sys.stderr)
     if args.impl == "reference":
         run_reference(args)
+    elif args.workload == "c4":
+        run_gpu_c4(args)
     else:
         run_gpu(args)
 

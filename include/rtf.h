@@ -198,6 +198,57 @@ int rtf_sample_host(const rtf_forest *f, const uint32_t *xi_host, uint64_t count
                     int32_t *out_host, uint32_t *xi_dev, int32_t *out_dev, uint64_t chunk,
                     void *stream);
 
+/* ---------------------------------------- sharded build across GPUs (config 4) */
+/*
+ * The distribution p[0..n_global) is split into contiguous shards; shard r
+ * holds p[index_base_r .. index_base_r + n_local_r).  The build needs two tiny
+ * exchanges between the calls below and one replication step; the library
+ * does no communication itself (the caller runs NCCL, see
+ * paper_1901_05423_b200/sharded.py):
+ *   1. rtf_shard_scale            -> view.scale (4 words); MAX-reduce across shards
+ *   2. rtf_shard_totals           -> view.total (16 B);    gather all shards' totals
+ *      (the cross-GPU scan of per-shard totals: every shard derives its prefix
+ *       and the grand total T from the gathered totals, on the device)
+ *   3. rtf_shard_build            -> this shard's node records [J_r, J_r + n'_r),
+ *      split levels, guide-table cells (others INT32_MIN), pending edge leaves
+ *      and leftover deposits
+ *   4. replicate records / split levels (broadcast from each owner), MAX-reduce
+ *      the table, gather pending leaves and deposit lists
+ *   5. rtf_shard_finish           -> cross-tile Alg. 1 over the assembled state;
+ *      every shard then holds the identical full forest (byte-equal to rtf_build).
+ * Each shard owns a forest buffer sized for (n_global, m) and a shard workspace.
+ */
+typedef struct rtf_shard_view {  /* device pointers into a shard workspace */
+    uint8_t *lam;        /* n_global split levels, indexed by global leaf index  */
+    void *pend;          /* nt_local x 8 B pending edge leaves {int32 j, int32 ~orig} */
+    void *deps;          /* nt_local x dep_stride x dep_bytes leftover deposits   */
+    uint32_t *ndeps;     /* nt_local deposit counts                              */
+    uint32_t *scale;     /* 4 words {max float bits, nan, inf, negative}          */
+    void *total;         /* 16 B {u64 W, u32 n', i32 last positive index}        */
+    uint32_t nt_local;   /* tiles of this shard                                  */
+    uint32_t dep_stride; /* deposit entries per tile                             */
+    uint32_t dep_bytes;  /* bytes per deposit entry                              */
+    uint32_t reserved;
+} rtf_shard_view;
+
+size_t rtf_shard_workspace_bytes(uint32_t n_local, uint32_t n_global, uint32_t m);
+int rtf_shard_workspace_init(void *ws, size_t ws_bytes, uint32_t n_local, uint32_t n_global,
+                             uint32_t m, void *stream);
+int rtf_shard_get_view(void *ws, size_t ws_bytes, uint32_t n_local, uint32_t n_global,
+                       uint32_t m, rtf_shard_view *out);
+int rtf_shard_scale(const float *p, uint32_t n_local, uint32_t n_global, uint32_t m, void *ws,
+                    size_t ws_bytes, void *stream);
+int rtf_shard_totals(const float *p, uint32_t n_local, uint32_t n_global, uint32_t m,
+                     uint32_t index_base, void *ws, size_t ws_bytes, void *stream);
+int rtf_shard_build(const float *p, uint32_t n_local, uint32_t n_global, uint32_t m,
+                    uint32_t index_base, uint32_t rank, uint32_t count, const void *totals,
+                    void *forest_buf, size_t forest_bytes, void *ws, size_t ws_bytes,
+                    void *stream, rtf_forest *out);
+int rtf_shard_finish(uint32_t n_local, uint32_t n_global, uint32_t m, const void *pend_all,
+                     const void *deps_all, const uint32_t *ndeps_all, uint32_t nt_all,
+                     void *forest_buf, size_t forest_bytes, void *ws, size_t ws_bytes,
+                     void *stream, rtf_forest *out);
+
 /* ---------------------------------------------------------- utilities */
 
 /* Input generator (not part of the method): Philox4x32-10 u32 stream,

@@ -78,6 +78,18 @@ class Forest:
         check(L.rtf_workspace_init(_ptr(self._buf.ws), wb, self.n, self.m, self.flags,
                                    _stream()), "rtf_workspace_init")
 
+    @classmethod
+    def from_buffer(cls, n: int, m: int, forest_buf: torch.Tensor) -> "Forest":
+        """A read-only view (sampling, inspection) of a forest buffer built
+        elsewhere, e.g. by the sharded build (paper_1901_05423_b200.sharded)."""
+        f = cls.__new__(cls)
+        f.n, f.m, f.flags, f.device = int(n), int(m), 0, forest_buf.device
+        f._buf = _Buffers(forest_buf, None)
+        f.view = rtf_forest()
+        check(lib().rtf_forest_view(_ptr(forest_buf), forest_buf.numel(), f.n, f.m, 1,
+                                    ctypes.byref(f.view)), "rtf_forest_view")
+        return f
+
     # ---------------------------------------------------------------- build
     def build(self, p: torch.Tensor, stream=None) -> "Forest":
         if p.dtype != torch.float32 or not p.is_cuda or not p.is_contiguous():

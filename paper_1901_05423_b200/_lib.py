@@ -26,6 +26,13 @@ class rtf_forest(ctypes.Structure):
                 ("table", ctypes.c_void_p), ("header", ctypes.c_void_p)]
 
 
+class rtf_shard_view(ctypes.Structure):
+    _fields_ = [("lam", ctypes.c_void_p), ("pend", ctypes.c_void_p), ("deps", ctypes.c_void_p),
+                ("ndeps", ctypes.c_void_p), ("scale", ctypes.c_void_p), ("total", ctypes.c_void_p),
+                ("nt_local", ctypes.c_uint32), ("dep_stride", ctypes.c_uint32),
+                ("dep_bytes", ctypes.c_uint32), ("reserved", ctypes.c_uint32)]
+
+
 # name -> (restype, argtypes)
 _P, _U32, _U64, _I32, _SZ = (ctypes.c_void_p, ctypes.c_uint32, ctypes.c_uint64, ctypes.c_int,
                              ctypes.c_size_t)
@@ -48,6 +55,14 @@ PROTOTYPES = {
     "rtf_build_host": (_I32, [_P, _U32, _U32, _U32, _P, _P, _SZ, _P, _SZ, _P, _F, _H]),
     "rtf_sample_host": (_I32, [_F, _P, _U64, _P, _P, _P, _U64, _P]),
     "rtf_philox_u32": (_I32, [_U64, _U64, _U64, _P, _P]),
+    "rtf_shard_workspace_bytes": (_SZ, [_U32, _U32, _U32]),
+    "rtf_shard_workspace_init": (_I32, [_P, _SZ, _U32, _U32, _U32, _P]),
+    "rtf_shard_get_view": (_I32, [_P, _SZ, _U32, _U32, _U32, ctypes.POINTER(rtf_shard_view)]),
+    "rtf_shard_scale": (_I32, [_P, _U32, _U32, _U32, _P, _SZ, _P]),
+    "rtf_shard_totals": (_I32, [_P, _U32, _U32, _U32, _U32, _P, _SZ, _P]),
+    "rtf_shard_build": (_I32, [_P, _U32, _U32, _U32, _U32, _U32, _U32, _P, _P, _SZ, _P, _SZ, _P,
+                               _F]),
+    "rtf_shard_finish": (_I32, [_U32, _U32, _U32, _P, _P, _P, _U32, _P, _SZ, _P, _SZ, _P, _F]),
     "rtf_launch_count": (_U64, []),
     "rtf_status_string": (ctypes.c_char_p, [_I32]),
     "rtf_version": (ctypes.c_char_p, []),

@@ -315,4 +315,117 @@ int rtf_philox_u32(uint64_t seed, uint64_t start, uint64_t count, uint32_t* out,
     return finish(e, launches);
 }
 
+// ------------------------------------------------------------------ sharded build (config 4)
+
+size_t rtf_shard_workspace_bytes(uint32_t n_local, uint32_t n_global, uint32_t m) {
+    rtf::WsLayout L;
+    return rtf::build_workspace_layout(n_local ? n_local : 1, m ? m : 1, rtf::kBuildShardedLayout,
+                                       &L, n_global);
+}
+
+static int shard_layout(void* ws, size_t ws_bytes, uint32_t n_local, uint32_t n_global, uint32_t m,
+                        rtf::WsLayout* L) {
+    if (!ws) return RTF_EINVAL;
+    if (n_local == 0 || n_local > n_global) return RTF_EINVAL;
+    if (int s = check_nm(n_global, m)) return s;
+    if (((uintptr_t)ws & (kAlign - 1)) != 0) return RTF_EINVAL;
+    if (ws_bytes < rtf::build_workspace_layout(n_local, m, rtf::kBuildShardedLayout, L, n_global))
+        return RTF_ENOSPACE;
+    return RTF_OK;
+}
+
+int rtf_shard_workspace_init(void* ws, size_t ws_bytes, uint32_t n_local, uint32_t n_global,
+                             uint32_t m, void* stream) {
+    rtf::WsLayout L;
+    if (int s = shard_layout(ws, ws_bytes, n_local, n_global, m, &L)) return s;
+    unsigned char* w = static_cast<unsigned char*>(ws);
+    cudaStream_t st = as_stream(stream);
+    cudaError_t e = cudaMemsetAsync(w, 0, L.ob, st);
+    if (e == cudaSuccess)
+        e = cudaMemsetAsync(w + L.ob, 0xFF, sizeof(uint64_t) * (size_t)n_global, st);
+    if (e == cudaSuccess) e = cudaMemsetAsync(w + L.pend, 0xFF, L.ndeps - L.pend, st);
+    return e == cudaSuccess ? RTF_OK : RTF_ECUDA;
+}
+
+int rtf_shard_get_view(void* ws, size_t ws_bytes, uint32_t n_local, uint32_t n_global, uint32_t m,
+                       rtf_shard_view* out) {
+    rtf::WsLayout L;
+    if (!out) return RTF_EINVAL;
+    if (int s = shard_layout(ws, ws_bytes, n_local, n_global, m, &L)) return s;
+    unsigned char* w = static_cast<unsigned char*>(ws);
+    out->lam = w + L.lam;
+    out->pend = w + L.pend;
+    out->deps = w + L.deps;
+    out->ndeps = reinterpret_cast<uint32_t*>(w + L.ndeps);
+    out->scale = reinterpret_cast<uint32_t*>(w + L.scale);
+    out->total = w + L.total;
+    out->nt_local = L.nt;
+    out->dep_stride = (uint32_t)rtf::shard_deps_per_tile();
+    out->dep_bytes = (uint32_t)rtf::shard_dep_bytes();
+    return RTF_OK;
+}
+
+int rtf_shard_scale(const float* p, uint32_t n_local, uint32_t n_global, uint32_t m, void* ws,
+                    size_t ws_bytes, void* stream) {
+    rtf::WsLayout L;
+    if (!p || ((uintptr_t)p & 3u)) return RTF_EINVAL;
+    if (int s = shard_layout(ws, ws_bytes, n_local, n_global, m, &L)) return s;
+    rtf::ShardCall sc{rtf::kPhScale, n_global, 0, 0, 1, 0, nullptr, nullptr, nullptr, nullptr};
+    int launches = 0;
+    cudaError_t e = rtf::launch_build(p, n_local, m, rtf::kBuildShardedLayout, nullptr, nullptr,
+                                      nullptr, nullptr, ws, L, as_stream(stream), &launches, &sc);
+    return finish(e, launches);
+}
+
+int rtf_shard_totals(const float* p, uint32_t n_local, uint32_t n_global, uint32_t m,
+                     uint32_t index_base, void* ws, size_t ws_bytes, void* stream) {
+    rtf::WsLayout L;
+    if (!p || ((uintptr_t)p & 3u)) return RTF_EINVAL;
+    if (int s = shard_layout(ws, ws_bytes, n_local, n_global, m, &L)) return s;
+    if ((uint64_t)index_base + n_local > n_global) return RTF_EINVAL;
+    rtf::ShardCall sc{rtf::kPhTotals | rtf::kPhSpine, n_global, index_base, 0, 1, 0,
+                      nullptr, nullptr, nullptr, nullptr};
+    int launches = 0;
+    cudaError_t e = rtf::launch_build(p, n_local, m, rtf::kBuildShardedLayout, nullptr, nullptr,
+                                      nullptr, nullptr, ws, L, as_stream(stream), &launches, &sc);
+    return finish(e, launches);
+}
+
+int rtf_shard_build(const float* p, uint32_t n_local, uint32_t n_global, uint32_t m,
+                    uint32_t index_base, uint32_t rank, uint32_t count, const void* totals,
+                    void* forest_buf, size_t forest_bytes, void* ws, size_t ws_bytes, void* stream,
+                    rtf_forest* out) {
+    rtf::WsLayout L;
+    if (!p || !totals || ((uintptr_t)p & 3u) || count == 0 || rank >= count) return RTF_EINVAL;
+    if (int s = shard_layout(ws, ws_bytes, n_local, n_global, m, &L)) return s;
+    if ((uint64_t)index_base + n_local > n_global) return RTF_EINVAL;
+    if (int s = rtf_forest_view(forest_buf, forest_bytes, n_global, m, 1, out)) return s;
+    rtf::ShardCall sc{rtf::kPhTiles | rtf::kPhRuns, n_global, index_base, rank, count, 0,
+                      totals, nullptr, nullptr, nullptr};
+    int launches = 0;
+    cudaError_t e =
+        rtf::launch_build(p, n_local, m, rtf::kBuildShardedLayout, out->header, out->nodes,
+                          out->table, nullptr, ws, L, as_stream(stream), &launches, &sc);
+    return finish(e, launches);
+}
+
+int rtf_shard_finish(uint32_t n_local, uint32_t n_global, uint32_t m, const void* pend_all,
+                     const void* deps_all, const uint32_t* ndeps_all, uint32_t nt_all,
+                     void* forest_buf, size_t forest_bytes, void* ws, size_t ws_bytes,
+                     void* stream, rtf_forest* out) {
+    rtf::WsLayout L;
+    if (!pend_all || !deps_all || !ndeps_all) return RTF_EINVAL;
+    if (int s = shard_layout(ws, ws_bytes, n_local, n_global, m, &L)) return s;
+    if (int s = rtf_forest_view(forest_buf, forest_bytes, n_global, m, 1, out)) return s;
+    rtf::ShardCall sc{rtf::kPhScatter | rtf::kPhWalk, n_global, 0, 0, 1, nt_all,
+                      nullptr, pend_all, deps_all, ndeps_all};
+    int launches = 0;
+    // any valid p pointer is fine: phases A-D do not run
+    const float* dummy = reinterpret_cast<const float*>(ws);
+    cudaError_t e =
+        rtf::launch_build(dummy, n_local, m, rtf::kBuildShardedLayout, out->header, out->nodes,
+                          out->table, nullptr, ws, L, as_stream(stream), &launches, &sc);
+    return finish(e, launches);
+}
+
 }  // extern "C"

@@ -44,10 +44,28 @@ struct PendingLeaf {
     int32_t ref;  // ~orig(j)
 };
 
+constexpr uint32_t kDepsPerTile = 128;  // leftover deposits of a tile: <= 2 x 64 ancestors
+
+struct ShardDep {
+    uint32_t slot, pad;
+    unsigned long long value;
+};
+
 struct BuildArgs {
     const float* p;
     uint32_t n, m, nt;
-    int B;              // 62 - ceil(log2 n)
+    int B;              // 62 - ceil(log2 n_global)
+    uint32_t phases;
+    uint32_t index_base;       // global index of p[0] (sharded build), else 0
+    uint32_t* scale_io;        // sharded: 4 words {max bits, nan, inf, neg} (MAX-reducible)
+    const Pfx* shard_totals;   // sharded: every shard's total, shard_count entries
+    uint32_t shard_rank, shard_count;
+    Pfx* total_out;            // sharded: this shard's total
+    ShardDep* deps;            // sharded: leftover deposits, kDepsPerTile per tile
+    uint32_t* ndeps;           // sharded: count per tile
+    const ShardDep* deps_in;   // sharded finish: all shards' deposits (ndeps_in[t] per tile)
+    const uint32_t* ndeps_in;
+    uint32_t nt_in;            // sharded finish: number of tiles in pend / deps_in
     uint32_t* maxpart;  // 2 per CTA
     uint32_t* counters;
     Pfx* excl;          // per tile: aggregate (phase B), then exclusive prefix (phase C)
@@ -202,9 +220,13 @@ __global__ void __launch_bounds__(THREADS, MINB) k_build(BuildArgs A) {
     const int lane = tid & 31, warp = tid >> 5;
     uint32_t* gbar = &A.counters[kCtrGridBar];
 
+    const uint32_t ph = A.phases;
+    const int32_t ib = (int32_t)A.index_base;  // original indices are global
+    const bool sharded = A.shard_count > 0;
+
     // ---------------------------------------------------------- A: scale
-    if (b == 0 && tid == 0) A.counters[kCtrQueue] = 0;
-    {
+    if (b == 0 && tid == 0 && (ph & kPhTiles)) A.counters[kCtrQueue] = 0;
+    if (ph & kPhScale) {
         uint32_t mx = 0, fl = 0;
         auto visit = [&](float x) {
             const uint32_t bits = __float_as_uint(x);
@@ -248,14 +270,28 @@ __global__ void __launch_bounds__(THREADS, MINB) k_build(BuildArgs A) {
     }
     grid_barrier(gbar);
     uint32_t mx = 0, fl = 0;
-    for (uint32_t i = tid; i < G; i += THREADS) {
-        mx = max(mx, __ldcg(&A.maxpart[2 * i]));
-        fl |= __ldcg(&A.maxpart[2 * i + 1]);
+    if (ph & kPhScale) {
+        for (uint32_t i = tid; i < G; i += THREADS) {
+            mx = max(mx, __ldcg(&A.maxpart[2 * i]));
+            fl |= __ldcg(&A.maxpart[2 * i + 1]);
+        }
+        block_max_or<THREADS>(mx, fl, s_red);
+        if (sharded && b == 0 && tid == 0) {  // this shard's word, MAX-reduced across shards
+            A.scale_io[0] = mx;
+            A.scale_io[1] = (fl & RTF_DATA_NAN) ? 1u : 0u;
+            A.scale_io[2] = (fl & RTF_DATA_INF) ? 1u : 0u;
+            A.scale_io[3] = (fl & RTF_DATA_NEG) ? 1u : 0u;
+        }
+        if (sharded) return;  // sharded: phase A runs alone
+    } else {                  // sharded: the reduced word of all shards
+        mx = __ldcg(&A.scale_io[0]);
+        fl = (__ldcg(&A.scale_io[1]) ? RTF_DATA_NAN : 0u) |
+             (__ldcg(&A.scale_io[2]) ? RTF_DATA_INF : 0u) |
+             (__ldcg(&A.scale_io[3]) ? RTF_DATA_NEG : 0u);
     }
-    block_max_or<THREADS>(mx, fl, s_red);
     const uint32_t status = fl | (mx == 0 ? RTF_DATA_ALLZERO : 0u);
     if (status) {  // poisoned build: report and stop (uniform across the grid)
-        if (b == 0 && tid == 0) A.hdr->status = status;
+        if (b == 0 && tid == 0 && A.hdr) A.hdr->status = status;
         return;
     }
     const int E = floor_log2_bits(mx);
@@ -263,7 +299,7 @@ __global__ void __launch_bounds__(THREADS, MINB) k_build(BuildArgs A) {
 
     // ---------------------------------------------------------- B: tile totals
     // two tiles per step so each thread has 2*VPT/4 float4 loads in flight
-    for (uint32_t t0 = b; t0 < nt; t0 += 2 * G) {
+    for (uint32_t t0 = b; (ph & kPhTotals) && t0 < nt; t0 += 2 * G) {
         Pfx acc[2];
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
@@ -285,7 +321,7 @@ __global__ void __launch_bounds__(THREADS, MINB) k_build(BuildArgs A) {
                         const uint64_t w = quantize(xs[u], scale);
                         acc[h].W += w;
                         acc[h].cnt += w != 0;
-                        if (w) acc[h].last = e + u;
+                        if (w) acc[h].last = e + u + ib;
                     }
                 }
             } else {
@@ -293,7 +329,7 @@ __global__ void __launch_bounds__(THREADS, MINB) k_build(BuildArgs A) {
                     const uint64_t w = quantize(A.p[e], scale);
                     acc[h].W += w;
                     acc[h].cnt += w != 0;
-                    if (w) acc[h].last = (int32_t)e;
+                    if (w) acc[h].last = (int32_t)e + ib;
                 }
             }
         }
@@ -320,9 +356,9 @@ __global__ void __launch_bounds__(THREADS, MINB) k_build(BuildArgs A) {
         }
     }
     // the tile weights of phase D can stream in while the spine scan runs
-    const bool tma = !CDF && A.vec;
+    const bool tma = !CDF && A.vec && (ph & kPhTiles);
     auto tma_tile = [&](uint32_t t) { return tma && t < nt && (t + 1) * TILE <= n; };
-    if (!CDF && tid == 0) {
+    if (tma && tid == 0) {
         mbar_init(&s_bar, 1);
         fence_proxy_async_smem();
         if (tma_tile(b)) {
@@ -330,10 +366,14 @@ __global__ void __launch_bounds__(THREADS, MINB) k_build(BuildArgs A) {
             tma_load_1d(s_p, A.p + (size_t)b * TILE, TILE * 4, &s_bar);
         }
     }
+    // sharded: this shard writes only the table cells its leaves own; the rest
+    // stays INT32_MIN so a MAX-reduction across shards assembles the table
+    if (sharded && (ph & kPhTiles))
+        for (uint32_t g = b * THREADS + tid; g < m; g += G * THREADS) A.table[g] = INT32_MIN;
     grid_barrier(gbar);
 
     // ---------------------------------------------------------- C: spine scan (CTA 0)
-    if (b == 0) {
+    if (b == 0 && (ph & kPhSpine)) {
         constexpr int BATCH = 4;
         const uint32_t per = (nt + THREADS - 1) / THREADS;  // contiguous chunk per thread
         const uint32_t u0 = min(nt, tid * per), u1 = min(nt, u0 + per);
@@ -369,21 +409,52 @@ __global__ void __launch_bounds__(THREADS, MINB) k_build(BuildArgs A) {
                 run.last = max(run.last, a[u].last);
             }
         }
-        if (tid == THREADS - 1) {  // whole-array totals -> header
+        if (tid == THREADS - 1) {
+            if (sharded) {  // this shard's total, for the cross-GPU scan of shard totals
+                st_pfx(A.total_out, Pfx{w_tot, c_tot, max(l_ex, own.last)});
+            } else {  // whole-array totals -> header
+                rtf_header h;
+                h.total = w_tot;
+                h.n_pos = c_tot;
+                h.exponent = E;
+                h.scale_bits = A.B;
+                h.status = 0;
+                h.reserved = 0;
+                const uint32_t s = (uint32_t)__clzll((long long)w_tot);  // T >= 1
+                h.norm_shift = s;
+                h.recip = reciprocal_of(w_tot << s);
+                *A.hdr = h;
+            }
+        }
+    }
+    if (sharded && !(ph & (kPhTiles | kPhWalk | kPhScatter))) return;  // totals launch ends here
+    grid_barrier(gbar);
+
+    // sharded: the exclusive prefix of this shard and the grand total come from
+    // the gathered shard totals (the cross-GPU scan, done redundantly per CTA)
+    Pfx shard_pre{0ull, 0u, -1};
+    if (sharded && (ph & kPhTiles)) {
+        Pfx tot{0ull, 0u, -1};
+        for (uint32_t r = 0; r < A.shard_count; ++r) {
+            const Pfx s = ld_pfx_cg(&A.shard_totals[r]);
+            if (r == A.shard_rank) shard_pre = tot;
+            tot = combine(tot, s);
+        }
+        if (b == 0 && tid == 0) {
             rtf_header h;
-            h.total = w_tot;
-            h.n_pos = c_tot;
+            h.total = tot.W;
+            h.n_pos = tot.cnt;
             h.exponent = E;
             h.scale_bits = A.B;
             h.status = 0;
             h.reserved = 0;
-            const uint32_t s = (uint32_t)__clzll((long long)w_tot);  // T >= 1
+            const uint32_t s = (uint32_t)__clzll((long long)tot.W);
             h.norm_shift = s;
-            h.recip = reciprocal_of(w_tot << s);
+            h.recip = reciprocal_of(tot.W << s);
             *A.hdr = h;
         }
+        grid_barrier(gbar);
     }
-    grid_barrier(gbar);
 
     const rtf_header* hdr = A.hdr;
     const uint64_t T = __ldcg(&hdr->total);
@@ -421,9 +492,9 @@ __global__ void __launch_bounds__(THREADS, MINB) k_build(BuildArgs A) {
 
     // ---------------------------------------------------------- D: tiles
     uint32_t phase = 0;
-    for (uint32_t t = b; t < nt; t += G) {
-        const Pfx pre = ld_pfx_cg(&A.excl[t]);
-        const uint32_t first = t * TILE + tid * VPT;
+    for (uint32_t t = b; (ph & kPhTiles) && t < nt; t += G) {
+        const Pfx pre = sharded ? combine(shard_pre, ld_pfx_cg(&A.excl[t])) : ld_pfx_cg(&A.excl[t]);
+        const uint32_t first = t * TILE + tid * VPT;  // local index into p (global: + ib)
 
         // (0) weights of this thread's VPT consecutive entries
         float x[VPT];
@@ -452,7 +523,7 @@ __global__ void __launch_bounds__(THREADS, MINB) k_build(BuildArgs A) {
             if (w[k]) {
                 ++tc;
                 posmask |= 1u << k;
-                tl = (int32_t)(first + k);
+                tl = (int32_t)(first + k) + ib;
             }
         }
         // (1) block scan (its barriers also retire every read of s_p);
@@ -478,7 +549,7 @@ __global__ void __launch_bounds__(THREADS, MINB) k_build(BuildArgs A) {
 #pragma unroll
             for (int k = 0; k < VPT; ++k) {
                 if (w[k]) {
-                    const int32_t i = (int32_t)(first + k);
+                    const int32_t i = (int32_t)(first + k) + ib;
                     const uint32_t q = pad8(jl);
                     s_key[q] = fixed_point(W, nm);
                     s_c0[q] = ~(prevo >= 0 ? prevo : i);
@@ -490,7 +561,7 @@ __global__ void __launch_bounds__(THREADS, MINB) k_build(BuildArgs A) {
         }
         // the tile's first and last leaf stay pending for phase 2 (E)
         if (tc && c_ex == 0)
-            A.pend[2 * t] = PendingLeaf{(int32_t)j0, ~(int32_t)(first + __ffs(posmask) - 1)};
+            A.pend[2 * t] = PendingLeaf{(int32_t)j0, ~((int32_t)(first + __ffs(posmask) - 1) + ib)};
         if (tc && c_ex + tc == cnt)
             A.pend[2 * t + 1] = cnt >= 2 ? PendingLeaf{(int32_t)(j0 + cnt - 1), ~tl}
                                          : PendingLeaf{-1, 0};
@@ -516,7 +587,7 @@ __global__ void __launch_bounds__(THREADS, MINB) k_build(BuildArgs A) {
                 if (j == 0) A.table[0] = 0;
                 if (lam == kLamBoundary)
                     table_runs(A.table, m, A.counters, A.queue, A.qcap, j,
-                               (int32_t)(first + __ffs(mask) - 1), cell, cn);
+                               (int32_t)(first + __ffs(mask) - 1) + ib, cell, cn);
                 key = kn;
             }
         }
@@ -546,7 +617,7 @@ __global__ void __launch_bounds__(THREADS, MINB) k_build(BuildArgs A) {
                     mask &= mask - 1;
                     active = true;
                     lo = hi = (int32_t)l;
-                    node = ~(int32_t)(first + k);
+                    node = ~((int32_t)(first + k) + ib);
                     lamL = lds_u8(a_lam + pad8(l - 1));
                     lamR = lds_u8(a_lam + pad8(l));
                     ++l;
@@ -579,13 +650,22 @@ __global__ void __launch_bounds__(THREADS, MINB) k_build(BuildArgs A) {
 
         // (4) flush: leftover deposits first, then the next tile's TMA copy can
         // reuse the buffer while records (coalesced 16 B) and split levels go out
+        if (sharded && tid == 0) s_red[0] = 0;
+        if (sharded) __syncthreads();
         for (uint32_t l = 1 + tid; l < cnt; l += THREADS) {
             const int32_t o = s_ob[pad8(l)];
-            if (o >= 0)
-                A.ob[j0 + l] = ((unsigned long long)((uint32_t)o >> 16) << 32) |
-                               (uint32_t)(j0 + (o & 0xffff));
+            if (o >= 0) {
+                const unsigned long long v = ((unsigned long long)((uint32_t)o >> 16) << 32) |
+                                             (uint32_t)(j0 + (o & 0xffff));
+                A.ob[j0 + l] = v;
+                if (sharded) {  // also listed, so every shard can replay it before phase 2
+                    const uint32_t k = atomicAdd(&s_red[0], 1u);
+                    if (k < kDepsPerTile) A.deps[t * kDepsPerTile + k] = ShardDep{j0 + l, 0u, v};
+                }
+            }
         }
         __syncthreads();
+        if (sharded && tid == 0) A.ndeps[t] = min(s_red[0], kDepsPerTile);
         if (tid == 0 && tma_tile(t + G)) {
             fence_proxy_async_smem();
             mbar_arrive_expect_tx(&s_bar, TILE * 4);
@@ -605,8 +685,19 @@ __global__ void __launch_bounds__(THREADS, MINB) k_build(BuildArgs A) {
     }
     grid_barrier(gbar);
 
+    // sharded finish: replay every shard's leftover deposits into otherBounds
+    if (ph & kPhScatter) {
+        for (uint32_t t = b; t < A.nt_in; t += G)
+            for (uint32_t k = tid; k < __ldcg(&A.ndeps_in[t]); k += THREADS) {
+                const ShardDep d = A.deps_in[t * kDepsPerTile + k];
+                A.ob[d.slot] = d.value;
+            }
+        grid_barrier(gbar);
+    }
+
     // ---------------------------------------------------------- E: cross-tile Alg. 1
-    for (uint32_t pi = b * THREADS + tid; pi < 2 * nt; pi += G * THREADS) {
+    const uint32_t npend = (ph & kPhScatter) ? 2 * A.nt_in : 2 * nt;
+    for (uint32_t pi = b * THREADS + tid; (ph & kPhWalk) && pi < npend; pi += G * THREADS) {
         const PendingLeaf pl = A.pend[pi];
         if (pl.j < 0) continue;
         int32_t lo = pl.j, hi = pl.j, node = pl.ref;
@@ -638,7 +729,7 @@ __global__ void __launch_bounds__(THREADS, MINB) k_build(BuildArgs A) {
         }
     }
     // long empty-cell runs of the guide table: one warp per chunk
-    const uint32_t nq = min(__ldcg(&A.counters[kCtrQueue]), A.qcap);
+    const uint32_t nq = (ph & kPhRuns) ? min(__ldcg(&A.counters[kCtrQueue]), A.qcap) : 0u;
     for (uint32_t q = b * NW + warp; q < nq; q += G * NW) {
         const RunChunk rc = A.queue[q];
         for (uint32_t g = lane; g < rc.len; g += 32) A.table[rc.start + g] = rc.value;
@@ -662,9 +753,17 @@ uint32_t build_tile_size(uint32_t flags) {
 
 uint32_t build_queue_capacity(uint32_t m) { return m / 32u + m / kChunk + 64u; }
 
-size_t build_workspace_layout(uint32_t n, uint32_t m, uint32_t flags, WsLayout* L) {
+size_t shard_dep_bytes() { return sizeof(ShardDep); }
+size_t shard_deps_per_tile() { return kDepsPerTile; }
+
+// n: entries this call processes (a shard's, for sharded builds); n_global: the
+// whole distribution (otherBounds and split levels are indexed globally).
+size_t build_workspace_layout(uint32_t n, uint32_t m, uint32_t flags, WsLayout* L,
+                              uint32_t n_global) {
+    if (n_global < n) n_global = n;
     const uint32_t tile = build_tile_size(flags);
     const uint32_t nt = (uint32_t)(((uint64_t)n + tile - 1) / tile);
+    const bool sharded = n_global != n || (flags & kBuildShardedLayout);
     size_t off = 0;
     auto take = [&](size_t bytes) {
         const size_t o = off;
@@ -674,13 +773,17 @@ size_t build_workspace_layout(uint32_t n, uint32_t m, uint32_t flags, WsLayout* 
     L->nt = nt;
     L->maxpart = take(sizeof(uint32_t) * 2 * kMaxGrid);
     L->counters = take(64);
+    L->scale = take(16);
+    L->total = take(16);
     L->excl = take(sizeof(Pfx) * (size_t)nt);
     L->pend = take(sizeof(PendingLeaf) * 2 * (size_t)nt);
-    L->ob = take(sizeof(unsigned long long) * (size_t)n);
-    L->lam = take((size_t)n);
+    L->ndeps = take(sharded ? sizeof(uint32_t) * (size_t)nt : 0);
+    L->deps = take(sharded ? sizeof(ShardDep) * kDepsPerTile * (size_t)nt : 0);
+    L->ob = take(sizeof(unsigned long long) * (size_t)n_global);
+    L->lam = take((size_t)n_global);
     L->qcap = build_queue_capacity(m);
     L->queue = take(sizeof(RunChunk) * (size_t)L->qcap);
-    L->total = off;
+    L->bytes = off;
     return off;
 }
 
@@ -722,14 +825,27 @@ static cudaError_t launch_fused(BuildArgs& A, cudaStream_t st, int* launches) {
 
 cudaError_t launch_build(const float* p, uint32_t n, uint32_t m, uint32_t flags, rtf_header* hdr,
                          rtf_node* nodes, int32_t* table, uint64_t* cdf, void* ws,
-                         const WsLayout& L, cudaStream_t st, int* launches) {
+                         const WsLayout& L, cudaStream_t st, int* launches,
+                         const ShardCall* sc) {
     unsigned char* w = reinterpret_cast<unsigned char*>(ws);
     BuildArgs A;
     A.p = p;
     A.n = n;
     A.m = m;
     A.nt = L.nt;
-    A.B = 62 - ceil_log2_u32(n);
+    A.B = 62 - ceil_log2_u32(sc ? sc->n_global : n);
+    A.phases = sc ? sc->phases : kPhFull;
+    A.index_base = sc ? sc->index_base : 0;
+    A.scale_io = reinterpret_cast<uint32_t*>(w + L.scale);
+    A.shard_totals = sc ? reinterpret_cast<const Pfx*>(sc->totals) : nullptr;
+    A.shard_rank = sc ? sc->rank : 0;
+    A.shard_count = sc ? sc->count : 0;
+    A.total_out = reinterpret_cast<Pfx*>(w + L.total);
+    A.deps = reinterpret_cast<ShardDep*>(w + L.deps);
+    A.ndeps = reinterpret_cast<uint32_t*>(w + L.ndeps);
+    A.deps_in = sc ? reinterpret_cast<const ShardDep*>(sc->deps_in) : nullptr;
+    A.ndeps_in = sc ? sc->ndeps_in : nullptr;
+    A.nt_in = sc ? sc->nt_in : 0;
     A.maxpart = reinterpret_cast<uint32_t*>(w + L.maxpart);
     A.counters = reinterpret_cast<uint32_t*>(w + L.counters);
     A.excl = reinterpret_cast<Pfx*>(w + L.excl);
@@ -738,7 +854,8 @@ cudaError_t launch_build(const float* p, uint32_t n, uint32_t m, uint32_t flags,
     A.table = table;
     A.lam = reinterpret_cast<uint8_t*>(w + L.lam);
     A.ob = reinterpret_cast<unsigned long long*>(w + L.ob);
-    A.pend = reinterpret_cast<PendingLeaf*>(w + L.pend);
+    A.pend = (sc && sc->pend_in) ? reinterpret_cast<PendingLeaf*>(const_cast<void*>(sc->pend_in))
+                                 : reinterpret_cast<PendingLeaf*>(w + L.pend);
     A.queue = reinterpret_cast<RunChunk*>(w + L.queue);
     A.qcap = L.qcap;
     A.cdf = cdf;

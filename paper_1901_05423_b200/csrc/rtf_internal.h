@@ -9,8 +9,20 @@
 
 namespace rtf {
 
-constexpr uint32_t kMaxScaleBlocks = 148 * 8;  // K1 grid cap (multiple of the SM count)
-constexpr uint32_t kRowsMax = 4096;            // rtf_build_rows: n_row, m_row limit
+constexpr uint32_t kRowsMax = 4096;  // rtf_build_rows: n_row, m_row limit
+
+// phases of the build kernel (bitmask); a single-GPU build runs kPhFull
+enum : uint32_t {
+    kPhScale = 1,     // A: max weight, data flags
+    kPhTotals = 2,    // B: tile aggregates
+    kPhSpine = 4,     // C: exclusive tile prefixes (+ header or shard total)
+    kPhTiles = 8,     // D: keys, split levels, table, in-tile Alg. 1, records
+    kPhRuns = 16,     // E: long empty-cell runs of the table
+    kPhWalk = 32,     // E: cross-tile Alg. 1
+    kPhScatter = 64,  // sharded finish: all shards' leftover deposits -> otherBounds
+    kPhFull = kPhScale | kPhTotals | kPhSpine | kPhTiles | kPhRuns | kPhWalk,
+};
+constexpr uint32_t kBuildShardedLayout = 0x100;  // internal flag: workspace with deposit lists
 
 inline int ceil_log2_u32(uint32_t n) {
     int c = 0;
@@ -21,15 +33,28 @@ inline int ceil_log2_u32(uint32_t n) {
 struct WsLayout {
     uint32_t nt;  // tiles
     uint32_t qcap;
-    size_t maxpart, counters, excl, pend, ob, lam, queue, total;
+    size_t maxpart, counters, scale, total, excl, pend, ndeps, deps, ob, lam, queue, bytes;
+};
+
+// one call of a sharded build (config 4); see rtf_shard_* in include/rtf.h
+struct ShardCall {
+    uint32_t phases, n_global, index_base, rank, count, nt_in;
+    const void* totals;        // device: count shard totals (16 B each)
+    const void* pend_in;       // device: finish -- all shards' pending leaves
+    const void* deps_in;       // device: finish -- all shards' deposit lists
+    const uint32_t* ndeps_in;  // device: finish -- deposits per tile
 };
 
 uint32_t build_tile_size(uint32_t flags);
-size_t build_workspace_layout(uint32_t n, uint32_t m, uint32_t flags, WsLayout* L);
+size_t build_workspace_layout(uint32_t n, uint32_t m, uint32_t flags, WsLayout* L,
+                              uint32_t n_global = 0);
+size_t shard_dep_bytes();       // bytes of one deposit-list entry
+size_t shard_deps_per_tile();   // deposit-list capacity per tile
 
 cudaError_t launch_build(const float* p, uint32_t n, uint32_t m, uint32_t flags, rtf_header* hdr,
                          rtf_node* nodes, int32_t* table, uint64_t* cdf, void* ws,
-                         const WsLayout& L, cudaStream_t st, int* launches);
+                         const WsLayout& L, cudaStream_t st, int* launches,
+                         const ShardCall* sc = nullptr);
 
 cudaError_t launch_build_rows(const float* p, uint32_t rows, uint32_t n_row, uint32_t m_row,
                               rtf_header* hdr, rtf_node* nodes, int32_t* table, cudaStream_t st,

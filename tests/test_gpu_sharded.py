@@ -1,0 +1,64 @@
+"""Sharded build (config 4) on one GPU with virtual shards: the shards run the
+per-shard kernels on their own buffers and exchange through LocalComm (the
+same collectives NCCL performs across GPUs).  Every shard must end with the
+forest the single-GPU build (and the oracle) produces, byte for byte."""
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+
+import oracle  # noqa: E402
+from workloads import philox_xi, power_law, random_small, spikes  # noqa: E402
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def rtf():
+    if not torch.cuda.is_available():
+        pytest.fail("CUDA device required for -m gpu tests")
+    import paper_1901_05423_b200 as rtf
+    rtf.lib()
+    return rtf
+
+
+def _check(rtf, p, m, count):
+    from paper_1901_05423_b200 import sharded
+    pd = torch.from_numpy(p).cuda()
+    shards = sharded.make_shards(pd, m, count)
+    sharded.build_sharded(shards, sharded.LocalComm())
+    ref = oracle.build(p, m)
+    single = rtf.build(pd, m)
+    want_nodes = single.nodes_numpy().tobytes()
+    want_table = single.table_numpy().tobytes()
+    assert np.array_equal(single.nodes_numpy()["c1"], ref.child1)
+    for s in shards:
+        f = rtf.Forest.from_buffer(s.n_global, m, s.forest)
+        assert f.status() == 0
+        assert f.n_pos() == ref.n_pos
+        assert f.nodes_numpy().tobytes() == want_nodes, f"shard {s.rank} records"
+        assert f.table_numpy().tobytes() == want_table, f"shard {s.rank} table"
+        xi = philox_xi(1 << 16, seed=s.rank)
+        got = f.sample(torch.from_numpy(xi.view(np.int32)).cuda()).cpu().numpy()
+        assert np.array_equal(got, ref.sample(xi))
+        # every deposit was consumed: the shard's otherBounds are idle again
+        ob = s._ws_slice(s.view.lam - 8 * s.n_global, 8 * s.n_global).cpu().numpy().view(np.int64)
+        assert np.all(ob == -1)
+
+
+@pytest.mark.parametrize("count", [1, 2, 3, 4])
+def test_sharded_power_law(rtf, count):
+    # the giant cell of p_i ~ i^20 spans every shard: many cross-shard merges
+    _check(rtf, power_law(1 << 18, "A"), 1 << 16, count)
+
+
+@pytest.mark.parametrize("count", [2, 5])
+def test_sharded_spikes_and_random(rtf, count):
+    _check(rtf, spikes(3 << 16), 1 << 15, count)
+    rng = np.random.default_rng(count)
+    _check(rtf, random_small(rng, 100003, zero_frac=0.3, dyn=12.0), 77777, count)
+
+
+def test_sharded_config4_shape(rtf):
+    """Config 4's distribution (4 spikes, uniform background) at 2^22 over 8 shards."""
+    _check(rtf, spikes(1 << 22), 1 << 20, 8)
