@@ -572,23 +572,27 @@ __global__ void __launch_bounds__(THREADS, MINB) k_build(BuildArgs A) {
         }
         __syncthreads();
 
-        // (2) own leaves: cell, split level, guide table
+        // (2) own leaves: cell, split level, guide table; the
+        // thread's own split levels also stay in registers (byte r = rank r)
+        uint64_t lampack = 0;
         {
             const uint64_t key_after = s_key_after;
-            uint32_t jl = c_ex;
+            uint32_t jl = c_ex, r = 0;
             uint64_t key = tc ? s_key[pad8(jl)] : 0ull;
-            for (uint32_t mask = posmask; mask; mask &= mask - 1, ++jl) {
+            uint32_t cell = cell_of(key, m);
+            for (uint32_t mask = posmask; mask; mask &= mask - 1, ++jl, ++r) {
                 const uint64_t kn = (jl + 1 < cnt) ? s_key[pad8(jl + 1)] : key_after;
-                const uint32_t cell = cell_of(key, m);
                 const uint32_t cn = (kn == kOne63) ? m : cell_of(kn, m);
                 const uint32_t lam = (cn != cell) ? kLamBoundary : split_level(key, kn);
                 s_lam[pad8(jl)] = (uint8_t)lam;
+                lampack |= (uint64_t)lam << (8 * r);
                 const uint32_t j = j0 + jl;
                 if (j == 0) A.table[0] = 0;
                 if (lam == kLamBoundary)
                     table_runs(A.table, m, A.counters, A.queue, A.qcap, j,
                                (int32_t)(first + __ffs(mask) - 1) + ib, cell, cn);
                 key = kn;
+                cell = cn;
             }
         }
         __syncthreads();
@@ -601,26 +605,77 @@ __global__ void __launch_bounds__(THREADS, MINB) k_build(BuildArgs A) {
         // 64 on both sides) is the right child of its anchor lo and needs no
         // exchange.  A deposit is (lambda beyond the bound) << 16 | bound.
         {
-            // own interior leaves [l, le): the tile's leaf 0 is this thread's
-            // lowest set bit if c_ex == 0, leaf cnt-1 its highest if it owns it
-            uint32_t mask = (c_ex == 0 && tc) ? posmask & (posmask - 1) : posmask;
-            uint32_t l = c_ex == 0 ? 1u : c_ex;
-            const uint32_t le = min(c_ex + tc, cnt >= 1 ? cnt - 1 : 0u);
             const uint32_t a_c0 = smem_u32(s_c0), a_c1 = smem_u32(s_c1);
             const uint32_t a_ob = smem_u32(s_ob), a_lam = smem_u32(s_lam);
+            // Stage A: the FIRST step of every own interior leaf, straight-line
+            // (half of all merge steps, without loop or divergence overhead).
+            // Leaf of rank r is l = c_ex + r; its split levels come from
+            // registers (lambda[l-1] of rank 0 from the previous thread).
+            const uint32_t lam_prev = c_ex ? lds_u8(a_lam + pad8(c_ex - 1)) : kLamBoundary;
+            uint32_t contw[VPT];  // second arrivals: the sibling's packed deposit
+            uint32_t pend = 0, rightbits = 0;
+            {
+                uint32_t mask = posmask;
+#pragma unroll
+                for (int r = 0; r < VPT; ++r) {
+                    contw[r] = 0;
+                    if ((uint32_t)r < tc) {
+                        const uint32_t k = __ffs(mask) - 1;
+                        mask &= mask - 1;
+                        const uint32_t l = c_ex + r;
+                        if (l >= 1 && l + 1 < cnt) {
+                            const uint32_t lamL =
+                                r ? (uint32_t)(lampack >> (8 * (r - 1))) & 0xffu : lam_prev;
+                            const uint32_t lamR = (uint32_t)(lampack >> (8 * r)) & 0xffu;
+                            const bool right = lamL <= lamR;
+                            const bool root = (lamL & lamR & kLamBoundary) != 0;
+                            const uint32_t q4 = 4 * pad8(right ? l : l + 1);
+                            sts_u32((right ? a_c1 : a_c0) + q4,
+                                    (uint32_t)~((int32_t)(first + k) + ib));
+                            if (!root) {
+                                const int32_t other = atoms_exch(
+                                    a_ob + q4, (int32_t)((right ? lamR : lamL) << 16 | l));
+                                if (other >= 0) {
+                                    sts_u32(a_ob + q4, 0xffffffffu);  // reset-on-consume
+                                    contw[r] = (uint32_t)other;
+                                    pend |= 1u << r;
+                                    rightbits |= (right ? 1u : 0u) << r;
+                                }
+                            }
+                        }
+                    }
+                }
+            }
+            // Stage B: the second arrivals climb on, one walker per lane at a time.
             bool active = false;
             int32_t lo = 0, hi = 0, node = 0;
             uint32_t lamL = 0, lamR = 0;
             while (true) {
-                if (!active && l < le) {
-                    const uint32_t k = __ffs(mask) - 1;
-                    mask &= mask - 1;
+                if (!active && pend) {
+                    const uint32_t r = __ffs(pend) - 1;
+                    pend &= pend - 1;
+                    uint32_t other = contw[0];
+#pragma unroll
+                    for (int u = 1; u < VPT; ++u) other = (r == (uint32_t)u) ? contw[u] : other;
+                    const uint32_t l = c_ex + r;
+                    const uint32_t bound = other & 0xffffu, lv = other >> 16;
+                    const uint32_t own_lo = r ? (uint32_t)(lampack >> (8 * (r - 1))) & 0xffu
+                                              : lam_prev;
+                    const uint32_t own_hi = (uint32_t)(lampack >> (8 * r)) & 0xffu;
                     active = true;
-                    lo = hi = (int32_t)l;
-                    node = ~((int32_t)(first + k) + ib);
-                    lamL = lds_u8(a_lam + pad8(l - 1));
-                    lamR = lds_u8(a_lam + pad8(l));
-                    ++l;
+                    if ((rightbits >> r) & 1u) {  // merged as the right child of node l
+                        lo = (int32_t)bound;
+                        hi = (int32_t)l;
+                        lamL = lv;
+                        lamR = own_hi;
+                        node = (int32_t)(j0 + l);
+                    } else {  // merged as the left child of node l + 1
+                        lo = (int32_t)l;
+                        hi = (int32_t)bound;
+                        lamL = own_lo;
+                        lamR = lv;
+                        node = (int32_t)(j0 + l + 1);
+                    }
                 }
                 if (!__any_sync(0xffffffffu, active)) break;
                 if (active) {

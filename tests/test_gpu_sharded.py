@@ -42,7 +42,8 @@ def _check(rtf, p, m, count):
         got = f.sample(torch.from_numpy(xi.view(np.int32)).cuda()).cpu().numpy()
         assert np.array_equal(got, ref.sample(xi))
         # every deposit was consumed: the shard's otherBounds are idle again
-        ob = s._ws_slice(s.view.lam - 8 * s.n_global, 8 * s.n_global).cpu().numpy().view(np.int64)
+        ob_bytes = (8 * s.n_global + 255) // 256 * 256  # otherBounds precede the split levels
+        ob = s._ws_slice(s.view.lam - ob_bytes, 8 * s.n_global).cpu().numpy().view(np.int64)
         assert np.all(ob == -1)
 
 
