@@ -31,7 +31,7 @@ constexpr uint32_t kChunk = 2048;   // longer runs: queued in chunks of this man
 constexpr uint32_t kMaxGrid = 8192; // partials capacity (CTAs of the cooperative grid)
 
 // workspace counters
-enum : int { kCtrGridBar = 0, kCtrQueue = 1 };
+enum : int { kCtrGridBar = 0, kCtrQueue = 1, kCtrTile = 2 };
 
 struct RunChunk {
     uint32_t start, len;
@@ -194,6 +194,26 @@ __device__ __noinline__ void table_runs(int32_t* __restrict__ table, uint32_t m,
     }
 }
 
+// ------------------------------------------------------------ phase timing (debug builds)
+// Compiled only with -DRTF_PHASE_TIMING (tools/phase_timing.py): thread 0 of
+// each CTA accumulates clock64() deltas per phase; read with
+// rtf_debug_phase_cycles().  The product library has neither.
+#ifdef RTF_PHASE_TIMING
+__device__ unsigned long long g_phase_cycles[kMaxGrid][16];
+#define RTF_TICK(slot)                                                       \
+    do {                                                                     \
+        if (threadIdx.x == 0) {                                              \
+            const long long now_ = clock64();                                \
+            g_phase_cycles[blockIdx.x][slot] += (unsigned long long)(now_ - t_tick_); \
+            t_tick_ = now_;                                                  \
+        }                                                                    \
+    } while (0)
+#else
+#define RTF_TICK(slot) \
+    do {               \
+    } while (0)
+#endif
+
 // ============================================================== the build kernel
 
 template <int THREADS, int VPT, bool CDF, int MINB = 2>
@@ -214,6 +234,10 @@ __global__ void __launch_bounds__(THREADS, MINB) k_build(BuildArgs A) {
     __shared__ int32_t s_l[2 * NW];
     __shared__ uint64_t s_key_after;
     __shared__ uint32_t s_red[2 * NW];
+    __shared__ uint32_t s_next;
+    __shared__ Pfx s_grp[THREADS];  // exclusive prefix of each group of `per` tiles
+    __shared__ Pfx s_tot, s_pre;
+    __shared__ uint64_t s_recip;
 
     const uint32_t G = gridDim.x, b = blockIdx.x, tid = threadIdx.x;
     const uint32_t n = A.n, m = A.m, nt = A.nt;
@@ -222,10 +246,16 @@ __global__ void __launch_bounds__(THREADS, MINB) k_build(BuildArgs A) {
 
     const uint32_t ph = A.phases;
     const int32_t ib = (int32_t)A.index_base;  // original indices are global
+#ifdef RTF_PHASE_TIMING
+    long long t_tick_ = clock64();
+#endif
     const bool sharded = A.shard_count > 0;
 
     // ---------------------------------------------------------- A: scale
-    if (b == 0 && tid == 0 && (ph & kPhTiles)) A.counters[kCtrQueue] = 0;
+    if (b == 0 && tid == 0 && (ph & kPhTiles)) {
+        A.counters[kCtrQueue] = 0;
+        A.counters[kCtrTile] = 0;  // phase D's tile dispenser (a grid barrier precedes D)
+    }
     if (ph & kPhScale) {
         uint32_t mx = 0, fl = 0;
         auto visit = [&](float x) {
@@ -269,6 +299,7 @@ __global__ void __launch_bounds__(THREADS, MINB) k_build(BuildArgs A) {
         }
     }
     grid_barrier(gbar);
+    RTF_TICK(0);
     uint32_t mx = 0, fl = 0;
     if (ph & kPhScale) {
         for (uint32_t i = tid; i < G; i += THREADS) {
@@ -371,11 +402,18 @@ __global__ void __launch_bounds__(THREADS, MINB) k_build(BuildArgs A) {
     if (sharded && (ph & kPhTiles))
         for (uint32_t g = b * THREADS + tid; g < m; g += G * THREADS) A.table[g] = INT32_MIN;
     grid_barrier(gbar);
+    RTF_TICK(1);
 
-    // ---------------------------------------------------------- C: spine scan (CTA 0)
-    if (b == 0 && (ph & kPhSpine)) {
+    // ---------------------------------------------------------- C: spine (every CTA)
+    // Each CTA scans the nt tile aggregates itself (nt x 16 B, from L2) and keeps
+    // the exclusive prefix of every group of `per` consecutive tiles in shared
+    // memory; a tile's prefix is its group's plus <= per-1 aggregates (warp 0,
+    // tile_prefix).  Redundant work instead of a single-CTA scan plus one more
+    // grid barrier.
+    const uint32_t per = (nt + THREADS - 1) / THREADS;  // tiles per group (per thread)
+    Pfx total{0ull, 0u, -1};
+    if (ph & (kPhSpine | kPhTiles)) {
         constexpr int BATCH = 4;
-        const uint32_t per = (nt + THREADS - 1) / THREADS;  // contiguous chunk per thread
         const uint32_t u0 = min(nt, tid * per), u1 = min(nt, u0 + per);
         Pfx own{0ull, 0u, -1};
         for (uint32_t tb = u0; tb < u1; tb += BATCH) {
@@ -395,77 +433,77 @@ __global__ void __launch_bounds__(THREADS, MINB) k_build(BuildArgs A) {
         int32_t l_ex;
         block_scan3_excl<THREADS>(own.W, own.cnt, own.last, w_ex, c_ex, l_ex, w_tot, c_tot, s_w,
                                   s_c, s_l);
-        Pfx run{w_ex, c_ex, l_ex};
-        for (uint32_t tb = u0; tb < u1; tb += BATCH) {
-            Pfx a[BATCH];
-#pragma unroll
-            for (int u = 0; u < BATCH; ++u)
-                a[u] = (tb + u < u1) ? ld_pfx_cg(&A.excl[tb + u]) : Pfx{0ull, 0u, -1};
-#pragma unroll
-            for (int u = 0; u < BATCH; ++u) {
-                if (tb + u < u1) st_pfx(&A.excl[tb + u], run);
-                run.W += a[u].W;
-                run.cnt += a[u].cnt;
-                run.last = max(run.last, a[u].last);
-            }
-        }
+        s_grp[tid] = Pfx{w_ex, c_ex, l_ex};
         if (tid == THREADS - 1) {
-            if (sharded) {  // this shard's total, for the cross-GPU scan of shard totals
-                st_pfx(A.total_out, Pfx{w_tot, c_tot, max(l_ex, own.last)});
-            } else {  // whole-array totals -> header
-                rtf_header h;
-                h.total = w_tot;
-                h.n_pos = c_tot;
-                h.exponent = E;
-                h.scale_bits = A.B;
-                h.status = 0;
-                h.reserved = 0;
-                const uint32_t s = (uint32_t)__clzll((long long)w_tot);  // T >= 1
-                h.norm_shift = s;
-                h.recip = reciprocal_of(w_tot << s);
-                *A.hdr = h;
-            }
+            s_tot = Pfx{w_tot, c_tot, max(l_ex, own.last)};
+            // sharded: this shard's total, for the cross-GPU scan of shard totals
+            if (sharded && b == 0 && (ph & kPhSpine)) st_pfx(A.total_out, s_tot);
         }
+        __syncthreads();
+        total = s_tot;
     }
     if (sharded && !(ph & (kPhTiles | kPhWalk | kPhScatter))) return;  // totals launch ends here
-    grid_barrier(gbar);
+    RTF_TICK(2);
 
     // sharded: the exclusive prefix of this shard and the grand total come from
     // the gathered shard totals (the cross-GPU scan, done redundantly per CTA)
-    Pfx shard_pre{0ull, 0u, -1};
     if (sharded && (ph & kPhTiles)) {
-        Pfx tot{0ull, 0u, -1};
+        Pfx tot{0ull, 0u, -1}, shard_pre{0ull, 0u, -1};
         for (uint32_t r = 0; r < A.shard_count; ++r) {
             const Pfx s = ld_pfx_cg(&A.shard_totals[r]);
             if (r == A.shard_rank) shard_pre = tot;
             tot = combine(tot, s);
         }
-        if (b == 0 && tid == 0) {
-            rtf_header h;
-            h.total = tot.W;
-            h.n_pos = tot.cnt;
-            h.exponent = E;
-            h.scale_bits = A.B;
-            h.status = 0;
-            h.reserved = 0;
-            const uint32_t s = (uint32_t)__clzll((long long)tot.W);
-            h.norm_shift = s;
-            h.recip = reciprocal_of(tot.W << s);
-            *A.hdr = h;
-        }
-        grid_barrier(gbar);
+        total = tot;
+        s_grp[tid] = combine(shard_pre, s_grp[tid]);  // group prefixes become global
     }
-
-    const rtf_header* hdr = A.hdr;
-    const uint64_t T = __ldcg(&hdr->total);
+    // T and its reciprocal (one thread per CTA); CTA 0 publishes the header
+    const uint64_t T = total.W;  // >= 1: the largest weight quantises to >= 2^B
     Norm nm;
-    nm.s = __ldcg(&hdr->norm_shift);
+    nm.s = (uint32_t)__clzll((long long)T);
     nm.d = T << nm.s;
-    nm.v = __ldcg(&hdr->recip);
+    if (ph & kPhTiles) {
+        if (tid == THREADS - 1) {
+            s_recip = reciprocal_of(nm.d);
+            if (b == 0) {
+                rtf_header h;
+                h.total = T;
+                h.n_pos = total.cnt;
+                h.exponent = E;
+                h.scale_bits = A.B;
+                h.status = 0;
+                h.reserved = 0;
+                h.norm_shift = nm.s;
+                h.recip = s_recip;
+                *A.hdr = h;
+            }
+        }
+        __syncthreads();
+    }
+    nm.v = s_recip;
+
+    // exclusive prefix of tile t (warp 0 calls; every lane gets it)
+    auto tile_prefix = [&](uint32_t t) -> Pfx {
+        const uint32_t g = t / per;
+        Pfx acc{0ull, 0u, -1};
+        for (uint32_t u = g * per + lane; u < t; u += 32) {
+            const Pfx a = ld_pfx_cg(&A.excl[u]);
+            acc.W += a.W;
+            acc.cnt += a.cnt;
+            acc.last = max(acc.last, a.last);
+        }
+        warp_sum_pfx(acc);
+        return combine(s_grp[g], acc);
+    };
 
     if (CDF) {  // baseline: K[i] = floor(W_i 2^63 / T) for every entry, zeros included
         for (uint32_t t = b; t < nt; t += G) {
-            const Pfx pre = ld_pfx_cg(&A.excl[t]);
+            if (warp == 0) {
+                const Pfx pt = tile_prefix(t);
+                if (lane == 0) s_pre = pt;
+            }
+            __syncthreads();
+            const Pfx pre = s_pre;
             const uint32_t first = t * TILE + tid * VPT;
             float x[VPT];
             load_tile<VPT>(A.p, first, n, A.vec, x);
@@ -491,9 +529,17 @@ __global__ void __launch_bounds__(THREADS, MINB) k_build(BuildArgs A) {
     }
 
     // ---------------------------------------------------------- D: tiles
+    // tiles are dealt dynamically (their cost varies several-fold with the
+    // zero fraction and the tree shape): CTA b starts with tile b, then takes
+    // G + the next ticket; the ticket is drawn early so TMA can prefetch it
     uint32_t phase = 0;
-    for (uint32_t t = b; (ph & kPhTiles) && t < nt; t += G) {
-        const Pfx pre = sharded ? combine(shard_pre, ld_pfx_cg(&A.excl[t])) : ld_pfx_cg(&A.excl[t]);
+    if ((ph & kPhTiles) && warp == 0 && b < nt) {
+        const Pfx p0 = tile_prefix(b);
+        if (lane == 0) s_pre = p0;
+    }
+    __syncthreads();
+    for (uint32_t t = b; (ph & kPhTiles) && t < nt; t = s_next) {
+        const Pfx pre = s_pre;
         const uint32_t first = t * TILE + tid * VPT;  // local index into p (global: + ib)
 
         // (0) weights of this thread's VPT consecutive entries
@@ -572,6 +618,7 @@ __global__ void __launch_bounds__(THREADS, MINB) k_build(BuildArgs A) {
         }
         __syncthreads();
 
+        RTF_TICK(3);
         // (2) own leaves: cell, split level, guide table; the
         // thread's own split levels also stay in registers (byte r = rank r)
         uint64_t lampack = 0;
@@ -597,6 +644,7 @@ __global__ void __launch_bounds__(THREADS, MINB) k_build(BuildArgs A) {
         }
         __syncthreads();
 
+        RTF_TICK(4);
         // (3) phase 1: Alg. 1 for the tile's interior leaves 1..cnt-2 with
         // shared-memory atomicExch.  A range that would contain the pending
         // first/last leaf can never complete here, so every range stays in
@@ -703,6 +751,7 @@ __global__ void __launch_bounds__(THREADS, MINB) k_build(BuildArgs A) {
         }
         __syncthreads();
 
+        RTF_TICK(5);
         // (4) flush: leftover deposits first, then the next tile's TMA copy can
         // reuse the buffer while records (coalesced 16 B) and split levels go out
         if (sharded && tid == 0) s_red[0] = 0;
@@ -721,10 +770,22 @@ __global__ void __launch_bounds__(THREADS, MINB) k_build(BuildArgs A) {
         }
         __syncthreads();
         if (sharded && tid == 0) A.ndeps[t] = min(s_red[0], kDepsPerTile);
-        if (tid == 0 && tma_tile(t + G)) {
-            fence_proxy_async_smem();
-            mbar_arrive_expect_tx(&s_bar, TILE * 4);
-            tma_load_1d(s_p, A.p + (size_t)(t + G) * TILE, TILE * 4, &s_bar);
+        if (warp == 0) {  // next tile: ticket, TMA prefetch, prefix
+            uint32_t nx = 0;
+            if (lane == 0) {
+                nx = G + atomicAdd(&A.counters[kCtrTile], 1u);
+                if (tma_tile(nx)) {
+                    fence_proxy_async_smem();
+                    mbar_arrive_expect_tx(&s_bar, TILE * 4);
+                    tma_load_1d(s_p, A.p + (size_t)nx * TILE, TILE * 4, &s_bar);
+                }
+            }
+            nx = __shfl_sync(0xffffffffu, nx, 0);
+            const Pfx pn = nx < nt ? tile_prefix(nx) : Pfx{0ull, 0u, -1};
+            if (lane == 0) {
+                s_next = nx;
+                s_pre = pn;
+            }
         }
         {
             uint4* gnode = reinterpret_cast<uint4*>(A.nodes + j0);
@@ -737,8 +798,10 @@ __global__ void __launch_bounds__(THREADS, MINB) k_build(BuildArgs A) {
             }
         }
         __syncthreads();  // keys, children and split levels are free for the next tile
+        RTF_TICK(6);
     }
     grid_barrier(gbar);
+    RTF_TICK(7);
 
     // sharded finish: replay every shard's leftover deposits into otherBounds
     if (ph & kPhScatter) {
@@ -789,6 +852,8 @@ __global__ void __launch_bounds__(THREADS, MINB) k_build(BuildArgs A) {
         const RunChunk rc = A.queue[q];
         for (uint32_t g = lane; g < rc.len; g += 32) A.table[rc.start + g] = rc.value;
     }
+    __syncthreads();
+    RTF_TICK(8);
 }
 
 // ============================================================== host-side launch
@@ -809,6 +874,17 @@ uint32_t build_tile_size(uint32_t flags) {
 uint32_t build_queue_capacity(uint32_t m) { return m / 32u + m / kChunk + 64u; }
 
 size_t shard_dep_bytes() { return sizeof(ShardDep); }
+
+#ifdef RTF_PHASE_TIMING
+extern "C" int rtf_debug_phase_cycles(unsigned long long* host, int rows, int reset) {
+    cudaError_t e = cudaMemcpyFromSymbol(host, g_phase_cycles, sizeof(unsigned long long) * 16 * rows);
+    if (reset && e == cudaSuccess) {
+        static unsigned long long zeros[kMaxGrid][16];
+        e = cudaMemcpyToSymbol(g_phase_cycles, zeros, sizeof(zeros));
+    }
+    return e == cudaSuccess ? 0 : 5;
+}
+#endif
 size_t shard_deps_per_tile() { return kDepsPerTile; }
 
 // n: entries this call processes (a shard's, for sharded builds); n_global: the

@@ -1,0 +1,76 @@
+"""Per-phase cycle breakdown of k_build (debug aid, not part of the product).
+
+Builds tools/librtf_timing.so with -DRTF_PHASE_TIMING (thread 0 of every CTA
+accumulates clock64() deltas per phase), runs the config-3 build a few times
+and prints the mean cycles per CTA per phase.
+
+  python tools/phase_timing.py --build      # here (nvcc cross-compiles)
+  python tools/phase_timing.py              # on the GPU box
+"""
+import argparse
+import ctypes
+import os
+import subprocess
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+LIB = os.path.join(ROOT, "tools", "librtf_timing.so")
+SLOTS = ["A scale (+barrier)", "B totals (+barrier)", "C spine (+barrier)",
+         "D0 load+quantise+scan+keys", "D2 cells/lambda/table", "D3 Alg.1 phase 1",
+         "D4 flush", "D tail (barrier wait)", "E cross-tile + runs"]
+
+
+def build():
+    from paper_1901_05423_b200 import _build_lib as b
+    cmd = [b.NVCC, *b.NVCC_FLAGS, "-DRTF_PHASE_TIMING", "-o", LIB, *b.sources()]
+    subprocess.check_call(cmd)
+    print(LIB)
+
+
+def run(reps, workload):
+    import numpy as np
+    import torch
+    import paper_1901_05423_b200 as rtf
+    from paper_1901_05423_b200 import _lib
+    _lib.LIB_PATH = LIB
+    rtf.lib()
+    fn = ctypes.CDLL(LIB).rtf_debug_phase_cycles
+    fn.argtypes = [ctypes.c_void_p, ctypes.c_int, ctypes.c_int]
+    import bench
+    wl = bench.WORKLOADS[workload]
+    p = torch.from_numpy(bench.make_p(wl)).cuda()
+    f = rtf.build(p, wl["m"])
+    torch.cuda.synchronize()
+    rows = 8192
+    buf = np.zeros((rows, 16), np.uint64)
+    fn(buf.ctypes.data, rows, 1)  # reset after warm-up
+    start, stop = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    start.record()
+    for _ in range(reps):
+        f.build(p)
+    stop.record()
+    torch.cuda.synchronize()
+    print(f"{workload}: {start.elapsed_time(stop) / reps * 1e3:.1f} us per build ({reps} builds)")
+    fn(buf.ctypes.data, rows, 0)
+    used = buf[:, :9].sum(axis=1) > 0
+    per = buf[used, :9].astype(np.float64) / reps
+    tot = per.sum(axis=1)
+    print(f"CTAs {used.sum()}, mean cycles per CTA per build {tot.mean():.0f} "
+          f"(min {tot.min():.0f}, max {tot.max():.0f})")
+    for s, name in enumerate(SLOTS):
+        col = per[:, s]
+        print(f"  {name:30s} mean {col.mean():9.0f}  max {col.max():9.0f}  "
+              f"{100 * col.mean() / tot.mean():5.1f} %")
+
+
+if __name__ == "__main__":
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--build", action="store_true")
+    ap.add_argument("--reps", type=int, default=20)
+    ap.add_argument("--workload", default="c3")
+    a = ap.parse_args()
+    if a.build:
+        build()
+    else:
+        run(a.reps, a.workload)
