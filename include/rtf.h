@@ -92,8 +92,8 @@ typedef struct rtf_forest {
 
 /* rtf_build flags */
 #define RTF_BUILD_DEFAULT 0u
-#define RTF_BUILD_SMALL_TILES 1u /* 128-entry tiles: a test/debug schedule that moves most
-                                    merges into the cross-tile phase; same result bytes */
+#define RTF_BUILD_SMALL_TILES 1u /* 256-entry tiles: a test/debug schedule that moves most
+                                    links into the cross-tile phase; same result bytes */
 
 /* ------------------------------------------------------------- sizing */
 
@@ -104,15 +104,10 @@ size_t rtf_forest_bytes(uint32_t n, uint32_t m, uint32_t rows);
 /* Bytes of scratch workspace rtf_build needs for (n, m, flags).  Host only. */
 size_t rtf_workspace_bytes(uint32_t n, uint32_t m, uint32_t flags);
 
-/* Byte offset of Alg. 1's synchronisation array otherBounds inside the
- * workspace: uint64[n], each a deposit {bound (low 32 bits), split level beyond
- * it (high 32 bits)}, all ones (= -1) whenever no build is running.  For tests
- * and debugging only.  Host only. */
-size_t rtf_workspace_sync_offset(uint32_t n, uint32_t m, uint32_t flags);
-
-/* Initialise a workspace once after allocating it (enqueues memsets).  Every
- * rtf_build leaves the workspace initialised again (reset-on-consume of the
- * Alg. 1 synchronisation array), so this is needed only once. */
+/* Initialise a workspace once after allocating it (enqueues a memset of its
+ * counters; Alg. 1's synchronisation array otherBounds, lives in shared
+ * memory per tile).  Every rtf_build leaves it reusable, so this is needed
+ * only once. */
 int rtf_workspace_init(void *ws, size_t ws_bytes, uint32_t n, uint32_t m, uint32_t flags,
                        void *stream);
 
@@ -124,9 +119,12 @@ int rtf_workspace_init(void *ws, size_t ws_bytes, uint32_t n, uint32_t m, uint32
  *   forest_buf / forest_bytes: >= rtf_forest_bytes(n, m, 1), 256-B aligned.
  *   ws / ws_bytes: >= rtf_workspace_bytes(n, m, flags), initialised once.
  *   out (host): receives the view of the forest.
- * Asynchronous: 4 kernels on `stream` (scale, tile totals with decoupled
- * look-back, scan+normalise+in-tile Alg. 1, cross-tile Alg. 1 + table).
- * The result bytes are independent of the schedule and of `flags`. */
+ * Asynchronous: ONE cooperative kernel on `stream` whose phases are separated
+ * by grid barriers (scale; tile totals; tiles: scan + exact normalisation +
+ * cells/split levels/table + Alg. 1 in shared memory; cross-tile links from
+ * the tiles' spines + long table runs).  The result bytes are independent of
+ * the schedule and of `flags`.  Errors in the data (NaN, Inf, negative, all
+ * zero) are reported in header->status (rtf_forest_status), not here. */
 int rtf_build(const float *p, uint32_t n, uint32_t m, uint32_t flags, void *forest_buf,
               size_t forest_bytes, void *ws, size_t ws_bytes, void *stream, rtf_forest *out);
 
@@ -210,24 +208,23 @@ int rtf_sample_host(const rtf_forest *f, const uint32_t *xi_host, uint64_t count
  *      (the cross-GPU scan of per-shard totals: every shard derives its prefix
  *       and the grand total T from the gathered totals, on the device)
  *   3. rtf_shard_build            -> this shard's node records [J_r, J_r + n'_r),
- *      split levels, guide-table cells (others INT32_MIN), pending edge leaves
- *      and leftover deposits
- *   4. replicate records / split levels (broadcast from each owner), MAX-reduce
- *      the table, gather pending leaves and deposit lists
- *   5. rtf_shard_finish           -> cross-tile Alg. 1 over the assembled state;
+ *      guide-table cells (others INT32_MIN) and one spine row per tile
+ *      (view.spine: nt_local rows of view.spine_row_bytes)
+ *   4. replicate records (broadcast from each owner), MAX-reduce the table,
+ *      gather the spine rows of all shards, shard r's at rows
+ *      [r * nt_max, r * nt_max + nt_local_r) (nt_max = the largest nt_local;
+ *      pad with zero bytes: a row with zero leaves is skipped)
+ *   5. rtf_shard_finish           -> the cross-tile links over all rows;
  *      every shard then holds the identical full forest (byte-equal to rtf_build).
  * Each shard owns a forest buffer sized for (n_global, m) and a shard workspace.
  */
 typedef struct rtf_shard_view {  /* device pointers into a shard workspace */
-    uint8_t *lam;        /* n_global split levels, indexed by global leaf index  */
-    void *pend;          /* nt_local x 8 B pending edge leaves {int32 j, int32 ~orig} */
-    void *deps;          /* nt_local x dep_stride x dep_bytes leftover deposits   */
-    uint32_t *ndeps;     /* nt_local deposit counts                              */
-    uint32_t *scale;     /* 4 words {max float bits, nan, inf, negative}          */
-    void *total;         /* 16 B {u64 W, u32 n', i32 last positive index}        */
-    uint32_t nt_local;   /* tiles of this shard                                  */
-    uint32_t dep_stride; /* deposit entries per tile                             */
-    uint32_t dep_bytes;  /* bytes per deposit entry                              */
+    void *spine;              /* nt_local rows of spine_row_bytes (opaque)             */
+    uint32_t *scale;          /* 4 words {max float bits, nan, inf, negative}           */
+    void *total;              /* 16 B {u64 W, u32 n', i32 last positive index}         */
+    uint32_t nt_local;        /* tiles (spine rows) of this shard                      */
+    uint32_t spine_row_bytes; /* bytes per spine row (a multiple of 16)                */
+    uint32_t nt_cap;          /* most rows rtf_shard_finish accepts                    */
     uint32_t reserved;
 } rtf_shard_view;
 
@@ -244,10 +241,11 @@ int rtf_shard_build(const float *p, uint32_t n_local, uint32_t n_global, uint32_
                     uint32_t index_base, uint32_t rank, uint32_t count, const void *totals,
                     void *forest_buf, size_t forest_bytes, void *ws, size_t ws_bytes,
                     void *stream, rtf_forest *out);
-int rtf_shard_finish(uint32_t n_local, uint32_t n_global, uint32_t m, const void *pend_all,
-                     const void *deps_all, const uint32_t *ndeps_all, uint32_t nt_all,
-                     void *forest_buf, size_t forest_bytes, void *ws, size_t ws_bytes,
-                     void *stream, rtf_forest *out);
+/* spine_all: the gathered rows (device, 16-B aligned), nt_all of them
+ * (<= view.nt_cap).  Writes the cross-tile links into this shard's full forest. */
+int rtf_shard_finish(uint32_t n_local, uint32_t n_global, uint32_t m, const void *spine_all,
+                     uint32_t nt_all, void *forest_buf, size_t forest_bytes, void *ws,
+                     size_t ws_bytes, void *stream, rtf_forest *out);
 
 /* ---------------------------------------------------------- utilities */
 

@@ -147,13 +147,6 @@ class Forest:
     def table_numpy(self) -> np.ndarray:
         return self._section(self.view.table, 4 * self.m).cpu().numpy().view(np.int32)
 
-    def other_bounds_numpy(self) -> np.ndarray:
-        """Alg. 1's otherBounds array in the workspace; all -1 between
-        builds (reset-on-consume)."""
-        off = lib().rtf_workspace_sync_offset(self.n, self.m, self.flags)
-        # 64-bit deposits {bound, split level}; all ones (-1) when empty
-        return self._buf.ws[off: off + 8 * self.n].cpu().numpy().view(np.int64)
-
 
 class RowsForest:
     """`rows` independent forests of n_row entries / m_row cells (config 5)."""

@@ -27,10 +27,9 @@ class rtf_forest(ctypes.Structure):
 
 
 class rtf_shard_view(ctypes.Structure):
-    _fields_ = [("lam", ctypes.c_void_p), ("pend", ctypes.c_void_p), ("deps", ctypes.c_void_p),
-                ("ndeps", ctypes.c_void_p), ("scale", ctypes.c_void_p), ("total", ctypes.c_void_p),
-                ("nt_local", ctypes.c_uint32), ("dep_stride", ctypes.c_uint32),
-                ("dep_bytes", ctypes.c_uint32), ("reserved", ctypes.c_uint32)]
+    _fields_ = [("spine", ctypes.c_void_p), ("scale", ctypes.c_void_p), ("total", ctypes.c_void_p),
+                ("nt_local", ctypes.c_uint32), ("spine_row_bytes", ctypes.c_uint32),
+                ("nt_cap", ctypes.c_uint32), ("reserved", ctypes.c_uint32)]
 
 
 # name -> (restype, argtypes)
@@ -41,7 +40,6 @@ _H = ctypes.POINTER(rtf_header)
 PROTOTYPES = {
     "rtf_forest_bytes": (_SZ, [_U32, _U32, _U32]),
     "rtf_workspace_bytes": (_SZ, [_U32, _U32, _U32]),
-    "rtf_workspace_sync_offset": (_SZ, [_U32, _U32, _U32]),
     "rtf_workspace_init": (_I32, [_P, _SZ, _U32, _U32, _U32, _P]),
     "rtf_build": (_I32, [_P, _U32, _U32, _U32, _P, _SZ, _P, _SZ, _P, _F]),
     "rtf_build_rows": (_I32, [_P, _U32, _U32, _U32, _P, _SZ, _P, _F]),
@@ -62,7 +60,7 @@ PROTOTYPES = {
     "rtf_shard_totals": (_I32, [_P, _U32, _U32, _U32, _U32, _P, _SZ, _P]),
     "rtf_shard_build": (_I32, [_P, _U32, _U32, _U32, _U32, _U32, _U32, _P, _P, _SZ, _P, _SZ, _P,
                                _F]),
-    "rtf_shard_finish": (_I32, [_U32, _U32, _U32, _P, _P, _P, _U32, _P, _SZ, _P, _SZ, _P, _F]),
+    "rtf_shard_finish": (_I32, [_U32, _U32, _U32, _P, _U32, _P, _SZ, _P, _SZ, _P, _F]),
     "rtf_launch_count": (_U64, []),
     "rtf_status_string": (ctypes.c_char_p, [_I32]),
     "rtf_version": (ctypes.c_char_p, []),

@@ -76,12 +76,6 @@ size_t rtf_workspace_bytes(uint32_t n, uint32_t m, uint32_t flags) {
     return rtf::build_workspace_layout(n ? n : 1, m ? m : 1, flags, &L);
 }
 
-size_t rtf_workspace_sync_offset(uint32_t n, uint32_t m, uint32_t flags) {
-    rtf::WsLayout L;
-    rtf::build_workspace_layout(n ? n : 1, m ? m : 1, flags, &L);
-    return L.ob;
-}
-
 int rtf_workspace_init(void* ws, size_t ws_bytes, uint32_t n, uint32_t m, uint32_t flags,
                        void* stream) {
     if (!ws) return RTF_EINVAL;
@@ -90,10 +84,9 @@ int rtf_workspace_init(void* ws, size_t ws_bytes, uint32_t n, uint32_t m, uint32
     if (ws_bytes < rtf::build_workspace_layout(n, m, flags, &L)) return RTF_ENOSPACE;
     cudaStream_t st = as_stream(stream);
     unsigned char* w = static_cast<unsigned char*>(ws);
-    // partials, counters (grid barrier word, queue length), prefixes, pending leaves
-    cudaError_t e = cudaMemsetAsync(w, 0, L.ob, st);
-    // otherBounds: 64-bit {bound, split level} deposits, all ones = empty
-    if (e == cudaSuccess) e = cudaMemsetAsync(w + L.ob, 0xFF, sizeof(uint64_t) * (size_t)n, st);
+    // partials, counters (the grid barrier word must start at 0), prefixes;
+    // the rest is written by every build before it is read
+    const cudaError_t e = cudaMemsetAsync(w, 0, L.spine, st);
     return e == cudaSuccess ? RTF_OK : RTF_ECUDA;
 }
 
@@ -340,10 +333,7 @@ int rtf_shard_workspace_init(void* ws, size_t ws_bytes, uint32_t n_local, uint32
     if (int s = shard_layout(ws, ws_bytes, n_local, n_global, m, &L)) return s;
     unsigned char* w = static_cast<unsigned char*>(ws);
     cudaStream_t st = as_stream(stream);
-    cudaError_t e = cudaMemsetAsync(w, 0, L.ob, st);
-    if (e == cudaSuccess)
-        e = cudaMemsetAsync(w + L.ob, 0xFF, sizeof(uint64_t) * (size_t)n_global, st);
-    if (e == cudaSuccess) e = cudaMemsetAsync(w + L.pend, 0xFF, L.ndeps - L.pend, st);
+    const cudaError_t e = cudaMemsetAsync(w, 0, L.spine, st);
     return e == cudaSuccess ? RTF_OK : RTF_ECUDA;
 }
 
@@ -353,15 +343,13 @@ int rtf_shard_get_view(void* ws, size_t ws_bytes, uint32_t n_local, uint32_t n_g
     if (!out) return RTF_EINVAL;
     if (int s = shard_layout(ws, ws_bytes, n_local, n_global, m, &L)) return s;
     unsigned char* w = static_cast<unsigned char*>(ws);
-    out->lam = w + L.lam;
-    out->pend = w + L.pend;
-    out->deps = w + L.deps;
-    out->ndeps = reinterpret_cast<uint32_t*>(w + L.ndeps);
+    out->spine = w + L.spine;
     out->scale = reinterpret_cast<uint32_t*>(w + L.scale);
     out->total = w + L.total;
     out->nt_local = L.nt;
-    out->dep_stride = (uint32_t)rtf::shard_deps_per_tile();
-    out->dep_bytes = (uint32_t)rtf::shard_dep_bytes();
+    out->spine_row_bytes = (uint32_t)rtf::spine_row_bytes();
+    out->nt_cap = L.nt_cap;
+    out->reserved = 0;
     return RTF_OK;
 }
 
@@ -370,7 +358,7 @@ int rtf_shard_scale(const float* p, uint32_t n_local, uint32_t n_global, uint32_
     rtf::WsLayout L;
     if (!p || ((uintptr_t)p & 3u)) return RTF_EINVAL;
     if (int s = shard_layout(ws, ws_bytes, n_local, n_global, m, &L)) return s;
-    rtf::ShardCall sc{rtf::kPhScale, n_global, 0, 0, 1, 0, nullptr, nullptr, nullptr, nullptr};
+    rtf::ShardCall sc{rtf::kPhScale, n_global, 0, 0, 1, 0, nullptr, nullptr};
     int launches = 0;
     cudaError_t e = rtf::launch_build(p, n_local, m, rtf::kBuildShardedLayout, nullptr, nullptr,
                                       nullptr, nullptr, ws, L, as_stream(stream), &launches, &sc);
@@ -384,7 +372,7 @@ int rtf_shard_totals(const float* p, uint32_t n_local, uint32_t n_global, uint32
     if (int s = shard_layout(ws, ws_bytes, n_local, n_global, m, &L)) return s;
     if ((uint64_t)index_base + n_local > n_global) return RTF_EINVAL;
     rtf::ShardCall sc{rtf::kPhTotals | rtf::kPhSpine, n_global, index_base, 0, 1, 0,
-                      nullptr, nullptr, nullptr, nullptr};
+                      nullptr, nullptr};
     int launches = 0;
     cudaError_t e = rtf::launch_build(p, n_local, m, rtf::kBuildShardedLayout, nullptr, nullptr,
                                       nullptr, nullptr, ws, L, as_stream(stream), &launches, &sc);
@@ -401,7 +389,7 @@ int rtf_shard_build(const float* p, uint32_t n_local, uint32_t n_global, uint32_
     if ((uint64_t)index_base + n_local > n_global) return RTF_EINVAL;
     if (int s = rtf_forest_view(forest_buf, forest_bytes, n_global, m, 1, out)) return s;
     rtf::ShardCall sc{rtf::kPhTiles | rtf::kPhRuns, n_global, index_base, rank, count, 0,
-                      totals, nullptr, nullptr, nullptr};
+                      totals, nullptr};
     int launches = 0;
     cudaError_t e =
         rtf::launch_build(p, n_local, m, rtf::kBuildShardedLayout, out->header, out->nodes,
@@ -409,16 +397,15 @@ int rtf_shard_build(const float* p, uint32_t n_local, uint32_t n_global, uint32_
     return finish(e, launches);
 }
 
-int rtf_shard_finish(uint32_t n_local, uint32_t n_global, uint32_t m, const void* pend_all,
-                     const void* deps_all, const uint32_t* ndeps_all, uint32_t nt_all,
-                     void* forest_buf, size_t forest_bytes, void* ws, size_t ws_bytes,
-                     void* stream, rtf_forest* out) {
+int rtf_shard_finish(uint32_t n_local, uint32_t n_global, uint32_t m, const void* spine_all,
+                     uint32_t nt_all, void* forest_buf, size_t forest_bytes, void* ws,
+                     size_t ws_bytes, void* stream, rtf_forest* out) {
     rtf::WsLayout L;
-    if (!pend_all || !deps_all || !ndeps_all) return RTF_EINVAL;
+    if (!spine_all || ((uintptr_t)spine_all & 15u)) return RTF_EINVAL;
     if (int s = shard_layout(ws, ws_bytes, n_local, n_global, m, &L)) return s;
+    if (nt_all > L.nt_cap) return RTF_EINVAL;
     if (int s = rtf_forest_view(forest_buf, forest_bytes, n_global, m, 1, out)) return s;
-    rtf::ShardCall sc{rtf::kPhScatter | rtf::kPhWalk, n_global, 0, 0, 1, nt_all,
-                      nullptr, pend_all, deps_all, ndeps_all};
+    rtf::ShardCall sc{rtf::kPhCross, n_global, 0, 0, 1, nt_all, nullptr, spine_all};
     int launches = 0;
     // any valid p pointer is fine: phases A-D do not run
     const float* dummy = reinterpret_cast<const float*>(ws);

@@ -39,17 +39,27 @@ struct RunChunk {
     uint32_t pad;
 };
 
-struct PendingLeaf {
-    int32_t j;    // compacted leaf index, -1 if none
-    int32_t ref;  // ~orig(j)
+// What phase 1 leaves open in a tile, for the cross-tile links (phase E).
+// The tile's split levels lambda_0..lambda_{cnt-1} (gap l lies between leaves
+// l and l+1; the last one reaches the next tile's first leaf) have a left
+// spine -- the strict prefix maxima -- and a right spine -- the strict suffix
+// maxima.  Exactly the spine gaps (and the tile's first leaf) have a parent
+// outside what phase 1 can see; every other node was linked in the tile.
+// Along the left spine lambda increases, along the right spine it decreases,
+// so each spine is a set of distinct split levels: a mask plus the local gap
+// index per level.  lambda = 64 (a cell boundary) is a wall: it needs no parent.
+struct TileSpine {
+    unsigned long long mL, mR;  // split levels 0..63 on the left / right spine
+    uint32_t j0, cnt;           // global index of the tile's first leaf; leaves
+    uint32_t walls;             // bit 0: a wall on the left spine; bit 1: on the right
+    int32_t c0_next;            // left child of the last gap, linked in the tile (kNoLink: none)
+    int32_t ref0;               // ~orig of the tile's first leaf
+    uint32_t pad[3];
+    uint16_t iL[65], iR[65];    // local gap index per split level (where the mask is set)
+    uint32_t pad2[3];
 };
-
-constexpr uint32_t kDepsPerTile = 128;  // leftover deposits of a tile: <= 2 x 64 ancestors
-
-struct ShardDep {
-    uint32_t slot, pad;
-    unsigned long long value;
-};
+static_assert(sizeof(TileSpine) % 16 == 0, "TileSpine rows stay 16-B aligned");
+constexpr int32_t kNoLink = INT32_MIN;
 
 struct BuildArgs {
     const float* p;
@@ -61,20 +71,17 @@ struct BuildArgs {
     const Pfx* shard_totals;   // sharded: every shard's total, shard_count entries
     uint32_t shard_rank, shard_count;
     Pfx* total_out;            // sharded: this shard's total
-    ShardDep* deps;            // sharded: leftover deposits, kDepsPerTile per tile
-    uint32_t* ndeps;           // sharded: count per tile
-    const ShardDep* deps_in;   // sharded finish: all shards' deposits (ndeps_in[t] per tile)
-    const uint32_t* ndeps_in;
-    uint32_t nt_in;            // sharded finish: number of tiles in pend / deps_in
+    TileSpine* spine;          // phase D: one row per tile of this call
+    const TileSpine* spine_in; // phase E: the rows to link (a sharded finish: all shards')
+    uint32_t nt_in;            // rows in spine_in
+    uint8_t* tmax;             // phase E: per row, 1 + the largest split level (0: empty)
+    uint32_t* bmax;            // phase E: per 64 rows, the maximum of tmax
     uint32_t* maxpart;  // 2 per CTA
     uint32_t* counters;
     Pfx* excl;          // per tile: aggregate (phase B), then exclusive prefix (phase C)
     rtf_header* hdr;
     rtf_node* nodes;
     int32_t* table;
-    uint8_t* lam;                 // global split levels (phase E)
-    unsigned long long* ob;       // global otherBounds: {bound, lambda} or ~0
-    PendingLeaf* pend;            // 2 per tile
     RunChunk* queue;
     uint32_t qcap;
     uint64_t* cdf;                // CDF mode only
@@ -159,7 +166,7 @@ __device__ __forceinline__ uint32_t pad8(uint32_t j) { return j + (j >> 3); }
 
 template <int THREADS, int VPT>
 __host__ __device__ constexpr size_t tile_padded() {
-    return (size_t)THREADS * VPT + (size_t)THREADS * VPT / 8;
+    return (size_t)THREADS * VPT + (size_t)THREADS * VPT / 8 + 4;  // + slot pad8(TILE)
 }
 
 template <int THREADS, int VPT>
@@ -192,6 +199,73 @@ __device__ __noinline__ void table_runs(int32_t* __restrict__ table, uint32_t m,
         rc.pad = 0;
         queue[q + c] = rc;
     }
+}
+
+// ------------------------------------------------------------ phase E helpers
+
+// smallest split level above v on a spine (levels 0..63 in m, the wall 64 in
+// wall); 0xff if none.  v in [0, 63].
+__device__ __forceinline__ uint32_t spine_above(unsigned long long m, bool wall, uint32_t v) {
+    const unsigned long long x = v >= 63 ? 0ull : (m & (~0ull << (v + 1)));
+    return x ? (uint32_t)(__ffsll((long long)x) - 1) : (wall ? 64u : 0xffu);
+}
+
+// lowest split level on a spine: lambda of the tile's first gap (left spine)
+// or of its last gap (right spine)
+__device__ __forceinline__ uint32_t spine_lowest(unsigned long long m, bool wall) {
+    return m ? (uint32_t)(__ffsll((long long)m) - 1) : (wall ? 64u : 0xffu);
+}
+
+// position of the k-th (0-based) set bit
+__device__ __forceinline__ uint32_t nth_bit(unsigned long long m, uint32_t k) {
+    for (uint32_t i = 0; i < k; ++i) m &= m - 1;
+    return (uint32_t)(__ffsll((long long)m) - 1);
+}
+
+// the 64 rows of block bb whose tmax exceeds thr, as a bit mask
+__device__ __forceinline__ unsigned long long block_rows_above(const uint8_t* tmax, uint32_t bb,
+                                                               uint32_t thr) {
+    const uint4* p4 = reinterpret_cast<const uint4*>(tmax + 64ull * bb);
+    const uint32_t t4 = thr * 0x01010101u;
+    unsigned long long mask = 0;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        const uint4 v = __ldcg(p4 + i);
+        const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {  // byte flags 0x80 -> one nibble
+            const uint32_t c = __vcmpgtu4(w[k], t4) & 0x80808080u;
+            mask |= (unsigned long long)((c * 0x00204081u) >> 28) << (16 * i + 4 * k);
+        }
+    }
+    return mask;
+}
+
+// nearest row u < t (u > t) whose tmax exceeds thr; -1 if none
+__device__ int32_t row_left(const uint8_t* tmax, const uint32_t* bmax, uint32_t t, uint32_t thr) {
+    if (t == 0) return -1;
+    if (__ldcg(tmax + t - 1) > thr) return (int32_t)t - 1;
+    const uint32_t bb = t >> 6;
+    const unsigned long long mk = block_rows_above(tmax, bb, thr) & ((1ull << (t & 63)) - 1);
+    if (mk) return (int32_t)(64 * bb + 63 - __clzll((long long)mk));
+    for (int32_t c = (int32_t)bb - 1; c >= 0; --c)
+        if (__ldcg(bmax + c) > thr)
+            return 64 * c + 63 - __clzll((long long)block_rows_above(tmax, (uint32_t)c, thr));
+    return -1;
+}
+
+__device__ int32_t row_right(const uint8_t* tmax, const uint32_t* bmax, uint32_t nrows, uint32_t t,
+                             uint32_t thr) {
+    if (t + 1 >= nrows) return -1;
+    if (__ldcg(tmax + t + 1) > thr) return (int32_t)t + 1;
+    const uint32_t bb = t >> 6, sh = (t & 63) + 1;
+    const unsigned long long mk = sh >= 64 ? 0ull : (block_rows_above(tmax, bb, thr) & (~0ull << sh));
+    if (mk) return (int32_t)(64 * bb + __ffsll((long long)mk) - 1);
+    const uint32_t nb = (nrows + 63) / 64;
+    for (uint32_t c = bb + 1; c < nb; ++c)
+        if (__ldcg(bmax + c) > thr)
+            return (int32_t)(64 * c + __ffsll((long long)block_rows_above(tmax, c, thr)) - 1);
+    return -1;
 }
 
 // ------------------------------------------------------------ phase timing (debug builds)
@@ -238,6 +312,10 @@ __global__ void __launch_bounds__(THREADS, MINB) k_build(BuildArgs A) {
     __shared__ Pfx s_grp[THREADS];  // exclusive prefix of each group of `per` tiles
     __shared__ Pfx s_tot, s_pre;
     __shared__ uint64_t s_recip;
+    __shared__ unsigned long long s_mL, s_mR;  // this tile's spines (TileSpine)
+    __shared__ uint32_t s_walls;
+    __shared__ int32_t s_ref0;
+    __shared__ uint16_t s_iL[65], s_iR[65];
 
     const uint32_t G = gridDim.x, b = blockIdx.x, tid = threadIdx.x;
     const uint32_t n = A.n, m = A.m, nt = A.nt;
@@ -257,13 +335,23 @@ __global__ void __launch_bounds__(THREADS, MINB) k_build(BuildArgs A) {
         A.counters[kCtrTile] = 0;  // phase D's tile dispenser (a grid barrier precedes D)
     }
     if (ph & kPhScale) {
-        uint32_t mx = 0, fl = 0;
+        // Fast path: two integer maxima of the raw bits.  As signed integers the
+        // positive finite floats order like their values and stay below +Inf
+        // (0x7f800000); as unsigned integers anything with the sign bit set
+        // exceeds 0x80000000 (-0.0) -- so valid data (no NaN, Inf or negative
+        // value) is exactly smax < 0x7f800000 and umax <= 0x80000000, and then
+        // max(smax, 0) is the bit pattern of the largest weight.  A CTA whose
+        // share is not valid rescans it classifying every value (error path).
+        int32_t smax = 0;
+        uint32_t umax = 0;
         auto visit = [&](float x) {
-            const uint32_t bits = __float_as_uint(x);
-            if (x != x) fl |= RTF_DATA_NAN;
-            else if (fabsf(x) == __int_as_float(0x7f800000)) fl |= RTF_DATA_INF;
-            else if (x < 0.0f) fl |= RTF_DATA_NEG;
-            else if (x > 0.0f) mx = max(mx, bits);
+            smax = max(smax, __float_as_int(x));
+            umax = max(umax, __float_as_uint(x));
+        };
+        auto classify = [&](float x, uint32_t& f) {
+            if (x != x) f |= RTF_DATA_NAN;
+            else if (fabsf(x) == __int_as_float(0x7f800000)) f |= RTF_DATA_INF;
+            else if (x < 0.0f) f |= RTF_DATA_NEG;
         };
         const uint32_t gs = G * THREADS, gt = b * THREADS + tid;
         if (A.vec) {
@@ -291,6 +379,26 @@ __global__ void __launch_bounds__(THREADS, MINB) k_build(BuildArgs A) {
             for (uint32_t i = 4 * n4 + gt; i < n; i += gs) visit(A.p[i]);
         } else {
             for (uint32_t i = gt; i < n; i += gs) visit(A.p[i]);
+        }
+        uint32_t mx = (uint32_t)smax, fl = (smax >= 0x7f800000 || umax > 0x80000000u) ? 1u : 0u;
+        block_max_or<THREADS>(mx, fl, s_red);
+        if (fl) {  // invalid data somewhere in this CTA's share: exact flags
+            fl = 0;
+            if (A.vec) {
+                const uint32_t n4 = n >> 2;
+                for (uint32_t q = gt; q < n4; q += gs) {
+                    const float4 v = ld_stream_f4(A.p + 4ull * q);
+                    classify(v.x, fl);
+                    classify(v.y, fl);
+                    classify(v.z, fl);
+                    classify(v.w, fl);
+                }
+                for (uint32_t i = 4 * n4 + gt; i < n; i += gs) classify(A.p[i], fl);
+            } else {
+                for (uint32_t i = gt; i < n; i += gs) classify(A.p[i], fl);
+            }
+            uint32_t dummy = 0;
+            block_max_or<THREADS>(dummy, fl, s_red);
         }
         block_max_or<THREADS>(mx, fl, s_red);
         if (tid == 0) {
@@ -326,7 +434,7 @@ __global__ void __launch_bounds__(THREADS, MINB) k_build(BuildArgs A) {
         return;
     }
     const int E = floor_log2_bits(mx);
-    const double scale = pow2_f64(A.B - E);
+    const QScale scale = qscale(A.B - E);
 
     // ---------------------------------------------------------- B: tile totals
     // two tiles per step so each thread has 2*VPT/4 float4 loads in flight
@@ -442,7 +550,7 @@ __global__ void __launch_bounds__(THREADS, MINB) k_build(BuildArgs A) {
         __syncthreads();
         total = s_tot;
     }
-    if (sharded && !(ph & (kPhTiles | kPhWalk | kPhScatter))) return;  // totals launch ends here
+    if (sharded && !(ph & (kPhTiles | kPhCross))) return;  // totals launch ends here
     RTF_TICK(2);
 
     // sharded: the exclusive prefix of this shard and the grand total come from
@@ -533,6 +641,10 @@ __global__ void __launch_bounds__(THREADS, MINB) k_build(BuildArgs A) {
     // zero fraction and the tree shape): CTA b starts with tile b, then takes
     // G + the next ticket; the ticket is drawn early so TMA can prefetch it
     uint32_t phase = 0;
+    if (tid == 0) {
+        s_mL = s_mR = 0ull;
+        s_walls = 0u;
+    }
     if ((ph & kPhTiles) && warp == 0 && b < nt) {
         const Pfx p0 = tile_prefix(b);
         if (lane == 0) s_pre = p0;
@@ -605,13 +717,11 @@ __global__ void __launch_bounds__(THREADS, MINB) k_build(BuildArgs A) {
                 W += w[k];
             }
         }
-        // the tile's first and last leaf stay pending for phase 2 (E)
-        if (tc && c_ex == 0)
-            A.pend[2 * t] = PendingLeaf{(int32_t)j0, ~((int32_t)(first + __ffs(posmask) - 1) + ib)};
-        if (tc && c_ex + tc == cnt)
-            A.pend[2 * t + 1] = cnt >= 2 ? PendingLeaf{(int32_t)(j0 + cnt - 1), ~tl}
-                                         : PendingLeaf{-1, 0};
-        if (cnt == 0 && tid == 0) A.pend[2 * t] = A.pend[2 * t + 1] = PendingLeaf{-1, 0};
+        // the tile's first leaf is linked in phase E (its left split level
+        // belongs to the previous tile); the slot after the last leaf collects
+        // the left child of the last gap, if phase 1 links it
+        if (tc && c_ex == 0) s_ref0 = ~((int32_t)(first + __ffs(posmask) - 1) + ib);
+        if (tid == 0) s_c0[pad8(cnt)] = kNoLink;
         if (tid == THREADS - 1) {  // key of the first leaf after the tile (or "1")
             const uint64_t We = pre.W + w_tot;
             s_key_after = (We == T) ? kOne63 : fixed_point(We, nm);
@@ -645,21 +755,22 @@ __global__ void __launch_bounds__(THREADS, MINB) k_build(BuildArgs A) {
         __syncthreads();
 
         RTF_TICK(4);
-        // (3) phase 1: Alg. 1 for the tile's interior leaves 1..cnt-2 with
-        // shared-memory atomicExch.  A range that would contain the pending
-        // first/last leaf can never complete here, so every range stays in
-        // [1, cnt-2] and every parent slot in [1, cnt-1] -- inside the tile.
-        // Each lane walks its own leaves back to back.  A cell root (lambda =
-        // 64 on both sides) is the right child of its anchor lo and needs no
-        // exchange.  A deposit is (lambda beyond the bound) << 16 | bound.
+        // (3) phase 1: Alg. 1 for the tile's leaves 1..cnt-1 with shared-memory
+        // atomicExch.  A range containing leaf 0 (whose left split level is
+        // the previous tile's) never completes here; a range ending at the
+        // last leaf may still become the left child of the last gap, whose
+        // slot is cnt.  Every parent slot is in [1, cnt].  What stays open
+        // (first arrivals without a sibling in the tile) is exactly what the
+        // spines describe; those deposits are dropped.  Each lane walks its
+        // own leaves back to back.  A cell root (lambda = 64 on both sides) is
+        // the right child of its anchor lo and needs no exchange.  A deposit
+        // is (lambda beyond the bound) << 16 | bound.
         {
-            const uint32_t a_c0 = smem_u32(s_c0), a_c1 = smem_u32(s_c1);
-            const uint32_t a_ob = smem_u32(s_ob), a_lam = smem_u32(s_lam);
             // Stage A: the FIRST step of every own interior leaf, straight-line
             // (half of all merge steps, without loop or divergence overhead).
             // Leaf of rank r is l = c_ex + r; its split levels come from
             // registers (lambda[l-1] of rank 0 from the previous thread).
-            const uint32_t lam_prev = c_ex ? lds_u8(a_lam + pad8(c_ex - 1)) : kLamBoundary;
+            const uint32_t lam_prev = c_ex ? (uint32_t)s_lam[pad8(c_ex - 1)] : kLamBoundary;
             uint32_t contw[VPT];  // second arrivals: the sibling's packed deposit
             uint32_t pend = 0, rightbits = 0;
             {
@@ -671,20 +782,19 @@ __global__ void __launch_bounds__(THREADS, MINB) k_build(BuildArgs A) {
                         const uint32_t k = __ffs(mask) - 1;
                         mask &= mask - 1;
                         const uint32_t l = c_ex + r;
-                        if (l >= 1 && l + 1 < cnt) {
+                        if (l >= 1) {
                             const uint32_t lamL =
                                 r ? (uint32_t)(lampack >> (8 * (r - 1))) & 0xffu : lam_prev;
                             const uint32_t lamR = (uint32_t)(lampack >> (8 * r)) & 0xffu;
                             const bool right = lamL <= lamR;
                             const bool root = (lamL & lamR & kLamBoundary) != 0;
-                            const uint32_t q4 = 4 * pad8(right ? l : l + 1);
-                            sts_u32((right ? a_c1 : a_c0) + q4,
-                                    (uint32_t)~((int32_t)(first + k) + ib));
+                            const uint32_t q = pad8(right ? l : l + 1);
+                            s_c0[q + (right ? P : 0)] = ~((int32_t)(first + k) + ib);
                             if (!root) {
-                                const int32_t other = atoms_exch(
-                                    a_ob + q4, (int32_t)((right ? lamR : lamL) << 16 | l));
+                                const int32_t other = atomicExch(
+                                    &s_ob[q], (int32_t)((right ? lamR : lamL) << 16 | l));
                                 if (other >= 0) {
-                                    sts_u32(a_ob + q4, 0xffffffffu);  // reset-on-consume
+                                    s_ob[q] = -1;  // reset-on-consume
                                     contw[r] = (uint32_t)other;
                                     pend |= 1u << r;
                                     rightbits |= (right ? 1u : 0u) << r;
@@ -730,14 +840,14 @@ __global__ void __launch_bounds__(THREADS, MINB) k_build(BuildArgs A) {
                     const bool right = lamL <= lamR;  // Alg. 1: child 1 unless left is farther
                     const bool root = (lamL & lamR & kLamBoundary) != 0;
                     const int32_t parent = right ? lo : hi + 1;
-                    const uint32_t q4 = 4 * pad8((uint32_t)parent);
-                    sts_u32((right ? a_c1 : a_c0) + q4, (uint32_t)node);
+                    const uint32_t q = pad8((uint32_t)parent);
+                    s_c0[q + (right ? P : 0)] = node;
                     const int32_t dep = right ? (int32_t)(lamR << 16 | (uint32_t)hi)
                                               : (int32_t)(lamL << 16 | (uint32_t)lo);
-                    const int32_t other = root ? -1 : atoms_exch(a_ob + q4, dep);
+                    const int32_t other = root ? -1 : atomicExch(&s_ob[q], dep);
                     active = other >= 0;  // first to arrive (or a root): stop
                     if (active) {
-                        sts_u32(a_ob + q4, 0xffffffffu);  // reset-on-consume
+                        s_ob[q] = -1;  // reset-on-consume
                         const int32_t bound = other & 0xffff;
                         const uint32_t lv = (uint32_t)other >> 16;
                         lo = right ? bound : lo;
@@ -752,25 +862,58 @@ __global__ void __launch_bounds__(THREADS, MINB) k_build(BuildArgs A) {
         __syncthreads();
 
         RTF_TICK(5);
-        // (4) flush: leftover deposits first, then the next tile's TMA copy can
-        // reuse the buffer while records (coalesced 16 B) and split levels go out
-        if (sharded && tid == 0) s_red[0] = 0;
-        if (sharded) __syncthreads();
-        for (uint32_t l = 1 + tid; l < cnt; l += THREADS) {
-            const int32_t o = s_ob[pad8(l)];
-            if (o >= 0) {
-                const unsigned long long v = ((unsigned long long)((uint32_t)o >> 16) << 32) |
-                                             (uint32_t)(j0 + (o & 0xffff));
-                A.ob[j0 + l] = v;
-                if (sharded) {  // also listed, so every shard can replay it before phase 2
-                    const uint32_t k = atomicAdd(&s_red[0], 1u);
-                    if (k < kDepsPerTile) A.deps[t * kDepsPerTile + k] = ShardDep{j0 + l, 0u, v};
+        // (4) the spines of the tile (TileSpine): strict prefix / suffix maxima
+        // of its split levels, from a block-wide exclusive max-scan of the
+        // per-thread maxima in both directions
+        {
+            int32_t tm = -1;
+#pragma unroll
+            for (int r = 0; r < VPT; ++r)
+                if ((uint32_t)r < tc) tm = max(tm, (int32_t)((lampack >> (8 * r)) & 0xffu));
+            int32_t ip = tm, is = tm;
+#pragma unroll
+            for (int d = 1; d < 32; d <<= 1) {
+                const int32_t a = __shfl_up_sync(0xffffffffu, ip, d);
+                const int32_t c = __shfl_down_sync(0xffffffffu, is, d);
+                if (lane >= d) ip = max(ip, a);
+                if (lane + d < 32) is = max(is, c);
+            }
+            const int32_t ip1 = __shfl_up_sync(0xffffffffu, ip, 1);
+            const int32_t is1 = __shfl_down_sync(0xffffffffu, is, 1);
+            int32_t* s_wm = reinterpret_cast<int32_t*>(s_red);
+            if (lane == 31) s_wm[warp] = ip;  // warp maximum
+            __syncthreads();
+            int32_t runL = lane ? ip1 : -1, runR = lane < 31 ? is1 : -1;
+#pragma unroll
+            for (int w = 0; w < NW; ++w) {
+                const int32_t v = s_wm[w];
+                if (w < warp) runL = max(runL, v);
+                if (w > warp) runR = max(runR, v);
+            }
+#pragma unroll
+            for (int r = 0; r < VPT; ++r) {
+                const int32_t lv = (int32_t)((lampack >> (8 * r)) & 0xffu);
+                if ((uint32_t)r < tc && lv > runL) {
+                    runL = lv;
+                    s_iL[lv] = (uint16_t)(c_ex + r);
+                    if (lv < 64) atomicOr(&s_mL, 1ull << lv);
+                    else atomicOr(&s_walls, 1u);
+                }
+            }
+#pragma unroll
+            for (int r = VPT - 1; r >= 0; --r) {
+                const int32_t lv = (int32_t)((lampack >> (8 * r)) & 0xffu);
+                if ((uint32_t)r < tc && lv > runR) {
+                    runR = lv;
+                    s_iR[lv] = (uint16_t)(c_ex + r);
+                    if (lv < 64) atomicOr(&s_mR, 1ull << lv);
+                    else atomicOr(&s_walls, 2u);
                 }
             }
         }
-        __syncthreads();
-        if (sharded && tid == 0) A.ndeps[t] = min(s_red[0], kDepsPerTile);
-        if (warp == 0) {  // next tile: ticket, TMA prefetch, prefix
+        // (5) the next tile: ticket, TMA prefetch into the consumed weight
+        // buffer (otherBounds is no longer read), prefix
+        if (warp == 0) {
             uint32_t nx = 0;
             if (lane == 0) {
                 nx = G + atomicAdd(&A.counters[kCtrTile], 1u);
@@ -787,6 +930,7 @@ __global__ void __launch_bounds__(THREADS, MINB) k_build(BuildArgs A) {
                 s_pre = pn;
             }
         }
+        // (6) node records, coalesced 16 B
         {
             uint4* gnode = reinterpret_cast<uint4*>(A.nodes + j0);
             for (uint32_t l = tid; l < cnt; l += THREADS) {
@@ -794,56 +938,132 @@ __global__ void __launch_bounds__(THREADS, MINB) k_build(BuildArgs A) {
                 const uint64_t key = s_key[q];
                 gnode[l] = make_uint4((uint32_t)key, (uint32_t)(key >> 32), (uint32_t)s_c0[q],
                                       (uint32_t)s_c1[q]);
-                A.lam[j0 + l] = s_lam[q];
             }
         }
-        __syncthreads();  // keys, children and split levels are free for the next tile
+        __syncthreads();  // spines complete; keys and children are free
+        {
+            TileSpine* row = A.spine + t;
+            for (uint32_t u = tid; u < 65; u += THREADS) {
+                row->iL[u] = s_iL[u];
+                row->iR[u] = s_iR[u];
+            }
+            if (tid == 0) {
+                row->mL = s_mL;
+                row->mR = s_mR;
+                row->j0 = j0;
+                row->cnt = cnt;
+                row->walls = s_walls;
+                row->c0_next = cnt ? s_c0[pad8(cnt)] : kNoLink;
+                row->ref0 = cnt ? s_ref0 : 0;
+                s_mL = s_mR = 0ull;  // the next tile's atomics follow its scan barriers
+                s_walls = 0u;
+            }
+        }
+        // no barrier here: the next tile writes shared memory only after its scan
         RTF_TICK(6);
     }
     grid_barrier(gbar);
     RTF_TICK(7);
 
-    // sharded finish: replay every shard's leftover deposits into otherBounds
-    if (ph & kPhScatter) {
-        for (uint32_t t = b; t < A.nt_in; t += G)
-            for (uint32_t k = tid; k < __ldcg(&A.ndeps_in[t]); k += THREADS) {
-                const ShardDep d = A.deps_in[t * kDepsPerTile + k];
-                A.ob[d.slot] = d.value;
+    // ---------------------------------------------------------- E: cross-tile links
+    // Phase 1 linked every node whose parent lies in its tile.  The rest --
+    // the spine gaps and each tile's first leaf -- take the parent Alg. 1
+    // gives them: of the nearest greater split levels on either
+    // side, the smaller one (ties only between two walls: a cell root, the
+    // right child of its anchor).  The tree is unique, so this is the forest
+    // the bottom-up merge builds; the neighbours come from the rows' spines.
+    if (ph & kPhCross) {
+        const TileSpine* SP = A.spine_in;
+        const uint32_t NR = A.nt_in, NB = (NR + 63) / 64;
+        // E0: per row 1 + its largest split level (0: no leaves); per 64 rows the max
+        for (uint32_t bb = b * NW + warp; bb < NB; bb += G * NW) {
+            uint32_t mx = 0;
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                const uint32_t u = 64 * bb + 32 * h + lane;
+                uint32_t e = 0;
+                if (u < NR && __ldcg(&SP[u].cnt))
+                    e = (__ldcg(&SP[u].walls) & 1u)
+                            ? 65u
+                            : 64u - (uint32_t)__clzll((long long)__ldcg(&SP[u].mL));
+                A.tmax[u] = (uint8_t)e;
+                mx = max(mx, e);
             }
+            mx = __reduce_max_sync(0xffffffffu, mx);
+            if (lane == 0) A.bmax[bb] = mx;
+        }
         grid_barrier(gbar);
-    }
-
-    // ---------------------------------------------------------- E: cross-tile Alg. 1
-    const uint32_t npend = (ph & kPhScatter) ? 2 * A.nt_in : 2 * nt;
-    for (uint32_t pi = b * THREADS + tid; (ph & kPhWalk) && pi < npend; pi += G * THREADS) {
-        const PendingLeaf pl = A.pend[pi];
-        if (pl.j < 0) continue;
-        int32_t lo = pl.j, hi = pl.j, node = pl.ref;
-        uint32_t lamL = lo ? __ldcg(A.lam + lo - 1) : kLamBoundary;
-        uint32_t lamR = __ldcg(A.lam + hi);
-        while (true) {
-            const bool right = lamL <= lamR;
-            const int32_t parent = right ? lo : hi + 1;
-            A.nodes[parent].child[right ? 1 : 0] = node;
-            if (lamL & lamR & kLamBoundary) break;  // cell root: right child of its anchor
-            const unsigned long long dep =
-                right ? ((unsigned long long)lamR << 32 | (uint32_t)hi)
-                      : ((unsigned long long)lamL << 32 | (uint32_t)lo);
-            const unsigned long long o = atomicExch(&A.ob[parent], dep);
-            if (o == ~0ull) break;  // first to arrive
-            A.ob[parent] = ~0ull;   // reset-on-consume
-            const int32_t bound = (int32_t)(uint32_t)o;
-            // a sibling's bound always extends the range; anything else means an
-            // uninitialised workspace -- stop instead of wandering
-            if (right ? bound >= lo : bound <= hi) break;
-            if (right) {
-                lo = bound;
-                lamL = (uint32_t)(o >> 32);
-            } else {
-                hi = bound;
-                lamR = (uint32_t)(o >> 32);
+        // E1: one warp per row; lane e links entry e
+        auto far_left = [&](uint32_t t, uint32_t v, uint32_t& lam, int32_t& gap) {
+            const int32_t u = row_left(A.tmax, A.bmax, t, v + 1);
+            lam = 64u;
+            gap = -1;  // the start of the array: a wall
+            if (u >= 0) {
+                const TileSpine* U = SP + u;
+                lam = spine_above(__ldcg(&U->mR), __ldcg(&U->walls) & 2u, v);
+                gap = (int32_t)(__ldcg(&U->j0) + __ldcg(&U->iR[lam]));
             }
-            node = parent;
+        };
+        auto far_right = [&](uint32_t t, uint32_t v, uint32_t& lam, int32_t& gap) {
+            const int32_t u = row_right(A.tmax, A.bmax, NR, t, v + 1);
+            lam = 0xffu;  // cannot happen: the last gap of the array is a wall
+            gap = INT32_MAX;
+            if (u >= 0) {
+                const TileSpine* U = SP + u;
+                lam = spine_above(__ldcg(&U->mL), __ldcg(&U->walls) & 1u, v);
+                gap = (int32_t)(__ldcg(&U->j0) + __ldcg(&U->iL[lam]));
+            }
+        };
+        for (uint32_t t = b * NW + warp; t < NR; t += G * NW) {
+            const TileSpine* S = SP + t;
+            const uint32_t cnt = __ldcg(&S->cnt);
+            if (!cnt) continue;
+            const uint32_t j0 = __ldcg(&S->j0), walls = __ldcg(&S->walls);
+            const unsigned long long mL = __ldcg(&S->mL), mR = __ldcg(&S->mR);
+            const bool wL = walls & 1u, wR = walls & 2u;
+            // right-spine entries except the row maximum (linked as a left entry)
+            const unsigned long long mRx =
+                wR ? mR : (mR & ~(1ull << (63 - __clzll((long long)mR))));
+            const uint32_t nL = __popcll(mL), nE = 2 + nL + __popcll(mRx);
+            for (uint32_t e = lane; e < nE; e += 32) {
+                if (e == 0) {  // the first leaf: right child of the gap before it, or
+                               // left child of the gap after it
+                    const uint32_t lam0 = spine_lowest(mL, wL);
+                    const int32_t u = row_left(A.tmax, A.bmax, t, 0u);
+                    uint32_t lamp = 64u;
+                    if (u >= 0)
+                        lamp = spine_lowest(__ldcg(&SP[u].mR), __ldcg(&SP[u].walls) & 2u);
+                    const int32_t ref = __ldcg(&S->ref0);
+                    if (lamp <= lam0) A.nodes[j0].child[1] = ref;
+                    else A.nodes[j0 + 1].child[0] = ref;
+                } else if (e == 1) {  // left child of the last gap, linked in the tile
+                    const int32_t c = __ldcg(&S->c0_next);
+                    if (c != kNoLink) A.nodes[j0 + cnt].child[0] = c;
+                } else {
+                    const bool left = e - 2 < nL;
+                    const uint32_t v = left ? nth_bit(mL, e - 2) : nth_bit(mRx, e - 2 - nL);
+                    const uint32_t g = j0 + __ldcg(left ? &S->iL[v] : &S->iR[v]);
+                    uint32_t lamL, lamR;
+                    int32_t gL, gR;
+                    if (left) {  // next left entry, else (the row maximum) beyond the row
+                        const uint32_t a = spine_above(mL, wL, v);
+                        if (a != 0xffu) {
+                            lamR = a;
+                            gR = (int32_t)(j0 + __ldcg(&S->iL[a]));
+                        } else {
+                            far_right(t, v, lamR, gR);
+                        }
+                        far_left(t, v, lamL, gL);
+                    } else {  // previous right entry; beyond the row on the right
+                        lamL = spine_above(mR, wR, v);
+                        gL = (int32_t)(j0 + __ldcg(&S->iR[lamL]));
+                        far_right(t, v, lamR, gR);
+                    }
+                    const int32_t node = (int32_t)(g + 1);
+                    if (lamL <= lamR) A.nodes[gL + 1].child[1] = node;
+                    else A.nodes[gR + 1].child[0] = node;
+                }
+            }
         }
     }
     // long empty-cell runs of the guide table: one warp per chunk
@@ -873,7 +1093,7 @@ uint32_t build_tile_size(uint32_t flags) {
 
 uint32_t build_queue_capacity(uint32_t m) { return m / 32u + m / kChunk + 64u; }
 
-size_t shard_dep_bytes() { return sizeof(ShardDep); }
+size_t spine_row_bytes() { return sizeof(TileSpine); }
 
 #ifdef RTF_PHASE_TIMING
 extern "C" int rtf_debug_phase_cycles(unsigned long long* host, int rows, int reset) {
@@ -885,10 +1105,9 @@ extern "C" int rtf_debug_phase_cycles(unsigned long long* host, int rows, int re
     return e == cudaSuccess ? 0 : 5;
 }
 #endif
-size_t shard_deps_per_tile() { return kDepsPerTile; }
 
 // n: entries this call processes (a shard's, for sharded builds); n_global: the
-// whole distribution (otherBounds and split levels are indexed globally).
+// whole distribution (a sharded finish links all shards' tiles).
 size_t build_workspace_layout(uint32_t n, uint32_t m, uint32_t flags, WsLayout* L,
                               uint32_t n_global) {
     if (n_global < n) n_global = n;
@@ -907,11 +1126,14 @@ size_t build_workspace_layout(uint32_t n, uint32_t m, uint32_t flags, WsLayout* 
     L->scale = take(16);
     L->total = take(16);
     L->excl = take(sizeof(Pfx) * (size_t)nt);
-    L->pend = take(sizeof(PendingLeaf) * 2 * (size_t)nt);
-    L->ndeps = take(sharded ? sizeof(uint32_t) * (size_t)nt : 0);
-    L->deps = take(sharded ? sizeof(ShardDep) * kDepsPerTile * (size_t)nt : 0);
-    L->ob = take(sizeof(unsigned long long) * (size_t)n_global);
-    L->lam = take((size_t)n_global);
+    // a sharded finish links count x nt_max rows; shards are 4096-entry aligned
+    const uint32_t cap = sharded ? (uint32_t)(((uint64_t)n_global + tile - 1) / tile) +
+                                       (4096u / tile) * kMaxShards
+                                 : nt;
+    L->nt_cap = std::max(cap, nt);
+    L->spine = take(sizeof(TileSpine) * (size_t)nt);
+    L->tmax = take(64 * (((size_t)L->nt_cap + 63) / 64));
+    L->bmax = take(sizeof(uint32_t) * (((size_t)L->nt_cap + 63) / 64));
     L->qcap = build_queue_capacity(m);
     L->queue = take(sizeof(RunChunk) * (size_t)L->qcap);
     L->bytes = off;
@@ -972,21 +1194,19 @@ cudaError_t launch_build(const float* p, uint32_t n, uint32_t m, uint32_t flags,
     A.shard_rank = sc ? sc->rank : 0;
     A.shard_count = sc ? sc->count : 0;
     A.total_out = reinterpret_cast<Pfx*>(w + L.total);
-    A.deps = reinterpret_cast<ShardDep*>(w + L.deps);
-    A.ndeps = reinterpret_cast<uint32_t*>(w + L.ndeps);
-    A.deps_in = sc ? reinterpret_cast<const ShardDep*>(sc->deps_in) : nullptr;
-    A.ndeps_in = sc ? sc->ndeps_in : nullptr;
-    A.nt_in = sc ? sc->nt_in : 0;
+    A.spine = reinterpret_cast<TileSpine*>(w + L.spine);
+    const bool gathered = sc && sc->spine_in;
+    A.spine_in = gathered ? reinterpret_cast<const TileSpine*>(sc->spine_in) : A.spine;
+    A.nt_in = gathered ? sc->nt_in : L.nt;
+    if (A.nt_in > L.nt_cap) return cudaErrorInvalidValue;
+    A.tmax = reinterpret_cast<uint8_t*>(w + L.tmax);
+    A.bmax = reinterpret_cast<uint32_t*>(w + L.bmax);
     A.maxpart = reinterpret_cast<uint32_t*>(w + L.maxpart);
     A.counters = reinterpret_cast<uint32_t*>(w + L.counters);
     A.excl = reinterpret_cast<Pfx*>(w + L.excl);
     A.hdr = hdr;
     A.nodes = nodes;
     A.table = table;
-    A.lam = reinterpret_cast<uint8_t*>(w + L.lam);
-    A.ob = reinterpret_cast<unsigned long long*>(w + L.ob);
-    A.pend = (sc && sc->pend_in) ? reinterpret_cast<PendingLeaf*>(const_cast<void*>(sc->pend_in))
-                                 : reinterpret_cast<PendingLeaf*>(w + L.pend);
     A.queue = reinterpret_cast<RunChunk*>(w + L.queue);
     A.qcap = L.qcap;
     A.cdf = cdf;

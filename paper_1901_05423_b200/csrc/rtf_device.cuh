@@ -158,18 +158,26 @@ __device__ __forceinline__ int floor_log2_bits(uint32_t b) {
     return (31 - __clz((int)b)) - 149;  // subnormal: frac * 2^-149
 }
 
-// w = max(1, floor(x 2^shift)) for x > 0, 0 otherwise.  Exact in FP64: the
-// 24-bit mantissa of x converts exactly, scaling by 2^shift is exact (shift is
-// in [-96, 211], so the product is a normal double), x 2^shift < 2^63, and the
-// round-toward-zero conversion is the floor.
-__device__ __forceinline__ double pow2_f64(int shift) {
-    return __longlong_as_double((long long)(1023 + shift) << 52);
+// w = max(1, floor(x 2^shift)) for x > 0, 0 for x = +-0 (the build rejects
+// negative, NaN and Inf data before quantising).  Exact in FP32: shift lies in
+// [-97, 211], so 2^shift = s1 s2 with s1 = 2^min(shift, 127) and s2 = 2^(shift
+// - 127) or 1, both normal floats; multiplying by a power of two is exact
+// unless the result leaves the normal range, and here the product overflows
+// never (x 2^shift < 2^63) and underflows only below 2^-126, where floor = 0
+// and the max with 1 decides anyway.  The round-toward-zero conversion is the
+// floor.  (FMUL, FMUL, FSETP, FSEL, FMNMX, F2I.U64: no FP64 pipe.)
+struct QScale {
+    float s1, s2;
+};
+
+__device__ __forceinline__ QScale qscale(int shift) {
+    const int a = shift > 127 ? 127 : shift;
+    return QScale{__int_as_float((127 + a) << 23), __int_as_float((127 + shift - a) << 23)};
 }
 
-__device__ __forceinline__ uint64_t quantize(float x, double scale) {
-    if (!(x > 0.0f)) return 0;
-    const uint64_t v = __double2ull_rz((double)x * scale);
-    return v ? v : 1ull;
+__device__ __forceinline__ uint64_t quantize(float x, QScale q) {
+    const float y = fmaxf((x * q.s1) * q.s2, x > 0.0f ? 1.0f : 0.0f);
+    return __float2ull_rz(y);
 }
 
 // ------------------------------------------------------------ exact normalisation

@@ -18,11 +18,11 @@ enum : uint32_t {
     kPhSpine = 4,     // C: exclusive tile prefixes (+ header or shard total)
     kPhTiles = 8,     // D: keys, split levels, table, in-tile Alg. 1, records
     kPhRuns = 16,     // E: long empty-cell runs of the table
-    kPhWalk = 32,     // E: cross-tile Alg. 1
-    kPhScatter = 64,  // sharded finish: all shards' leftover deposits -> otherBounds
-    kPhFull = kPhScale | kPhTotals | kPhSpine | kPhTiles | kPhRuns | kPhWalk,
+    kPhCross = 32,    // E: cross-tile links from the tiles' spines
+    kPhFull = kPhScale | kPhTotals | kPhSpine | kPhTiles | kPhRuns | kPhCross,
 };
-constexpr uint32_t kBuildShardedLayout = 0x100;  // internal flag: workspace with deposit lists
+constexpr uint32_t kBuildShardedLayout = 0x100;  // internal flag: room for all shards' rows
+constexpr uint32_t kMaxShards = 1024;
 
 inline int ceil_log2_u32(uint32_t n) {
     int c = 0;
@@ -33,23 +33,21 @@ inline int ceil_log2_u32(uint32_t n) {
 struct WsLayout {
     uint32_t nt;  // tiles
     uint32_t qcap;
-    size_t maxpart, counters, scale, total, excl, pend, ndeps, deps, ob, lam, queue, bytes;
+    uint32_t nt_cap;  // rows phase E can link (a sharded finish: all shards' tiles)
+    size_t maxpart, counters, scale, total, excl, spine, tmax, bmax, queue, bytes;
 };
 
 // one call of a sharded build (config 4); see rtf_shard_* in include/rtf.h
 struct ShardCall {
     uint32_t phases, n_global, index_base, rank, count, nt_in;
     const void* totals;        // device: count shard totals (16 B each)
-    const void* pend_in;       // device: finish -- all shards' pending leaves
-    const void* deps_in;       // device: finish -- all shards' deposit lists
-    const uint32_t* ndeps_in;  // device: finish -- deposits per tile
+    const void* spine_in;      // device: finish -- all shards' tile spines (nt_in rows)
 };
 
 uint32_t build_tile_size(uint32_t flags);
 size_t build_workspace_layout(uint32_t n, uint32_t m, uint32_t flags, WsLayout* L,
                               uint32_t n_global = 0);
-size_t shard_dep_bytes();       // bytes of one deposit-list entry
-size_t shard_deps_per_tile();   // deposit-list capacity per tile
+size_t spine_row_bytes();       // bytes of one tile-spine row
 
 cudaError_t launch_build(const float* p, uint32_t n, uint32_t m, uint32_t flags, rtf_header* hdr,
                          rtf_node* nodes, int32_t* table, uint64_t* cdf, void* ws,

@@ -99,12 +99,13 @@ __global__ void __launch_bounds__(THREADS) k_build_rows(RowsArgs A) {
     }
     const int E = floor_log2_bits(mx);
     const int B = 62 - (n > 1 ? 32 - __clz((int)(n - 1)) : 0);
+    const QScale qs = qscale(B - E);
     uint64_t w[VPT];
     uint64_t tw = 0;
     uint32_t tc = 0;
 #pragma unroll
     for (int k = 0; k < VPT; ++k) {
-        w[k] = quantize(x[k], pow2_f64(B - E));
+        w[k] = quantize(x[k], qs);
         tw += w[k];
         tc += w[k] != 0;
     }

@@ -11,9 +11,9 @@ with collectives.  Two communicators implement the same four collectives:
              by the single-GPU parity tests
 
 Protocol (include/rtf.h, "sharded build"): scale -> MAX-reduce -> totals ->
-gather (the cross-GPU scan) -> per-shard build -> replicate records, split
-levels (broadcast from the owner), table (MAX-reduce), pending leaves and
-deposit lists (gather) -> finish (cross-tile Alg. 1) on every shard.
+gather (the cross-GPU scan) -> per-shard build -> replicate records (broadcast
+from the owner), table (MAX-reduce), tile spine rows (gather) -> finish (the
+cross-tile links) on every shard.
 """
 from __future__ import annotations
 
@@ -139,24 +139,14 @@ class Shard:
     def total_bytes(self):
         return self._ws_slice(self.view.total, 16)
 
-    def lam_bytes(self, j0, cnt):
-        return self._ws_slice(self.view.lam + j0, cnt)
-
     def node_bytes(self, j0, cnt):
         return self._forest_slice(self.fview.nodes + 16 * j0, 16 * cnt)
 
     def table_words(self):
         return self._forest_slice(self.fview.table, 4 * self.m).view(torch.int32)
 
-    def pend_bytes(self):
-        return self._ws_slice(self.view.pend, 8 * 2 * self.view.nt_local)
-
-    def deps_bytes(self):
-        return self._ws_slice(self.view.deps,
-                              self.view.dep_bytes * self.view.dep_stride * self.view.nt_local)
-
-    def ndeps_words(self):
-        return self._ws_slice(self.view.ndeps, 4 * self.view.nt_local).view(torch.int32)
+    def spine_bytes(self):
+        return self._ws_slice(self.view.spine, self.view.spine_row_bytes * self.view.nt_local)
 
 
 def _padded(t: torch.Tensor, nbytes: int, fill: int) -> torch.Tensor:
@@ -194,22 +184,18 @@ def build_sharded(shards: list[Shard], comm) -> None:
         j0, cnt = int(starts[r]), int(tot["cnt"][r])
         if cnt:
             comm.broadcast([s.node_bytes(j0, cnt) for s in shards], src=r)
-            comm.broadcast([s.lam_bytes(j0, cnt) for s in shards], src=r)
     comm.allreduce_max([s.table_words() for s in shards])
     nt_max = max(s.view.nt_local for s in shards)
     if hasattr(comm, "dist"):  # shards of other processes may have more tiles
         t = torch.tensor([nt_max], dtype=torch.int64, device=sh0.p.device)
         comm.allreduce_max([t])
         nt_max = int(t.item())
-    dep_row = sh0.view.dep_bytes * sh0.view.dep_stride
-    pend_all = comm.allgather([_padded(s.pend_bytes(), 16 * nt_max, 0xFF) for s in shards])
-    deps_all = comm.allgather([_padded(s.deps_bytes(), dep_row * nt_max, 0) for s in shards])
-    ndeps_all = comm.allgather([_padded(s.ndeps_words().view(torch.uint8), 4 * nt_max, 0)
-                                for s in shards])
-    # 5. cross-tile Alg. 1 over the assembled state, on every shard
-    for s, pa, da, na in zip(shards, pend_all, deps_all, ndeps_all):
-        check(L.rtf_shard_finish(*args(s), _ptr(pa), _ptr(da), _ptr(na), s.count * nt_max,
-                                 _ptr(s.forest), s.forest.numel(), _ptr(s.ws), s.ws.numel(), st,
+    row = sh0.view.spine_row_bytes
+    spine_all = comm.allgather([_padded(s.spine_bytes(), row * nt_max, 0) for s in shards])
+    # 5. cross-tile links over all shards' spine rows, on every shard
+    for s, sa in zip(shards, spine_all):
+        check(L.rtf_shard_finish(*args(s), _ptr(sa), s.count * nt_max, _ptr(s.forest),
+                                 s.forest.numel(), _ptr(s.ws), s.ws.numel(), st,
                                  ctypes.byref(s.fview)), "shard finish")
 
 
