@@ -78,7 +78,8 @@ struct BuildArgs {
     uint32_t* bmax;            // phase E: per 64 rows, the maximum of tmax
     uint32_t* maxpart;  // 2 per CTA
     uint32_t* counters;
-    Pfx* excl;          // per tile: aggregate (phase B), then exclusive prefix (phase C)
+    Pfx* excl;          // per tile: exclusive prefix within its range (phase B)
+    Pfx* rng;           // per range of tiles: total (phase B)
     rtf_header* hdr;
     rtf_node* nodes;
     int32_t* table;
@@ -308,12 +309,14 @@ __global__ void __launch_bounds__(THREADS, MINB) k_build(BuildArgs A) {
     __shared__ int32_t s_l[2 * NW];
     __shared__ uint64_t s_key_after;
     __shared__ uint32_t s_red[2 * NW];
-    __shared__ uint32_t s_next;
     __shared__ Pfx s_grp[THREADS];  // exclusive prefix of each group of `per` tiles
-    __shared__ Pfx s_tot, s_pre;
+    __shared__ Pfx s_tot;
+    __shared__ uint32_t s_next;
+    __shared__ __align__(16) Pfx s_pin;  // TMA target: the next tile's prefix within its range
     __shared__ uint64_t s_recip;
     __shared__ unsigned long long s_mL, s_mR;  // this tile's spines (TileSpine)
     __shared__ uint32_t s_walls;
+    __shared__ uint32_t s_fw, s_lw, s_mx;  // first / last wall, (max split level << 16 | gap)
     __shared__ int32_t s_ref0;
     __shared__ uint16_t s_iL[65], s_iR[65];
 
@@ -333,6 +336,12 @@ __global__ void __launch_bounds__(THREADS, MINB) k_build(BuildArgs A) {
     if (b == 0 && tid == 0 && (ph & kPhTiles)) {
         A.counters[kCtrQueue] = 0;
         A.counters[kCtrTile] = 0;  // phase D's tile dispenser (a grid barrier precedes D)
+    }
+    if (ph & kPhTiles) {  // row maxima for phase E: padding rows stay 0
+        const uint32_t nb = (nt + 63) / 64;
+        for (uint32_t i = b * THREADS + tid; i < 16 * nb; i += G * THREADS)
+            reinterpret_cast<uint32_t*>(A.tmax)[i] = 0u;
+        for (uint32_t i = b * THREADS + tid; i < nb; i += G * THREADS) A.bmax[i] = 0u;
     }
     if (ph & kPhScale) {
         // Fast path: two integer maxima of the raw bits.  As signed integers the
@@ -437,62 +446,78 @@ __global__ void __launch_bounds__(THREADS, MINB) k_build(BuildArgs A) {
     const QScale scale = qscale(A.B - E);
 
     // ---------------------------------------------------------- B: tile totals
-    // two tiles per step so each thread has 2*VPT/4 float4 loads in flight
-    for (uint32_t t0 = b; (ph & kPhTotals) && t0 < nt; t0 += 2 * G) {
-        Pfx acc[2];
-#pragma unroll
-        for (int h = 0; h < 2; ++h) {
-            acc[h] = Pfx{0ull, 0u, -1};
-            const uint32_t t = t0 + h * G;
-            if (t >= nt) continue;
-            const uint32_t base = t * TILE;
-            constexpr int NF4 = VPT / 4;  // striped float4 loads of the tile
-            if (A.vec && base + TILE <= n) {
-                float4 v[NF4];
-#pragma unroll
-                for (int k = 0; k < NF4; ++k) v[k] = ld_stream_f4(A.p + base + 4 * (k * THREADS + tid));
-#pragma unroll
-                for (int k = 0; k < NF4; ++k) {
-                    const int32_t e = (int32_t)(base + 4 * (k * THREADS + tid));
-                    const float xs[4] = {v[k].x, v[k].y, v[k].z, v[k].w};
-#pragma unroll
-                    for (int u = 0; u < 4; ++u) {
-                        const uint64_t w = quantize(xs[u], scale);
-                        acc[h].W += w;
-                        acc[h].cnt += w != 0;
-                        if (w) acc[h].last = e + u + ib;
-                    }
-                }
-            } else {
-                for (uint32_t e = base + tid; e < min(n, base + TILE); e += THREADS) {
-                    const uint64_t w = quantize(A.p[e], scale);
-                    acc[h].W += w;
-                    acc[h].cnt += w != 0;
-                    if (w) acc[h].last = (int32_t)e + ib;
-                }
-            }
-        }
-        warp_sum_pfx(acc[0]);
-        warp_sum_pfx(acc[1]);
-        __syncthreads();
-        if (lane == 0) {
+    // The tiles form NRG ranges of krng consecutive tiles; CTA r < NRG sums
+    // range r, two tiles per step (2*VPT/4 float4 loads in flight per
+    // thread), and writes each tile's exclusive prefix within its range
+    // (excl) and the range total (rng).  Phase C scans only the NRG totals.
+    const uint32_t NRG = min(G, (uint32_t)THREADS);
+    const uint32_t krng = (nt + NRG - 1) / NRG;
+    if ((ph & kPhTotals) && b < NRG) {
+        Pfx run{0ull, 0u, -1};  // thread 0: the range so far
+        const uint32_t t_end = min(nt, (b + 1) * krng);
+        for (uint32_t t0 = b * krng; t0 < t_end; t0 += 2) {
+            Pfx acc[2];
 #pragma unroll
             for (int h = 0; h < 2; ++h) {
-                s_w[h * NW + warp] = acc[h].W;
-                s_c[h * NW + warp] = acc[h].cnt;
-                s_l[h * NW + warp] = acc[h].last;
+                acc[h] = Pfx{0ull, 0u, -1};
+                const uint32_t t = t0 + h;
+                if (t >= t_end) continue;
+                const uint32_t base = t * TILE;
+                constexpr int NF4 = VPT / 4;  // striped float4 loads of the tile
+                if (A.vec && base + TILE <= n) {
+                    float4 v[NF4];
+#pragma unroll
+                    for (int k = 0; k < NF4; ++k)
+                        v[k] = ld_stream_f4(A.p + base + 4 * (k * THREADS + tid));
+#pragma unroll
+                    for (int k = 0; k < NF4; ++k) {
+                        const int32_t e = (int32_t)(base + 4 * (k * THREADS + tid));
+                        const float xs[4] = {v[k].x, v[k].y, v[k].z, v[k].w};
+#pragma unroll
+                        for (int u = 0; u < 4; ++u) {
+                            const uint64_t w = quantize(xs[u], scale);
+                            acc[h].W += w;
+                            acc[h].cnt += w != 0;
+                            if (w) acc[h].last = e + u + ib;
+                        }
+                    }
+                } else {
+                    for (uint32_t e = base + tid; e < min(n, base + TILE); e += THREADS) {
+                        const uint64_t w = quantize(A.p[e], scale);
+                        acc[h].W += w;
+                        acc[h].cnt += w != 0;
+                        if (w) acc[h].last = (int32_t)e + ib;
+                    }
+                }
+            }
+            warp_sum_pfx(acc[0]);
+            warp_sum_pfx(acc[1]);
+            __syncthreads();
+            if (lane == 0) {
+#pragma unroll
+                for (int h = 0; h < 2; ++h) {
+                    s_w[h * NW + warp] = acc[h].W;
+                    s_c[h * NW + warp] = acc[h].cnt;
+                    s_l[h * NW + warp] = acc[h].last;
+                }
+            }
+            __syncthreads();
+            if (tid == 0) {
+#pragma unroll
+                for (int h = 0; h < 2; ++h) {
+                    if (t0 + h >= t_end) break;
+                    Pfx sum{0ull, 0u, -1};
+                    for (int w = 0; w < NW; ++w) {
+                        sum.W += s_w[h * NW + w];
+                        sum.cnt += s_c[h * NW + w];
+                        sum.last = max(sum.last, s_l[h * NW + w]);
+                    }
+                    st_pfx(&A.excl[t0 + h], run);
+                    run = combine(run, sum);
+                }
             }
         }
-        __syncthreads();
-        if (tid < 2 && t0 + tid * G < nt) {
-            Pfx s{0ull, 0u, -1};
-            for (int w = 0; w < NW; ++w) {
-                s.W += s_w[tid * NW + w];
-                s.cnt += s_c[tid * NW + w];
-                s.last = max(s.last, s_l[tid * NW + w]);
-            }
-            st_pfx(&A.excl[t0 + tid * G], s);
-        }
+        if (tid == 0) st_pfx(&A.rng[b], run);
     }
     // the tile weights of phase D can stream in while the spine scan runs
     const bool tma = !CDF && A.vec && (ph & kPhTiles);
@@ -513,29 +538,12 @@ __global__ void __launch_bounds__(THREADS, MINB) k_build(BuildArgs A) {
     RTF_TICK(1);
 
     // ---------------------------------------------------------- C: spine (every CTA)
-    // Each CTA scans the nt tile aggregates itself (nt x 16 B, from L2) and keeps
-    // the exclusive prefix of every group of `per` consecutive tiles in shared
-    // memory; a tile's prefix is its group's plus <= per-1 aggregates (warp 0,
-    // tile_prefix).  Redundant work instead of a single-CTA scan plus one more
-    // grid barrier.
-    const uint32_t per = (nt + THREADS - 1) / THREADS;  // tiles per group (per thread)
+    // Each CTA scans the NRG range totals itself (a few KB from L2) and keeps
+    // the exclusive prefix of every range in shared memory; a tile's prefix
+    // is its range's combined with its exclusive prefix within the range.
     Pfx total{0ull, 0u, -1};
     if (ph & (kPhSpine | kPhTiles)) {
-        constexpr int BATCH = 4;
-        const uint32_t u0 = min(nt, tid * per), u1 = min(nt, u0 + per);
-        Pfx own{0ull, 0u, -1};
-        for (uint32_t tb = u0; tb < u1; tb += BATCH) {
-            Pfx a[BATCH];
-#pragma unroll
-            for (int u = 0; u < BATCH; ++u)
-                a[u] = (tb + u < u1) ? ld_pfx_cg(&A.excl[tb + u]) : Pfx{0ull, 0u, -1};
-#pragma unroll
-            for (int u = 0; u < BATCH; ++u) {
-                own.W += a[u].W;
-                own.cnt += a[u].cnt;
-                own.last = max(own.last, a[u].last);
-            }
-        }
+        const Pfx own = tid < NRG ? ld_pfx_cg(&A.rng[tid]) : Pfx{0ull, 0u, -1};
         uint64_t w_ex, w_tot;
         uint32_t c_ex, c_tot;
         int32_t l_ex;
@@ -590,28 +598,12 @@ __global__ void __launch_bounds__(THREADS, MINB) k_build(BuildArgs A) {
     }
     nm.v = s_recip;
 
-    // exclusive prefix of tile t (warp 0 calls; every lane gets it)
-    auto tile_prefix = [&](uint32_t t) -> Pfx {
-        const uint32_t g = t / per;
-        Pfx acc{0ull, 0u, -1};
-        for (uint32_t u = g * per + lane; u < t; u += 32) {
-            const Pfx a = ld_pfx_cg(&A.excl[u]);
-            acc.W += a.W;
-            acc.cnt += a.cnt;
-            acc.last = max(acc.last, a.last);
-        }
-        warp_sum_pfx(acc);
-        return combine(s_grp[g], acc);
-    };
+    // exclusive prefix of tile t: its range's, then its own within the range
+    auto tile_prefix = [&](uint32_t t) -> Pfx { return combine(s_grp[t / krng], ld_pfx_cg(&A.excl[t])); };
 
     if (CDF) {  // baseline: K[i] = floor(W_i 2^63 / T) for every entry, zeros included
         for (uint32_t t = b; t < nt; t += G) {
-            if (warp == 0) {
-                const Pfx pt = tile_prefix(t);
-                if (lane == 0) s_pre = pt;
-            }
-            __syncthreads();
-            const Pfx pre = s_pre;
+            const Pfx pre = tile_prefix(t);
             const uint32_t first = t * TILE + tid * VPT;
             float x[VPT];
             load_tile<VPT>(A.p, first, n, A.vec, x);
@@ -637,28 +629,35 @@ __global__ void __launch_bounds__(THREADS, MINB) k_build(BuildArgs A) {
     }
 
     // ---------------------------------------------------------- D: tiles
-    // tiles are dealt dynamically (their cost varies several-fold with the
-    // zero fraction and the tree shape): CTA b starts with tile b, then takes
-    // G + the next ticket; the ticket is drawn early so TMA can prefetch it
+    // Tiles are dealt dynamically (their cost varies with the zero fraction
+    // and the tree shape): CTA b starts with tile b, then takes G + tickets.
+    // Thread 0 draws each ticket one tile ahead, so the atomic's latency is
+    // hidden; the TMA copy of the next tile's weights also brings its prefix
+    // within its range (one mbarrier for both).
     uint32_t phase = 0;
+    uint32_t ticket = 0;  // thread 0: the tile after the next one
     if (tid == 0) {
         s_mL = s_mR = 0ull;
         s_walls = 0u;
+        s_fw = 0xffffffffu;
+        s_lw = 0u;
+        s_mx = 0u;
     }
-    if ((ph & kPhTiles) && warp == 0 && b < nt) {
-        const Pfx p0 = tile_prefix(b);
-        if (lane == 0) s_pre = p0;
+    if (tid == 0) {
+        fence_proxy_async_global();  // phase B's prefixes, read by TMA below
+        if (ph & kPhTiles) ticket = G + atomicAdd(&A.counters[kCtrTile], 1u);
     }
     __syncthreads();
     for (uint32_t t = b; (ph & kPhTiles) && t < nt; t = s_next) {
-        const Pfx pre = s_pre;
         const uint32_t first = t * TILE + tid * VPT;  // local index into p (global: + ib)
 
         // (0) weights of this thread's VPT consecutive entries
         float x[VPT];
+        Pfx pre;
         if (tma_tile(t)) {
             mbar_wait(&s_bar, phase);
             phase ^= 1u;
+            pre = combine(s_grp[t / krng], t == b ? ld_pfx_cg(&A.excl[t]) : s_pin);
 #pragma unroll
             for (int k = 0; k < VPT; k += 4) {
                 const float4 v = *reinterpret_cast<const float4*>(s_p + tid * VPT + k);
@@ -669,6 +668,7 @@ __global__ void __launch_bounds__(THREADS, MINB) k_build(BuildArgs A) {
             }
         } else {
             load_tile<VPT>(A.p, first, n, A.vec, x);
+            pre = tile_prefix(t);
         }
         uint64_t w[VPT];
         uint64_t tw = 0;
@@ -751,6 +751,24 @@ __global__ void __launch_bounds__(THREADS, MINB) k_build(BuildArgs A) {
                 key = kn;
                 cell = cn;
             }
+        }
+        if (tc) {  // first / last wall and the largest other split level (byte SIMD)
+            const uint32_t h0 = (uint32_t)lampack, h1 = (uint32_t)(lampack >> 32);
+            const uint32_t w0 = __vcmpeq4(h0, 0x40404040u), w1 = __vcmpeq4(h1, 0x40404040u);
+            const uint32_t wm = (((w0 & 0x80808080u) * 0x00204081u) >> 28) |
+                                ((((w1 & 0x80808080u) * 0x00204081u) >> 28) << 4);
+            if (wm) {
+                atomicMin(&s_fw, c_ex + __ffs(wm) - 1);
+                atomicMax(&s_lw, c_ex + 31 - __clz(wm));
+            }
+            const uint32_t v0 = h0 & ~w0, v1 = h1 & ~w1;  // walls -> 0; bytes past tc are 0
+            uint32_t mv = __vmaxu4(v0, v1);
+            mv = __vmaxu4(mv, mv >> 16);
+            mv = max(mv & 0xffu, (mv >> 8) & 0xffu);
+            const uint32_t e0 = __vcmpeq4(v0, mv * 0x01010101u), e1 = __vcmpeq4(v1, mv * 0x01010101u);
+            const uint32_t em = (((e0 & 0x80808080u) * 0x00204081u) >> 28) |
+                                ((((e1 & 0x80808080u) * 0x00204081u) >> 28) << 4);
+            atomicMax(&s_mx, (mv + 1) << 16 | (c_ex + __ffs(em) - 1));
         }
         __syncthreads();
 
@@ -862,73 +880,61 @@ __global__ void __launch_bounds__(THREADS, MINB) k_build(BuildArgs A) {
         __syncthreads();
 
         RTF_TICK(5);
-        // (4) the spines of the tile (TileSpine): strict prefix / suffix maxima
-        // of its split levels, from a block-wide exclusive max-scan of the
-        // per-thread maxima in both directions
+        // (4) the spines of the tile (TileSpine).  Every spine gap except the
+        // tile's maximum got exactly one arrival here that found no sibling:
+        // from its right (bound >= slot) on the left spine, from its left on
+        // the right spine -- so the leftover deposits name them.  The walls
+        // (first / last cell boundary) and, in a tile without walls, the
+        // maximum complete the two spines.
         {
-            int32_t tm = -1;
-#pragma unroll
-            for (int r = 0; r < VPT; ++r)
-                if ((uint32_t)r < tc) tm = max(tm, (int32_t)((lampack >> (8 * r)) & 0xffu));
-            int32_t ip = tm, is = tm;
-#pragma unroll
-            for (int d = 1; d < 32; d <<= 1) {
-                const int32_t a = __shfl_up_sync(0xffffffffu, ip, d);
-                const int32_t c = __shfl_down_sync(0xffffffffu, is, d);
-                if (lane >= d) ip = max(ip, a);
-                if (lane + d < 32) is = max(is, c);
-            }
-            const int32_t ip1 = __shfl_up_sync(0xffffffffu, ip, 1);
-            const int32_t is1 = __shfl_down_sync(0xffffffffu, is, 1);
-            int32_t* s_wm = reinterpret_cast<int32_t*>(s_red);
-            if (lane == 31) s_wm[warp] = ip;  // warp maximum
-            __syncthreads();
-            int32_t runL = lane ? ip1 : -1, runR = lane < 31 ? is1 : -1;
-#pragma unroll
-            for (int w = 0; w < NW; ++w) {
-                const int32_t v = s_wm[w];
-                if (w < warp) runL = max(runL, v);
-                if (w > warp) runR = max(runR, v);
-            }
-#pragma unroll
-            for (int r = 0; r < VPT; ++r) {
-                const int32_t lv = (int32_t)((lampack >> (8 * r)) & 0xffu);
-                if ((uint32_t)r < tc && lv > runL) {
-                    runL = lv;
-                    s_iL[lv] = (uint16_t)(c_ex + r);
-                    if (lv < 64) atomicOr(&s_mL, 1ull << lv);
-                    else atomicOr(&s_walls, 1u);
+            auto add = [&](bool left, uint32_t lv, uint32_t gap) {
+                if (left) {
+                    s_iL[lv] = (uint16_t)gap;
+                    atomicOr(&s_mL, 1ull << lv);
+                } else {
+                    s_iR[lv] = (uint16_t)gap;
+                    atomicOr(&s_mR, 1ull << lv);
                 }
+            };
+            auto leftover = [&](uint32_t e, int32_t o) {
+                if (o < 0) return;
+                const uint32_t q = e - e / 9;  // slot (gap q - 1)
+                add((uint32_t)(o & 0xffff) >= q, s_lam[pad8(q - 1)], q - 1);
+            };
+            const int4* ob4 = reinterpret_cast<const int4*>(s_ob);
+            const uint32_t n4 = cnt ? pad8(cnt) / 4 + 1 : 0u;
+            for (uint32_t u = tid; u < n4; u += THREADS) {
+                const int4 v = ob4[u];
+                if ((v.x & v.y & v.z & v.w) < 0) continue;  // four empty slots
+                leftover(4 * u, v.x);
+                leftover(4 * u + 1, v.y);
+                leftover(4 * u + 2, v.z);
+                leftover(4 * u + 3, v.w);
             }
-#pragma unroll
-            for (int r = VPT - 1; r >= 0; --r) {
-                const int32_t lv = (int32_t)((lampack >> (8 * r)) & 0xffu);
-                if ((uint32_t)r < tc && lv > runR) {
-                    runR = lv;
-                    s_iR[lv] = (uint16_t)(c_ex + r);
-                    if (lv < 64) atomicOr(&s_mR, 1ull << lv);
-                    else atomicOr(&s_walls, 2u);
+            if (tid == 0 && cnt) {
+                if (s_fw != 0xffffffffu) {
+                    s_iL[64] = (uint16_t)s_fw;
+                    s_iR[64] = (uint16_t)s_lw;
+                    s_walls = 3u;
+                } else {  // no wall: the maximum heads both spines
+                    const uint32_t lv = (s_mx >> 16) - 1, gap = s_mx & 0xffffu;
+                    add(true, lv, gap);
+                    add(false, lv, gap);
                 }
             }
         }
-        // (5) the next tile: ticket, TMA prefetch into the consumed weight
-        // buffer (otherBounds is no longer read), prefix
-        if (warp == 0) {
-            uint32_t nx = 0;
-            if (lane == 0) {
-                nx = G + atomicAdd(&A.counters[kCtrTile], 1u);
-                if (tma_tile(nx)) {
-                    fence_proxy_async_smem();
-                    mbar_arrive_expect_tx(&s_bar, TILE * 4);
-                    tma_load_1d(s_p, A.p + (size_t)nx * TILE, TILE * 4, &s_bar);
-                }
+        // (5) the next tile's weights and prefix: TMA into the consumed weight
+        // buffer (otherBounds is no longer read); s_pin was read at step (0)
+        if (tid == 0) {
+            const uint32_t nx = ticket;
+            s_next = nx;  // read after the barrier below
+            if (tma_tile(nx)) {
+                fence_proxy_async_smem();
+                mbar_arrive_expect_tx(&s_bar, TILE * 4 + (uint32_t)sizeof(Pfx));
+                tma_load_1d(s_p, A.p + (size_t)nx * TILE, TILE * 4, &s_bar);
+                tma_load_1d(&s_pin, A.excl + nx, (uint32_t)sizeof(Pfx), &s_bar);
             }
-            nx = __shfl_sync(0xffffffffu, nx, 0);
-            const Pfx pn = nx < nt ? tile_prefix(nx) : Pfx{0ull, 0u, -1};
-            if (lane == 0) {
-                s_next = nx;
-                s_pre = pn;
-            }
+            if (nx < nt) ticket = G + atomicAdd(&A.counters[kCtrTile], 1u);
         }
         // (6) node records, coalesced 16 B
         {
@@ -955,8 +961,15 @@ __global__ void __launch_bounds__(THREADS, MINB) k_build(BuildArgs A) {
                 row->walls = s_walls;
                 row->c0_next = cnt ? s_c0[pad8(cnt)] : kNoLink;
                 row->ref0 = cnt ? s_ref0 : 0;
+                // phase E's row maxima: 1 + the largest split level, 0 if empty
+                const uint32_t enc = !cnt ? 0u : s_walls ? 65u : (s_mx >> 16);
+                A.tmax[t] = (uint8_t)enc;
+                if (enc) atomicMax(&A.bmax[t >> 6], enc);
                 s_mL = s_mR = 0ull;  // the next tile's atomics follow its scan barriers
                 s_walls = 0u;
+                s_fw = 0xffffffffu;
+                s_lw = 0u;
+                s_mx = 0u;
             }
         }
         // no barrier here: the next tile writes shared memory only after its scan
@@ -975,8 +988,10 @@ __global__ void __launch_bounds__(THREADS, MINB) k_build(BuildArgs A) {
     if (ph & kPhCross) {
         const TileSpine* SP = A.spine_in;
         const uint32_t NR = A.nt_in, NB = (NR + 63) / 64;
-        // E0: per row 1 + its largest split level (0: no leaves); per 64 rows the max
-        for (uint32_t bb = b * NW + warp; bb < NB; bb += G * NW) {
+        // E0 (gathered rows only; phase D records its own): per row 1 + its
+        // largest split level (0: no leaves), per 64 rows the maximum
+        const bool gathered = !(ph & kPhTiles);
+        for (uint32_t bb = b * NW + warp; gathered && bb < NB; bb += G * NW) {
             uint32_t mx = 0;
 #pragma unroll
             for (int h = 0; h < 2; ++h) {
@@ -992,7 +1007,7 @@ __global__ void __launch_bounds__(THREADS, MINB) k_build(BuildArgs A) {
             mx = __reduce_max_sync(0xffffffffu, mx);
             if (lane == 0) A.bmax[bb] = mx;
         }
-        grid_barrier(gbar);
+        if (gathered) grid_barrier(gbar);
         // E1: one warp per row; lane e links entry e
         auto far_left = [&](uint32_t t, uint32_t v, uint32_t& lam, int32_t& gap) {
             const int32_t u = row_left(A.tmax, A.bmax, t, v + 1);
@@ -1126,6 +1141,7 @@ size_t build_workspace_layout(uint32_t n, uint32_t m, uint32_t flags, WsLayout* 
     L->scale = take(16);
     L->total = take(16);
     L->excl = take(sizeof(Pfx) * (size_t)nt);
+    L->rng = take(sizeof(Pfx) * 1024);  // <= THREADS ranges
     // a sharded finish links count x nt_max rows; shards are 4096-entry aligned
     const uint32_t cap = sharded ? (uint32_t)(((uint64_t)n_global + tile - 1) / tile) +
                                        (4096u / tile) * kMaxShards
@@ -1204,6 +1220,7 @@ cudaError_t launch_build(const float* p, uint32_t n, uint32_t m, uint32_t flags,
     A.maxpart = reinterpret_cast<uint32_t*>(w + L.maxpart);
     A.counters = reinterpret_cast<uint32_t*>(w + L.counters);
     A.excl = reinterpret_cast<Pfx*>(w + L.excl);
+    A.rng = reinterpret_cast<Pfx*>(w + L.rng);
     A.hdr = hdr;
     A.nodes = nodes;
     A.table = table;

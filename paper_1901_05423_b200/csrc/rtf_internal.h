@@ -34,7 +34,7 @@ struct WsLayout {
     uint32_t nt;  // tiles
     uint32_t qcap;
     uint32_t nt_cap;  // rows phase E can link (a sharded finish: all shards' tiles)
-    size_t maxpart, counters, scale, total, excl, spine, tmax, bmax, queue, bytes;
+    size_t maxpart, counters, scale, total, excl, rng, spine, tmax, bmax, queue, bytes;
 };
 
 // one call of a sharded build (config 4); see rtf_shard_* in include/rtf.h
