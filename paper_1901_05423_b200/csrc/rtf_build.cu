@@ -177,19 +177,11 @@ constexpr size_t build_smem_bytes() {
            ((tile_padded<THREADS, VPT>() + 15) & ~(size_t)15);
 }
 
-// Guide-table entries owed by leaf j (orig i) whose split level is a boundary:
-// the anchor of the next non-empty cell and ~i for the empty cells between.
-__device__ __noinline__ void table_runs(int32_t* __restrict__ table, uint32_t m,
-                                        uint32_t* __restrict__ counters,
-                                        RunChunk* __restrict__ queue, uint32_t qcap, uint32_t j,
-                                        int32_t i, uint32_t cell, uint32_t cn) {
-    if (cn < m) table[cn] = (int32_t)(j + 1);
-    const uint32_t len = cn - cell - 1;
-    if (!len) return;
-    if (len <= kShortRun) {
-        for (uint32_t g = cell + 1; g < cn; ++g) table[g] = ~i;
-        return;
-    }
+// A long run of empty cells after the cell of leaf orig i: ~i for each, queued
+// in chunks for phase E (short runs are written in place).
+__device__ __noinline__ void table_queue(uint32_t* __restrict__ counters,
+                                         RunChunk* __restrict__ queue, uint32_t qcap, int32_t i,
+                                         uint32_t cell, uint32_t len) {
     const uint32_t nch = (len + kChunk - 1) / kChunk;
     const uint32_t q = atomicAdd(&counters[kCtrQueue], nch);
     for (uint32_t c = 0; c < nch && q + c < qcap; ++c) {
@@ -706,15 +698,17 @@ __global__ void __launch_bounds__(THREADS, MINB) k_build(BuildArgs A) {
             uint32_t jl = c_ex;
 #pragma unroll
             for (int k = 0; k < VPT; ++k) {
-                if (w[k]) {
+                const uint64_t wk = w[k];
+                if (wk) {
                     const int32_t i = (int32_t)(first + k) + ib;
                     const uint32_t q = pad8(jl);
-                    s_key[q] = fixed_point(W, nm);
+                    w[k] = fixed_point(W, nm);  // w[k] holds key_j from here on
+                    s_key[q] = w[k];
                     s_c0[q] = ~(prevo >= 0 ? prevo : i);
                     prevo = i;
                     ++jl;
                 }
-                W += w[k];
+                W += wk;
             }
         }
         // the tile's first leaf is linked in phase E (its left split level
@@ -731,25 +725,36 @@ __global__ void __launch_bounds__(THREADS, MINB) k_build(BuildArgs A) {
         RTF_TICK(3);
         // (2) own leaves: cell, split level, guide table; the
         // thread's own split levels also stay in registers (byte r = rank r)
+        // keys come from registers (w[k]); only the key after the thread's last
+        // leaf is read back (its owner's, or the one after the tile)
         uint64_t lampack = 0;
-        {
-            const uint64_t key_after = s_key_after;
-            uint32_t jl = c_ex, r = 0;
-            uint64_t key = tc ? s_key[pad8(jl)] : 0ull;
-            uint32_t cell = cell_of(key, m);
-            for (uint32_t mask = posmask; mask; mask &= mask - 1, ++jl, ++r) {
-                const uint64_t kn = (jl + 1 < cnt) ? s_key[pad8(jl + 1)] : key_after;
-                const uint32_t cn = (kn == kOne63) ? m : cell_of(kn, m);
-                const uint32_t lam = (cn != cell) ? kLamBoundary : split_level(key, kn);
-                s_lam[pad8(jl)] = (uint8_t)lam;
-                lampack |= (uint64_t)lam << (8 * r);
-                const uint32_t j = j0 + jl;
-                if (j == 0) A.table[0] = 0;
-                if (lam == kLamBoundary)
-                    table_runs(A.table, m, A.counters, A.queue, A.qcap, j,
-                               (int32_t)(first + __ffs(mask) - 1) + ib, cell, cn);
-                key = kn;
-                cell = cn;
+        if (tc) {
+            uint64_t kn = (c_ex + tc < cnt) ? s_key[pad8(c_ex + tc)] : s_key_after;
+            uint32_t cn = (kn == kOne63) ? m : cell_of(kn, m);
+            if (j0 == 0 && c_ex == 0) A.table[0] = 0;  // leaf 0 has key 0: cell 0's anchor
+#pragma unroll
+            for (int k = VPT - 1; k >= 0; --k) {
+                if ((posmask >> k) & 1u) {
+                    const uint64_t key = w[k];
+                    const uint32_t r = __popc(posmask & ((1u << k) - 1u));  // rank
+                    const uint32_t jl = c_ex + r;
+                    const uint32_t cell = cell_of(key, m);
+                    const uint32_t lam = (cn != cell) ? kLamBoundary : split_level(key, kn);
+                    s_lam[pad8(jl)] = (uint8_t)lam;
+                    lampack |= (uint64_t)lam << (8 * r);
+                    if (lam == kLamBoundary) {  // the table entries this leaf owes
+                        const int32_t i = (int32_t)(first + k) + ib;
+                        if (cn < m) A.table[cn] = (int32_t)(j0 + jl + 1);
+                        const uint32_t len = cn - cell - 1;
+                        if (len <= kShortRun) {
+                            for (uint32_t g = cell + 1; g < cn; ++g) A.table[g] = ~i;
+                        } else {
+                            table_queue(A.counters, A.queue, A.qcap, i, cell, len);
+                        }
+                    }
+                    kn = key;
+                    cn = cell;
+                }
             }
         }
         if (tc) {  // first / last wall and the largest other split level (byte SIMD)
