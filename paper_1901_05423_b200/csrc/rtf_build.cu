@@ -627,7 +627,7 @@ __global__ void __launch_bounds__(THREADS, MINB) k_build(BuildArgs A) {
     // hidden; the TMA copy of the next tile's weights also brings its prefix
     // within its range (one mbarrier for both).
     uint32_t phase = 0;
-    uint32_t ticket = 0;  // thread 0: the tile after the next one
+    uint32_t ticket = 0;  // issuer thread: the tile after the next one
     if (tid == 0) {
         s_mL = s_mR = 0ull;
         s_walls = 0u;
@@ -635,7 +635,8 @@ __global__ void __launch_bounds__(THREADS, MINB) k_build(BuildArgs A) {
         s_lw = 0u;
         s_mx = 0u;
     }
-    if (tid == 0) {
+    constexpr uint32_t kIssuer = THREADS - 1;  // TMA and tickets: the last warp (light duty)
+    if (tid == kIssuer) {
         fence_proxy_async_global();  // phase B's prefixes, read by TMA below
         if (ph & kPhTiles) ticket = G + atomicAdd(&A.counters[kCtrTile], 1u);
     }
@@ -916,7 +917,7 @@ __global__ void __launch_bounds__(THREADS, MINB) k_build(BuildArgs A) {
                 leftover(4 * u + 2, v.z);
                 leftover(4 * u + 3, v.w);
             }
-            if (tid == 0 && cnt) {
+            if (tid == THREADS - 33 && cnt) {  // another warp than the issuer's
                 if (s_fw != 0xffffffffu) {
                     s_iL[64] = (uint16_t)s_fw;
                     s_iR[64] = (uint16_t)s_lw;
@@ -929,8 +930,10 @@ __global__ void __launch_bounds__(THREADS, MINB) k_build(BuildArgs A) {
             }
         }
         // (5) the next tile's weights and prefix: TMA into the consumed weight
-        // buffer (otherBounds is no longer read); s_pin was read at step (0)
-        if (tid == 0) {
+        // buffer once every thread is done reading otherBounds; s_pin was read
+        // at step (0)
+        __syncthreads();
+        if (tid == kIssuer) {
             const uint32_t nx = ticket;
             s_next = nx;  // read after the barrier below
             if (tma_tile(nx)) {
