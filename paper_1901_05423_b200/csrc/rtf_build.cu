@@ -439,75 +439,62 @@ __global__ void __launch_bounds__(THREADS, MINB) k_build(BuildArgs A) {
 
     // ---------------------------------------------------------- B: tile totals
     // The tiles form NRG ranges of krng consecutive tiles; CTA r < NRG sums
-    // range r, two tiles per step (2*VPT/4 float4 loads in flight per
-    // thread), and writes each tile's exclusive prefix within its range
-    // (excl) and the range total (rng).  Phase C scans only the NRG totals.
+    // range r, one warp per tile (8 float4 loads in flight per lane, no block
+    // barrier per tile), then writes each tile's exclusive prefix within its
+    // range (excl) and the range total (rng).  Phase C scans only the NRG
+    // range totals.
     const uint32_t NRG = min(G, (uint32_t)THREADS);
     const uint32_t krng = (nt + NRG - 1) / NRG;
     if ((ph & kPhTotals) && b < NRG) {
+        Pfx* s_tagg = reinterpret_cast<Pfx*>(s_key);  // free until phase D
+        constexpr uint32_t CAP = (uint32_t)(tile_padded<THREADS, VPT>() * 8 / sizeof(Pfx));
+        constexpr int F = TILE / 128;  // float4 per lane per tile
+        constexpr int BATCH = F < 8 ? F : 8;
+        const uint32_t t_beg = b * krng, t_end = min(nt, t_beg + krng);
         Pfx run{0ull, 0u, -1};  // thread 0: the range so far
-        const uint32_t t_end = min(nt, (b + 1) * krng);
-        for (uint32_t t0 = b * krng; t0 < t_end; t0 += 2) {
-            Pfx acc[2];
-#pragma unroll
-            for (int h = 0; h < 2; ++h) {
-                acc[h] = Pfx{0ull, 0u, -1};
-                const uint32_t t = t0 + h;
-                if (t >= t_end) continue;
+        for (uint32_t c0 = t_beg; c0 < t_end; c0 += CAP) {
+            const uint32_t c1 = min(t_end, c0 + CAP);
+            for (uint32_t t = c0 + warp; t < c1; t += NW) {
+                Pfx acc{0ull, 0u, -1};
                 const uint32_t base = t * TILE;
-                constexpr int NF4 = VPT / 4;  // striped float4 loads of the tile
                 if (A.vec && base + TILE <= n) {
-                    float4 v[NF4];
+#pragma unroll 1
+                    for (int c = 0; c < F; c += BATCH) {
+                        float4 v[BATCH];
 #pragma unroll
-                    for (int k = 0; k < NF4; ++k)
-                        v[k] = ld_stream_f4(A.p + base + 4 * (k * THREADS + tid));
+                        for (int u = 0; u < BATCH; ++u)
+                            v[u] = ld_stream_f4(A.p + base + 4 * ((c + u) * 32 + lane));
 #pragma unroll
-                    for (int k = 0; k < NF4; ++k) {
-                        const int32_t e = (int32_t)(base + 4 * (k * THREADS + tid));
-                        const float xs[4] = {v[k].x, v[k].y, v[k].z, v[k].w};
+                        for (int u = 0; u < BATCH; ++u) {
+                            const int32_t e0 = (int32_t)(base + 4 * ((c + u) * 32 + lane)) + ib;
+                            const float xs[4] = {v[u].x, v[u].y, v[u].z, v[u].w};
 #pragma unroll
-                        for (int u = 0; u < 4; ++u) {
-                            const uint64_t w = quantize(xs[u], scale);
-                            acc[h].W += w;
-                            acc[h].cnt += w != 0;
-                            if (w) acc[h].last = e + u + ib;
+                            for (int q = 0; q < 4; ++q) {
+                                const uint64_t w = quantize(xs[q], scale);
+                                acc.W += w;
+                                acc.cnt += w != 0;
+                                if (w) acc.last = e0 + q;
+                            }
                         }
                     }
                 } else {
-                    for (uint32_t e = base + tid; e < min(n, base + TILE); e += THREADS) {
+                    for (uint32_t e = base + lane; e < min(n, base + TILE); e += 32) {
                         const uint64_t w = quantize(A.p[e], scale);
-                        acc[h].W += w;
-                        acc[h].cnt += w != 0;
-                        if (w) acc[h].last = (int32_t)e + ib;
+                        acc.W += w;
+                        acc.cnt += w != 0;
+                        if (w) acc.last = (int32_t)e + ib;
                     }
                 }
-            }
-            warp_sum_pfx(acc[0]);
-            warp_sum_pfx(acc[1]);
-            __syncthreads();
-            if (lane == 0) {
-#pragma unroll
-                for (int h = 0; h < 2; ++h) {
-                    s_w[h * NW + warp] = acc[h].W;
-                    s_c[h * NW + warp] = acc[h].cnt;
-                    s_l[h * NW + warp] = acc[h].last;
-                }
+                warp_sum_pfx(acc);
+                if (lane == 0) s_tagg[t - c0] = acc;
             }
             __syncthreads();
-            if (tid == 0) {
-#pragma unroll
-                for (int h = 0; h < 2; ++h) {
-                    if (t0 + h >= t_end) break;
-                    Pfx sum{0ull, 0u, -1};
-                    for (int w = 0; w < NW; ++w) {
-                        sum.W += s_w[h * NW + w];
-                        sum.cnt += s_c[h * NW + w];
-                        sum.last = max(sum.last, s_l[h * NW + w]);
-                    }
-                    st_pfx(&A.excl[t0 + h], run);
-                    run = combine(run, sum);
+            if (tid == 0)
+                for (uint32_t t = c0; t < c1; ++t) {
+                    st_pfx(&A.excl[t], run);
+                    run = combine(run, s_tagg[t - c0]);
                 }
-            }
+            __syncthreads();
         }
         if (tid == 0) st_pfx(&A.rng[b], run);
     }
@@ -1179,7 +1166,7 @@ static int num_sms() {
 template <int THREADS, int VPT, bool CDF, int MINB = 2>
 static cudaError_t launch_fused(BuildArgs& A, cudaStream_t st, int* launches) {
     auto kern = k_build<THREADS, VPT, CDF, MINB>;
-    const size_t smem = CDF ? 0 : build_smem_bytes<THREADS, VPT>();
+    const size_t smem = build_smem_bytes<THREADS, VPT>();  // phase B stages tile totals there
     static int max_grid = 0;  // per instantiation: co-resident CTAs
     if (!max_grid) {
         cudaError_t e = cudaSuccess;
