@@ -224,6 +224,38 @@ def run_gpu(args):
         tbs = t.item()
     bsearch_gs = world * S / (tbs * 1e-3) / 1e9
 
+    # ------------------------------------------------ baselines: cutpoint + binary / + linear
+    def time_call(fn, reps):
+        ts_ = []
+        for _ in range(reps):
+            flush.zero_()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            fn()
+            e1.record(stream)
+            torch.cuda.synchronize()
+            ts_.append(e0.elapsed_time(e1))
+        return statistics.median(ts_)
+
+    cut = cdf.cutpoint(m)
+    cb_out = torch.empty_like(out)
+    cut.sample(xi, cb_out, binary=True)
+    torch.cuda.synchronize()
+    cb_eq = bool(torch.equal(cb_out, out))
+    t_cb = time_call(lambda: cut.sample(xi, cb_out, binary=True), max(2, min(3, K)))
+    S_lin = min(S, 1 << 26)  # bounded: the linear scan is unbounded on skewed cells
+    cl_out = torch.empty(S_lin, dtype=torch.int32, device=dev)
+    cut.sample(xi[:S_lin], cl_out, binary=False)
+    torch.cuda.synchronize()
+    cl_eq = bool(torch.equal(cl_out, out[:S_lin]))
+    t_cl = time_call(lambda: cut.sample(xi[:S_lin], cl_out, binary=False), 2)
+    if world > 1:
+        t = torch.tensor([t_cb, t_cl], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        t_cb, t_cl = t.tolist()
+    cutbin_gs = world * S / (t_cb * 1e-3) / 1e9
+    cutlin_gs = world * S_lin / (t_cl * 1e-3) / 1e9
+
     # ------------------------------------------------ load statistics (E[visits], avg_32)
     loads = forest.sample_loads(xi[: 1 << 20]).double()
     e_loads = loads.mean().item()
@@ -311,6 +343,12 @@ def run_gpu(args):
                      "bsearch": {"value": round(bsearch_gs, 4), "unit": "G samples/s",
                                  "ms_per_batch": round(tbs, 4), "identical_indices": eq},
                      "speedup_vs_bsearch": round(sample_gs / bsearch_gs, 3),
+                     "cutpoint_binary": {"value": round(cutbin_gs, 4), "unit": "G samples/s",
+                                         "ms_per_batch": round(t_cb, 4), "cells": m,
+                                         "identical_indices": cb_eq},
+                     "cutpoint_linear": {"value": round(cutlin_gs, 4), "unit": "G samples/s",
+                                         "ms_per_batch": round(t_cl, 4), "samples": S_lin,
+                                         "identical_indices": cl_eq},
                      "loads_per_sample": {"avg": round(e_loads, 4), "avg32": round(avg32, 4),
                                           "max": max_loads, "of": 1 << 20}},
         "roofline": {"kernel": "k_sample (Alg. 2)", "bound": "hbm",
@@ -333,7 +371,8 @@ def run_gpu(args):
     if e2e:
         result["e2e"] = e2e
     if rank == 0 and not args.no_cpu_baseline:
-        result["cpu_baseline"] = cpu_baseline(p_host, m, xi[: 1 << 22].cpu().numpy().view(np.uint32))
+        result["cpu_baseline"] = cpu_baseline(p_host, m, xi[: 1 << 22].cpu().numpy().view(np.uint32),
+                                              cdf.cdf.cpu().numpy().view(np.uint64))
     if world > 1:
         dist.barrier()
         dist.destroy_process_group()
@@ -441,8 +480,10 @@ def run_gpu_c4(args):
         print(json.dumps(result), flush=True)
 
 
-def cpu_baseline(p_host, m, xi_sample):
-    """The CPU oracle as it stands (single thread), on a bounded sample."""
+def cpu_baseline(p_host, m, xi_sample, cdf_host):
+    """The CPU oracle as it stands (single thread), on a bounded sample; plus
+    the OpenMP binary search (baselines/cpu_bsearch.c) on the same CDF."""
+    import baselines
     import oracle
     n = p_host.size
     reps, tb = 0, 0.0
@@ -454,11 +495,20 @@ def cpu_baseline(p_host, m, xi_sample):
     t0 = time.perf_counter()
     f.sample(xi_sample)
     tsm = time.perf_counter() - t0
+    baselines.bsearch(cdf_host, xi_sample[:1024])  # warm-up (thread pool)
+    xs = np.tile(xi_sample, 4)
+    t0 = time.perf_counter()
+    baselines.bsearch(cdf_host, xs)
+    tbs = time.perf_counter() - t0
     return {"value": round(n * reps / tb / 1e9, 6), "unit": "G entries/s", "cores": 1,
             "kind": "oracle",
             "sample": f"{reps} full oracle builds of the same n={n} input; sampling "
                       f"{xi_sample.size} of the same xi",
-            "sampling": {"value": round(xi_sample.size / tsm / 1e9, 6), "unit": "G samples/s"}}
+            "sampling": {"value": round(xi_sample.size / tsm / 1e9, 6), "unit": "G samples/s"},
+            "bsearch_openmp": {"value": round(xs.size / tbs / 1e9, 6), "unit": "G samples/s",
+                               "cores": baselines.threads(),
+                               "sample": f"{xs.size} xi, binary search on the full u64 CDF "
+                                         "(baselines/cpu_bsearch.c)"}}
 
 
 # ============================================================================ reference arm

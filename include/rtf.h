@@ -179,6 +179,19 @@ int rtf_build_cdf(const float *p, uint32_t n, uint64_t *cdf, rtf_header *header,
 int rtf_sample_bsearch(const uint64_t *cdf, uint32_t n, const rtf_header *header,
                        const uint32_t *xi, uint64_t count, int32_t *out, void *stream);
 
+/* Cutpoint baselines (guide table of the classic cutpoint method, Sec.2.3
+ * P:168-232; the "cutpoint + linear / binary" rows of Table 1) on
+ * the same full CDF.  rtf_build_cutpoint: cut[g] (u32[m + 1], device) = the
+ * index the smallest xi of cell g maps to (cut[m] = n - 1), one binary search
+ * per cell.  rtf_sample_cutpoint: out[k] as rtf_sample_bsearch, by a linear
+ * scan upwards from cut[g] (binary = 0; unbounded on skewed inputs -- the
+ * degenerate case the paper sets out to avoid) or a binary search in
+ * [cut[g], cut[g + 1]] (binary = 1).  Asynchronous on `stream`. */
+int rtf_build_cutpoint(const uint64_t *cdf, uint32_t n, uint32_t m, uint32_t *cut, void *stream);
+int rtf_sample_cutpoint(const uint64_t *cdf, uint32_t n, const rtf_header *header,
+                        const uint32_t *cut, uint32_t m, int binary, const uint32_t *xi,
+                        uint64_t count, int32_t *out, void *stream);
+
 /* ------------------------------------------- host-buffer entry points */
 
 /* End-to-end build from HOST weights: copies p_host (pinned for full speed)

@@ -245,6 +245,31 @@ class Cdf:
         return out
 
 
+    def cutpoint(self, m: int, stream=None) -> "Cutpoint":
+        """The cutpoint table (m cells) over this CDF, for the cutpoint baselines."""
+        return Cutpoint(self, m, stream)
+
+
+class Cutpoint:
+    """Classic cutpoint guide table over a Cdf (baselines of Sec.2.3 / Table 1)."""
+
+    def __init__(self, cdf: Cdf, m: int, stream=None):
+        self.cdf, self.m = cdf, int(m)
+        self.cut = torch.empty(self.m + 1, dtype=torch.int32, device=cdf.cdf.device)
+        check(lib().rtf_build_cutpoint(_ptr(cdf.cdf), cdf.n, self.m, _ptr(self.cut),
+                                       _stream(stream)), "rtf_build_cutpoint")
+
+    def sample(self, xi: torch.Tensor, out=None, binary: bool = True, stream=None):
+        xi = _u32_view(xi)
+        if out is None:
+            out = torch.empty(xi.numel(), dtype=torch.int32, device=xi.device)
+        check(lib().rtf_sample_cutpoint(_ptr(self.cdf.cdf), self.cdf.n, _ptr(self.cdf.header),
+                                        _ptr(self.cut), self.m, int(binary), _ptr(xi),
+                                        xi.numel(), _ptr(out), _stream(stream)),
+              "rtf_sample_cutpoint")
+        return out
+
+
 def build_cdf(p: torch.Tensor, stream=None) -> Cdf:
     return Cdf(p.numel(), p.device).build(p, stream)
 

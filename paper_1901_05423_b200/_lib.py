@@ -50,6 +50,8 @@ PROTOTYPES = {
     "rtf_sample_rows": (_I32, [_F, _P, _P, _U64, _P, _P]),
     "rtf_build_cdf": (_I32, [_P, _U32, _P, _P, _P, _SZ, _P]),
     "rtf_sample_bsearch": (_I32, [_P, _U32, _P, _P, _U64, _P, _P]),
+    "rtf_build_cutpoint": (_I32, [_P, _U32, _U32, _P, _P]),
+    "rtf_sample_cutpoint": (_I32, [_P, _U32, _P, _P, _U32, _I32, _P, _U64, _P, _P]),
     "rtf_build_host": (_I32, [_P, _U32, _U32, _U32, _P, _P, _SZ, _P, _SZ, _P, _F, _H]),
     "rtf_sample_host": (_I32, [_F, _P, _U64, _P, _P, _P, _U64, _P]),
     "rtf_philox_u32": (_I32, [_U64, _U64, _U64, _P, _P]),

@@ -222,6 +222,28 @@ int rtf_sample_bsearch(const uint64_t* cdf, uint32_t n, const rtf_header* header
     return finish(e, launches);
 }
 
+int rtf_build_cutpoint(const uint64_t* cdf, uint32_t n, uint32_t m, uint32_t* cut, void* stream) {
+    if (!cdf || !cut) return RTF_EINVAL;
+    if (int s = check_nm(n, m)) return s;
+    if (m == 0xffffffffu) return RTF_ETOOLARGE;
+    int launches = 0;
+    cudaError_t e = rtf::launch_cutpoint_build(cdf, n, m, cut, as_stream(stream), &launches);
+    return finish(e, launches);
+}
+
+int rtf_sample_cutpoint(const uint64_t* cdf, uint32_t n, const rtf_header* header,
+                        const uint32_t* cut, uint32_t m, int binary, const uint32_t* xi,
+                        uint64_t count, int32_t* out, void* stream) {
+    if (!cdf || !header || !cut) return RTF_EINVAL;
+    if (int s = check_nm(n, m)) return s;
+    if (count && (!xi || !out)) return RTF_EINVAL;
+    if ((((uintptr_t)xi | (uintptr_t)out) & 3u) != 0) return RTF_EINVAL;
+    int launches = 0;
+    cudaError_t e = rtf::launch_cutpoint(cdf, n, header, cut, m, binary != 0, xi, count, out,
+                                         as_stream(stream), &launches);
+    return finish(e, launches);
+}
+
 int rtf_build_host(const float* p_host, uint32_t n, uint32_t m, uint32_t flags, float* p_dev,
                    void* forest_buf, size_t forest_bytes, void* ws, size_t ws_bytes, void* stream,
                    rtf_forest* out, rtf_header* header_host) {

@@ -22,6 +22,7 @@
 
 #include "rtf_device.cuh"
 #include "rtf_internal.h"
+#include <atomic>
 #include <cstdlib>
 
 namespace rtf {
@@ -31,7 +32,7 @@ constexpr uint32_t kChunk = 2048;   // longer runs: queued in chunks of this man
 constexpr uint32_t kMaxGrid = 8192; // partials capacity (CTAs of the cooperative grid)
 
 // workspace counters
-enum : int { kCtrGridBar = 0, kCtrQueue = 1, kCtrTile = 2 };
+enum : int { kCtrGridBar = 0, kCtrQueue = 1, kCtrTile = 2, kCtrRpre = 3 };
 
 struct RunChunk {
     uint32_t start, len;
@@ -80,6 +81,8 @@ struct BuildArgs {
     uint32_t* counters;
     Pfx* excl;          // per tile: exclusive prefix within its range (phase B)
     Pfx* rng;           // per range of tiles: total (phase B)
+    Pfx* rpre;          // per range of tiles: exclusive prefix (phase C, CTA 0)
+    uint32_t epoch;     // this launch's number: CTA 0 publishes rpre with it
     rtf_header* hdr;
     rtf_node* nodes;
     int32_t* table;
@@ -301,7 +304,7 @@ __global__ void __launch_bounds__(THREADS, MINB) k_build(BuildArgs A) {
     __shared__ int32_t s_l[2 * NW];
     __shared__ uint64_t s_key_after;
     __shared__ uint32_t s_red[2 * NW];
-    __shared__ Pfx s_grp[THREADS];  // exclusive prefix of each group of `per` tiles
+    __shared__ __align__(16) Pfx s_rpre;  // the next tile's range prefix (issuer thread)
     __shared__ Pfx s_tot;
     __shared__ uint32_t s_next;
     __shared__ __align__(16) Pfx s_pin;  // TMA target: the next tile's prefix within its range
@@ -517,10 +520,12 @@ __global__ void __launch_bounds__(THREADS, MINB) k_build(BuildArgs A) {
     RTF_TICK(1);
 
     // ---------------------------------------------------------- C: spine (every CTA)
-    // Each CTA scans the NRG range totals itself (a few KB from L2) and keeps
-    // the exclusive prefix of every range in shared memory; a tile's prefix
-    // is its range's combined with its exclusive prefix within the range.
+    // Each CTA scans the NRG range totals itself (a few KB from L2) for the
+    // total; CTA 0 publishes the exclusive prefix of every range (rpre, then
+    // the epoch flag).  A tile's prefix is its range's combined with its
+    // exclusive prefix within the range.
     Pfx total{0ull, 0u, -1};
+    Pfx gpre{0ull, 0u, -1};  // thread tid: the exclusive prefix of range tid
     if (ph & (kPhSpine | kPhTiles)) {
         const Pfx own = tid < NRG ? ld_pfx_cg(&A.rng[tid]) : Pfx{0ull, 0u, -1};
         uint64_t w_ex, w_tot;
@@ -528,7 +533,7 @@ __global__ void __launch_bounds__(THREADS, MINB) k_build(BuildArgs A) {
         int32_t l_ex;
         block_scan3_excl<THREADS>(own.W, own.cnt, own.last, w_ex, c_ex, l_ex, w_tot, c_tot, s_w,
                                   s_c, s_l);
-        s_grp[tid] = Pfx{w_ex, c_ex, l_ex};
+        gpre = Pfx{w_ex, c_ex, l_ex};
         if (tid == THREADS - 1) {
             s_tot = Pfx{w_tot, c_tot, max(l_ex, own.last)};
             // sharded: this shard's total, for the cross-GPU scan of shard totals
@@ -550,8 +555,22 @@ __global__ void __launch_bounds__(THREADS, MINB) k_build(BuildArgs A) {
             tot = combine(tot, s);
         }
         total = tot;
-        s_grp[tid] = combine(shard_pre, s_grp[tid]);  // group prefixes become global
+        gpre = combine(shard_pre, gpre);  // range prefixes become global
     }
+    if ((ph & kPhTiles) && b == 0) {  // publish the range prefixes (read in phase D)
+        if (tid < NRG) st_pfx(&A.rpre[tid], gpre);
+        __syncthreads();
+        if (tid == 0) {
+            __threadfence();
+            st_release_u32(&A.counters[kCtrRpre], A.epoch);
+        }
+    }
+    // the range prefixes of CTA 0 are visible once the flag carries this epoch
+    auto wait_rpre = [&]() {
+        if (tid == 0)
+            while (ld_acquire_u32(&A.counters[kCtrRpre]) != A.epoch) __nanosleep(32);
+        __syncthreads();
+    };
     // T and its reciprocal (one thread per CTA); CTA 0 publishes the header
     const uint64_t T = total.W;  // >= 1: the largest weight quantises to >= 2^B
     Norm nm;
@@ -578,9 +597,12 @@ __global__ void __launch_bounds__(THREADS, MINB) k_build(BuildArgs A) {
     nm.v = s_recip;
 
     // exclusive prefix of tile t: its range's, then its own within the range
-    auto tile_prefix = [&](uint32_t t) -> Pfx { return combine(s_grp[t / krng], ld_pfx_cg(&A.excl[t])); };
+    auto tile_prefix = [&](uint32_t t) -> Pfx {
+        return combine(ld_pfx_cg(&A.rpre[t / krng]), ld_pfx_cg(&A.excl[t]));
+    };
 
     if (CDF) {  // baseline: K[i] = floor(W_i 2^63 / T) for every entry, zeros included
+        wait_rpre();
         for (uint32_t t = b; t < nt; t += G) {
             const Pfx pre = tile_prefix(t);
             const uint32_t first = t * TILE + tid * VPT;
@@ -627,7 +649,7 @@ __global__ void __launch_bounds__(THREADS, MINB) k_build(BuildArgs A) {
         fence_proxy_async_global();  // phase B's prefixes, read by TMA below
         if (ph & kPhTiles) ticket = G + atomicAdd(&A.counters[kCtrTile], 1u);
     }
-    __syncthreads();
+    if (ph & kPhTiles) wait_rpre();
     for (uint32_t t = b; (ph & kPhTiles) && t < nt; t = s_next) {
         const uint32_t first = t * TILE + tid * VPT;  // local index into p (global: + ib)
 
@@ -637,7 +659,7 @@ __global__ void __launch_bounds__(THREADS, MINB) k_build(BuildArgs A) {
         if (tma_tile(t)) {
             mbar_wait(&s_bar, phase);
             phase ^= 1u;
-            pre = combine(s_grp[t / krng], t == b ? ld_pfx_cg(&A.excl[t]) : s_pin);
+            pre = t == b ? tile_prefix(t) : combine(s_rpre, s_pin);
 #pragma unroll
             for (int k = 0; k < VPT; k += 4) {
                 const float4 v = *reinterpret_cast<const float4*>(s_p + tid * VPT + k);
@@ -929,7 +951,10 @@ __global__ void __launch_bounds__(THREADS, MINB) k_build(BuildArgs A) {
                 tma_load_1d(s_p, A.p + (size_t)nx * TILE, TILE * 4, &s_bar);
                 tma_load_1d(&s_pin, A.excl + nx, (uint32_t)sizeof(Pfx), &s_bar);
             }
-            if (nx < nt) ticket = G + atomicAdd(&A.counters[kCtrTile], 1u);
+            if (nx < nt) {
+                s_rpre = ld_pfx_cg(&A.rpre[nx / krng]);  // read at the next tile's step (0)
+                ticket = G + atomicAdd(&A.counters[kCtrTile], 1u);
+            }
         }
         // (6) node records, coalesced 16 B
         {
@@ -1137,6 +1162,7 @@ size_t build_workspace_layout(uint32_t n, uint32_t m, uint32_t flags, WsLayout* 
     L->total = take(16);
     L->excl = take(sizeof(Pfx) * (size_t)nt);
     L->rng = take(sizeof(Pfx) * 1024);  // <= THREADS ranges
+    L->rpre = take(sizeof(Pfx) * 1024);
     // a sharded finish links count x nt_max rows; shards are 4096-entry aligned
     const uint32_t cap = sharded ? (uint32_t)(((uint64_t)n_global + tile - 1) / tile) +
                                        (4096u / tile) * kMaxShards
@@ -1216,6 +1242,9 @@ cudaError_t launch_build(const float* p, uint32_t n, uint32_t m, uint32_t flags,
     A.counters = reinterpret_cast<uint32_t*>(w + L.counters);
     A.excl = reinterpret_cast<Pfx*>(w + L.excl);
     A.rng = reinterpret_cast<Pfx*>(w + L.rng);
+    A.rpre = reinterpret_cast<Pfx*>(w + L.rpre);
+    static std::atomic<uint32_t> s_epoch{0};
+    A.epoch = 1u + s_epoch.fetch_add(1u, std::memory_order_relaxed) % 0xfffffffeu;  // never 0
     A.hdr = hdr;
     A.nodes = nodes;
     A.table = table;
@@ -1229,6 +1258,8 @@ cudaError_t launch_build(const float* p, uint32_t n, uint32_t m, uint32_t flags,
                      : launch_fused<512, 8, true>(A, st, launches);
     // 512 x 8 at 2 CTAs/SM measured best on B200 (vs 512x8 @1, 256x16 @2,
     // 1024x4 @1: 336 vs 399 / 352 / 403 us for config 3)
+    // (2048-entry tiles at 4 or 3 CTAs/SM and 1024-entry tiles at 8 CTAs/SM
+    // were measured again with the fused kernel: 293 / 315 / 399 us for c3)
     return small ? launch_fused<64, 4, false>(A, st, launches)
                  : launch_fused<512, 8, false>(A, st, launches);
 }

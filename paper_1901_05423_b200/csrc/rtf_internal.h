@@ -34,7 +34,7 @@ struct WsLayout {
     uint32_t nt;  // tiles
     uint32_t qcap;
     uint32_t nt_cap;  // rows phase E can link (a sharded finish: all shards' tiles)
-    size_t maxpart, counters, scale, total, excl, rng, spine, tmax, bmax, queue, bytes;
+    size_t maxpart, counters, scale, total, excl, rng, rpre, spine, tmax, bmax, queue, bytes;
 };
 
 // one call of a sharded build (config 4); see rtf_shard_* in include/rtf.h
@@ -67,6 +67,13 @@ cudaError_t launch_sample_loads(const rtf_forest& f, const uint32_t* xi, uint64_
 cudaError_t launch_bsearch(const uint64_t* cdf, uint32_t n, const rtf_header* hdr,
                            const uint32_t* xi, uint64_t count, int32_t* out, cudaStream_t st,
                            int* launches);
+
+cudaError_t launch_cutpoint_build(const uint64_t* cdf, uint32_t n, uint32_t m, uint32_t* cut,
+                                  cudaStream_t st, int* launches);
+
+cudaError_t launch_cutpoint(const uint64_t* cdf, uint32_t n, const rtf_header* hdr,
+                            const uint32_t* cut, uint32_t m, bool binary, const uint32_t* xi,
+                            uint64_t count, int32_t* out, cudaStream_t st, int* launches);
 
 cudaError_t launch_philox(uint64_t seed, uint64_t start, uint64_t count, uint32_t* out,
                           cudaStream_t st, int* launches);

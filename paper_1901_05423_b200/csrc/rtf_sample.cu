@@ -166,6 +166,58 @@ __global__ void __launch_bounds__(kSampleThreads)
     }
 }
 
+// ------------------------------------------------------------ cutpoint baselines
+// The guide-table methods the paper compares against (Sec.2.3, Table 1
+// P:1458-1482): cut[g] = the answer for the smallest xi of cell g (an index
+// into the full CDF), then a linear scan (cutpoint + linear) or a binary
+// search bounded by cut[g+1] (cutpoint + binary).  Same fixed-point CDF and
+// the same results as k_bsearch / k_sample.
+
+__device__ __forceinline__ uint32_t last_le(const uint64_t* __restrict__ cdf, uint32_t base,
+                                            uint32_t len, uint64_t x63) {
+    while (len > 1) {  // last index in [base, base + len) with cdf <= x63
+        const uint32_t half = len >> 1;
+        if (__ldg(cdf + base + half) <= x63) base += half;
+        len -= half;
+    }
+    return base;
+}
+
+__global__ void k_cutpoint_build(const uint64_t* __restrict__ cdf, uint32_t n, uint32_t m,
+                                 uint32_t* __restrict__ cut) {
+    const uint32_t gs = gridDim.x * blockDim.x;
+    for (uint32_t g = blockIdx.x * blockDim.x + threadIdx.x; g <= m; g += gs) {
+        if (g == m) {
+            cut[m] = n - 1;
+            continue;
+        }
+        const uint64_t xmin = (((uint64_t)g << 32) + m - 1) / m;  // ceil(g 2^32 / m)
+        cut[g] = last_le(cdf, 0, n, xmin << 31);
+    }
+}
+
+template <bool BINARY>
+__global__ void __launch_bounds__(kSampleThreads)
+    k_sample_cutpoint(const uint64_t* __restrict__ cdf, uint32_t n,
+                      const rtf_header* __restrict__ hdr, const uint32_t* __restrict__ cut,
+                      uint32_t m, const uint32_t* __restrict__ xi, uint64_t count,
+                      int32_t* __restrict__ out) {
+    const uint64_t gs = (uint64_t)gridDim.x * blockDim.x;
+    const bool bad = hdr->status != 0;
+    for (uint64_t k = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; k < count; k += gs) {
+        const uint32_t x = xi[k];
+        const uint64_t x63 = (uint64_t)x << 31;
+        const uint32_t g = (uint32_t)(((uint64_t)x * m) >> 32);
+        uint32_t i = __ldg(cut + g);
+        if (BINARY) {
+            i = last_le(cdf, i, __ldg(cut + g + 1) - i + 1, x63);
+        } else {
+            while (i + 1 < n && __ldg(cdf + i + 1) <= x63) ++i;
+        }
+        out[k] = bad ? INT32_MAX : (int32_t)i;
+    }
+}
+
 // ------------------------------------------------------------ Philox4x32-10 input generator
 
 __device__ __forceinline__ uint4 philox4x32_10(uint4 c, uint32_t k0, uint32_t k1) {
@@ -243,6 +295,27 @@ cudaError_t launch_bsearch(const uint64_t* cdf, uint32_t n, const rtf_header* hd
     const bool vec = (((uintptr_t)xi | (uintptr_t)out) & 15u) == 0;
     k_bsearch<<<grid_for(vec ? (count + 3) / 4 : count), kSampleThreads, 0, st>>>(cdf, n, hdr, xi,
                                                                                   count, out, vec);
+    ++*launches;
+    return cudaGetLastError();
+}
+
+cudaError_t launch_cutpoint_build(const uint64_t* cdf, uint32_t n, uint32_t m, uint32_t* cut,
+                                  cudaStream_t st, int* launches) {
+    k_cutpoint_build<<<grid_for((uint64_t)m + 1), kSampleThreads, 0, st>>>(cdf, n, m, cut);
+    ++*launches;
+    return cudaGetLastError();
+}
+
+cudaError_t launch_cutpoint(const uint64_t* cdf, uint32_t n, const rtf_header* hdr,
+                            const uint32_t* cut, uint32_t m, bool binary, const uint32_t* xi,
+                            uint64_t count, int32_t* out, cudaStream_t st, int* launches) {
+    if (count == 0) return cudaSuccess;
+    if (binary)
+        k_sample_cutpoint<true><<<grid_for(count), kSampleThreads, 0, st>>>(cdf, n, hdr, cut, m,
+                                                                            xi, count, out);
+    else
+        k_sample_cutpoint<false><<<grid_for(count), kSampleThreads, 0, st>>>(cdf, n, hdr, cut, m,
+                                                                             xi, count, out);
     ++*launches;
     return cudaGetLastError();
 }

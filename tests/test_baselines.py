@@ -1,0 +1,41 @@
+"""The comparison baselines bench.py reports give the inverse-CDF answers of
+the oracle: the OpenMP binary search (CPU) here, the GPU cutpoint baselines in
+the -m gpu part."""
+import numpy as np
+import pytest
+
+import baselines
+import oracle
+from workloads import philox_xi, power_law, random_small
+
+
+def test_cpu_bsearch_matches_oracle():
+    rng = np.random.default_rng(31)
+    for n in (1, 2, 17, 5000, 70001):
+        p = random_small(rng, n, zero_frac=0.3, dyn=8.0)
+        K, _ = oracle.cdf_all(p)
+        xi = philox_xi(50000, seed=n)
+        assert np.array_equal(baselines.bsearch(K, xi), oracle.build(p, 64).sample(xi))
+
+
+@pytest.mark.gpu
+def test_gpu_cutpoint_baselines_match_oracle():
+    torch = pytest.importorskip("torch")
+    if not torch.cuda.is_available():
+        pytest.fail("CUDA device required for -m gpu tests")
+    import paper_1901_05423_b200 as rtf
+    rng = np.random.default_rng(32)
+    cases = [(random_small(rng, n, zero_frac=z, dyn=8.0), m)
+             for n, m, z in ((1, 1, 0.0), (17, 5, 0.3), (4097, 4096, 0.5), (70001, 333, 0.2))]
+    cases.append((power_law(1 << 18, "A"), 1 << 16))
+    for p, m in cases:
+        ref = oracle.build(p, m)
+        cdf = rtf.build_cdf(torch.from_numpy(p).cuda())
+        cut = cdf.cutpoint(m)
+        xi = np.concatenate([philox_xi(1 << 16, seed=m),
+                             ((np.arange(m, dtype=np.uint64) << 32) // m).astype(np.uint32)])
+        xd = torch.from_numpy(xi.view(np.int32)).cuda()
+        want = ref.sample(xi)
+        for binary in (True, False):
+            got = cut.sample(xd, binary=binary).cpu().numpy()
+            assert np.array_equal(got, want), (p.size, m, binary)
