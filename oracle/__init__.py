@@ -128,6 +128,57 @@ class Forest:
                            _ptr(loads) if with_loads else None)
         return (out, loads) if with_loads else out
 
+    def table2(self) -> np.ndarray:
+        """O13: the guide table with the paper's "exactly two intervals" flag
+        (Sec.3.2: "further information could also be stored in the
+        reference, such as a flag that there are exactly two intervals that
+        overlap the cell.  Then, only one comparison must be performed and
+        there is no need to explicitly store a node"; reading R18).  Entry
+        (key32, ref), from the O10 table, written out cell by cell:
+          * empty cell (table = ~i):              (0, ~i)
+          * a cell holding exactly one leaf a, overlapped by intervals a-1 and a,
+            with orig(a) = orig(a-1) + 1 (no zero weight between them):
+            (ceil(key_a / 2^31), ~orig(a)) -- xi < key32 means interval a-1,
+            whose reference ~orig(a-1) is ~orig(a) + 1;
+            if ceil(key_a / 2^31) = 2^32 no xi of the cell reaches a: (0, ~orig(a-1));
+            if a = 0 (key 0) every xi of the cell is in a: (0, ~orig(0))
+          * any other non-empty cell: (0, anchor a) -- the node of O10.
+        Sampling: ref >= 0 -> Alg. 2 from node ref; ref < 0 -> the leaf
+        ~(xi < key32 ? ref + 1 : ref)."""
+        out = np.zeros(self.m, dtype=TABLE2_DTYPE)
+        out["ref"] = self.table
+        leaves_per_cell = np.bincount(self.cell.astype(np.int64), minlength=self.m)
+        one = np.flatnonzero((self.table >= 0) & (leaves_per_cell == 1))  # two intervals
+        a = self.table[one].astype(np.int64)
+        kc = [-(-int(k) >> 31) for k in self.key[a]]  # ceil(key_a / 2^31), exact ints
+        for g, ai, c in zip(one.tolist(), a.tolist(), kc):
+            if c == 0:                      # a = 0: the cell lies inside interval a
+                out[g] = (0, ~int(self.orig[ai]))
+            elif c == 1 << 32:              # no xi of the cell reaches interval a
+                out[g] = (0, ~int(self.orig[ai - 1]))
+            elif int(self.orig[ai]) == int(self.orig[ai - 1]) + 1:
+                out[g] = (c, ~int(self.orig[ai]))
+        return out
+
+    def sample_table2(self, xi) -> np.ndarray:
+        """Alg. 2 through the O13 table: plain Python loop."""
+        t2 = self.table2()
+        rec = self.records()
+        out = np.empty(len(xi), dtype=np.int32)
+        for k, x in enumerate(np.asarray(xi, dtype=np.uint64).tolist()):
+            key32, ref = int(t2[(x * self.m) >> 32]["key32"]), int(t2[(x * self.m) >> 32]["ref"])
+            if ref < 0:
+                out[k] = ~(ref + 1 if x < key32 else ref)
+                continue
+            j = ref
+            while j >= 0:
+                j = int(rec[j]["c0"]) if (x << 31) < int(rec[j]["key"]) else int(rec[j]["c1"])
+            out[k] = ~j
+        return out
+
+
+TABLE2_DTYPE = np.dtype([("key32", "<u4"), ("ref", "<i4")])
+
 
 def build(p, m: int) -> Forest:
     """O1-O11 for one distribution."""

@@ -334,6 +334,62 @@ def test_brute_force_inverse_cdf():
         assert np.all(p[got] > 0)                  # zero weights never returned
 
 
+def test_table2_fig6_hand_derived(fig6):
+    """O13 on Fig. 6: cells 2, 6, 7, 8 hold exactly one leaf (6, 9, 10, 11; the
+    figure's cell lines) and are overlapped by exactly two intervals
+    (P:1335-1338): key32 = ceil(key_a / 2^31) with key_a = floor(W_a 2^63 / 113),
+    ref = ~a (no zero weights: orig = index).  Cells 0, 1, 3 keep their anchor,
+    the empty cells their leaf (the figure's table)."""
+    f = oracle.build(np.array(fig6["weights"], F32), fig6["m"])
+    W = np.concatenate([[0], np.cumsum(fig6["weights"])[:-1]]).tolist()
+    per_cell = np.bincount(fig6["cells"], minlength=fig6["m"])
+    want = []
+    for g, t in enumerate(fig6["table"]):
+        if t >= 0 and per_cell[g] == 1:
+            key = (int(W[t]) << 63) // 113
+            want.append((-(-key >> 31), ~t))
+        else:
+            want.append((0, t))
+    assert sorted(g for g in range(12) if per_cell[g] == 1) == [2, 6, 7, 8]
+    got = [(int(e["key32"]), int(e["ref"])) for e in f.table2()]
+    assert got == want
+
+
+def test_table2_special_cases():
+    # a = 0 alone in cell 0: the whole cell is interval 0 -> (0, ~0)
+    f = oracle.build(np.array([1.0, 1.0], F32), 2)
+    assert [(int(e["key32"]), int(e["ref"])) for e in f.table2()] == [(0, ~0), (1 << 31, ~1)]
+    # ceil(key_a / 2^31) = 2^32: no xi of cell 1 reaches interval 1 -> (0, ~0)
+    f = oracle.build(np.array([1.0, 1e-30], F32), 2)
+    assert int(f.key[1]) > (1 << 63) - (1 << 31)
+    assert [(int(e["key32"]), int(e["ref"])) for e in f.table2()][1] == (0, ~0)
+    assert f.sample(np.array([2**32 - 1], np.uint32)).tolist() == [0]
+    # a zero weight between the two intervals: no flag, the anchor stays
+    f = oracle.build(np.array([1.0, 0.0, 1.0], F32), 2)
+    assert [(int(e["key32"]), int(e["ref"])) for e in f.table2()][1] == (0, 1)
+
+
+def test_table2_descent_brute_force():
+    """Alg. 2 through the O13 table reaches the inverse-CDF definition
+    (exact integers) on every boundary, cell edge and random xi."""
+    rng = np.random.default_rng(23)
+    for t in range(80):
+        n = int(rng.integers(1, 40))
+        m = int(rng.integers(1, 3 * n + 2))
+        p = random_small(rng, n, zero_frac=float(rng.choice([0.0, 0.3])), dyn=float(rng.choice([1, 6, 16])))
+        f = oracle.build(p, m)
+        w, _, _ = oracle.quantize(p)
+        xs = set(rng.integers(0, 2**32, 64).tolist()) | {0, 2**32 - 1}
+        for k in f.key.tolist():
+            b = -(-int(k) >> 31)
+            xs |= {b - 1, b, b + 1}
+        xs |= {(g << 32) // m for g in range(m)} | {((g << 32) // m) - 1 for g in range(1, m)}
+        xs = np.array(sorted(x for x in xs if 0 <= x < 2**32), np.uint32)
+        got = f.sample_table2(xs)
+        for x, g in zip(xs.tolist(), got.tolist()):
+            assert g == _definition_index(w, x), (t, x)
+
+
 def test_stratified_histogram_closed_form():
     """For a full stratified set of N = 2^k points, interval j receives
     ceil(N key_{j+1}/2^63) - ceil(N key_j/2^63) points (key_{n'} = 2^63)."""
