@@ -257,18 +257,21 @@ def run_gpu(args):
     cutlin_gs = world * S_lin / (t_cl * 1e-3) / 1e9
 
     # ------------------------------------------------ load statistics (E[visits], avg_32)
-    loads = forest.sample_loads(xi[: 1 << 20]).double()
+    loads, loads_p = forest.sample_loads(xi[: 1 << 20], plain=True)
+    loads, loads_p = loads.double(), loads_p.double()
     e_loads = loads.mean().item()
     avg32 = loads.view(-1, 32).max(dim=1).values.mean().item()
     max_loads = int(loads.max().item())
+    e_loads_p = loads_p.mean().item()
+    avg32_p = loads_p.view(-1, 32).max(dim=1).values.mean().item()
 
     # ------------------------------------------------ roofline
     peak, peak_src = peaks()
     n_pos = forest.n_pos()
-    bytes_sample = 4 + 4 + 4 + 16 * (e_loads - 1.0)   # xi, out, table entry, visited records
+    bytes_sample = 4 + 4 + 8 + 16 * (e_loads - 1.0)   # xi, out, table cell, visited records
     t_sample_launch = ts / K * 1e-3
     ach_s = S * bytes_sample / t_sample_launch / 1e9
-    bytes_build = 4 * n + 16 * n_pos + 4 * m          # read p, write records, write table
+    bytes_build = 4 * n + 16 * n_pos + 8 * m          # read p, write records, write table
     t_build = tb / K * 1e-3
     ach_b = bytes_build / t_build / 1e9
 
@@ -350,7 +353,10 @@ def run_gpu(args):
                                          "ms_per_batch": round(t_cl, 4), "samples": S_lin,
                                          "identical_indices": cl_eq},
                      "loads_per_sample": {"avg": round(e_loads, 4), "avg32": round(avg32, 4),
-                                          "max": max_loads, "of": 1 << 20}},
+                                          "max": max_loads, "of": 1 << 20,
+                                          "without_two_interval_flag": {
+                                              "avg": round(e_loads_p, 4),
+                                              "avg32": round(avg32_p, 4)}}},
         "roofline": {"kernel": "k_sample (Alg. 2)", "bound": "hbm",
                      "achieved": round(ach_s, 2), "peak": peak, "unit": "GB/s",
                      "frac": round(ach_s / peak, 4),
@@ -454,7 +460,7 @@ def run_gpu_c4(args):
     build_gs = n * K / (tb * 1e-3) / 1e9
     sample_gs = S * world * K / (ts * 1e-3) / 1e9
     peak, peak_src = peaks()
-    bytes_build = 4 * n + 16 * forest.n_pos() + 4 * m
+    bytes_build = 4 * n + 16 * forest.n_pos() + 8 * m
     result = {
         "metric": METRIC, "value": round(build_gs, 4), "unit": "G entries/s", "n_gpus": world,
         "steps": K, "warmup": args.warmup, "ms_per_step": round((tb + ts) / K, 4),

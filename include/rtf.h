@@ -67,6 +67,21 @@ typedef struct rtf_node {
     int32_t child[2];  /* [0]: taken if xi 2^31 < key, [1]: otherwise          */
 } rtf_node;
 
+/* One guide-table cell, 8 bytes (Sec.3.2, reading R18):
+ *   ref >= 0: the anchor node of the cell; Alg. 2 descends from nodes[ref].
+ *   ref <  0: a leaf reference.  The cell is overlapped by one interval
+ *             (key32 == 0: the leaf is ~ref) or by exactly two intervals
+ *             ("a flag that there are exactly two intervals ... only one
+ *             comparison must be performed and there is no need to
+ *             explicitly store a node"): key32 = ceil(key_a /
+ *             2^31) of the cell's only leaf a, and xi < key32 selects interval
+ *             a-1, whose reference is ref + 1 (orig(a) = orig(a-1) + 1).
+ * A cell whose single leaf a follows a zero weight keeps its anchor. */
+typedef struct rtf_ref {
+    uint32_t key32;  /* 0, or the two-interval split ceil(key_a / 2^31) */
+    int32_t ref;     /* anchor node (>= 0) or leaf reference ~i (< 0)   */
+} rtf_ref;
+
 /* Device-resident build summary (one per row for batched forests). */
 typedef struct rtf_header {
     uint64_t total;      /* T = sum of quantised weights, 0 < T < 2^63            */
@@ -86,7 +101,7 @@ typedef struct rtf_forest {
     uint32_t rows;   /* 1, or the number of independent rows (batched)    */
     uint32_t flags;  /* build flags                                       */
     rtf_node *nodes; /* rows * n records (the first n_pos of each row valid) */
-    int32_t *table;  /* rows * m references: >= 0 anchor node, < 0 leaf ~i */
+    rtf_ref *table;  /* rows * m guide-table cells (rtf_ref)              */
     rtf_header *header; /* rows headers                                  */
 } rtf_forest;
 
@@ -148,18 +163,22 @@ int rtf_forest_status(const rtf_forest *f, void *stream, rtf_header *headers_hos
 /* ------------------------------------------------------------ sampling */
 
 /* Alg. 2 for count samples: out[k] = the ORIGINAL index i with
- * key_i <= xi[k] 2^31 < key_next (guide-table lookup g = floor(xi m / 2^32),
- * then descent while the reference is a node).  Read-only on the forest, so
+ * key_i <= xi[k] 2^31 < key_next (guide-table lookup g = floor(xi m / 2^32);
+ * a leaf cell answers at once, a two-interval cell with its one comparison;
+ * else descent while the reference is a node).  Read-only on the forest, so
  * concurrent calls on one forest are safe.  xi / out need 4-byte alignment
  * (16-byte alignment enables vector access). */
 int rtf_sample(const rtf_forest *f, const uint32_t *xi, uint64_t count, int32_t *out,
                void *stream);
 
-/* Measurement aid: loads[k] = number of memory loads Alg. 2 performs for
+/* Measurement aid: loads[k] = number of memory loads rtf_sample performs for
  * xi[k] (1 guide-table entry + 1 per node visited), the load-count convention
- * of Table 1.  Gives E[visits], the maximum and average_32. */
+ * of Table 1; gives E[visits], the maximum and average_32.
+ * loads_plain (may be NULL) receives the count without the two-interval flag
+ * (a flagged cell would cost its anchor visit: 2 loads), i.e. the paper's own
+ * structure. */
 int rtf_sample_loads(const rtf_forest *f, const uint32_t *xi, uint64_t count, int32_t *loads,
-                     void *stream);
+                     int32_t *loads_plain, void *stream);
 
 /* Batched: sample k uses row[k] (< f->rows); out is row-local. */
 int rtf_sample_rows(const rtf_forest *f, const uint32_t *row, const uint32_t *xi,
@@ -221,9 +240,10 @@ int rtf_sample_host(const rtf_forest *f, const uint32_t *xi_host, uint64_t count
  *      (the cross-GPU scan of per-shard totals: every shard derives its prefix
  *       and the grand total T from the gathered totals, on the device)
  *   3. rtf_shard_build            -> this shard's node records [J_r, J_r + n'_r),
- *      guide-table cells (others INT32_MIN) and one spine row per tile
+ *      guide-table cells (others {0, INT32_MIN}) and one spine row per tile
  *      (view.spine: nt_local rows of view.spine_row_bytes)
- *   4. replicate records (broadcast from each owner), MAX-reduce the table,
+ *   4. replicate records (broadcast from each owner), MAX-reduce the table as
+ *      int64 words (ref in the high half),
  *      gather the spine rows of all shards, shard r's at rows
  *      [r * nt_max, r * nt_max + nt_local_r) (nt_max = the largest nt_local;
  *      pad with zero bytes: a row with zero leaves is skipped)

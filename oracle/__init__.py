@@ -145,20 +145,7 @@ class Forest:
           * any other non-empty cell: (0, anchor a) -- the node of O10.
         Sampling: ref >= 0 -> Alg. 2 from node ref; ref < 0 -> the leaf
         ~(xi < key32 ? ref + 1 : ref)."""
-        out = np.zeros(self.m, dtype=TABLE2_DTYPE)
-        out["ref"] = self.table
-        leaves_per_cell = np.bincount(self.cell.astype(np.int64), minlength=self.m)
-        one = np.flatnonzero((self.table >= 0) & (leaves_per_cell == 1))  # two intervals
-        a = self.table[one].astype(np.int64)
-        kc = [-(-int(k) >> 31) for k in self.key[a]]  # ceil(key_a / 2^31), exact ints
-        for g, ai, c in zip(one.tolist(), a.tolist(), kc):
-            if c == 0:                      # a = 0: the cell lies inside interval a
-                out[g] = (0, ~int(self.orig[ai]))
-            elif c == 1 << 32:              # no xi of the cell reaches interval a
-                out[g] = (0, ~int(self.orig[ai - 1]))
-            elif int(self.orig[ai]) == int(self.orig[ai - 1]) + 1:
-                out[g] = (c, ~int(self.orig[ai]))
-        return out
+        return table2_of(self.table, self.key, self.orig, self.cell, self.m)
 
     def sample_table2(self, xi) -> np.ndarray:
         """Alg. 2 through the O13 table: plain Python loop."""
@@ -175,6 +162,25 @@ class Forest:
                 j = int(rec[j]["c0"]) if (x << 31) < int(rec[j]["key"]) else int(rec[j]["c1"])
             out[k] = ~j
         return out
+
+
+def table2_of(table, key, orig, cell, m) -> np.ndarray:
+    """O13 for one distribution's O10 table, keys, original indices and cells
+    (see Forest.table2)."""
+    out = np.zeros(m, dtype=TABLE2_DTYPE)
+    out["ref"] = table
+    leaves_per_cell = np.bincount(cell.astype(np.int64), minlength=m)
+    one = np.flatnonzero((table >= 0) & (leaves_per_cell == 1))  # two intervals
+    a = table[one].astype(np.int64)
+    kc = [-(-int(k) >> 31) for k in key[a]]  # ceil(key_a / 2^31), exact ints
+    for g, ai, c in zip(one.tolist(), a.tolist(), kc):
+        if c == 0:                  # a = 0: the cell lies inside interval a
+            out[g] = (0, ~int(orig[ai]))
+        elif c == 1 << 32:          # no xi of the cell reaches interval a
+            out[g] = (0, ~int(orig[ai - 1]))
+        elif int(orig[ai]) == int(orig[ai - 1]) + 1:
+            out[g] = (c, ~int(orig[ai]))
+    return out
 
 
 TABLE2_DTYPE = np.dtype([("key32", "<u4"), ("ref", "<i4")])

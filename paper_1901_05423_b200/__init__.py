@@ -28,6 +28,7 @@ __all__ = ["Forest", "RowsForest", "build", "build_rows", "sample", "sample_rows
            "launch_count", "RtfError", "lib"]
 
 NODE_DTYPE = np.dtype([("key", "<u8"), ("c0", "<i4"), ("c1", "<i4")])
+CELL_DTYPE = np.dtype([("key32", "<u4"), ("ref", "<i4")])  # rtf_ref
 
 
 def lib():
@@ -112,13 +113,16 @@ class Forest:
                                _stream(stream)), "rtf_sample")
         return out
 
-    def sample_loads(self, xi: torch.Tensor, stream=None) -> torch.Tensor:
-        """Per-sample memory loads of Alg. 2 (1 table entry + nodes visited)."""
+    def sample_loads(self, xi: torch.Tensor, stream=None, plain: bool = False):
+        """Per-sample memory loads of Alg. 2 (1 table cell + nodes visited);
+        with plain=True also the count without the two-interval flag."""
         xi = _u32_view(xi)
         out = torch.empty(xi.numel(), dtype=torch.int32, device=xi.device)
+        op = torch.empty_like(out) if plain else None
         check(lib().rtf_sample_loads(ctypes.byref(self.view), _ptr(xi), xi.numel(), _ptr(out),
-                                     _stream(stream)), "rtf_sample_loads")
-        return out
+                                     _ptr(op) if plain else None, _stream(stream)),
+              "rtf_sample_loads")
+        return (out, op) if plain else out
 
     # ---------------------------------------------------------------- inspection
     def header(self, stream=None) -> rtf_header:
@@ -145,7 +149,8 @@ class Forest:
         return raw.view(NODE_DTYPE)
 
     def table_numpy(self) -> np.ndarray:
-        return self._section(self.view.table, 4 * self.m).cpu().numpy().view(np.int32)
+        """The guide table as (key32, ref) cells (rtf_ref)."""
+        return self._section(self.view.table, 8 * self.m).cpu().numpy().view(CELL_DTYPE)
 
 
 class RowsForest:
@@ -194,7 +199,7 @@ class RowsForest:
         return self._section(self.view.nodes, 16 * self.rows * self.n).cpu().numpy().view(NODE_DTYPE)
 
     def table_numpy(self) -> np.ndarray:
-        return self._section(self.view.table, 4 * self.rows * self.m).cpu().numpy().view(np.int32)
+        return self._section(self.view.table, 8 * self.rows * self.m).cpu().numpy().view(CELL_DTYPE)
 
 
 # -------------------------------------------------------------------- functional API

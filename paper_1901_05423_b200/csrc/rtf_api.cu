@@ -27,7 +27,7 @@ ForestLayout forest_layout(uint32_t n, uint32_t m, uint32_t rows) {
     L.nodes = off;
     off += align_up(sizeof(rtf_node) * (size_t)n * rows);
     L.table = off;
-    off += align_up(sizeof(int32_t) * (size_t)m * rows);
+    off += align_up(sizeof(rtf_ref) * (size_t)m * rows);
     L.total = off;
     return L;
 }
@@ -104,7 +104,7 @@ int rtf_forest_view(void* buf, size_t bytes, uint32_t n, uint32_t m, uint32_t ro
     out->flags = 0;
     out->header = reinterpret_cast<rtf_header*>(b + L.header);
     out->nodes = reinterpret_cast<rtf_node*>(b + L.nodes);
-    out->table = reinterpret_cast<int32_t*>(b + L.table);
+    out->table = reinterpret_cast<rtf_ref*>(b + L.table);
     return RTF_OK;
 }
 
@@ -177,12 +177,14 @@ int rtf_sample(const rtf_forest* f, const uint32_t* xi, uint64_t count, int32_t*
 }
 
 int rtf_sample_loads(const rtf_forest* f, const uint32_t* xi, uint64_t count, int32_t* loads,
-                     void* stream) {
+                     int32_t* loads_plain, void* stream) {
     if (!f || !f->nodes || !f->table || !f->header || f->rows != 1) return RTF_EINVAL;
     if (count && (!xi || !loads)) return RTF_EINVAL;
-    if ((((uintptr_t)xi | (uintptr_t)loads) & 3u) != 0) return RTF_EINVAL;
+    if ((((uintptr_t)xi | (uintptr_t)loads | (uintptr_t)loads_plain) & 3u) != 0)
+        return RTF_EINVAL;
     int launches = 0;
-    cudaError_t e = rtf::launch_sample_loads(*f, xi, count, loads, as_stream(stream), &launches);
+    cudaError_t e = rtf::launch_sample_loads(*f, xi, count, loads, loads_plain,
+                                             as_stream(stream), &launches);
     return finish(e, launches);
 }
 

@@ -91,6 +91,12 @@ __device__ __forceinline__ float4 ld_stream_f4(const float* p) {
                        __uint_as_float(r.w));
 }
 
+__device__ __forceinline__ float4 ld_stream_f4_pol(const float* p, uint64_t pol) {
+    uint4 r = ld_stream_u4_pol(p, pol);
+    return make_float4(__uint_as_float(r.x), __uint_as_float(r.y), __uint_as_float(r.z),
+                       __uint_as_float(r.w));
+}
+
 // ------------------------------------------------------------ TMA bulk copies + mbarrier
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -125,6 +131,16 @@ __device__ __forceinline__ void tma_load_1d(void* dst, const void* src, uint32_t
         "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::
             "r"(smem_u32(dst)),
         "l"(src), "r"(bytes), "r"(smem_u32(bar))
+        : "memory");
+}
+
+// the same with an L2 cache policy (e.g. evict_first for a last read)
+__device__ __forceinline__ void tma_load_1d_pol(void* dst, const void* src, uint32_t bytes,
+                                                uint64_t* bar, uint64_t pol) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint "
+        "[%0], [%1], %2, [%3], %4;" ::"r"(smem_u32(dst)),
+        "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(pol)
         : "memory");
 }
 
@@ -237,6 +253,26 @@ __device__ __forceinline__ uint32_t cell_of(uint64_t key, uint32_t m) {
 
 __device__ __forceinline__ uint32_t split_level(uint64_t a, uint64_t b) {
     return 63u - (uint32_t)__clzll((long long)(a ^ b));  // msb(a ^ b)
+}
+
+// ------------------------------------------------------------ guide-table cells
+
+// Guide-table cell of a cell holding exactly one leaf a (rtf_ref, the
+// two-interval flag of P:1335-1338; reading R18): key32 = ceil(key_a / 2^31)
+// splits the cell between intervals a-1 and a when their references are
+// consecutive (no zero weight between them); key32 = 0 marks a cell inside a
+// single interval; otherwise the anchor node a stays.
+__device__ __forceinline__ uint2 single_leaf_cell(uint64_t key_a, int32_t orig_a,
+                                                  int32_t orig_prev, int32_t anchor) {
+    const uint64_t kc = (key_a + 0x7fffffffull) >> 31;  // key_a < 2^63: no overflow
+    if (kc == 0) return make_uint2(0u, (uint32_t)~orig_a);           // a = 0
+    if (kc == (1ull << 32)) return make_uint2(0u, (uint32_t)~orig_prev);  // a unreachable
+    if (orig_a == orig_prev + 1) return make_uint2((uint32_t)kc, (uint32_t)~orig_a);
+    return make_uint2(0u, (uint32_t)anchor);
+}
+
+__device__ __forceinline__ void st_cell(rtf_ref* table, uint32_t g, uint32_t key32, int32_t ref) {
+    *reinterpret_cast<uint2*>(table + g) = make_uint2(key32, (uint32_t)ref);
 }
 
 // ------------------------------------------------------------ scan prefix payload

@@ -50,19 +50,20 @@ size_t build_workspace_layout(uint32_t n, uint32_t m, uint32_t flags, WsLayout* 
 size_t spine_row_bytes();       // bytes of one tile-spine row
 
 cudaError_t launch_build(const float* p, uint32_t n, uint32_t m, uint32_t flags, rtf_header* hdr,
-                         rtf_node* nodes, int32_t* table, uint64_t* cdf, void* ws,
+                         rtf_node* nodes, rtf_ref* table, uint64_t* cdf, void* ws,
                          const WsLayout& L, cudaStream_t st, int* launches,
                          const ShardCall* sc = nullptr);
 
 cudaError_t launch_build_rows(const float* p, uint32_t rows, uint32_t n_row, uint32_t m_row,
-                              rtf_header* hdr, rtf_node* nodes, int32_t* table, cudaStream_t st,
+                              rtf_header* hdr, rtf_node* nodes, rtf_ref* table, cudaStream_t st,
                               int* launches);
 
 cudaError_t launch_sample(const rtf_forest& f, const uint32_t* row, const uint32_t* xi,
                           uint64_t count, int32_t* out, cudaStream_t st, int* launches);
 
 cudaError_t launch_sample_loads(const rtf_forest& f, const uint32_t* xi, uint64_t count,
-                                int32_t* loads, cudaStream_t st, int* launches);
+                                int32_t* loads, int32_t* loads_plain, cudaStream_t st,
+                                int* launches);
 
 cudaError_t launch_bsearch(const uint64_t* cdf, uint32_t n, const rtf_header* hdr,
                            const uint32_t* xi, uint64_t count, int32_t* out, cudaStream_t st,

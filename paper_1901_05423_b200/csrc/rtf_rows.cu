@@ -16,7 +16,7 @@ struct RowsArgs {
     uint32_t rows, n_row, m_row;
     rtf_header* hdr;
     rtf_node* nodes;
-    int32_t* table;
+    rtf_ref* table;
     bool vec;
 };
 
@@ -168,13 +168,21 @@ __global__ void __launch_bounds__(THREADS) k_build_rows(RowsArgs A) {
         for (int w2 = 0; w2 < warp; ++w2) before = max(before, s_wmax[w2]);
         int32_t run = max(before, __shfl_up_sync(0xffffffffu, inc, 1));
         if (lane == 0) run = before;
-        int32_t* tab = A.table + (size_t)r * m;
+        rtf_ref* tab = A.table + (size_t)r * m;
 #pragma unroll
         for (int k = 0; k < MPT; ++k) {
             const uint32_t g = g0 + k;
             if (g < m) {
                 const int32_t a = s_anc[g];
-                tab[g] = a >= 0 ? a : ~s_orig[run];
+                if (a < 0) {
+                    st_cell(tab, g, 0u, ~s_orig[run]);
+                } else if (s_lst[g] == a) {  // one leaf: two intervals
+                    const uint2 e = single_leaf_cell(s_rec[a].key, s_orig[a],
+                                                     s_orig[a ? a - 1 : 0], a);
+                    st_cell(tab, g, e.x, (int32_t)e.y);
+                } else {
+                    st_cell(tab, g, 0u, a);
+                }
                 run = max(run, s_lst[g]);
             }
         }
@@ -237,7 +245,7 @@ static cudaError_t launch_rows_t(const RowsArgs& A, cudaStream_t st) {
 }
 
 cudaError_t launch_build_rows(const float* p, uint32_t rows, uint32_t n_row, uint32_t m_row,
-                              rtf_header* hdr, rtf_node* nodes, int32_t* table, cudaStream_t st,
+                              rtf_header* hdr, rtf_node* nodes, rtf_ref* table, cudaStream_t st,
                               int* launches) {
     RowsArgs A;
     A.p = p;

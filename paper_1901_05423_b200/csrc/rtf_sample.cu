@@ -24,9 +24,17 @@ __device__ __forceinline__ int32_t descend_step(const rtf_node* __restrict__ nod
     return (int32_t)(x63 < r.x ? (uint32_t)r.y : (uint32_t)(r.y >> 32));
 }
 
+// Alg. 2's first step on a guide-table cell (rtf_ref): a node reference, or a
+// leaf that a two-interval cell (key32 != 0) splits with one comparison.
+__device__ __forceinline__ int32_t cell_step(const rtf_ref* __restrict__ table, uint32_t m,
+                                             uint32_t x) {
+    const int2 e = __ldg(reinterpret_cast<const int2*>(table) + (uint32_t)(((uint64_t)x * m) >> 32));
+    return (e.y >= 0 || x >= (uint32_t)e.x) ? e.y : e.y + 1;
+}
+
 template <bool ROWS>
 __device__ __forceinline__ int32_t sample_one(const rtf_node* __restrict__ nodes,
-                                              const int32_t* __restrict__ table,
+                                              const rtf_ref* __restrict__ table,
                                               const rtf_header* __restrict__ hdr, uint32_t n,
                                               uint32_t m, uint32_t r, uint32_t x) {
     if (ROWS) {
@@ -34,27 +42,25 @@ __device__ __forceinline__ int32_t sample_one(const rtf_node* __restrict__ nodes
         nodes += (size_t)r * n;
         table += (size_t)r * m;
     }
-    int32_t j = __ldg(table + (uint32_t)(((uint64_t)x * m) >> 32));
+    int32_t j = cell_step(table, m, x);
     const uint64_t x63 = (uint64_t)x << 31;
     for (int d = 0; j >= 0 && d < kMaxVisits; ++d) j = descend_step(nodes, j, x63);
     return j >= 0 ? kCorrupt : ~j;
 }
 
-// COUNT: write the number of memory loads per sample (1 table entry + 1 per
-// node visited; the load-count convention of Table 1) instead of
-// the index -- a measurement aid for E[visits], max and average_32.
-template <bool ROWS, bool COUNT = false>
+template <bool ROWS>
 __global__ void __launch_bounds__(kSampleThreads)
-    k_sample(const rtf_node* __restrict__ nodes, const int32_t* __restrict__ table,
+    k_sample(const rtf_node* __restrict__ nodes, const rtf_ref* __restrict__ table,
              const rtf_header* __restrict__ hdr, uint32_t n, uint32_t m,
              const uint32_t* __restrict__ row, const uint32_t* __restrict__ xi, uint64_t count,
              int32_t* __restrict__ out, bool vec) {
     const uint64_t gt = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
     const uint64_t gs = (uint64_t)gridDim.x * blockDim.x;
     const bool bad = !ROWS && hdr->status != 0;
-    // (L2 evict-first on the xi/out streams with evict-last on the forest was
-    // measured slower: 8.0 vs 7.4 ms for config 3 -- the kernel is bound by L2
-    // sector throughput of the random table/record reads, not by eviction)
+    // The kernel is bound by the L1TEX -> L2 request rate (about one request
+    // per clock per SM for scattered loads; ncu): what counts
+    // is loads per sample, which the two-interval cells cut.  (L2 evict-first
+    // on the xi/out streams was measured slower: 8.0 vs 7.4 ms for config 3.)
     uint64_t done = 0;
     if (vec) {
         const uint64_t nq = count >> 2;
@@ -71,7 +77,7 @@ __global__ void __launch_bounds__(kSampleThreads)
 #pragma unroll
             for (int k = 0; k < 4; ++k) {
                 const rtf_node* nk = nodes;
-                const int32_t* tk = table;
+                const rtf_ref* tk = table;
                 dead[k] = bad;
                 if (ROWS) {
                     dead[k] = hdr[rr[k]].status != 0;
@@ -80,21 +86,12 @@ __global__ void __launch_bounds__(kSampleThreads)
                 }
                 nb[k] = nk;
                 x63[k] = (uint64_t)x[k] << 31;
-                j[k] = dead[k] ? -1 : __ldg(tk + (uint32_t)(((uint64_t)x[k] * m) >> 32));
+                j[k] = dead[k] ? -1 : cell_step(tk, m, x[k]);
             }
-            int32_t loads[4] = {1, 1, 1, 1};
             for (int it = 0; (j[0] & j[1] & j[2] & j[3]) >= 0 && it < kMaxVisits; ++it) {
 #pragma unroll
                 for (int k = 0; k < 4; ++k)
-                    if (j[k] >= 0) {
-                        j[k] = descend_step(nb[k], j[k], x63[k]);
-                        if (COUNT) ++loads[k];
-                    }
-            }
-            if (COUNT) {
-                __stcs(reinterpret_cast<int4*>(out + 4 * q),
-                       make_int4(loads[0], loads[1], loads[2], loads[3]));
-                continue;
+                    if (j[k] >= 0) j[k] = descend_step(nb[k], j[k], x63[k]);
             }
             int4 o;
             o.x = dead[0] ? INT32_MAX : (j[0] >= 0 ? kCorrupt : ~j[0]);
@@ -107,16 +104,27 @@ __global__ void __launch_bounds__(kSampleThreads)
     }
     for (uint64_t k = done + gt; k < count; k += gs) {
         const uint32_t r = ROWS ? row[k] : 0u;
-        if (COUNT) {
-            const rtf_node* nk = nodes + (ROWS ? (size_t)r * n : 0);
-            int32_t j = __ldg(table + (ROWS ? (size_t)r * m : 0) +
-                              (uint32_t)(((uint64_t)xi[k] * m) >> 32));
-            int32_t l = 1;
-            for (; j >= 0 && l <= kMaxVisits; ++l) j = descend_step(nk, j, (uint64_t)xi[k] << 31);
-            out[k] = l;
-            continue;
-        }
         out[k] = bad ? INT32_MAX : sample_one<ROWS>(nodes, table, hdr, n, m, r, xi[k]);
+    }
+}
+
+// Load counts (a measurement aid, not the sampler): 1 table cell + 1 per node
+// visited (Table 1's convention); loads_plain: the same without
+// the two-interval flag, where a flagged cell costs its anchor visit too.
+__global__ void __launch_bounds__(kSampleThreads)
+    k_sample_loads(const rtf_node* __restrict__ nodes, const rtf_ref* __restrict__ table,
+                   uint32_t m, const uint32_t* __restrict__ xi, uint64_t count,
+                   int32_t* __restrict__ loads, int32_t* __restrict__ loads_plain) {
+    const uint64_t gs = (uint64_t)gridDim.x * blockDim.x;
+    for (uint64_t k = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; k < count; k += gs) {
+        const uint32_t x = xi[k];
+        const uint32_t g = (uint32_t)(((uint64_t)x * m) >> 32);
+        const bool flagged = table[g].key32 != 0;
+        int32_t j = cell_step(table, m, x);
+        int32_t l = 1;
+        for (; j >= 0 && l <= kMaxVisits; ++l) j = descend_step(nodes, j, (uint64_t)x << 31);
+        loads[k] = l;
+        if (loads_plain) loads_plain[k] = l + (flagged ? 1 : 0);
     }
 }
 
@@ -279,11 +287,11 @@ cudaError_t launch_sample(const rtf_forest& f, const uint32_t* row, const uint32
 }
 
 cudaError_t launch_sample_loads(const rtf_forest& f, const uint32_t* xi, uint64_t count,
-                                int32_t* loads, cudaStream_t st, int* launches) {
+                                int32_t* loads, int32_t* loads_plain, cudaStream_t st,
+                                int* launches) {
     if (count == 0) return cudaSuccess;
-    const bool vec = (((uintptr_t)xi | (uintptr_t)loads) & 15u) == 0;
-    k_sample<false, true><<<grid_for(vec ? (count + 3) / 4 : count), kSampleThreads, 0, st>>>(
-        f.nodes, f.table, f.header, f.n, f.m, nullptr, xi, count, loads, vec);
+    k_sample_loads<<<grid_for(count), kSampleThreads, 0, st>>>(f.nodes, f.table, f.m, xi, count,
+                                                              loads, loads_plain);
     ++*launches;
     return cudaGetLastError();
 }

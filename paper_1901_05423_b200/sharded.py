@@ -143,7 +143,9 @@ class Shard:
         return self._forest_slice(self.fview.nodes + 16 * j0, 16 * cnt)
 
     def table_words(self):
-        return self._forest_slice(self.fview.table, 4 * self.m).view(torch.int32)
+        # 8-B cells {u32 key32, i32 ref} as little-endian int64: ref is the high
+        # half, so a MAX-reduction keeps the owner's cell over {0, INT32_MIN}
+        return self._forest_slice(self.fview.table, 8 * self.m).view(torch.int64)
 
     def spine_bytes(self):
         return self._ws_slice(self.view.spine, self.view.spine_row_bytes * self.view.nt_local)

@@ -30,7 +30,7 @@ def _inputs(rank):
     return {
         "scale": torch.randint(0, 2**31 - 1, (4,), generator=g, dtype=torch.int32),
         "total": torch.randint(0, 255, (16,), generator=g, dtype=torch.uint8),
-        "table": torch.randint(-2**31, 2**31 - 1, (1000,), generator=g, dtype=torch.int32),
+        "table": torch.randint(-2**63, 2**63 - 1, (1000,), generator=g, dtype=torch.int64),
         "pend": torch.randint(0, 255, (64,), generator=g, dtype=torch.uint8),
         "records": torch.randint(0, 255, (16 * 37,), generator=g, dtype=torch.uint8),
         "nt": torch.tensor([3 + rank], dtype=torch.int64),

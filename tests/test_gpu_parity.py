@@ -42,7 +42,8 @@ def assert_forest_equal(f, ref, what=""):
     bad = np.flatnonzero((nodes["c0"] != ref.child0) | (nodes["c1"] != ref.child1))
     assert bad.size == 0, f"{what}: {bad.size} node records differ, first at {bad[:5]}"
     tab = f.table_numpy()
-    badt = np.flatnonzero(tab != ref.table)
+    want = ref.table2()
+    badt = np.flatnonzero((tab["ref"] != want["ref"]) | (tab["key32"] != want["key32"]))
     assert badt.size == 0, f"{what}: {badt.size} table cells differ, first at {badt[:5]}"
 
 
@@ -231,7 +232,7 @@ def test_config5_rows_full(rtf):
     assert np.array_equal(nodes["key"][valid], ref["key"][valid])
     assert np.array_equal(nodes["c0"][valid], ref["child0"][valid])
     assert np.array_equal(nodes["c1"][valid], ref["child1"][valid])
-    assert np.array_equal(f.table_numpy(), ref["table"])
+    assert_cells_equal(f.table_numpy(), rows_table2(ref, rows, n_row, m_row), "rows")
     # sampling (row, xi) pairs against per-row oracle forests
     rng = np.random.default_rng(2)
     r = rng.integers(0, rows, 1 << 16).astype(np.uint32)
@@ -241,6 +242,24 @@ def test_config5_rows_full(rtf):
         sel = r == k
         fr = oracle.build(p[k], m_row)
         assert np.array_equal(got[sel], fr.sample(xi[sel]))
+
+
+def rows_table2(ref, rows, n_row, m_row, ok=None):
+    """O13 per row from the oracle's batched build (each row independent, R15)."""
+    out = np.zeros(rows * m_row, dtype=[("key32", "<u4"), ("ref", "<i4")])
+    for r in range(rows):
+        if ok is None or ok[r]:
+            k = int(ref["n_pos"][r])
+            sl = slice(r * n_row, r * n_row + k)
+            out[r * m_row:(r + 1) * m_row] = oracle.table2_of(
+                ref["table"][r * m_row:(r + 1) * m_row], ref["key"][sl], ref["orig"][sl],
+                ref["cell"][sl], m_row)
+    return out
+
+
+def assert_cells_equal(got, want, what=""):
+    bad = np.flatnonzero((got["ref"] != want["ref"]) | (got["key32"] != want["key32"]))
+    assert bad.size == 0, f"{what}: {bad.size} table cells differ, first at {bad[:5]}"
 
 
 def test_rows_random_shapes(rtf):
@@ -262,7 +281,8 @@ def test_rows_random_shapes(rtf):
         assert np.array_equal(nodes["c0"][valid], ref["child0"][valid])
         assert np.array_equal(nodes["c1"][valid], ref["child1"][valid])
         tab = f.table_numpy().reshape(rows, m_row)
-        assert np.array_equal(tab[ok], ref["table"].reshape(rows, m_row)[ok])
+        want = rows_table2(ref, rows, n_row, m_row, ok).reshape(rows, m_row)
+        assert_cells_equal(tab[ok].reshape(-1), want[ok].reshape(-1), f"rows {n_row}x{m_row}")
         r = np.repeat(np.arange(rows, dtype=np.uint32), 64)
         xi = philox_xi(r.size, seed=n_row)
         got = f.sample(dev_u32(r), dev_u32(xi)).cpu().numpy()

@@ -32,6 +32,7 @@ def _check(rtf, p, m, count):
     want_nodes = single.nodes_numpy().tobytes()
     want_table = single.table_numpy().tobytes()
     assert np.array_equal(single.nodes_numpy()["c1"], ref.child1)
+    assert want_table == ref.table2().tobytes()
     for s in shards:
         f = rtf.Forest.from_buffer(s.n_global, m, s.forest)
         assert f.status() == 0
