@@ -23,11 +23,30 @@ with open(os.path.join(P, f"{R}_launches.csv"), "w", newline="") as f:
         if len(r) > vi and r[mi] == "gpu__time_duration.sum":
             w.writerow([r[ii], r[ki][:90], f"{float(r[vi].replace(',', '')) / 1000:.2f}"])
 
-# full capture
-out = subprocess.run(["ncu", "-i", os.path.join(G, f"{R}_full.ncu-rep"), "--page", "raw", "--csv"],
-                     capture_output=True, text=True).stdout
-rows = list(csv.reader(io.StringIO(out)))
-h, units = rows[0], rows[1]
+# full captures: the main-path kernels (tools/gpu_ncu_main.sh) and the baselines
+# (tools/gpu_round_profile.sh)
+rows, h, units = [], None, None
+for rep in (f"{R}_build.ncu-rep", f"{R}_sample.ncu-rep", f"{R}_full.ncu-rep"):
+    if not os.path.exists(os.path.join(G, rep)):
+        continue
+    out = subprocess.run(["ncu", "-i", os.path.join(G, rep), "--page", "raw", "--csv"],
+                         capture_output=True, text=True).stdout
+    rr = list(csv.reader(io.StringIO(out)))
+    if h is None:
+        h, units = rr[0], rr[1]
+        rows = [h, units]
+    idx = [rr[0].index(c) if c in rr[0] else None for c in h]
+    sc = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
+    for r in rr[2:]:
+        row = []
+        for c, i in zip(h, idx):
+            v = r[i] if i is not None else ""
+            if c.startswith("dram__bytes_") and v:  # per-report units -> bytes
+                v = str(int(float(v.replace(",", "")) * sc.get(rr[1][i], 1)))
+            row.append(v)
+        rows.append(row)
+for c in ("dram__bytes_read.sum", "dram__bytes_write.sum"):
+    units[h.index(c)] = "byte"
 want = ["Kernel Name", "gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum",
         "gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed", "lts__t_sector_hit_rate.pct",
         "sm__throughput.avg.pct_of_peak_sustained_elapsed", "sm__inst_executed.avg.per_cycle_elapsed",
@@ -46,7 +65,7 @@ with open(os.path.join(P, f"{R}_ncu_full.csv"), "w", newline="") as f:
         name = r[h.index("Kernel Name")].replace("void ", "").replace("rtf::", "")
         rd = float(r[h.index("dram__bytes_read.sum")].replace(",", "")) * scale.get(units[h.index("dram__bytes_read.sum")], 1)
         wr = float(r[h.index("dram__bytes_write.sum")].replace(",", "")) * scale.get(units[h.index("dram__bytes_write.sum")], 1)
-        key = "k_sample" if name.startswith("k_sample<0, 0>") else \
+        key = "k_sample_2^28" if name.startswith("k_sample<0>") else \
               "build" if name.startswith("k_build") else "k_bsearch" if name.startswith("k_bsearch") else None
         if key and key not in tr:
             tr[key] = int(rd + wr)
