@@ -47,6 +47,9 @@ WORKLOADS = {
                desc="config 4: n=2^28 spiky (4 spikes x 0.24 + uniform 0.04), m=2^22; sharded "
                     "build (cross-GPU scan of shard totals) + replication; 2^32 Philox xi split "
                     "over the GPUs"),
+    "c5": dict(name="c5_rows", n=65536 * 1024, m=1024, rows=65536, n_row=1024, samples=1 << 26,
+               desc="config 5: 65536 independent rows of n=1024 (p = exp(3 N(0,1)), every 16th row "
+                    "4 spikes), m_row=1024, one CTA per row; 2^26 (row, Philox xi) samples"),
 }
 
 
@@ -56,6 +59,9 @@ def make_p(wl):
         return power_law(wl["n"], "A")
     if wl["name"] == "c4_spikes":
         return spikes(wl["n"])
+    if wl["name"] == "c5_rows":
+        from workloads import rows_lognormal
+        return rows_lognormal(wl["rows"], wl["n_row"])
     return env_map()
 
 
@@ -489,6 +495,102 @@ def run_gpu_c4(args):
         print(json.dumps(result), flush=True)
 
 
+def run_gpu_c5(args):
+    """Config 5: batched rebuilds of 65536 independent rows (rtf_build_rows, one CTA
+    per row, everything in shared memory) + sampling (row, xi) pairs.  Rows are
+    independent, so N GPUs each take their own 65536 rows (weak scaling)."""
+    import torch
+    import torch.distributed as dist
+
+    import paper_1901_05423_b200 as rtf
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    wl = WORKLOADS["c5"]
+    rows, n_row, m_row = wl["rows"], wl["n_row"], wl["m"]
+    S = args.samples or wl["samples"]
+    p_host = make_p(wl)
+    p = torch.from_numpy(p_host).to(dev)
+    forest = rtf.RowsForest(rows, n_row, m_row, device=dev)
+    row = torch.from_numpy((np.arange(S, dtype=np.uint64) * 2654435761 % rows)
+                           .astype(np.uint32).view(np.int32)).to(dev)
+    xi = rtf.philox(S, seed=0x5EED, start=rank * S, device=dev)
+    out = torch.empty(S, dtype=torch.int32, device=dev)
+    flush = torch.empty(L2_FLUSH_BYTES, dtype=torch.uint8, device=dev)
+    stream = torch.cuda.current_stream()
+
+    def step(ev=None):
+        if ev:
+            ev[0].record(stream)
+        forest.build(p)
+        if ev:
+            ev[1].record(stream)
+        forest.sample(row, xi, out)
+        if ev:
+            ev[2].record(stream)
+
+    for _ in range(args.warmup):
+        step()
+        flush.zero_()
+    torch.cuda.synchronize()
+    forest.headers()
+    assert forest.last_status == 0
+    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(args.steps)]
+    sampler = ClockSampler(local)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    l0 = rtf.launch_count()
+    with sampler:
+        for k in range(args.steps):
+            step(evs[k])
+            flush.zero_()
+        torch.cuda.synchronize()
+    launches = rtf.launch_count() - l0
+    tb = sum(e[0].elapsed_time(e[1]) for e in evs)
+    ts = sum(e[1].elapsed_time(e[2]) for e in evs)
+    if world > 1:
+        t = torch.tensor([tb, ts], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        tb, ts = t.tolist()
+    K = args.steps
+    N = rows * n_row
+    build_gs = world * N * K / (tb * 1e-3) / 1e9
+    sample_gs = world * S * K / (ts * 1e-3) / 1e9
+    peak, peak_src = peaks()
+    n_pos = int(forest.headers()["n_pos"].astype(np.int64).sum())
+    bytes_build = 4 * N + 16 * n_pos + 8 * m_row * rows
+    ach_b = bytes_build / (tb / K * 1e-3) / 1e9
+    result = {
+        "metric": METRIC, "value": round(build_gs, 4), "unit": "G entries/s", "n_gpus": world,
+        "steps": K, "warmup": args.warmup, "ms_per_step": round((tb + ts) / K, 4),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u64",
+        "data": "synthetic",
+        "config": {"workload": wl["desc"], "rows": rows, "n_row": n_row, "m_row": m_row,
+                   "samples_per_gpu": S,
+                   "l2": f"flushed between steps ({L2_FLUSH_BYTES >> 20} MiB write, untimed)",
+                   "parallelism": f"replicas x{world}: each GPU builds its own rows"},
+        "build": {"value": round(build_gs, 4), "unit": "G entries/s", "ms_per_build": round(tb / K, 5)},
+        "sampling": {"value": round(sample_gs, 4), "unit": "G samples/s",
+                     "ms_per_batch": round(ts / K, 4)},
+        "roofline_build": {"kernel": "k_build_rows (one CTA per row)", "bound": "hbm",
+                           "achieved": round(ach_b, 2), "peak": peak, "unit": "GB/s",
+                           "frac": round(ach_b / peak, 4), "traffic": None,
+                           "algorithmic_bytes_per_launch": bytes_build, "peak_source": peak_src},
+        "gpu_launches": launches, "clocks": sampler.summary(),
+    }
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+    if rank == 0:
+        print(json.dumps(result), flush=True)
+
+
 def cpu_baseline(p_host, m, xi_sample, cdf_host):
     """The CPU oracle as it stands (single thread), on a bounded sample; plus
     the OpenMP binary search (baselines/cpu_bsearch.c) on the same CDF."""
@@ -582,6 +684,8 @@ def main():
         run_reference(args)
     elif args.workload == "c4":
         run_gpu_c4(args)
+    elif args.workload == "c5":
+        run_gpu_c5(args)
     else:
         run_gpu(args)
 
