@@ -834,6 +834,16 @@ __global__ void __launch_bounds__(THREADS, MINB) k_build(BuildArgs A) {
                                     pend |= 1u << r;
                                     rightbits |= (right ? 1u : 0u) << r;
                                 }
+                            } else {
+                                // a one-leaf cell: exactly two intervals overlap it
+                                // (P:1335-1338); slot q = l holds its key and the
+                                // anchor's left child ~orig(l-1)
+                                const uint64_t key = s_key[q];
+                                const int32_t a = (int32_t)(j0 + l);
+                                const uint2 e =
+                                    single_leaf_cell(key, (int32_t)(first + k) + ib, ~s_c0[q], a);
+                                if ((int32_t)e.y != a)
+                                    st_cell(A.table, cell_of(key, m), e.x, (int32_t)e.y);
                             }
                         }
                     }
@@ -973,14 +983,6 @@ __global__ void __launch_bounds__(THREADS, MINB) k_build(BuildArgs A) {
                 const uint64_t key = s_key[q];
                 gnode[l] = make_uint4((uint32_t)key, (uint32_t)(key >> 32), (uint32_t)s_c0[q],
                                       (uint32_t)s_c1[q]);
-                // an anchor (a wall before it) that is also its cell's last leaf (a
-                // wall after it): the cell is overlapped by exactly two intervals
-                // (P:1335-1338); its root is the leaf itself (child 1 of slot l)
-                if (l && s_lam[pad8(l - 1)] == kLamBoundary && s_lam[q] == kLamBoundary) {
-                    const int32_t a = (int32_t)(j0 + l);
-                    const uint2 e = single_leaf_cell(key, ~s_c1[q], ~s_c0[q], a);
-                    if ((int32_t)e.y != a) st_cell(A.table, cell_of(key, m), e.x, (int32_t)e.y);
-                }
             }
         }
         __syncthreads();  // spines complete; keys and children are free
