@@ -13,6 +13,7 @@ DESIGN.md section 3 for the readings (R1..R17) and the pin of each function.
 from __future__ import annotations
 
 import ctypes
+import math
 import os
 import subprocess
 from dataclasses import dataclass
@@ -233,3 +234,99 @@ def build_rows(p, rows: int, n_row: int, m_row: int):
     _load().orc_build_rows(_ptr(p), rows, n_row, m_row, *(_ptr(out[k]) for k in (
         "key", "orig", "cell", "lam", "child0", "child1", "table", "T", "n_pos", "status")))
     return out
+
+
+# ---------------------------------------------------------------- 2-D (Sec.6)
+
+def _f32_floor_log2(x: np.float32) -> int:
+    """floor(log2 x) of a positive finite float32, from its bits (O2)."""
+    b = int(np.float32(x).view(np.uint32))
+    e = (b >> 23) & 0xFF
+    if e:
+        return e - 127
+    return (b & 0x7FFFFF).bit_length() - 1 - 149
+
+
+def marginal_weights(p2d) -> np.ndarray:
+    """O14: the row weights of a 2-D distribution (Sec.6: "first
+    calculating the cumulative distribution function of the image rows").  Row
+    y's quantised mass is T_y 2^(E_y - B_y) (O2-O5 applied to the row alone,
+    reading R15); with K = max over non-empty rows of E_y - B_y the weight is
+    q_y = float32(float64(T_y) * 2^(E_y - B_y - K)) (two round-to-nearest steps,
+    reading R19); an all-zero row gets 0."""
+    p2d = np.ascontiguousarray(np.asarray(p2d, dtype=np.float32))
+    H, W = p2d.shape
+    B = 62 - max(0, (W - 1).bit_length())
+    T, k = [], []
+    for y in range(H):
+        row = p2d[y]
+        if not np.any(row > 0):
+            T.append(0)
+            k.append(None)
+            continue
+        f = build(row, 1)
+        T.append(int(f.T))
+        k.append(_f32_floor_log2(row.max()) - B)
+    K = max(v for v in k if v is not None)
+    q = np.zeros(H, np.float32)
+    for y in range(H):
+        if T[y]:
+            q[y] = np.float32(math.ldexp(float(T[y]), k[y] - K))
+    return q
+
+
+def _f32_rz(d: float) -> np.float32:
+    """float64 -> float32 rounded toward zero."""
+    f = np.float32(d)
+    if abs(float(f)) > abs(d):
+        f = np.nextafter(f, np.float32(0))
+    return f
+
+
+@dataclass
+class Forest2D:
+    """O14-O15: marginal forest over the row weights + one conditional forest
+    per row (Sec.6)."""
+    W: int
+    H: int
+    marginal: Forest
+    rows: list  # Forest per row (None for an all-zero row)
+
+    def _interval(self, f: Forest, idx: int, xi: int) -> float:
+        """Relative position of xi inside interval idx of forest f (the
+        sub-pixel rescale of P:1526-1528): float64(xi 2^31 - key_j) /
+        float64(key_{j+1} - key_j), each integer rounded to nearest once."""
+        j = int(np.flatnonzero(f.orig == idx)[0])
+        lo = int(f.key[j])
+        hi = int(f.key[j + 1]) if j + 1 < f.n_pos else ONE
+        return float((xi << 31) - lo) / float(hi - lo)
+
+    def sample(self, xi1, xi2):
+        """O15: y = marginal^-1(xi1); x = row_y^-1(xi2); the continuous position
+        ((x + v) / W, (y + u) / H) in float64, rounded toward zero to float32
+        (so it stays below 1, reading R19), u and v the relative
+        positions inside the chosen intervals.  Returns (pixel = y W + x,
+        pos float32[N, 2] as (x, y))."""
+        xi1 = np.asarray(xi1, dtype=np.uint32)
+        xi2 = np.asarray(xi2, dtype=np.uint32)
+        ys = self.marginal.sample(xi1)
+        pix = np.empty(xi1.size, np.int32)
+        pos = np.empty((xi1.size, 2), np.float32)
+        for k in range(xi1.size):
+            y = int(ys[k])
+            fr = self.rows[y]
+            x = int(fr.sample(xi2[k:k + 1])[0])
+            u = self._interval(self.marginal, y, int(xi1[k]))
+            v = self._interval(fr, x, int(xi2[k]))
+            pix[k] = y * self.W + x
+            pos[k, 0] = _f32_rz((float(x) + v) / float(self.W))
+            pos[k, 1] = _f32_rz((float(y) + u) / float(self.H))
+        return pix, pos
+
+
+def build_2d(p2d, m_x: int, m_y: int) -> Forest2D:
+    p2d = np.ascontiguousarray(np.asarray(p2d, dtype=np.float32))
+    H, W = p2d.shape
+    q = marginal_weights(p2d)
+    rows = [build(p2d[y], m_x) if np.any(p2d[y] > 0) else None for y in range(H)]
+    return Forest2D(W, H, build(q, m_y), rows)
