@@ -47,6 +47,11 @@ WORKLOADS = {
                desc="config 4: n=2^28 spiky (4 spikes x 0.24 + uniform 0.04), m=2^22; sharded "
                     "build (cross-GPU scan of shard totals) + replication; 2^32 Philox xi split "
                     "over the GPUs"),
+    "c2d": dict(name="c2_envmap_2d", n=2048 * 1024, m=2048, W=2048, H=1024, my=1024,
+                samples=1 << 26,
+                desc="2-D (Sec.6 P:1523-1529): the 2048x1024 env map as marginal over rows "
+                     "(my=1024 cells) + 1024 row forests (mx=2048 cells); 2^26 Philox (xi1, xi2) "
+                     "pairs -> pixel + sub-pixel position"),
     "c5": dict(name="c5_rows", n=65536 * 1024, m=1024, rows=65536, n_row=1024, samples=1 << 26,
                desc="config 5: 65536 independent rows of n=1024 (p = exp(3 N(0,1)), every 16th row "
                     "4 spikes), m_row=1024, one CTA per row; 2^26 (row, Philox xi) samples"),
@@ -495,6 +500,93 @@ def run_gpu_c4(args):
         print(json.dumps(result), flush=True)
 
 
+def run_gpu_2d(args):
+    """2-D sampling: build = rtf_build_2d (rows, row weights,
+    marginal), sample = rtf_sample_2d with positions.  Replicas for N > 1."""
+    import torch
+    import torch.distributed as dist
+
+    import paper_1901_05423_b200 as rtf
+    from workloads import env_map
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    wl = WORKLOADS["c2d"]
+    W, H, mx, my = wl["W"], wl["H"], wl["m"], wl["my"]
+    S = args.samples or wl["samples"]
+    p = torch.from_numpy(env_map(W, H)).to(dev)
+    f = rtf.Forest2D(W, H, mx, my, device=dev)
+    xi1 = rtf.philox(S, seed=0x5EED, start=2 * rank * S, device=dev)
+    xi2 = rtf.philox(S, seed=0x5EED, start=(2 * rank + 1) * S, device=dev)
+    pix = torch.empty(S, dtype=torch.int32, device=dev)
+    pos = torch.empty((S, 2), dtype=torch.float32, device=dev)
+    flush = torch.empty(L2_FLUSH_BYTES, dtype=torch.uint8, device=dev)
+    stream = torch.cuda.current_stream()
+
+    def step(ev=None):
+        if ev:
+            ev[0].record(stream)
+        f.build(p)
+        if ev:
+            ev[1].record(stream)
+        f.sample(xi1, xi2, pix, pos)
+        if ev:
+            ev[2].record(stream)
+
+    for _ in range(args.warmup):
+        step()
+        flush.zero_()
+    torch.cuda.synchronize()
+    assert f.status() == 0
+    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(args.steps)]
+    sampler = ClockSampler(local)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    l0 = rtf.launch_count()
+    with sampler:
+        for k in range(args.steps):
+            step(evs[k])
+            flush.zero_()
+        torch.cuda.synchronize()
+    launches = rtf.launch_count() - l0
+    tb = sum(e[0].elapsed_time(e[1]) for e in evs)
+    ts = sum(e[1].elapsed_time(e[2]) for e in evs)
+    if world > 1:
+        t = torch.tensor([tb, ts], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        tb, ts = t.tolist()
+    K = args.steps
+    build_gs = world * W * H * K / (tb * 1e-3) / 1e9
+    sample_gs = world * S * K / (ts * 1e-3) / 1e9
+    result = {
+        "metric": METRIC, "value": round(build_gs, 4), "unit": "G entries/s", "n_gpus": world,
+        "steps": K, "warmup": args.warmup, "ms_per_step": round((tb + ts) / K, 4),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u64",
+        "data": "synthetic",
+        "config": {"workload": wl["desc"], "W": W, "H": H, "mx": mx, "my": my,
+                   "samples_per_gpu": S,
+                   "l2": f"flushed between steps ({L2_FLUSH_BYTES >> 20} MiB write, untimed)",
+                   "parallelism": f"replicas x{world}"},
+        "build": {"value": round(build_gs, 4), "unit": "G entries/s", "ms_per_build": round(tb / K, 5),
+                  "launches": "rows build + row weights + marginal build"},
+        "sampling": {"value": round(sample_gs, 4), "unit": "G 2-D samples/s",
+                     "ms_per_batch": round(ts / K, 4),
+                     "output": "pixel (int32) + sub-pixel position (2 x float32) per sample"},
+        "gpu_launches": launches, "clocks": sampler.summary(),
+    }
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+    if rank == 0:
+        print(json.dumps(result), flush=True)
+
+
 def run_gpu_c5(args):
     """Config 5: batched rebuilds of 65536 independent rows (rtf_build_rows, one CTA
     per row, everything in shared memory) + sampling (row, xi) pairs.  Rows are
@@ -686,6 +778,8 @@ def main():
         run_gpu_c4(args)
     elif args.workload == "c5":
         run_gpu_c5(args)
+    elif args.workload == "c2d":
+        run_gpu_2d(args)
     else:
         run_gpu(args)
 

@@ -184,6 +184,47 @@ int rtf_sample_loads(const rtf_forest *f, const uint32_t *xi, uint64_t count, in
 int rtf_sample_rows(const rtf_forest *f, const uint32_t *row, const uint32_t *xi,
                     uint64_t count, int32_t *out, void *stream);
 
+/* ------------------------------------------- 2-D distributions (Sec.6) */
+/*
+ * "A multi-dimensional inversion method proceeds component by component"
+ * (P:1523-1529): a marginal forest over the image rows selects y with xi1, the
+ * forest of row y selects x with xi2, and the relative positions inside the
+ * two chosen intervals give the sub-pixel position.  Rows are
+ * built by the batched build (the row index boundary is the partition
+ * criterion); the row weights are the rows' quantised masses
+ * (reading R19).  Limits: W, H, mx, my <= 4096 (rtf_build_rows).
+ */
+typedef struct rtf_forest2d {
+    uint32_t W, H;       /* columns, rows                                          */
+    uint32_t mx, my;     /* cells per row / of the marginal                         */
+    rtf_forest rows;     /* H rows of W entries: the conditional forests            */
+    rtf_forest marginal; /* 1 row of H entries: the forest of the row weights       */
+    int32_t *rows_jmap;  /* H*W: row-local node index of entry (y, x), -1 for p = 0 */
+    int32_t *marg_jmap;  /* H:   node index of row y in the marginal, -1 if q_y = 0 */
+    float *weights;      /* H:   the row weights q_y (reading R19)                   */
+} rtf_forest2d;
+
+/* Bytes of a 2-D forest buffer (both forests, index maps, weights).  Host only. */
+size_t rtf_forest2d_bytes(uint32_t W, uint32_t H, uint32_t mx, uint32_t my);
+
+/* Build from p (H x W float32, row-major, device; >= 0, finite).  Three
+ * launches on `stream` (rows, row weights, marginal); asynchronous.  A NaN /
+ * Inf / negative weight poisons the marginal (rtf_forest2d_status -> EDATA);
+ * an all-zero row is legal (weight 0, never chosen). */
+int rtf_build_2d(const float *p, uint32_t W, uint32_t H, uint32_t mx, uint32_t my, void *buf,
+                 size_t bytes, void *stream, rtf_forest2d *out);
+
+/* Synchronous: RTF_OK, RTF_EDATA (invalid data anywhere) or RTF_EALLZERO (no
+ * positive weight at all). */
+int rtf_forest2d_status(const rtf_forest2d *f, void *stream);
+
+/* pixel[k] = y W + x for the pair (xi1[k], xi2[k]) (u32 fixed point);
+ * pos (may be NULL): 2 floats per sample, ((x + v) / W, (y + u) / H) with u, v
+ * the relative positions inside the chosen intervals, computed in float64 and
+ * rounded toward zero (reading R19).  A poisoned forest gives INT32_MAX. */
+int rtf_sample_2d(const rtf_forest2d *f, const uint32_t *xi1, const uint32_t *xi2,
+                  uint64_t count, int32_t *pixel, float *pos, void *stream);
+
 /* ----------------------------------------------- baselines (same CDF) */
 
 /* The full fixed-point CDF over all n entries, zeros included:

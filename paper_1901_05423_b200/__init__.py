@@ -21,9 +21,9 @@ import torch
 from . import _lib
 from ._lib import (RTF_BUILD_DEFAULT, RTF_BUILD_SMALL_TILES, RTF_DATA_ALLZERO,  # noqa: F401
                    RTF_DATA_INF, RTF_DATA_NAN, RTF_DATA_NEG, RtfError, check, rtf_forest,
-                   rtf_header)
+                   rtf_forest2d, rtf_header)
 
-__all__ = ["Forest", "RowsForest", "build", "build_rows", "sample", "sample_rows",
+__all__ = ["Forest", "RowsForest", "Forest2D", "build", "build_rows", "build_2d", "sample", "sample_rows",
            "build_cdf", "sample_bsearch", "philox", "build_host", "sample_host",
            "launch_count", "RtfError", "lib"]
 
@@ -200,6 +200,57 @@ class RowsForest:
 
     def table_numpy(self) -> np.ndarray:
         return self._section(self.view.table, 8 * self.rows * self.m).cpu().numpy().view(CELL_DTYPE)
+
+
+class Forest2D:
+    """A 2-D distribution (Sec.6): marginal forest over the rows + one forest per
+    row (rtf_build_2d / rtf_sample_2d)."""
+
+    def __init__(self, W: int, H: int, mx: int, my: int, device="cuda"):
+        L = lib()
+        self.W, self.H, self.mx, self.my = int(W), int(H), int(mx), int(my)
+        self._buf = _bytes_tensor(L.rtf_forest2d_bytes(self.W, self.H, self.mx, self.my),
+                                  torch.device(device))
+        self.view = rtf_forest2d()
+
+    def build(self, p: torch.Tensor, stream=None) -> "Forest2D":
+        if p.dtype != torch.float32 or not p.is_cuda or not p.is_contiguous():
+            raise TypeError("p must be a contiguous float32 CUDA tensor")
+        if p.numel() != self.W * self.H:
+            raise ValueError("p must hold H x W weights")
+        self._p = p
+        check(lib().rtf_build_2d(_ptr(p), self.W, self.H, self.mx, self.my, _ptr(self._buf),
+                                 self._buf.numel(), _stream(stream), ctypes.byref(self.view)),
+              "rtf_build_2d")
+        return self
+
+    def status(self, stream=None) -> int:
+        return lib().rtf_forest2d_status(ctypes.byref(self.view), _stream(stream))
+
+    def sample(self, xi1: torch.Tensor, xi2: torch.Tensor, pixel=None, pos=None,
+               with_pos: bool = True, stream=None):
+        """Returns pixel (int32, y W + x) and, with_pos, pos (float32 [N, 2], (x, y) in [0,1))."""
+        xi1, xi2 = _u32_view(xi1), _u32_view(xi2)
+        if xi1.numel() != xi2.numel():
+            raise ValueError("xi1 and xi2 must have the same length")
+        n = xi1.numel()
+        if pixel is None:
+            pixel = torch.empty(n, dtype=torch.int32, device=xi1.device)
+        if with_pos and pos is None:
+            pos = torch.empty((n, 2), dtype=torch.float32, device=xi1.device)
+        check(lib().rtf_sample_2d(ctypes.byref(self.view), _ptr(xi1), _ptr(xi2), n, _ptr(pixel),
+                                  _ptr(pos) if with_pos else None, _stream(stream)),
+              "rtf_sample_2d")
+        return (pixel, pos) if with_pos else pixel
+
+    def weights(self) -> np.ndarray:
+        off = self.view.weights - self._buf.data_ptr()
+        return self._buf[off: off + 4 * self.H].cpu().numpy().view(np.float32)
+
+
+def build_2d(p: torch.Tensor, mx: int, my: int, stream=None) -> Forest2D:
+    H, W = p.shape
+    return Forest2D(W, H, mx, my, device=p.device).build(p.contiguous().view(-1), stream)
 
 
 # -------------------------------------------------------------------- functional API

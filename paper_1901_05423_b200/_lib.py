@@ -26,6 +26,13 @@ class rtf_forest(ctypes.Structure):
                 ("table", ctypes.c_void_p), ("header", ctypes.c_void_p)]
 
 
+class rtf_forest2d(ctypes.Structure):
+    _fields_ = [("W", ctypes.c_uint32), ("H", ctypes.c_uint32), ("mx", ctypes.c_uint32),
+                ("my", ctypes.c_uint32), ("rows", rtf_forest), ("marginal", rtf_forest),
+                ("rows_jmap", ctypes.c_void_p), ("marg_jmap", ctypes.c_void_p),
+                ("weights", ctypes.c_void_p)]
+
+
 class rtf_shard_view(ctypes.Structure):
     _fields_ = [("spine", ctypes.c_void_p), ("scale", ctypes.c_void_p), ("total", ctypes.c_void_p),
                 ("nt_local", ctypes.c_uint32), ("spine_row_bytes", ctypes.c_uint32),
@@ -50,6 +57,11 @@ PROTOTYPES = {
     "rtf_sample_rows": (_I32, [_F, _P, _P, _U64, _P, _P]),
     "rtf_build_cdf": (_I32, [_P, _U32, _P, _P, _P, _SZ, _P]),
     "rtf_sample_bsearch": (_I32, [_P, _U32, _P, _P, _U64, _P, _P]),
+    "rtf_forest2d_bytes": (_SZ, [_U32, _U32, _U32, _U32]),
+    "rtf_build_2d": (_I32, [_P, _U32, _U32, _U32, _U32, _P, _SZ, _P,
+                            ctypes.POINTER(rtf_forest2d)]),
+    "rtf_forest2d_status": (_I32, [ctypes.POINTER(rtf_forest2d), _P]),
+    "rtf_sample_2d": (_I32, [ctypes.POINTER(rtf_forest2d), _P, _P, _U64, _P, _P, _P]),
     "rtf_build_cutpoint": (_I32, [_P, _U32, _U32, _P, _P]),
     "rtf_sample_cutpoint": (_I32, [_P, _U32, _P, _P, _U32, _I32, _P, _U64, _P, _P]),
     "rtf_build_host": (_I32, [_P, _U32, _U32, _U32, _P, _P, _SZ, _P, _SZ, _P, _F, _H]),

@@ -1,0 +1,112 @@
+// rtf_2d.cu -- 2-D distributions (Sec.6): the row weights of the
+// marginal from the rows' build headers, and the component-wise sampler with
+// the sub-pixel rescale.  Reading R19.
+#include "rtf_device.cuh"
+#include "rtf_internal.h"
+
+namespace rtf {
+
+constexpr int kRowWeightThreads = 1024;
+constexpr int k2dThreads = 256;
+constexpr int kMaxVisits2d = 64;
+
+// q_y = float32(float64(T_y) 2^(E_y - B_y - K)), K = max over non-empty rows of
+// E_y - B_y; an all-zero row gets 0, a row with NaN / Inf / negative data NaN
+// (so the marginal build reports the data error).  One CTA; H <= 4096.
+__global__ void __launch_bounds__(kRowWeightThreads)
+    k_row_weights(const rtf_header* __restrict__ hdr, uint32_t H, float* __restrict__ q) {
+    __shared__ int s_max[kRowWeightThreads / 32];
+    int k = INT_MIN;
+    for (uint32_t y = threadIdx.x; y < H; y += kRowWeightThreads)
+        if (hdr[y].status == 0) k = max(k, hdr[y].exponent - hdr[y].scale_bits);
+    k = __reduce_max_sync(0xffffffffu, k);
+    if ((threadIdx.x & 31) == 0) s_max[threadIdx.x >> 5] = k;
+    __syncthreads();
+    int K = INT_MIN;
+    for (int w = 0; w < kRowWeightThreads / 32; ++w) K = max(K, s_max[w]);
+    for (uint32_t y = threadIdx.x; y < H; y += kRowWeightThreads) {
+        const rtf_header h = hdr[y];
+        float v;
+        if (h.status & (RTF_DATA_NAN | RTF_DATA_INF | RTF_DATA_NEG)) v = __int_as_float(0x7fc00000);
+        else if (h.status) v = 0.0f;  // all-zero row
+        else v = __double2float_rn(ldexp(__ull2double_rn(h.total), h.exponent - h.scale_bits - K));
+        q[y] = v;
+    }
+}
+
+// one Alg. 2 descent in a row forest (nodes + table of that row); returns ~leaf
+__device__ __forceinline__ int32_t descend_row(const rtf_node* __restrict__ nodes,
+                                               const rtf_ref* __restrict__ table, uint32_t m,
+                                               uint32_t x) {
+    const int2 e = __ldg(reinterpret_cast<const int2*>(table) + (uint32_t)(((uint64_t)x * m) >> 32));
+    int32_t j = (e.y >= 0 || x >= (uint32_t)e.x) ? e.y : e.y + 1;
+    const uint64_t x63 = (uint64_t)x << 31;
+    for (int d = 0; j >= 0 && d < kMaxVisits2d; ++d) {
+        const ulonglong2 r = __ldg(reinterpret_cast<const ulonglong2*>(nodes + j));
+        j = (int32_t)(x63 < r.x ? (uint32_t)r.y : (uint32_t)(r.y >> 32));
+    }
+    return j;
+}
+
+// relative position of x inside the interval of node j of a forest with n_pos leaves
+__device__ __forceinline__ double rel_pos(const rtf_node* __restrict__ nodes, int32_t j,
+                                          uint32_t n_pos, uint32_t x) {
+    const uint64_t lo = __ldg(&nodes[j].key);
+    const uint64_t hi = (uint32_t)(j + 1) < n_pos ? __ldg(&nodes[j + 1].key) : kOne63;
+    return __ddiv_rn(__ull2double_rn(((uint64_t)x << 31) - lo), __ull2double_rn(hi - lo));
+}
+
+__global__ void __launch_bounds__(k2dThreads)
+    k_sample_2d(rtf_forest2d f, const uint32_t* __restrict__ xi1, const uint32_t* __restrict__ xi2,
+                uint64_t count, int32_t* __restrict__ pixel, float* __restrict__ pos) {
+    const uint64_t gs = (uint64_t)gridDim.x * blockDim.x;
+    const bool bad = f.marginal.header->status != 0;
+    for (uint64_t k = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; k < count; k += gs) {
+        const uint32_t a = xi1[k], b = xi2[k];
+        int32_t out = INT32_MAX;
+        float px = __int_as_float(0x7fc00000), py = px;
+        if (!bad) {
+            const int32_t jy = descend_row(f.marginal.nodes, f.marginal.table, f.my, a);
+            const int32_t y = ~jy;
+            const rtf_node* rn = f.rows.nodes + (size_t)y * f.W;
+            const int32_t jx = descend_row(rn, f.rows.table + (size_t)y * f.mx, f.mx, b);
+            const int32_t x = ~jx;
+            if (jy >= 0 || jx >= 0) {
+                out = INT32_MIN;  // corrupted forest (a descent did not end in a leaf)
+            } else {
+                out = y * (int32_t)f.W + x;
+                if (pos) {
+                    const double u = rel_pos(f.marginal.nodes, __ldg(&f.marg_jmap[y]),
+                                             f.marginal.header->n_pos, a);
+                    const double v = rel_pos(rn, __ldg(&f.rows_jmap[(size_t)y * f.W + x]),
+                                             f.rows.header[y].n_pos, b);
+                    px = __double2float_rz(__ddiv_rn(__dadd_rn((double)x, v), (double)f.W));
+                    py = __double2float_rz(__ddiv_rn(__dadd_rn((double)y, u), (double)f.H));
+                }
+            }
+        }
+        pixel[k] = out;
+        if (pos) reinterpret_cast<float2*>(pos)[k] = make_float2(px, py);
+    }
+}
+
+cudaError_t launch_row_weights(const rtf_header* rows_hdr, uint32_t H, uint32_t W, float* q,
+                               cudaStream_t st, int* launches) {
+    (void)W;
+    k_row_weights<<<1, kRowWeightThreads, 0, st>>>(rows_hdr, H, q);
+    ++*launches;
+    return cudaGetLastError();
+}
+
+cudaError_t launch_sample_2d(const rtf_forest2d& f, const uint32_t* xi1, const uint32_t* xi2,
+                             uint64_t count, int32_t* pixel, float* pos, cudaStream_t st,
+                             int* launches) {
+    if (count == 0) return cudaSuccess;
+    const uint64_t want = (count + k2dThreads - 1) / k2dThreads;
+    const uint32_t grid = (uint32_t)std::max<uint64_t>(1, std::min<uint64_t>(want, 148ull * 32ull));
+    k_sample_2d<<<grid, k2dThreads, 0, st>>>(f, xi1, xi2, count, pixel, pos);
+    ++*launches;
+    return cudaGetLastError();
+}
+
+}  // namespace rtf

@@ -133,7 +133,7 @@ int rtf_build_rows(const float* p, uint32_t rows, uint32_t n_row, uint32_t m_row
     if (int s = rtf_forest_view(forest_buf, forest_bytes, n_row, m_row, rows, out)) return s;
     int launches = 0;
     cudaError_t e = rtf::launch_build_rows(p, rows, n_row, m_row, out->header, out->nodes,
-                                           out->table, as_stream(stream), &launches);
+                                           out->table, nullptr, as_stream(stream), &launches);
     return finish(e, launches);
 }
 
@@ -195,6 +195,89 @@ int rtf_sample_rows(const rtf_forest* f, const uint32_t* row, const uint32_t* xi
     if ((((uintptr_t)xi | (uintptr_t)out | (uintptr_t)row) & 3u) != 0) return RTF_EINVAL;
     int launches = 0;
     cudaError_t e = rtf::launch_sample(*f, row, xi, count, out, as_stream(stream), &launches);
+    return finish(e, launches);
+}
+
+// ------------------------------------------------------------------ 2-D (Sec.6)
+
+namespace {
+struct Layout2d {
+    size_t rows, marginal, rows_jmap, marg_jmap, weights, total;
+};
+Layout2d layout_2d(uint32_t W, uint32_t H, uint32_t mx, uint32_t my) {
+    Layout2d L;
+    size_t off = 0;
+    L.rows = off;
+    off += align_up(rtf_forest_bytes(W, mx, H));
+    L.marginal = off;
+    off += align_up(rtf_forest_bytes(H, my, 1));
+    L.rows_jmap = off;
+    off += align_up(sizeof(int32_t) * (size_t)W * H);
+    L.marg_jmap = off;
+    off += align_up(sizeof(int32_t) * (size_t)H);
+    L.weights = off;
+    off += align_up(sizeof(float) * (size_t)H);
+    L.total = off;
+    return L;
+}
+int check_2d(uint32_t W, uint32_t H, uint32_t mx, uint32_t my) {
+    if (W == 0 || H == 0 || mx == 0 || my == 0) return RTF_EINVAL;
+    if (W > rtf::kRowsMax || H > rtf::kRowsMax || mx > rtf::kRowsMax || my > rtf::kRowsMax)
+        return RTF_ETOOLARGE;
+    return RTF_OK;
+}
+}  // namespace
+
+size_t rtf_forest2d_bytes(uint32_t W, uint32_t H, uint32_t mx, uint32_t my) {
+    return layout_2d(W ? W : 1, H ? H : 1, mx ? mx : 1, my ? my : 1).total;
+}
+
+int rtf_build_2d(const float* p, uint32_t W, uint32_t H, uint32_t mx, uint32_t my, void* buf,
+                 size_t bytes, void* stream, rtf_forest2d* out) {
+    if (!p || !buf || !out || ((uintptr_t)p & 3u)) return RTF_EINVAL;
+    if (int s = check_2d(W, H, mx, my)) return s;
+    if (((uintptr_t)buf & (kAlign - 1)) != 0) return RTF_EINVAL;
+    const Layout2d L = layout_2d(W, H, mx, my);
+    if (bytes < L.total) return RTF_ENOSPACE;
+    unsigned char* b = static_cast<unsigned char*>(buf);
+    out->W = W;
+    out->H = H;
+    out->mx = mx;
+    out->my = my;
+    if (int s = rtf_forest_view(b + L.rows, L.marginal - L.rows, W, mx, H, &out->rows)) return s;
+    if (int s = rtf_forest_view(b + L.marginal, L.rows_jmap - L.marginal, H, my, 1, &out->marginal))
+        return s;
+    out->rows_jmap = reinterpret_cast<int32_t*>(b + L.rows_jmap);
+    out->marg_jmap = reinterpret_cast<int32_t*>(b + L.marg_jmap);
+    out->weights = reinterpret_cast<float*>(b + L.weights);
+    cudaStream_t st = as_stream(stream);
+    int launches = 0;
+    cudaError_t e = rtf::launch_build_rows(p, H, W, mx, out->rows.header, out->rows.nodes,
+                                           out->rows.table, out->rows_jmap, st, &launches);
+    if (e == cudaSuccess)
+        e = rtf::launch_row_weights(out->rows.header, H, W, out->weights, st, &launches);
+    if (e == cudaSuccess)
+        e = rtf::launch_build_rows(out->weights, 1, H, my, out->marginal.header,
+                                   out->marginal.nodes, out->marginal.table, out->marg_jmap, st,
+                                   &launches);
+    return finish(e, launches);
+}
+
+int rtf_forest2d_status(const rtf_forest2d* f, void* stream) {
+    if (!f) return RTF_EINVAL;
+    return rtf_forest_status(&f->marginal, stream, nullptr);
+}
+
+int rtf_sample_2d(const rtf_forest2d* f, const uint32_t* xi1, const uint32_t* xi2, uint64_t count,
+                  int32_t* pixel, float* pos, void* stream) {
+    if (!f || !f->rows.nodes || !f->marginal.nodes || !f->rows_jmap || !f->marg_jmap)
+        return RTF_EINVAL;
+    if (count && (!xi1 || !xi2 || !pixel)) return RTF_EINVAL;
+    if ((((uintptr_t)xi1 | (uintptr_t)xi2 | (uintptr_t)pixel) & 3u) || ((uintptr_t)pos & 7u))
+        return RTF_EINVAL;
+    int launches = 0;
+    cudaError_t e = rtf::launch_sample_2d(*f, xi1, xi2, count, pixel, pos, as_stream(stream),
+                                          &launches);
     return finish(e, launches);
 }
 

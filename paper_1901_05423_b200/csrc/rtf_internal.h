@@ -55,8 +55,15 @@ cudaError_t launch_build(const float* p, uint32_t n, uint32_t m, uint32_t flags,
                          const ShardCall* sc = nullptr);
 
 cudaError_t launch_build_rows(const float* p, uint32_t rows, uint32_t n_row, uint32_t m_row,
-                              rtf_header* hdr, rtf_node* nodes, rtf_ref* table, cudaStream_t st,
-                              int* launches);
+                              rtf_header* hdr, rtf_node* nodes, rtf_ref* table, int32_t* jmap,
+                              cudaStream_t st, int* launches);
+
+// 2-D (Sec.6): row weights from the rows' headers, and the component-wise sampler
+cudaError_t launch_row_weights(const rtf_header* rows_hdr, uint32_t H, uint32_t W, float* q,
+                               cudaStream_t st, int* launches);
+cudaError_t launch_sample_2d(const rtf_forest2d& f, const uint32_t* xi1, const uint32_t* xi2,
+                             uint64_t count, int32_t* pixel, float* pos, cudaStream_t st,
+                             int* launches);
 
 cudaError_t launch_sample(const rtf_forest& f, const uint32_t* row, const uint32_t* xi,
                           uint64_t count, int32_t* out, cudaStream_t st, int* launches);

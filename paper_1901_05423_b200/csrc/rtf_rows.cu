@@ -17,6 +17,7 @@ struct RowsArgs {
     rtf_header* hdr;
     rtf_node* nodes;
     rtf_ref* table;
+    int32_t* jmap;  // optional: row-local compacted leaf index per entry (-1: zero weight)
     bool vec;
 };
 
@@ -121,7 +122,11 @@ __global__ void __launch_bounds__(THREADS) k_build_rows(RowsArgs A) {
 
 #pragma unroll
     for (int k = 0; k < VPT; ++k) {
-        if (!w[k]) continue;
+        if (!w[k]) {
+            if (A.jmap && first + k < n) A.jmap[(size_t)r * n + first + k] = -1;
+            continue;
+        }
+        if (A.jmap) A.jmap[(size_t)r * n + first + k] = (int32_t)jl;
         const uint64_t key = fixed_point(W, nm);
         const uint64_t Wn = W + w[k];
         const bool last = Wn == T;
@@ -245,8 +250,8 @@ static cudaError_t launch_rows_t(const RowsArgs& A, cudaStream_t st) {
 }
 
 cudaError_t launch_build_rows(const float* p, uint32_t rows, uint32_t n_row, uint32_t m_row,
-                              rtf_header* hdr, rtf_node* nodes, rtf_ref* table, cudaStream_t st,
-                              int* launches) {
+                              rtf_header* hdr, rtf_node* nodes, rtf_ref* table, int32_t* jmap,
+                              cudaStream_t st, int* launches) {
     RowsArgs A;
     A.p = p;
     A.rows = rows;
@@ -255,6 +260,7 @@ cudaError_t launch_build_rows(const float* p, uint32_t rows, uint32_t n_row, uin
     A.hdr = hdr;
     A.nodes = nodes;
     A.table = table;
+    A.jmap = jmap;
     A.vec = (((uintptr_t)p & 15u) == 0) && (n_row % 4 == 0);
     const uint32_t need = std::max(n_row, m_row);
     cudaError_t e;
