@@ -83,6 +83,7 @@ struct BuildArgs {
     Pfx* rng;           // per range of tiles: total (phase B)
     Pfx* rpre;          // per range of tiles: exclusive prefix (phase C, CTA 0)
     uint32_t epoch;     // this launch's number: CTA 0 publishes rpre with it
+    uint32_t mshift;    // m a power of two: cell = key >> mshift (63 - log2 m)
     rtf_header* hdr;
     rtf_node* nodes;
     rtf_ref* table;
@@ -286,7 +287,7 @@ __device__ unsigned long long g_phase_cycles[kMaxGrid][16];
 
 // ============================================================== the build kernel
 
-template <int THREADS, int VPT, bool CDF, int MINB = 2>
+template <int THREADS, int VPT, bool CDF, int MINB = 2, bool POW2 = false>
 __global__ void __launch_bounds__(THREADS, MINB) k_build(BuildArgs A) {
     constexpr int TILE = THREADS * VPT;
     constexpr int NW = THREADS / 32;
@@ -317,6 +318,10 @@ __global__ void __launch_bounds__(THREADS, MINB) k_build(BuildArgs A) {
 
     const uint32_t G = gridDim.x, b = blockIdx.x, tid = threadIdx.x;
     const uint32_t n = A.n, m = A.m, nt = A.nt;
+    // the cell of a key (Alg. 1): a shift when m is a power of two
+    auto cell_fn = [&](uint64_t key) -> uint32_t {
+        return POW2 ? (uint32_t)(key >> A.mshift) : cell_of(key, m);
+    };
     const int lane = tid & 31, warp = tid >> 5;
     uint32_t* gbar = &A.counters[kCtrGridBar];
 
@@ -740,7 +745,7 @@ __global__ void __launch_bounds__(THREADS, MINB) k_build(BuildArgs A) {
         uint64_t lampack = 0;
         if (tc) {
             uint64_t kn = (c_ex + tc < cnt) ? s_key[pad8(c_ex + tc)] : s_key_after;
-            uint32_t cn = (kn == kOne63) ? m : cell_of(kn, m);
+            uint32_t cn = POW2 ? 0u : ((kn == kOne63) ? m : cell_of(kn, m));
             if (j0 == 0 && c_ex == 0) st_cell(A.table, 0, 0u, 0);  // leaf 0 (key 0): cell 0's anchor
 #pragma unroll
             for (int k = VPT - 1; k >= 0; --k) {
@@ -748,8 +753,17 @@ __global__ void __launch_bounds__(THREADS, MINB) k_build(BuildArgs A) {
                     const uint64_t key = w[k];
                     const uint32_t r = __popc(posmask & ((1u << k) - 1u));  // rank
                     const uint32_t jl = c_ex + r;
-                    const uint32_t cell = cell_of(key, m);
-                    const uint32_t lam = (cn != cell) ? kLamBoundary : split_level(key, kn);
+                    uint32_t cell, lam;
+                    if (POW2) {  // a cell boundary lies between iff the keys differ at or
+                                 // above bit mshift (kn = 2^63 "1" differs at bit 63)
+                        const uint32_t d = split_level(key, kn);
+                        lam = d >= A.mshift ? kLamBoundary : d;
+                        cell = (uint32_t)(key >> A.mshift);
+                        cn = (uint32_t)(kn >> A.mshift);
+                    } else {
+                        cell = cell_of(key, m);
+                        lam = (cn != cell) ? kLamBoundary : split_level(key, kn);
+                    }
                     s_lam[pad8(jl)] = (uint8_t)lam;
                     lampack |= (uint64_t)lam << (8 * r);
                     if (lam == kLamBoundary) {  // the table entries this leaf owes
@@ -843,7 +857,7 @@ __global__ void __launch_bounds__(THREADS, MINB) k_build(BuildArgs A) {
                                 const uint2 e =
                                     single_leaf_cell(key, (int32_t)(first + k) + ib, ~s_c0[q], a);
                                 if ((int32_t)e.y != a)
-                                    st_cell(A.table, cell_of(key, m), e.x, (int32_t)e.y);
+                                    st_cell(A.table, cell_fn(key), e.x, (int32_t)e.y);
                             }
                         }
                     }
@@ -1095,7 +1109,7 @@ __global__ void __launch_bounds__(THREADS, MINB) k_build(BuildArgs A) {
                         const uint2 e = single_leaf_cell(key, ~ref, ~__ldcg(&A.nodes[j0].child[0]),
                                                          (int32_t)j0);
                         if ((int32_t)e.y != (int32_t)j0)
-                            st_cell(A.table, cell_of(key, m), e.x, (int32_t)e.y);
+                            st_cell(A.table, cell_fn(key), e.x, (int32_t)e.y);
                     }
                 } else if (e == 1) {  // left child of the last gap, linked in the tile
                     const int32_t c = __ldcg(&S->c0_next);
@@ -1215,9 +1229,9 @@ static int num_sms() {
     return sms;
 }
 
-template <int THREADS, int VPT, bool CDF, int MINB = 2>
+template <int THREADS, int VPT, bool CDF, int MINB = 2, bool POW2 = false>
 static cudaError_t launch_fused(BuildArgs& A, cudaStream_t st, int* launches) {
-    auto kern = k_build<THREADS, VPT, CDF, MINB>;
+    auto kern = k_build<THREADS, VPT, CDF, MINB, POW2>;
     const size_t smem = build_smem_bytes<THREADS, VPT>();  // phase B stages tile totals there
     static int max_grid = 0;  // per instantiation: co-resident CTAs
     if (!max_grid) {
@@ -1286,8 +1300,13 @@ cudaError_t launch_build(const float* p, uint32_t n, uint32_t m, uint32_t flags,
     // 1024x4 @1: 336 vs 399 / 352 / 403 us for config 3)
     // (2048-entry tiles at 4 or 3 CTAs/SM and 1024-entry tiles at 8 CTAs/SM
     // were measured again with the fused kernel: 293 / 315 / 399 us for c3)
-    return small ? launch_fused<64, 4, false>(A, st, launches)
-                 : launch_fused<512, 8, false>(A, st, launches);
+    const bool pow2 = (m & (m - 1)) == 0;
+    A.mshift = 63u - (uint32_t)ceil_log2_u32(m);
+    if (small)
+        return pow2 ? launch_fused<64, 4, false, 2, true>(A, st, launches)
+                    : launch_fused<64, 4, false>(A, st, launches);
+    return pow2 ? launch_fused<512, 8, false, 2, true>(A, st, launches)
+                : launch_fused<512, 8, false>(A, st, launches);
 }
 
 }  // namespace rtf
