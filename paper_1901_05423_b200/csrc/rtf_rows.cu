@@ -266,6 +266,7 @@ cudaError_t launch_build_rows(const float* p, uint32_t rows, uint32_t n_row, uin
     cudaError_t e;
     if (need <= 256) e = launch_rows_t<64, 4>(A, st);
     else if (need <= 1024) e = launch_rows_t<256, 4>(A, st);
+    else if (need <= 2048) e = launch_rows_t<256, 8>(A, st);  // 67 KB: 3 CTAs per SM
     else e = launch_rows_t<512, 8>(A, st);
     ++*launches;
     return e;
