@@ -390,6 +390,8 @@ def run_gpu(args):
     }
     if e2e:
         result["e2e"] = e2e
+    if wl["name"] == "c3_powerlaw" and not args.no_c2:
+        result["config2_envmap"] = c2_summary(args, dev, stream, flush, world)
     if rank == 0 and not args.no_cpu_baseline:
         result["cpu_baseline"] = cpu_baseline(p_host, m, xi[: 1 << 22].cpu().numpy().view(np.uint32),
                                               cdf.cdf.cpu().numpy().view(np.uint64))
@@ -398,6 +400,67 @@ def run_gpu(args):
         dist.destroy_process_group()
     if rank == 0:
         print(json.dumps(result), flush=True)
+
+
+def c2_summary(args, dev, stream, flush, world):
+    """BASELINE configs[1] in the same run: the 2048x1024 env map (n = m = 2^21),
+    build + 2^26 Sobol samples, binary search on the same CDF.  Device-timed
+    like the headline (CUDA events, L2 flushed between steps), max over ranks."""
+    import torch
+    import torch.distributed as dist
+
+    import paper_1901_05423_b200 as rtf
+    from workloads import sobol0_xi
+    wl = WORKLOADS["c2"]
+    n, m, S = wl["n"], wl["m"], wl["samples"]
+    rank = int(os.environ.get("RANK", "0"))
+    p = torch.from_numpy(make_p(wl)).to(dev)
+    f = rtf.Forest(n, m, device=dev)
+    xi = torch.from_numpy(sobol0_xi(S, start=rank * S).view(np.int32)).to(dev)
+    out = torch.empty(S, dtype=torch.int32, device=dev)
+    cdf = rtf.build_cdf(p)
+    bs = torch.empty_like(out)
+
+    def timed(fn, reps):
+        ts_ = []
+        for _ in range(reps):
+            flush.zero_()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            fn()
+            e1.record(stream)
+            torch.cuda.synchronize()
+            ts_.append(e0.elapsed_time(e1))
+        return statistics.median(ts_)
+
+    for _ in range(3):
+        f.build(p)
+        f.sample(xi, out)
+    cdf.sample(xi, bs)
+    torch.cuda.synchronize()
+    assert f.status() == 0
+    tb = timed(lambda: f.build(p), max(args.steps, 5))
+    ts = timed(lambda: f.sample(xi, out), max(args.steps, 5))
+    tbs = timed(lambda: cdf.sample(xi, bs), 3)
+    eq = bool(torch.equal(out, bs))
+    if world > 1:
+        t = torch.tensor([tb, ts, tbs], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        tb, ts, tbs = t.tolist()
+    peak, _ = peaks()
+    loads = f.sample_loads(xi[: 1 << 20]).double().mean().item()
+    bytes_b = 4 * n + 16 * f.n_pos() + 8 * m
+    bytes_s = 4 + 4 + 8 + 16 * (loads - 1.0)
+    return {"workload": wl["desc"],
+            "build": {"value": round(world * n / (tb * 1e-3) / 1e9, 4), "unit": "G entries/s",
+                      "ms_per_build": round(tb, 5),
+                      "roofline_frac": round(bytes_b / (tb * 1e-3) / 1e9 / peak, 4)},
+            "sampling": {"value": round(world * S / (ts * 1e-3) / 1e9, 4), "unit": "G samples/s",
+                         "ms_per_batch": round(ts, 4),
+                         "roofline_frac": round(S * bytes_s / (ts * 1e-3) / 1e9 / peak, 4)},
+            "bsearch": {"value": round(world * S / (tbs * 1e-3) / 1e9, 4), "unit": "G samples/s",
+                        "identical_indices": eq},
+            "timing": "median of >= 5 device-timed runs, L2 flushed before each"}
 
 
 def run_gpu_c4(args):
@@ -769,6 +832,7 @@ def main():
     ap.add_argument("--samples", type=int, default=0, help="override samples per GPU")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-c2", action="store_true", help="skip the config-2 summary")
     args = ap.parse_args()
     if args.warmup < 3 and args.impl != "reference":
         print("warning: fewer than 3 warm-up steps", file=sys.stderr)
