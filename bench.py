@@ -215,6 +215,30 @@ def run_gpu(args):
     build_gs = world * n * K / (tb * 1e-3) / 1e9
     sample_gs = world * S * K / (ts * 1e-3) / 1e9
 
+    # ------------------------------------------------ replication alternative (N > 1)
+    # each rank rebuilds its forest (no collective on the
+    # data path); for comparison, the cost of replicating rank 0's forest over
+    # NVLink instead (ncclBroadcast of the whole forest buffer), max over ranks.
+    replication = None
+    if world > 1:
+        fbuf = forest._buf.forest
+        rts = []
+        for _ in range(3):
+            dist.barrier()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            dist.broadcast(fbuf, src=0)
+            e1.record(stream)
+            torch.cuda.synchronize()
+            rts.append(e0.elapsed_time(e1))
+        t = torch.tensor([statistics.median(rts)], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        replication = {"ms_broadcast": round(t.item(), 4), "bytes": int(fbuf.numel()),
+                       "ms_rebuild": round(tb / args.steps, 4),
+                       "note": "the bench rebuilds per rank; this is the NCCL alternative"}
+        forest.build(p)  # every rank's own forest again (the broadcast overwrote it)
+        torch.cuda.synchronize()
+
     # ------------------------------------------------ baseline: binary search on the same CDF
     cdf = rtf.build_cdf(p)
     bs_out = torch.empty_like(out)
@@ -390,6 +414,8 @@ def run_gpu(args):
     }
     if e2e:
         result["e2e"] = e2e
+    if replication:
+        result["replication"] = replication
     if wl["name"] == "c3_powerlaw" and not args.no_c2:
         result["config2_envmap"] = c2_summary(args, dev, stream, flush, world)
     if rank == 0 and not args.no_cpu_baseline:
