@@ -583,7 +583,7 @@ __global__ void __launch_bounds__(THREADS, MINB) k_build(BuildArgs A) {
     nm.d = T << nm.s;
     if (ph & kPhTiles) {
         if (tid == THREADS - 1) {
-            s_recip = reciprocal_of(nm.d);
+            s_recip = reciprocal_fast(nm.d);
             if (b == 0) {
                 rtf_header h;
                 h.total = T;

@@ -229,6 +229,32 @@ __device__ __forceinline__ uint64_t reciprocal_of(uint64_t d) {
     return q;
 }
 
+// The same v without the 64-step loop: a float64 estimate of 2^128 / d (within
+// a few 2^12 of v), then an exact correction from the signed remainder
+// e = (2^128 - 1) - (2^64 + v) d, computed mod 2^128 (|e| < 2^80).
+__device__ __forceinline__ uint64_t reciprocal_fast(uint64_t d) {
+    typedef unsigned __int128 u128;
+    typedef __int128 s128;
+    const double t = __dadd_rn(__ddiv_rn(0x1p128, __ull2double_rn(d)), -0x1p64);
+    uint64_t v = t >= 0x1p64 ? ~0ull : (t <= 0.0 ? 0ull : __double2ull_rz(t));
+    const u128 D = d;
+    s128 e = (s128)(~(u128)0 - (((u128)1 << 64) + v) * D);
+    const double ed = __dadd_rn(__dmul_rn((double)(int64_t)(e >> 64), 0x1p64),
+                                __ull2double_rn((uint64_t)e));
+    const int64_t c = (int64_t)floor(__ddiv_rn(ed, __ull2double_rn(d)));
+    v += (uint64_t)c;
+    e -= (s128)c * (s128)D;
+    while (e < 0) {
+        --v;
+        e += (s128)D;
+    }
+    while (e >= (s128)D) {
+        ++v;
+        e -= (s128)D;
+    }
+    return v;
+}
+
 __device__ __forceinline__ uint64_t fixed_point(uint64_t W, const Norm& nm) {
     uint64_t u1 = W << (nm.s - 1);
     uint64_t q0 = nm.v * u1;

@@ -103,47 +103,70 @@ __global__ void __launch_bounds__(THREADS) k_build_rows(RowsArgs A) {
     const QScale qs = qscale(B - E);
     uint64_t w[VPT];
     uint64_t tw = 0;
-    uint32_t tc = 0;
+    uint32_t tc = 0, posmask = 0;
 #pragma unroll
     for (int k = 0; k < VPT; ++k) {
         w[k] = quantize(x[k], qs);
         tw += w[k];
-        tc += w[k] != 0;
+        if (w[k]) {
+            ++tc;
+            posmask |= 1u << k;
+        }
     }
     uint64_t W, T;
-    uint32_t jl, cnt;
-    block_scan_excl<THREADS>(tw, tc, W, jl, T, cnt, s_w, s_c);
+    uint32_t c_ex, cnt;
+    block_scan_excl<THREADS>(tw, tc, W, c_ex, T, cnt, s_w, s_c);
     Norm nm;
     nm.s = (uint32_t)__clzll((long long)T);
     nm.d = T << nm.s;
-    if (threadIdx.x == 0) s_recip = reciprocal_of(nm.d);
+    if (threadIdx.x == 0) s_recip = reciprocal_fast(nm.d);
     __syncthreads();
     nm.v = s_recip;
 
+    // keys (one exact division per positive entry; w[k] holds key_j from here on)
+    {
+        uint32_t jl = c_ex;
 #pragma unroll
-    for (int k = 0; k < VPT; ++k) {
-        if (!w[k]) {
-            if (A.jmap && first + k < n) A.jmap[(size_t)r * n + first + k] = -1;
-            continue;
+        for (int k = 0; k < VPT; ++k) {
+            if (!w[k]) {
+                if (A.jmap && first + k < n) A.jmap[(size_t)r * n + first + k] = -1;
+                continue;
+            }
+            if (A.jmap) A.jmap[(size_t)r * n + first + k] = (int32_t)jl;
+            const uint64_t Wn = W + w[k];
+            w[k] = fixed_point(W, nm);
+            s_rec[jl].key = w[k];
+            s_orig[jl] = (int32_t)(first + k);
+            W = Wn;
+            ++jl;
         }
-        if (A.jmap) A.jmap[(size_t)r * n + first + k] = (int32_t)jl;
-        const uint64_t key = fixed_point(W, nm);
-        const uint64_t Wn = W + w[k];
-        const bool last = Wn == T;
-        const uint64_t kn = last ? kOne63 : fixed_point(Wn, nm);
-        const uint32_t cell = cell_of(key, m);
-        const uint32_t cn = last ? m : cell_of(kn, m);
-        const uint32_t lam = cn != cell ? kLamBoundary : split_level(key, kn);
-        s_rec[jl].key = key;
-        s_lam[jl] = (uint8_t)lam;
-        s_orig[jl] = (int32_t)(first + k);
-        if (jl == 0) s_anc[0] = 0;
-        if (lam == kLamBoundary) {
-            s_lst[cell] = (int32_t)jl;
-            if (cn < m) s_anc[cn] = (int32_t)(jl + 1);
+    }
+    if (threadIdx.x == 0 && cnt) s_anc[0] = 0;
+    __syncthreads();
+    // cells and split levels of the own leaves (the row boundary is a wall);
+    // the key after the thread's last leaf is its neighbour's (or "1")
+    uint64_t lampack = 0;
+    if (tc) {
+        uint64_t kn = (c_ex + tc < cnt) ? s_rec[c_ex + tc].key : kOne63;
+        uint32_t cn = (kn == kOne63) ? m : cell_of(kn, m);
+#pragma unroll
+        for (int k = VPT - 1; k >= 0; --k) {
+            if ((posmask >> k) & 1u) {
+                const uint64_t key = w[k];
+                const uint32_t rk = __popc(posmask & ((1u << k) - 1u));
+                const uint32_t jl = c_ex + rk;
+                const uint32_t cell = cell_of(key, m);
+                const uint32_t lam = cn != cell ? kLamBoundary : split_level(key, kn);
+                s_lam[jl] = (uint8_t)lam;
+                lampack |= (uint64_t)lam << (8 * rk);
+                if (lam == kLamBoundary) {
+                    s_lst[cell] = (int32_t)jl;
+                    if (cn < m) s_anc[cn] = (int32_t)(jl + 1);
+                }
+                kn = key;
+                cn = cell;
+            }
         }
-        W = Wn;
-        ++jl;
     }
     __syncthreads();
     for (uint32_t l = threadIdx.x; l < cnt; l += THREADS) {
@@ -193,27 +216,102 @@ __global__ void __launch_bounds__(THREADS) k_build_rows(RowsArgs A) {
         }
     }
     __syncthreads();
-    // Alg. 1 over all leaves of the row (the row boundary is lambda = 64 at both ends)
-    for (uint32_t l = threadIdx.x; l < cnt; l += THREADS) {
-        int32_t lo = (int32_t)l, hi = (int32_t)l;
-        int32_t node = ~s_orig[l];
-        while (true) {
-            const uint32_t lamL = lo ? s_lam[lo - 1] : kLamBoundary;
-            const uint32_t lamR = s_lam[hi];
-            if (lamL == kLamBoundary && lamR == kLamBoundary) {
-                s_rec[lo].c1 = node;
-                break;
+    // Alg. 1 over all leaves of the row (the row boundary is lambda = 64 at
+    // both ends).  Stage A: the first step of every own leaf, straight-line;
+    // stage B: the second arrivals climb on, one walker per lane at a time.
+    // A deposit is (split level beyond the bound) << 16 | bound.
+    {
+        const uint32_t lam_prev = c_ex ? (uint32_t)s_lam[c_ex - 1] : kLamBoundary;
+        uint32_t contw[VPT];
+        uint32_t pend = 0, rightbits = 0;
+        {
+            uint32_t mask = posmask;
+#pragma unroll
+            for (int rk = 0; rk < VPT; ++rk) {
+                contw[rk] = 0;
+                if ((uint32_t)rk < tc) {
+                    const uint32_t k = __ffs(mask) - 1;
+                    mask &= mask - 1;
+                    const uint32_t l = c_ex + rk;
+                    const uint32_t lamL = rk ? (uint32_t)(lampack >> (8 * (rk - 1))) & 0xffu : lam_prev;
+                    const uint32_t lamR = (uint32_t)(lampack >> (8 * rk)) & 0xffu;
+                    const bool right = lamL <= lamR;
+                    const int32_t leaf = ~(int32_t)(first + k);
+                    if ((lamL & lamR & kLamBoundary) != 0) {  // a cell root
+                        s_rec[l].c1 = leaf;
+                        continue;
+                    }
+                    const uint32_t q = right ? l : l + 1;
+                    if (right) s_rec[q].c1 = leaf;
+                    else s_rec[q].c0 = leaf;
+                    const int32_t other = atomicExch(&s_ob[q], (int32_t)((right ? lamR : lamL) << 16 | l));
+                    if (other >= 0) {
+                        s_ob[q] = -1;
+                        contw[rk] = (uint32_t)other;
+                        pend |= 1u << rk;
+                        rightbits |= (right ? 1u : 0u) << rk;
+                    }
+                }
             }
-            const int c = lamL > lamR ? 0 : 1;
-            const int32_t parent = c ? lo : hi + 1;
-            if (c) s_rec[parent].c1 = node;
-            else s_rec[parent].c0 = node;
-            const int32_t other = atomicExch(&s_ob[parent], c ? hi : lo);
-            if (other < 0) break;
-            s_ob[parent] = -1;
-            if (c) lo = other;
-            else hi = other;
-            node = parent;
+        }
+        bool active = false;
+        int32_t lo = 0, hi = 0, node = 0;
+        uint32_t lamL = 0, lamR = 0;
+        while (true) {
+            if (!active && pend) {
+                const uint32_t rk = __ffs(pend) - 1;
+                pend &= pend - 1;
+                uint32_t sel[VPT];
+#pragma unroll
+                for (int u = 0; u < VPT; ++u) sel[u] = contw[u];
+#pragma unroll
+                for (int wd = VPT / 2, bit = 1; wd >= 1; wd /= 2, bit <<= 1)
+#pragma unroll
+                    for (int u = 0; u < wd; ++u) sel[u] = (rk & bit) ? sel[2 * u + 1] : sel[2 * u];
+                const uint32_t other = sel[0];
+                const uint32_t l = c_ex + rk;
+                const uint32_t bound = other & 0xffffu, lv = other >> 16;
+                active = true;
+                if ((rightbits >> rk) & 1u) {  // merged as the right child of node l
+                    lo = (int32_t)bound;
+                    hi = (int32_t)l;
+                    lamL = lv;
+                    lamR = (uint32_t)(lampack >> (8 * rk)) & 0xffu;
+                    node = (int32_t)l;
+                } else {  // merged as the left child of node l + 1
+                    lo = (int32_t)l;
+                    hi = (int32_t)bound;
+                    lamL = rk ? (uint32_t)(lampack >> (8 * (rk - 1))) & 0xffu : lam_prev;
+                    lamR = lv;
+                    node = (int32_t)(l + 1);
+                }
+            }
+            if (!__any_sync(0xffffffffu, active)) break;
+            if (active) {
+                if ((lamL & lamR & kLamBoundary) != 0) {  // a cell root: right child of its anchor
+                    s_rec[lo].c1 = node;
+                    active = false;
+                    continue;
+                }
+                const bool right = lamL <= lamR;
+                const int32_t parent = right ? lo : hi + 1;
+                if (right) s_rec[parent].c1 = node;
+                else s_rec[parent].c0 = node;
+                const int32_t dep = right ? (int32_t)(lamR << 16 | (uint32_t)hi)
+                                          : (int32_t)(lamL << 16 | (uint32_t)lo);
+                const int32_t other = atomicExch(&s_ob[parent], dep);
+                active = other >= 0;
+                if (active) {
+                    s_ob[parent] = -1;
+                    const int32_t bound = other & 0xffff;
+                    const uint32_t lv = (uint32_t)other >> 16;
+                    lo = right ? bound : lo;
+                    hi = right ? hi : bound;
+                    lamL = right ? lv : lamL;
+                    lamR = right ? lamR : lv;
+                    node = parent;
+                }
+            }
         }
     }
     __syncthreads();
