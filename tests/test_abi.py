@@ -91,3 +91,14 @@ def test_python_binding_fails_loudly_without_library(tmp_path, monkeypatch):
     monkeypatch.setattr(_lib, "_lib", None)
     with pytest.raises(ImportError):
         _lib.load()
+
+
+def test_product_package_never_imports_the_oracle():
+    """The product path shares no code with oracle/ (DESIGN.md section 3)."""
+    pkg = os.path.join(ROOT, "paper_1901_05423_b200")
+    for dirpath, _, files in os.walk(pkg):
+        for f in files:
+            if f.endswith((".py", ".cu", ".cuh", ".h")):
+                src = open(os.path.join(dirpath, f)).read()
+                assert "import oracle" not in src and "from oracle" not in src, f
+                assert "rtf_oracle" not in src and "liboracle" not in src, f
