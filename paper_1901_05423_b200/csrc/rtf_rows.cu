@@ -96,6 +96,10 @@ __global__ void __launch_bounds__(THREADS) k_build_rows(RowsArgs A) {
             h.status = status;
             A.hdr[r] = h;
         }
+        // a poisoned row's cells answer the leaf ~INT32_MIN = INT32_MAX (the
+        // data-error output) without a header read in the sampler
+        for (uint32_t g = threadIdx.x; g < m; g += THREADS)
+            st_cell(A.table + (size_t)r * m, g, 0u, INT32_MIN);
         return;
     }
     const int E = floor_log2_bits(mx);

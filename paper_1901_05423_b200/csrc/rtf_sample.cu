@@ -37,8 +37,7 @@ __device__ __forceinline__ int32_t sample_one(const rtf_node* __restrict__ nodes
                                               const rtf_ref* __restrict__ table,
                                               const rtf_header* __restrict__ hdr, uint32_t n,
                                               uint32_t m, uint32_t r, uint32_t x) {
-    if (ROWS) {
-        if (hdr[r].status) return INT32_MAX;
+    if (ROWS) {  // a poisoned row's cells are {0, INT32_MIN}: the answer is INT32_MAX
         nodes += (size_t)r * n;
         table += (size_t)r * m;
     }
@@ -80,7 +79,6 @@ __global__ void __launch_bounds__(kSampleThreads)
                 const rtf_ref* tk = table;
                 dead[k] = bad;
                 if (ROWS) {
-                    dead[k] = hdr[rr[k]].status != 0;
                     nk += (size_t)rr[k] * n;
                     tk += (size_t)rr[k] * m;
                 }
