@@ -60,3 +60,34 @@ def test_sharded_spikes_and_random(rtf, count):
 def test_sharded_config4_shape(rtf):
     """Config 4's distribution (4 spikes, uniform background) at 2^22 over 8 shards."""
     _check(rtf, spikes(1 << 22), 1 << 20, 8)
+
+
+def test_config4_full_size_sampled(rtf):
+    """Config 4 at its full size (n = 2^28 spikes, m = 2^22, the bench's shape):
+    the single-GPU build and the sharded protocol over 4 virtual shards give
+    byte-identical forests, and 2^20 Philox samples match the oracle's binary
+    search over the oracle's full fixed-point CDF (O1-O6 + the P:61-63
+    definition, computed independently of any forest) one by one."""
+    from paper_1901_05423_b200 import sharded
+    n, m = 1 << 28, 1 << 22
+    p = spikes(n)
+    K, _ = oracle.cdf_all(p)
+    xi = philox_xi(1 << 20, seed=0x5EED)
+    want = oracle.sample_bsearch(K, xi)
+    del K
+    pd = torch.from_numpy(p).cuda()
+    xd = torch.from_numpy(xi.view(np.int32)).cuda()
+    single = rtf.build(pd, m)
+    assert single.status() == 0
+    assert np.array_equal(single.sample(xd).cpu().numpy(), want)
+    nodes = single.nodes_numpy()
+    table = single.table_numpy()
+    del single
+    torch.cuda.empty_cache()
+    shards = sharded.make_shards(pd, m, 4)
+    sharded.build_sharded(shards, sharded.LocalComm())
+    for s in shards[:2]:  # every shard holds the same forest; compare two
+        f = rtf.Forest.from_buffer(s.n_global, m, s.forest)
+        assert f.nodes_numpy().tobytes() == nodes.tobytes(), f"shard {s.rank} records"
+        assert f.table_numpy().tobytes() == table.tobytes(), f"shard {s.rank} table"
+        assert np.array_equal(f.sample(xd).cpu().numpy(), want)
