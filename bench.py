@@ -521,7 +521,10 @@ def run_gpu_c4(args):
     shards = sharded.make_shards_local(p_local, n, m, rank, world, base)
     comm = sharded.DistComm() if world > 1 else sharded.LocalComm()
     forest = rtf.Forest.from_buffer(n, m, shards[0].forest)
+    ranged = not args.c4_replicate
     xi = rtf.philox(S, seed=0x5EED, start=rank * S, device=dev)
+    if ranged:  # this rank samples its own xi range (its cell slice), stratified
+        xi = sharded.ranged_xi(xi, rank, world, m)
     out = torch.empty(S, dtype=torch.int32, device=dev)
     flush = torch.empty(L2_FLUSH_BYTES, dtype=torch.uint8, device=dev)
     stream = torch.cuda.current_stream()
@@ -529,7 +532,7 @@ def run_gpu_c4(args):
     def step(ev=None):
         if ev:
             ev[0].record(stream)
-        sharded.build_sharded(shards, comm)
+        sharded.build_sharded(shards, comm, ranged=ranged)
         if ev:
             ev[1].record(stream)
         forest.sample(xi, out)
@@ -571,8 +574,12 @@ def run_gpu_c4(args):
         "data": "synthetic",
         "config": {"workload": wl["desc"], "n": n, "m": m, "samples_total": S * world,
                    "l2": f"flushed between steps ({L2_FLUSH_BYTES >> 20} MiB write, untimed)",
-                   "parallelism": f"sharded build over {world} GPU(s) + replicated forest; "
-                                  "sampling split across GPUs"},
+                   "parallelism": (f"sharded build over {world} GPU(s); ranged: rank r keeps "
+                                   "the cells [r m/N, (r+1) m/N) (records all-to-all, table "
+                                   "reduce-scatter) and samples that xi stratum"
+                                   if ranged else
+                                   f"sharded build over {world} GPU(s) + replicated forest; "
+                                   "sampling split across GPUs")},
         "sampling": {"value": round(sample_gs, 4), "unit": "G samples/s",
                      "ms_per_batch": round(ts / K, 4)},
         "roofline_build": {"kernel": "sharded build (all calls, incl. exchanges)",
@@ -859,6 +866,8 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-c2", action="store_true", help="skip the config-2 summary")
+    ap.add_argument("--c4-replicate", action="store_true",
+                    help="config 4: replicate the whole forest instead of ranged sharding")
     args = ap.parse_args()
     if args.warmup < 3 and args.impl != "reference":
         print("warning: fewer than 3 warm-up steps", file=sys.stderr)

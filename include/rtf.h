@@ -321,6 +321,24 @@ int rtf_shard_finish(uint32_t n_local, uint32_t n_global, uint32_t m, const void
                      uint32_t nt_all, void *forest_buf, size_t forest_bytes, void *ws,
                      size_t ws_bytes, void *stream, rtf_forest *out);
 
+/* Ranged sharding (the north star's "per-shard build over contiguous cell
+ * ranges"): instead of replicating the whole forest, rank r keeps the cells
+ * [g_r, g_{r+1}) (g_r = r m / N) -- a contiguous xi range -- and samples only
+ * xi in it.  Its node slots are the leaves of those cells, [J_r, J_{r+1});
+ * J_k = sum over shards of rtf_shard_count_cells(.., bounds = g, ..).  After
+ * step 3, the records move to the rank of their cells (an all-to-all of
+ * contiguous slices), the table is MAX-reduce-scattered by cell slice, the
+ * spine rows are gathered, and rtf_shard_finish_range links only the slots
+ * in [j_lo, j_hi) = [J_r, J_{r+1}).  Its records and table slice are then
+ * byte-equal to the single build's. */
+int rtf_shard_count_cells(const void *forest_buf, size_t forest_bytes, uint32_t n_global,
+                          uint32_t m, uint32_t j0, uint32_t cnt, const uint32_t *bounds,
+                          uint32_t nb, uint32_t *counts, void *stream);
+int rtf_shard_finish_range(uint32_t n_local, uint32_t n_global, uint32_t m,
+                           const void *spine_all, uint32_t nt_all, uint32_t j_lo, uint32_t j_hi,
+                           void *forest_buf, size_t forest_bytes, void *ws, size_t ws_bytes,
+                           void *stream, rtf_forest *out);
+
 /* ---------------------------------------------------------- utilities */
 
 /* Input generator (not part of the method): Philox4x32-10 u32 stream,

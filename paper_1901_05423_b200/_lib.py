@@ -75,6 +75,9 @@ PROTOTYPES = {
     "rtf_shard_build": (_I32, [_P, _U32, _U32, _U32, _U32, _U32, _U32, _P, _P, _SZ, _P, _SZ, _P,
                                _F]),
     "rtf_shard_finish": (_I32, [_U32, _U32, _U32, _P, _U32, _P, _SZ, _P, _SZ, _P, _F]),
+    "rtf_shard_finish_range": (_I32, [_U32, _U32, _U32, _P, _U32, _U32, _U32, _P, _SZ, _P, _SZ,
+                                      _P, _F]),
+    "rtf_shard_count_cells": (_I32, [_P, _SZ, _U32, _U32, _U32, _U32, _P, _U32, _P, _P]),
     "rtf_launch_count": (_U64, []),
     "rtf_status_string": (ctypes.c_char_p, [_I32]),
     "rtf_version": (ctypes.c_char_p, []),

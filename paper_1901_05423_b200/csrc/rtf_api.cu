@@ -504,21 +504,45 @@ int rtf_shard_build(const float* p, uint32_t n_local, uint32_t n_global, uint32_
     return finish(e, launches);
 }
 
-int rtf_shard_finish(uint32_t n_local, uint32_t n_global, uint32_t m, const void* spine_all,
-                     uint32_t nt_all, void* forest_buf, size_t forest_bytes, void* ws,
-                     size_t ws_bytes, void* stream, rtf_forest* out) {
+int rtf_shard_finish_range(uint32_t n_local, uint32_t n_global, uint32_t m,
+                           const void* spine_all, uint32_t nt_all, uint32_t j_lo, uint32_t j_hi,
+                           void* forest_buf, size_t forest_bytes, void* ws, size_t ws_bytes,
+                           void* stream, rtf_forest* out) {
     rtf::WsLayout L;
-    if (!spine_all || ((uintptr_t)spine_all & 15u)) return RTF_EINVAL;
+    if (!spine_all || ((uintptr_t)spine_all & 15u) || j_lo > j_hi) return RTF_EINVAL;
     if (int s = shard_layout(ws, ws_bytes, n_local, n_global, m, &L)) return s;
     if (nt_all > L.nt_cap) return RTF_EINVAL;
     if (int s = rtf_forest_view(forest_buf, forest_bytes, n_global, m, 1, out)) return s;
     rtf::ShardCall sc{rtf::kPhCross, n_global, 0, 0, 1, nt_all, nullptr, spine_all};
+    sc.j_lo = j_lo;
+    sc.j_hi = j_hi;
     int launches = 0;
     // any valid p pointer is fine: phases A-D do not run
     const float* dummy = reinterpret_cast<const float*>(ws);
     cudaError_t e =
         rtf::launch_build(dummy, n_local, m, rtf::kBuildShardedLayout, out->header, out->nodes,
                           out->table, nullptr, ws, L, as_stream(stream), &launches, &sc);
+    return finish(e, launches);
+}
+
+int rtf_shard_finish(uint32_t n_local, uint32_t n_global, uint32_t m, const void* spine_all,
+                     uint32_t nt_all, void* forest_buf, size_t forest_bytes, void* ws,
+                     size_t ws_bytes, void* stream, rtf_forest* out) {
+    return rtf_shard_finish_range(n_local, n_global, m, spine_all, nt_all, 0u, 0xffffffffu,
+                                  forest_buf, forest_bytes, ws, ws_bytes, stream, out);
+}
+
+int rtf_shard_count_cells(const void* forest_buf, size_t forest_bytes, uint32_t n_global,
+                          uint32_t m, uint32_t j0, uint32_t cnt, const uint32_t* bounds,
+                          uint32_t nb, uint32_t* counts, void* stream) {
+    rtf_forest f;
+    if (!bounds || !counts || nb == 0) return RTF_EINVAL;
+    if (int s = rtf_forest_view(const_cast<void*>(forest_buf), forest_bytes, n_global, m, 1, &f))
+        return s;
+    if ((uint64_t)j0 + cnt > n_global) return RTF_EINVAL;
+    int launches = 0;
+    cudaError_t e = rtf::launch_count_cells(f.nodes, j0, cnt, m, bounds, nb, counts,
+                                            as_stream(stream), &launches);
     return finish(e, launches);
 }
 

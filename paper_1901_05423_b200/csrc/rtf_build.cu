@@ -84,6 +84,7 @@ struct BuildArgs {
     Pfx* rpre;          // per range of tiles: exclusive prefix (phase C, CTA 0)
     uint32_t epoch;     // this launch's number: CTA 0 publishes rpre with it
     uint32_t mshift;    // m a power of two: cell = key >> mshift (63 - log2 m)
+    uint32_t j_lo, j_hi;  // phase E writes only node slots in [j_lo, j_hi) (a ranged finish)
     rtf_header* hdr;
     rtf_node* nodes;
     rtf_ref* table;
@@ -1061,6 +1062,9 @@ __global__ void __launch_bounds__(THREADS, MINB) k_build(BuildArgs A) {
             if (lane == 0) A.bmax[bb] = mx;
         }
         if (gathered) grid_barrier(gbar);
+        // a ranged finish (sharded.py, ranged=True) holds only the records of
+        // its cell range [j_lo, j_hi): the other links are other ranks'
+        auto local = [&](uint32_t slot) { return slot >= A.j_lo && slot < A.j_hi; };
         // E1: one warp per row; lane e links entry e
         auto far_left = [&](uint32_t t, uint32_t v, uint32_t& lam, int32_t& gap) {
             const int32_t u = row_left(A.tmax, A.bmax, t, v + 1);
@@ -1102,9 +1106,12 @@ __global__ void __launch_bounds__(THREADS, MINB) k_build(BuildArgs A) {
                     if (u >= 0)
                         lamp = spine_lowest(__ldcg(&SP[u].mR), __ldcg(&SP[u].walls) & 2u);
                     const int32_t ref = __ldcg(&S->ref0);
-                    if (lamp <= lam0) A.nodes[j0].child[1] = ref;
-                    else A.nodes[j0 + 1].child[0] = ref;
-                    if ((lamp & lam0 & kLamBoundary) != 0) {  // a one-leaf cell
+                    if (lamp <= lam0) {
+                        if (local(j0)) A.nodes[j0].child[1] = ref;
+                    } else if (local(j0 + 1)) {
+                        A.nodes[j0 + 1].child[0] = ref;
+                    }
+                    if ((lamp & lam0 & kLamBoundary) != 0 && local(j0)) {  // a one-leaf cell
                         const uint64_t key = __ldcg(&A.nodes[j0].key);
                         const uint2 e = single_leaf_cell(key, ~ref, ~__ldcg(&A.nodes[j0].child[0]),
                                                          (int32_t)j0);
@@ -1113,7 +1120,7 @@ __global__ void __launch_bounds__(THREADS, MINB) k_build(BuildArgs A) {
                     }
                 } else if (e == 1) {  // left child of the last gap, linked in the tile
                     const int32_t c = __ldcg(&S->c0_next);
-                    if (c != kNoLink) A.nodes[j0 + cnt].child[0] = c;
+                    if (c != kNoLink && local(j0 + cnt)) A.nodes[j0 + cnt].child[0] = c;
                 } else {
                     const bool left = e - 2 < nL;
                     const uint32_t v = left ? nth_bit(mL, e - 2) : nth_bit(mRx, e - 2 - nL);
@@ -1135,8 +1142,11 @@ __global__ void __launch_bounds__(THREADS, MINB) k_build(BuildArgs A) {
                         far_right(t, v, lamR, gR);
                     }
                     const int32_t node = (int32_t)(g + 1);
-                    if (lamL <= lamR) A.nodes[gL + 1].child[1] = node;
-                    else A.nodes[gR + 1].child[0] = node;
+                    if (lamL <= lamR) {
+                        if (local((uint32_t)(gL + 1))) A.nodes[gL + 1].child[1] = node;
+                    } else if (local((uint32_t)(gR + 1))) {
+                        A.nodes[gR + 1].child[0] = node;
+                    }
                 }
             }
         }
@@ -1266,6 +1276,8 @@ cudaError_t launch_build(const float* p, uint32_t n, uint32_t m, uint32_t flags,
     A.B = 62 - ceil_log2_u32(sc ? sc->n_global : n);
     A.phases = sc ? sc->phases : kPhFull;
     A.index_base = sc ? sc->index_base : 0;
+    A.j_lo = sc ? sc->j_lo : 0u;
+    A.j_hi = sc ? sc->j_hi : 0xffffffffu;
     A.scale_io = reinterpret_cast<uint32_t*>(w + L.scale);
     A.shard_totals = sc ? reinterpret_cast<const Pfx*>(sc->totals) : nullptr;
     A.shard_rank = sc ? sc->rank : 0;

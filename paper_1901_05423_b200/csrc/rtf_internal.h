@@ -42,7 +42,13 @@ struct ShardCall {
     uint32_t phases, n_global, index_base, rank, count, nt_in;
     const void* totals;        // device: count shard totals (16 B each)
     const void* spine_in;      // device: finish -- all shards' tile spines (nt_in rows)
+    uint32_t j_lo = 0, j_hi = 0xffffffffu;  // finish: node slots this rank holds
 };
+
+// leaves of nodes[j0, j0 + cnt) whose cell is below bound[k]: counts[k], k < nb
+cudaError_t launch_count_cells(const rtf_node* nodes, uint32_t j0, uint32_t cnt, uint32_t m,
+                               const uint32_t* bounds, uint32_t nb, uint32_t* counts,
+                               cudaStream_t st, int* launches);
 
 uint32_t build_tile_size(uint32_t flags);
 size_t build_workspace_layout(uint32_t n, uint32_t m, uint32_t flags, WsLayout* L,

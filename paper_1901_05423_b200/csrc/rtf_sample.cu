@@ -326,6 +326,33 @@ cudaError_t launch_cutpoint(const uint64_t* cdf, uint32_t n, const rtf_header* h
     return cudaGetLastError();
 }
 
+// ------------------------------------------------------------ ranged sharding helper
+
+// counts[k] = number of leaves among nodes[j0, j0 + cnt) whose cell
+// floor(key m / 2^63) lies below bounds[k] (keys increase, so a binary search)
+__global__ void k_count_cells(const rtf_node* __restrict__ nodes, uint32_t j0, uint32_t cnt,
+                              uint32_t m, const uint32_t* __restrict__ bounds, uint32_t nb,
+                              uint32_t* __restrict__ counts) {
+    const uint32_t k = blockIdx.x * blockDim.x + threadIdx.x;
+    if (k >= nb) return;
+    const uint32_t g = bounds[k];
+    uint32_t lo = 0, hi = cnt;  // first local leaf with cell >= g
+    while (lo < hi) {
+        const uint32_t mid = lo + (hi - lo) / 2;
+        if (cell_of(nodes[j0 + mid].key, m) < g) lo = mid + 1;
+        else hi = mid;
+    }
+    counts[k] = lo;
+}
+
+cudaError_t launch_count_cells(const rtf_node* nodes, uint32_t j0, uint32_t cnt, uint32_t m,
+                               const uint32_t* bounds, uint32_t nb, uint32_t* counts,
+                               cudaStream_t st, int* launches) {
+    k_count_cells<<<(nb + 127) / 128, 128, 0, st>>>(nodes, j0, cnt, m, bounds, nb, counts);
+    ++*launches;
+    return cudaGetLastError();
+}
+
 cudaError_t launch_philox(uint64_t seed, uint64_t start, uint64_t count, uint32_t* out,
                           cudaStream_t st, int* launches) {
     if (count == 0) return cudaSuccess;

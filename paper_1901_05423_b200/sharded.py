@@ -58,6 +58,30 @@ class LocalComm:
             if i != src:
                 t.copy_(ts[src])
 
+    def allreduce_sum(self, ts):
+        tot = ts[0].clone()
+        for t in ts[1:]:
+            tot += t
+        for t in ts:
+            t.copy_(tot)
+
+    def alltoallv(self, sends, recvs):
+        """sends[q][r]: shard q's piece for shard r; recvs[r][q]: where shard r
+        receives shard q's piece (None on the diagonal: already in place)."""
+        for r in range(len(sends)):
+            for q in range(len(sends)):
+                if q != r and sends[q][r] is not None and sends[q][r].numel():
+                    recvs[r][q].copy_(sends[q][r])
+
+    def reduce_scatter_max(self, full, lo, hi):
+        """full[r]: shard r's whole array; on return full[r][lo[r]:hi[r]] holds
+        the element-wise maximum over all shards of that slice."""
+        for r in range(len(full)):
+            mx = full[0][lo[r]: hi[r]].clone()
+            for t in full[1:]:
+                torch.maximum(mx, t[lo[r]: hi[r]], out=mx)
+            full[r][lo[r]: hi[r]].copy_(mx)
+
 
 class DistComm:
     """One shard per process (torch.distributed); lists hold the local tensor."""
@@ -83,6 +107,35 @@ class DistComm:
 
     def broadcast(self, ts, src):
         self.dist.broadcast(ts[0], src=src, group=self.group)
+
+    def allreduce_sum(self, ts):
+        self.dist.all_reduce(ts[0], op=self.dist.ReduceOp.SUM, group=self.group)
+
+    def alltoallv(self, sends, recvs):
+        """Grouped point-to-point transfers of the local pieces (sends[0][r] to
+        rank r, recvs[0][q] from rank q) straight between their final places."""
+        me = self.dist.get_rank(self.group)
+        ops = []
+        for r, t in enumerate(sends[0]):
+            if r != me and t is not None and t.numel():
+                ops.append(self.dist.P2POp(self.dist.isend, t, r, group=self.group))
+        for q, t in enumerate(recvs[0]):
+            if q != me and t is not None and t.numel():
+                ops.append(self.dist.P2POp(self.dist.irecv, t, q, group=self.group))
+        if ops:
+            for w in self.dist.batch_isend_irecv(ops):
+                w.wait()
+
+    def reduce_scatter_max(self, full, lo, hi):
+        me = self.dist.get_rank(self.group)
+        t = full[0]
+        equal = len(set(int(h) - int(l) for l, h in zip(lo, hi))) == 1 and int(lo[0]) == 0
+        if t.is_cuda and equal and int(hi[-1]) == t.numel():  # NCCL: one reduce-scatter
+            out = torch.empty(int(hi[me]) - int(lo[me]), dtype=t.dtype, device=t.device)
+            self.dist.reduce_scatter_tensor(out, t, op=self.dist.ReduceOp.MAX, group=self.group)
+            t[int(lo[me]): int(hi[me])].copy_(out)
+        else:  # gloo (no reduce-scatter): the all-reduce covers the slice
+            self.dist.all_reduce(t, op=self.dist.ReduceOp.MAX, group=self.group)
 
 
 # --------------------------------------------------------------------- shard state
@@ -147,6 +200,10 @@ class Shard:
         # half, so a MAX-reduction keeps the owner's cell over {0, INT32_MIN}
         return self._forest_slice(self.fview.table, 8 * self.m).view(torch.int64)
 
+    def node_words(self, j0, cnt):
+        """Records [j0, j0 + cnt) as int64 pairs (2 words per 16-B record)."""
+        return self._forest_slice(self.fview.nodes + 16 * j0, 16 * cnt).view(torch.int64)
+
     def spine_bytes(self):
         return self._ws_slice(self.view.spine, self.view.spine_row_bytes * self.view.nt_local)
 
@@ -157,10 +214,12 @@ def _padded(t: torch.Tensor, nbytes: int, fill: int) -> torch.Tensor:
     return out
 
 
-def build_sharded(shards: list[Shard], comm) -> None:
+def build_sharded(shards: list[Shard], comm, ranged: bool = False) -> None:
     """Run the sharded build for the local shards (all of them for LocalComm,
     the process's own for DistComm).  On return every shard's forest buffer
-    holds the full forest."""
+    holds the full forest -- or, with ranged=True, shard r holds the cells
+    [g_r, g_{r+1}) = [r m / N, (r + 1) m / N) (node slots [J_r, J_{r+1}),
+    stored in s.cells / s.slots), the xi range it samples."""
     L = _lib.load()
     st = _stream()
     sh0 = shards[0]
@@ -182,6 +241,11 @@ def build_sharded(shards: list[Shard], comm) -> None:
     # 4. replication: owner ranges from the gathered totals (16 B per shard)
     tot = totals[0].cpu().numpy().view(np.dtype([("W", "<u8"), ("cnt", "<u4"), ("last", "<i4")]))
     starts = np.concatenate([[0], np.cumsum(tot["cnt"].astype(np.int64))])
+    if ranged and sh0.count > 1:
+        _redistribute_and_finish(shards, comm, starts, tot["cnt"].astype(np.int64), st)
+        return
+    if ranged:  # one shard: its cell range is everything
+        shards[0].cells, shards[0].slots = (0, sh0.m), (0, int(starts[-1]))
     for r in range(sh0.count):
         j0, cnt = int(starts[r]), int(tot["cnt"][r])
         if cnt:
@@ -218,3 +282,65 @@ def make_shards(p: torch.Tensor, m: int, count: int, ranks=None) -> list[Shard]:
             raise ValueError("more shards than 4096-entry blocks")
         out.append(Shard(r, count, n, m, base, nl, p[base: base + nl]))
     return out
+
+
+def _redistribute_and_finish(shards, comm, starts, counts, st) -> None:
+    """Ranged sharding (include/rtf.h): records to the rank of their cells (an
+    all-to-all of contiguous slices), the table reduce-scattered by cell slice,
+    the spine rows gathered, then the cross-tile links of the own slots."""
+    L = _lib.load()
+    sh0 = shards[0]
+    N, m, dev = sh0.count, sh0.m, sh0.p.device
+    g = np.array([k * m // N for k in range(N + 1)], np.int64)
+    bounds = torch.from_numpy(g.astype(np.uint32).view(np.int32)).to(dev)
+    # J_k: global index of the first leaf with cell >= g_k (sum of the shards' counts)
+    cts = []
+    for s in shards:
+        c = torch.empty(N + 1, dtype=torch.int32, device=dev)
+        check(L.rtf_shard_count_cells(_ptr(s.forest), s.forest.numel(), s.n_global, m,
+                                      int(starts[s.rank]), int(counts[s.rank]), _ptr(bounds),
+                                      N + 1, _ptr(c), _stream()), "count cells")
+        cts.append(c.to(torch.int64))
+    comm.allreduce_sum(cts)
+    J = cts[0].cpu().numpy().astype(np.int64)
+    own = [(int(starts[q]), int(starts[q] + counts[q])) for q in range(N)]
+    need = [(int(J[r]), int(J[r + 1])) for r in range(N)]
+
+    def piece(s, a, b):  # records [max(a0, b0), min(a1, b1)) of shard s's buffer
+        lo, hi = max(a[0], b[0]), min(a[1], b[1])
+        return s.node_words(lo, hi - lo) if hi > lo else None
+
+    # a record stays at its global slot: the piece a rank already holds (its
+    # own cells among its own entries) does not move
+    sends = [[piece(s, own[s.rank], need[r]) for r in range(N)] for s in shards]
+    recvs = [[piece(s, own[q], need[s.rank]) for q in range(N)] for s in shards]
+    comm.alltoallv(sends, recvs)
+    # table: each rank's cell slice, MAX over the shards' partial tables
+    comm.reduce_scatter_max([s.table_words() for s in shards], g[:-1], g[1:])
+    nt_max = max(s.view.nt_local for s in shards)
+    if hasattr(comm, "dist"):
+        t = torch.tensor([nt_max], dtype=torch.int64, device=dev)
+        comm.allreduce_max([t])
+        nt_max = int(t.item())
+    row = sh0.view.spine_row_bytes
+    spine_all = comm.allgather([_padded(s.spine_bytes(), row * nt_max, 0) for s in shards])
+    args = lambda s: (s.n_local, s.n_global, s.m)  # noqa: E731
+    for s, sa in zip(shards, spine_all):
+        lo, hi = need[s.rank]
+        check(L.rtf_shard_finish_range(*args(s), _ptr(sa), s.count * nt_max, lo, hi,
+                                       _ptr(s.forest), s.forest.numel(), _ptr(s.ws),
+                                       s.ws.numel(), st, ctypes.byref(s.fview)),
+              "shard finish (ranged)")
+        s.cells = (int(g[s.rank]), int(g[s.rank + 1]))
+        s.slots = (lo, hi)
+
+
+def ranged_xi(xi: torch.Tensor, rank: int, count: int, m: int) -> torch.Tensor:
+    """Map u32 xi (as int32) into rank's xi range [g_r 2^32 / m, g_{r+1} 2^32 / m)
+    for a power-of-two count: xi' = g_r 2^32 / m + (xi >> log2 count) -- a
+    stratified split of the unit interval (input generation, not the method)."""
+    if count & (count - 1):
+        raise ValueError("ranged sampling needs a power-of-two shard count")
+    lo = (rank * m // count) * (1 << 32) // m
+    v = (xi.to(torch.int64) & 0xFFFFFFFF) >> (count.bit_length() - 1)
+    return ((v + lo) & 0xFFFFFFFF).to(torch.int32)

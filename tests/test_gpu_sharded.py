@@ -91,3 +91,42 @@ def test_config4_full_size_sampled(rtf):
         assert f.nodes_numpy().tobytes() == nodes.tobytes(), f"shard {s.rank} records"
         assert f.table_numpy().tobytes() == table.tobytes(), f"shard {s.rank} table"
         assert np.array_equal(f.sample(xd).cpu().numpy(), want)
+
+
+def _check_ranged(rtf, p, m, count):
+    from paper_1901_05423_b200 import sharded
+    pd = torch.from_numpy(p).cuda()
+    single = rtf.build(pd, m)
+    nodes, table = single.nodes_numpy(), single.table_numpy()
+    ref = oracle.build(p, m)
+    shards = sharded.make_shards(pd, m, count)
+    sharded.build_sharded(shards, sharded.LocalComm(), ranged=True)
+    covered = 0
+    for s in shards:
+        f = rtf.Forest.from_buffer(s.n_global, m, s.forest)
+        (j0, j1), (g0, g1) = s.slots, s.cells
+        covered += j1 - j0
+        allrec = f._section(f.view.nodes, 16 * ref.n_pos).cpu().numpy().view(rtf.NODE_DTYPE)
+        assert allrec[j0:j1].tobytes() == nodes[j0:j1].tobytes(), f"shard {s.rank} records"
+        assert f.table_numpy()[g0:g1].tobytes() == table[g0:g1].tobytes(), f"shard {s.rank} table"
+        xi = philox_xi(1 << 15, seed=s.rank + 7)
+        xr = sharded.ranged_xi(torch.from_numpy(xi.view(np.int32)), s.rank, count, m)
+        cells = (xr.numpy().view(np.uint32).astype(np.uint64) * m) >> 32
+        assert np.all((cells >= g0) & (cells < g1))
+        got = f.sample(xr.cuda()).cpu().numpy()
+        assert np.array_equal(got, ref.sample(xr.numpy().view(np.uint32))), f"shard {s.rank} samples"
+    assert covered == ref.n_pos
+
+
+@pytest.mark.parametrize("count", [1, 2, 4, 8])
+def test_sharded_ranged_power_law(rtf, count):
+    # cell 0 of p_i ~ i^20 holds half the leaves: shard 0's cell range owns
+    # records built by most other shards
+    _check_ranged(rtf, power_law(1 << 18, "A"), 1 << 16, count)
+
+
+@pytest.mark.parametrize("count", [2, 4])
+def test_sharded_ranged_spikes_random(rtf, count):
+    _check_ranged(rtf, spikes(3 << 16), 1 << 15, count)
+    rng = np.random.default_rng(10 + count)
+    _check_ranged(rtf, random_small(rng, 100003, zero_frac=0.3, dyn=12.0), 1 << 16, count)
