@@ -518,8 +518,10 @@ def run_gpu_c4(args):
         pos = (2 * k + 1) * n // 8
         if base <= pos < base + n_local:
             p_local[pos - base] = 0.24
-    shards = sharded.make_shards_local(p_local, n, m, rank, world, base)
     comm = sharded.DistComm() if world > 1 else sharded.LocalComm()
+    fused = not args.c4_replicate and not args.c4_nccl and world > 1
+    shards = sharded.make_shards_local(p_local, n, m, rank, world, base,
+                                       alloc=comm.alloc if fused else None)
     forest = rtf.Forest.from_buffer(n, m, shards[0].forest)
     ranged = not args.c4_replicate
     xi = rtf.philox(S, seed=0x5EED, start=rank * S, device=dev)
@@ -532,7 +534,7 @@ def run_gpu_c4(args):
     def step(ev=None):
         if ev:
             ev[0].record(stream)
-        sharded.build_sharded(shards, comm, ranged=ranged)
+        sharded.build_sharded(shards, comm, ranged=ranged, fused=fused)
         if ev:
             ev[1].record(stream)
         forest.sample(xi, out)
@@ -575,8 +577,11 @@ def run_gpu_c4(args):
         "config": {"workload": wl["desc"], "n": n, "m": m, "samples_total": S * world,
                    "l2": f"flushed between steps ({L2_FLUSH_BYTES >> 20} MiB write, untimed)",
                    "parallelism": (f"sharded build over {world} GPU(s); ranged: rank r keeps "
-                                   "the cells [r m/N, (r+1) m/N) (records all-to-all, table "
-                                   "reduce-scatter) and samples that xi stratum"
+                                   "the cells [r m/N, (r+1) m/N) and samples that xi stratum; "
+                                   + ("records and table cells stored by the build kernel "
+                                      "straight into their owner's buffer (symmetric memory)"
+                                      if fused else "records by grouped send/recv, table "
+                                      "reduce-scatter")
                                    if ranged else
                                    f"sharded build over {world} GPU(s) + replicated forest; "
                                    "sampling split across GPUs")},
@@ -868,6 +873,9 @@ def main():
     ap.add_argument("--no-c2", action="store_true", help="skip the config-2 summary")
     ap.add_argument("--c4-replicate", action="store_true",
                     help="config 4: replicate the whole forest instead of ranged sharding")
+    ap.add_argument("--c4-nccl", action="store_true",
+                    help="config 4 ranged: move records with NCCL send/recv instead of the "
+                         "fused peer stores")
     args = ap.parse_args()
     if args.warmup < 3 and args.impl != "reference":
         print("warning: fewer than 3 warm-up steps", file=sys.stderr)

@@ -300,6 +300,8 @@ typedef struct rtf_shard_view {  /* device pointers into a shard workspace */
     uint32_t spine_row_bytes; /* bytes per spine row (a multiple of 16)                */
     uint32_t nt_cap;          /* most rows rtf_shard_finish accepts                    */
     uint32_t reserved;
+    uint32_t *jbound;         /* rtf_shard_build_peers: N + 1 words, J_k where this
+                                 shard saw the boundary (0 elsewhere; MAX-reduce)      */
 } rtf_shard_view;
 
 size_t rtf_shard_workspace_bytes(uint32_t n_local, uint32_t n_global, uint32_t m);
@@ -338,6 +340,22 @@ int rtf_shard_finish_range(uint32_t n_local, uint32_t n_global, uint32_t m,
                            const void *spine_all, uint32_t nt_all, uint32_t j_lo, uint32_t j_hi,
                            void *forest_buf, size_t forest_bytes, void *ws, size_t ws_bytes,
                            void *stream, rtf_forest *out);
+/* Fused ranged build (step 3 with the move folded in): the tile flush stores
+ * each record, and every table write goes, straight into the forest buffer of
+ * the rank owning its cell (peer_forest_bufs[r]: npeer device pointers valid
+ * in this process -- NVLink peer memory across GPUs, e.g. CUDA symmetric
+ * memory; plain device buffers for virtual shards; all laid out for
+ * (n_global, m); m % npeer == 0).  The rank whose leaves straddle an owner
+ * boundary k m / npeer writes J_k into view.jbound[k] (others 0), so a
+ * MAX-reduce of jbound gives every rank its slots [J_r, J_{r+1}).  After the
+ * spine rows are gathered (which also orders every rank's peer stores before
+ * the finish), rtf_shard_finish_range completes each rank's cells.  Blocks
+ * the host until the pointer upload is done. */
+int rtf_shard_build_peers(const float *p, uint32_t n_local, uint32_t n_global, uint32_t m,
+                          uint32_t index_base, uint32_t rank, uint32_t count, const void *totals,
+                          void *const *peer_forest_bufs, uint32_t npeer, void *forest_buf,
+                          size_t forest_bytes, void *ws, size_t ws_bytes, void *stream,
+                          rtf_forest *out);
 
 /* ---------------------------------------------------------- utilities */
 

@@ -36,7 +36,8 @@ class rtf_forest2d(ctypes.Structure):
 class rtf_shard_view(ctypes.Structure):
     _fields_ = [("spine", ctypes.c_void_p), ("scale", ctypes.c_void_p), ("total", ctypes.c_void_p),
                 ("nt_local", ctypes.c_uint32), ("spine_row_bytes", ctypes.c_uint32),
-                ("nt_cap", ctypes.c_uint32), ("reserved", ctypes.c_uint32)]
+                ("nt_cap", ctypes.c_uint32), ("reserved", ctypes.c_uint32),
+                ("jbound", ctypes.c_void_p)]
 
 
 # name -> (restype, argtypes)
@@ -77,6 +78,8 @@ PROTOTYPES = {
     "rtf_shard_finish": (_I32, [_U32, _U32, _U32, _P, _U32, _P, _SZ, _P, _SZ, _P, _F]),
     "rtf_shard_finish_range": (_I32, [_U32, _U32, _U32, _P, _U32, _U32, _U32, _P, _SZ, _P, _SZ,
                                       _P, _F]),
+    "rtf_shard_build_peers": (_I32, [_P, _U32, _U32, _U32, _U32, _U32, _U32, _P, _P, _U32, _P,
+                                     _SZ, _P, _SZ, _P, _F]),
     "rtf_shard_count_cells": (_I32, [_P, _SZ, _U32, _U32, _U32, _U32, _P, _U32, _P, _P]),
     "rtf_launch_count": (_U64, []),
     "rtf_status_string": (ctypes.c_char_p, [_I32]),

@@ -457,6 +457,7 @@ int rtf_shard_get_view(void* ws, size_t ws_bytes, uint32_t n_local, uint32_t n_g
     out->spine_row_bytes = (uint32_t)rtf::spine_row_bytes();
     out->nt_cap = L.nt_cap;
     out->reserved = 0;
+    out->jbound = reinterpret_cast<uint32_t*>(w + L.jbound);
     return RTF_OK;
 }
 
@@ -501,6 +502,43 @@ int rtf_shard_build(const float* p, uint32_t n_local, uint32_t n_global, uint32_
     cudaError_t e =
         rtf::launch_build(p, n_local, m, rtf::kBuildShardedLayout, out->header, out->nodes,
                           out->table, nullptr, ws, L, as_stream(stream), &launches, &sc);
+    return finish(e, launches);
+}
+
+int rtf_shard_build_peers(const float* p, uint32_t n_local, uint32_t n_global, uint32_t m,
+                          uint32_t index_base, uint32_t rank, uint32_t count, const void* totals,
+                          void* const* peer_forest_bufs, uint32_t npeer, void* forest_buf,
+                          size_t forest_bytes, void* ws, size_t ws_bytes, void* stream,
+                          rtf_forest* out) {
+    rtf::WsLayout L;
+    if (!p || !totals || ((uintptr_t)p & 3u) || count == 0 || rank >= count) return RTF_EINVAL;
+    if (!peer_forest_bufs || npeer == 0 || npeer > rtf::kMaxShards || m % npeer) return RTF_EINVAL;
+    if (int s = shard_layout(ws, ws_bytes, n_local, n_global, m, &L)) return s;
+    if ((uint64_t)index_base + n_local > n_global) return RTF_EINVAL;
+    if (int s = rtf_forest_view(forest_buf, forest_bytes, n_global, m, 1, out)) return s;
+    // the peers' record and table sections (every forest buffer has this layout)
+    void* ptrs[2 * rtf::kMaxShards];
+    for (uint32_t r = 0; r < npeer; ++r) {
+        rtf_forest f;
+        if (int s = rtf_forest_view(peer_forest_bufs[r], forest_bytes, n_global, m, 1, &f)) return s;
+        ptrs[r] = f.nodes;
+        ptrs[rtf::kMaxShards + r] = f.table;
+    }
+    unsigned char* w = static_cast<unsigned char*>(ws);
+    cudaStream_t st = as_stream(stream);
+    if (cudaMemcpyAsync(w + L.peers, ptrs, sizeof(void*) * npeer, cudaMemcpyHostToDevice, st) ||
+        cudaMemcpyAsync(w + L.peers + sizeof(void*) * rtf::kMaxShards, ptrs + rtf::kMaxShards,
+                        sizeof(void*) * npeer, cudaMemcpyHostToDevice, st) ||
+        cudaMemsetAsync(w + L.jbound, 0, sizeof(uint32_t) * (rtf::kMaxShards + 1), st))
+        return RTF_ECUDA;
+    cudaStreamSynchronize(st);  // the host pointer array is a stack buffer
+    rtf::ShardCall sc{rtf::kPhTiles | rtf::kPhRuns, n_global, index_base, rank, count, 0,
+                      totals, nullptr};
+    sc.npeer = npeer;
+    int launches = 0;
+    cudaError_t e =
+        rtf::launch_build(p, n_local, m, rtf::kBuildShardedLayout, out->header, out->nodes,
+                          out->table, nullptr, ws, L, st, &launches, &sc);
     return finish(e, launches);
 }
 

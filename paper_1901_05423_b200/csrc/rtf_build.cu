@@ -85,6 +85,13 @@ struct BuildArgs {
     uint32_t epoch;     // this launch's number: CTA 0 publishes rpre with it
     uint32_t mshift;    // m a power of two: cell = key >> mshift (63 - log2 m)
     uint32_t j_lo, j_hi;  // phase E writes only node slots in [j_lo, j_hi) (a ranged finish)
+    // fused ranged sharding: records and table cells are stored straight into
+    // the buffer of the rank owning their cell (cells [r cpo, (r + 1) cpo)),
+    // over NVLink peer memory; jbound[k] receives the first leaf of cell k cpo
+    rtf_node* const* peer_nodes;
+    rtf_ref* const* peer_table;
+    uint32_t npeer, cpo;
+    uint32_t* jbound;
     rtf_header* hdr;
     rtf_node* nodes;
     rtf_ref* table;
@@ -323,6 +330,10 @@ __global__ void __launch_bounds__(THREADS, MINB) k_build(BuildArgs A) {
     auto cell_fn = [&](uint64_t key) -> uint32_t {
         return POW2 ? (uint32_t)(key >> A.mshift) : cell_of(key, m);
     };
+    // where cell g's table entry lives (the owner rank's table when fused)
+    auto table_at = [&](uint32_t g) -> rtf_ref* {
+        return A.npeer ? A.peer_table[g / A.cpo] : A.table;
+    };
     const int lane = tid & 31, warp = tid >> 5;
     uint32_t* gbar = &A.counters[kCtrGridBar];
 
@@ -520,7 +531,7 @@ __global__ void __launch_bounds__(THREADS, MINB) k_build(BuildArgs A) {
     }
     // sharded: this shard writes only the table cells its leaves own; the rest
     // stays INT32_MIN so a MAX-reduction across shards assembles the table
-    if (sharded && (ph & kPhTiles))
+    if (sharded && (ph & kPhTiles) && !A.npeer)  // fused: every cell is written once by its builder
         for (uint32_t g = b * THREADS + tid; g < m; g += G * THREADS) st_cell(A.table, g, 0u, INT32_MIN);
     grid_barrier(gbar);
     RTF_TICK(1);
@@ -747,7 +758,7 @@ __global__ void __launch_bounds__(THREADS, MINB) k_build(BuildArgs A) {
         if (tc) {
             uint64_t kn = (c_ex + tc < cnt) ? s_key[pad8(c_ex + tc)] : s_key_after;
             uint32_t cn = POW2 ? 0u : ((kn == kOne63) ? m : cell_of(kn, m));
-            if (j0 == 0 && c_ex == 0) st_cell(A.table, 0, 0u, 0);  // leaf 0 (key 0): cell 0's anchor
+            if (j0 == 0 && c_ex == 0) st_cell(table_at(0), 0, 0u, 0);  // leaf 0 (key 0): cell 0's anchor
 #pragma unroll
             for (int k = VPT - 1; k >= 0; --k) {
                 if ((posmask >> k) & 1u) {
@@ -771,10 +782,13 @@ __global__ void __launch_bounds__(THREADS, MINB) k_build(BuildArgs A) {
                         const int32_t i = (int32_t)(first + k) + ib;
                         // the next cell's anchor (a one-leaf cell gets its
                         // two-interval entry from the anchor's tile, below)
-                        if (cn < m) st_cell(A.table, cn, 0u, (int32_t)(j0 + jl + 1));
+                        if (cn < m) st_cell(table_at(cn), cn, 0u, (int32_t)(j0 + jl + 1));
+                        if (A.npeer)  // the first leaf of every owner boundary k cpo in (cell, cn]
+                            for (uint32_t k = cell / A.cpo + 1; k <= min(A.npeer, cn / A.cpo); ++k)
+                                A.jbound[k] = j0 + jl + 1;
                         const uint32_t len = cn - cell - 1;
                         if (len <= kShortRun) {
-                            for (uint32_t g = cell + 1; g < cn; ++g) st_cell(A.table, g, 0u, ~i);
+                            for (uint32_t g = cell + 1; g < cn; ++g) st_cell(table_at(g), g, 0u, ~i);
                         } else {
                             table_queue(A.counters, A.queue, A.qcap, i, cell, len);
                         }
@@ -858,7 +872,8 @@ __global__ void __launch_bounds__(THREADS, MINB) k_build(BuildArgs A) {
                                 const uint2 e =
                                     single_leaf_cell(key, (int32_t)(first + k) + ib, ~s_c0[q], a);
                                 if ((int32_t)e.y != a)
-                                    st_cell(A.table, cell_fn(key), e.x, (int32_t)e.y);
+                                    st_cell(table_at(cell_fn(key)), cell_fn(key), e.x,
+                                            (int32_t)e.y);
                             }
                         }
                     }
@@ -996,8 +1011,12 @@ __global__ void __launch_bounds__(THREADS, MINB) k_build(BuildArgs A) {
             for (uint32_t l = tid; l < cnt; l += THREADS) {
                 const uint32_t q = pad8(l);
                 const uint64_t key = s_key[q];
-                gnode[l] = make_uint4((uint32_t)key, (uint32_t)(key >> 32), (uint32_t)s_c0[q],
-                                      (uint32_t)s_c1[q]);
+                const uint4 rec = make_uint4((uint32_t)key, (uint32_t)(key >> 32),
+                                             (uint32_t)s_c0[q], (uint32_t)s_c1[q]);
+                if (A.npeer)  // fused: to the rank owning the record's cell (peer memory)
+                    reinterpret_cast<uint4*>(A.peer_nodes[cell_fn(key) / A.cpo] + j0)[l] = rec;
+                else
+                    gnode[l] = rec;
             }
         }
         __syncthreads();  // spines complete; keys and children are free
@@ -1029,6 +1048,7 @@ __global__ void __launch_bounds__(THREADS, MINB) k_build(BuildArgs A) {
         // no barrier here: the next tile writes shared memory only after its scan
         RTF_TICK(6);
     }
+    if (A.npeer) __threadfence_system();  // peer stores visible before the next exchange
     grid_barrier(gbar);
     RTF_TICK(7);
 
@@ -1155,7 +1175,8 @@ __global__ void __launch_bounds__(THREADS, MINB) k_build(BuildArgs A) {
     const uint32_t nq = (ph & kPhRuns) ? min(__ldcg(&A.counters[kCtrQueue]), A.qcap) : 0u;
     for (uint32_t q = b * NW + warp; q < nq; q += G * NW) {
         const RunChunk rc = A.queue[q];
-        for (uint32_t g = lane; g < rc.len; g += 32) st_cell(A.table, rc.start + g, 0u, rc.value);
+        for (uint32_t g = lane; g < rc.len; g += 32)
+            st_cell(table_at(rc.start + g), rc.start + g, 0u, rc.value);
     }
     __syncthreads();
     RTF_TICK(8);
@@ -1223,6 +1244,8 @@ size_t build_workspace_layout(uint32_t n, uint32_t m, uint32_t flags, WsLayout* 
     L->bmax = take(sizeof(uint32_t) * (((size_t)L->nt_cap + 63) / 64));
     L->qcap = build_queue_capacity(m);
     L->queue = take(sizeof(RunChunk) * (size_t)L->qcap);
+    L->peers = take(2 * sizeof(void*) * kMaxShards);  // fused sharding: peer nodes, tables
+    L->jbound = take(sizeof(uint32_t) * (kMaxShards + 1));
     L->bytes = off;
     return off;
 }
@@ -1278,6 +1301,11 @@ cudaError_t launch_build(const float* p, uint32_t n, uint32_t m, uint32_t flags,
     A.index_base = sc ? sc->index_base : 0;
     A.j_lo = sc ? sc->j_lo : 0u;
     A.j_hi = sc ? sc->j_hi : 0xffffffffu;
+    A.npeer = sc ? sc->npeer : 0u;
+    A.cpo = A.npeer ? m / A.npeer : 0u;
+    A.peer_nodes = A.npeer ? reinterpret_cast<rtf_node* const*>(w + L.peers) : nullptr;
+    A.peer_table = A.npeer ? reinterpret_cast<rtf_ref* const*>(w + L.peers) + kMaxShards : nullptr;
+    A.jbound = reinterpret_cast<uint32_t*>(w + L.jbound);
     A.scale_io = reinterpret_cast<uint32_t*>(w + L.scale);
     A.shard_totals = sc ? reinterpret_cast<const Pfx*>(sc->totals) : nullptr;
     A.shard_rank = sc ? sc->rank : 0;

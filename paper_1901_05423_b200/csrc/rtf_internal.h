@@ -34,7 +34,8 @@ struct WsLayout {
     uint32_t nt;  // tiles
     uint32_t qcap;
     uint32_t nt_cap;  // rows phase E can link (a sharded finish: all shards' tiles)
-    size_t maxpart, counters, scale, total, excl, rng, rpre, spine, tmax, bmax, queue, bytes;
+    size_t maxpart, counters, scale, total, excl, rng, rpre, spine, tmax, bmax, queue, peers,
+        jbound, bytes;
 };
 
 // one call of a sharded build (config 4); see rtf_shard_* in include/rtf.h
@@ -43,6 +44,7 @@ struct ShardCall {
     const void* totals;        // device: count shard totals (16 B each)
     const void* spine_in;      // device: finish -- all shards' tile spines (nt_in rows)
     uint32_t j_lo = 0, j_hi = 0xffffffffu;  // finish: node slots this rank holds
+    uint32_t npeer = 0;  // fused ranged build: peer pointers already in the workspace
 };
 
 // leaves of nodes[j0, j0 + cnt) whose cell is below bound[k]: counts[k], k < nb

@@ -83,6 +83,10 @@ class LocalComm:
             full[r][lo[r]: hi[r]].copy_(mx)
 
 
+def _local_peers(shards):
+    return [s.forest.data_ptr() for s in shards]
+
+
 class DistComm:
     """One shard per process (torch.distributed); lists hold the local tensor."""
 
@@ -110,6 +114,18 @@ class DistComm:
 
     def allreduce_sum(self, ts):
         self.dist.all_reduce(ts[0], op=self.dist.ReduceOp.SUM, group=self.group)
+
+    # fused ranged sharding: forest buffers in CUDA symmetric memory, so every
+    # rank's kernels can store into every peer's buffer over NVLink
+    def alloc(self, nbytes, device):
+        import torch.distributed._symmetric_memory as symm_mem
+        return symm_mem.empty(nbytes, dtype=torch.uint8, device=device)
+
+    def peer_ptrs(self, buf):
+        import torch.distributed._symmetric_memory as symm_mem
+        group = self.group if self.group is not None else self.dist.group.WORLD
+        hdl = symm_mem.rendezvous(buf, group)
+        return [int(x) for x in hdl.buffer_ptrs]
 
     def alltoallv(self, sends, recvs):
         """Grouped point-to-point transfers of the local pieces (sends[0][r] to
@@ -162,12 +178,15 @@ class Shard:
     view: rtf_shard_view = field(init=False)
     fview: rtf_forest = field(init=False)
 
+    alloc: object = None                 # forest allocator (symmetric memory when fused)
+
     def __post_init__(self):
         L = _lib.load()
         dev = self.p.device
         fb = L.rtf_forest_bytes(self.n_global, self.m, 1)
         wb = L.rtf_shard_workspace_bytes(self.n_local, self.n_global, self.m)
-        self.forest = torch.empty(fb, dtype=torch.uint8, device=dev)
+        self.forest = (self.alloc(fb, dev) if self.alloc is not None
+                       else torch.empty(fb, dtype=torch.uint8, device=dev))
         self.ws = torch.empty(wb, dtype=torch.uint8, device=dev)
         self.view = rtf_shard_view()
         self.fview = rtf_forest()
@@ -214,12 +233,16 @@ def _padded(t: torch.Tensor, nbytes: int, fill: int) -> torch.Tensor:
     return out
 
 
-def build_sharded(shards: list[Shard], comm, ranged: bool = False) -> None:
+def build_sharded(shards: list[Shard], comm, ranged: bool = False, fused: bool = False) -> None:
     """Run the sharded build for the local shards (all of them for LocalComm,
     the process's own for DistComm).  On return every shard's forest buffer
     holds the full forest -- or, with ranged=True, shard r holds the cells
     [g_r, g_{r+1}) = [r m / N, (r + 1) m / N) (node slots [J_r, J_{r+1}),
-    stored in s.cells / s.slots), the xi range it samples."""
+    stored in s.cells / s.slots), the xi range it samples.  fused=True (ranged
+    only): the per-shard build stores records and table cells straight into
+    their owners' buffers (rtf_shard_build_peers: peer memory), so no
+    all-to-all and no reduce-scatter remain -- only the gather of the spine
+    rows and a MAX-reduce of N + 1 boundary words."""
     L = _lib.load()
     st = _stream()
     sh0 = shards[0]
@@ -233,6 +256,9 @@ def build_sharded(shards: list[Shard], comm, ranged: bool = False) -> None:
         check(L.rtf_shard_totals(_ptr(s.p), *args(s), s.base, _ptr(s.ws), s.ws.numel(), st),
               "shard totals")
     totals = comm.allgather([s.total_bytes() for s in shards])
+    if fused and sh0.count > 1:
+        _build_fused(shards, comm, totals, st)
+        return
     # 3. per-shard build with the global prefix
     for s, tot in zip(shards, totals):
         check(L.rtf_shard_build(_ptr(s.p), *args(s), s.base, s.rank, s.count, _ptr(tot),
@@ -266,9 +292,10 @@ def build_sharded(shards: list[Shard], comm, ranged: bool = False) -> None:
 
 
 def make_shards_local(p_local: torch.Tensor, n: int, m: int, rank: int, count: int,
-                      base: int) -> list[Shard]:
-    """The one shard this process holds (multi-GPU: one shard per rank)."""
-    return [Shard(rank, count, n, m, base, p_local.numel(), p_local)]
+                      base: int, alloc=None) -> list[Shard]:
+    """The one shard this process holds (multi-GPU: one shard per rank);
+    alloc=DistComm().alloc puts its forest in symmetric memory (fused mode)."""
+    return [Shard(rank, count, n, m, base, p_local.numel(), p_local, alloc)]
 
 
 def make_shards(p: torch.Tensor, m: int, count: int, ranks=None) -> list[Shard]:
@@ -344,3 +371,40 @@ def ranged_xi(xi: torch.Tensor, rank: int, count: int, m: int) -> torch.Tensor:
     lo = (rank * m // count) * (1 << 32) // m
     v = (xi.to(torch.int64) & 0xFFFFFFFF) >> (count.bit_length() - 1)
     return ((v + lo) & 0xFFFFFFFF).to(torch.int32)
+
+
+def _build_fused(shards, comm, totals, st) -> None:
+    """Fused ranged build: step 3 writes each record / table cell into the
+    buffer of the rank owning its cell; then the boundaries J and the spine
+    rows are exchanged and each rank finishes its own cells."""
+    L = _lib.load()
+    sh0 = shards[0]
+    N, m, dev = sh0.count, sh0.m, sh0.p.device
+    if m % N:
+        raise ValueError("fused ranged sharding needs m divisible by the shard count")
+    args = lambda s: (s.n_local, s.n_global, s.m)  # noqa: E731
+    for s, tot in zip(shards, totals):
+        peers = _local_peers(shards) if isinstance(comm, LocalComm) else comm.peer_ptrs(s.forest)
+        arr = (ctypes.c_void_p * N)(*peers)
+        check(L.rtf_shard_build_peers(_ptr(s.p), *args(s), s.base, s.rank, s.count, _ptr(tot),
+                                      arr, N, _ptr(s.forest), s.forest.numel(), _ptr(s.ws),
+                                      s.ws.numel(), st, ctypes.byref(s.fview)),
+              "shard build (fused)")
+    jb = [s._ws_slice(s.view.jbound, 4 * (N + 1)).view(torch.int32) for s in shards]
+    comm.allreduce_max(jb)
+    J = jb[0].cpu().numpy().astype(np.int64)
+    nt_max = max(s.view.nt_local for s in shards)
+    if hasattr(comm, "dist"):
+        t = torch.tensor([nt_max], dtype=torch.int64, device=dev)
+        comm.allreduce_max([t])
+        nt_max = int(t.item())
+    row = sh0.view.spine_row_bytes
+    spine_all = comm.allgather([_padded(s.spine_bytes(), row * nt_max, 0) for s in shards])
+    for s, sa in zip(shards, spine_all):
+        lo, hi = int(J[s.rank]), int(J[s.rank + 1])
+        check(L.rtf_shard_finish_range(*args(s), _ptr(sa), s.count * nt_max, lo, hi,
+                                       _ptr(s.forest), s.forest.numel(), _ptr(s.ws),
+                                       s.ws.numel(), st, ctypes.byref(s.fview)),
+              "shard finish (fused)")
+        s.cells = (s.rank * m // N, (s.rank + 1) * m // N)
+        s.slots = (lo, hi)

@@ -93,14 +93,14 @@ def test_config4_full_size_sampled(rtf):
         assert np.array_equal(f.sample(xd).cpu().numpy(), want)
 
 
-def _check_ranged(rtf, p, m, count):
+def _check_ranged(rtf, p, m, count, fused=False):
     from paper_1901_05423_b200 import sharded
     pd = torch.from_numpy(p).cuda()
     single = rtf.build(pd, m)
     nodes, table = single.nodes_numpy(), single.table_numpy()
     ref = oracle.build(p, m)
     shards = sharded.make_shards(pd, m, count)
-    sharded.build_sharded(shards, sharded.LocalComm(), ranged=True)
+    sharded.build_sharded(shards, sharded.LocalComm(), ranged=True, fused=fused)
     covered = 0
     for s in shards:
         f = rtf.Forest.from_buffer(s.n_global, m, s.forest)
@@ -130,3 +130,15 @@ def test_sharded_ranged_spikes_random(rtf, count):
     _check_ranged(rtf, spikes(3 << 16), 1 << 15, count)
     rng = np.random.default_rng(10 + count)
     _check_ranged(rtf, random_small(rng, 100003, zero_frac=0.3, dyn=12.0), 1 << 16, count)
+
+
+@pytest.mark.parametrize("count", [2, 4, 8])
+def test_sharded_fused_peer_stores(rtf, count):
+    """Fused ranged build: records and table cells stored straight into the
+    owner's buffer by the build kernel (peer pointers = the virtual shards'
+    buffers); byte-equal cell slices, exact samples."""
+    _check_ranged(rtf, power_law(1 << 18, "A"), 1 << 16, count, fused=True)
+    _check_ranged(rtf, spikes(3 << 16), 1 << 15, count, fused=True)
+    rng = np.random.default_rng(20 + count)
+    _check_ranged(rtf, random_small(rng, 4096 * 3 * count - 100, zero_frac=0.3, dyn=12.0),
+                  1 << 16, count, fused=True)
