@@ -295,7 +295,7 @@ __device__ unsigned long long g_phase_cycles[kMaxGrid][16];
 
 // ============================================================== the build kernel
 
-template <int THREADS, int VPT, bool CDF, int MINB = 2, bool POW2 = false>
+template <int THREADS, int VPT, bool CDF, int MINB = 2, bool POW2 = false, bool FUSED = false>
 __global__ void __launch_bounds__(THREADS, MINB) k_build(BuildArgs A) {
     constexpr int TILE = THREADS * VPT;
     constexpr int NW = THREADS / 32;
@@ -332,7 +332,7 @@ __global__ void __launch_bounds__(THREADS, MINB) k_build(BuildArgs A) {
     };
     // where cell g's table entry lives (the owner rank's table when fused)
     auto table_at = [&](uint32_t g) -> rtf_ref* {
-        return A.npeer ? A.peer_table[g / A.cpo] : A.table;
+        return FUSED ? A.peer_table[g / A.cpo] : A.table;
     };
     const int lane = tid & 31, warp = tid >> 5;
     uint32_t* gbar = &A.counters[kCtrGridBar];
@@ -531,7 +531,7 @@ __global__ void __launch_bounds__(THREADS, MINB) k_build(BuildArgs A) {
     }
     // sharded: this shard writes only the table cells its leaves own; the rest
     // stays INT32_MIN so a MAX-reduction across shards assembles the table
-    if (sharded && (ph & kPhTiles) && !A.npeer)  // fused: every cell is written once by its builder
+    if (sharded && (ph & kPhTiles) && !FUSED)  // fused: every cell is written once by its builder
         for (uint32_t g = b * THREADS + tid; g < m; g += G * THREADS) st_cell(A.table, g, 0u, INT32_MIN);
     grid_barrier(gbar);
     RTF_TICK(1);
@@ -783,7 +783,7 @@ __global__ void __launch_bounds__(THREADS, MINB) k_build(BuildArgs A) {
                         // the next cell's anchor (a one-leaf cell gets its
                         // two-interval entry from the anchor's tile, below)
                         if (cn < m) st_cell(table_at(cn), cn, 0u, (int32_t)(j0 + jl + 1));
-                        if (A.npeer)  // the first leaf of every owner boundary k cpo in (cell, cn]
+                        if (FUSED)  // the first leaf of every owner boundary k cpo in (cell, cn]
                             for (uint32_t k = cell / A.cpo + 1; k <= min(A.npeer, cn / A.cpo); ++k)
                                 A.jbound[k] = j0 + jl + 1;
                         const uint32_t len = cn - cell - 1;
@@ -1013,7 +1013,7 @@ __global__ void __launch_bounds__(THREADS, MINB) k_build(BuildArgs A) {
                 const uint64_t key = s_key[q];
                 const uint4 rec = make_uint4((uint32_t)key, (uint32_t)(key >> 32),
                                              (uint32_t)s_c0[q], (uint32_t)s_c1[q]);
-                if (A.npeer)  // fused: to the rank owning the record's cell (peer memory)
+                if (FUSED)  // fused: to the rank owning the record's cell (peer memory)
                     reinterpret_cast<uint4*>(A.peer_nodes[cell_fn(key) / A.cpo] + j0)[l] = rec;
                 else
                     gnode[l] = rec;
@@ -1048,7 +1048,7 @@ __global__ void __launch_bounds__(THREADS, MINB) k_build(BuildArgs A) {
         // no barrier here: the next tile writes shared memory only after its scan
         RTF_TICK(6);
     }
-    if (A.npeer) __threadfence_system();  // peer stores visible before the next exchange
+    if (FUSED) __threadfence_system();  // peer stores visible before the next exchange
     grid_barrier(gbar);
     RTF_TICK(7);
 
@@ -1262,9 +1262,9 @@ static int num_sms() {
     return sms;
 }
 
-template <int THREADS, int VPT, bool CDF, int MINB = 2, bool POW2 = false>
+template <int THREADS, int VPT, bool CDF, int MINB = 2, bool POW2 = false, bool FUSED = false>
 static cudaError_t launch_fused(BuildArgs& A, cudaStream_t st, int* launches) {
-    auto kern = k_build<THREADS, VPT, CDF, MINB, POW2>;
+    auto kern = k_build<THREADS, VPT, CDF, MINB, POW2, FUSED>;
     const size_t smem = build_smem_bytes<THREADS, VPT>();  // phase B stages tile totals there
     static int max_grid = 0;  // per instantiation: co-resident CTAs
     if (!max_grid) {
@@ -1342,6 +1342,9 @@ cudaError_t launch_build(const float* p, uint32_t n, uint32_t m, uint32_t flags,
     // were measured again with the fused kernel: 293 / 315 / 399 us for c3)
     const bool pow2 = (m & (m - 1)) == 0;
     A.mshift = 63u - (uint32_t)ceil_log2_u32(m);
+    if (A.npeer)  // fused ranged sharding (rtf_shard_build_peers)
+        return small ? launch_fused<64, 4, false, 2, false, true>(A, st, launches)
+                     : launch_fused<512, 8, false, 2, false, true>(A, st, launches);
     if (small)
         return pow2 ? launch_fused<64, 4, false, 2, true>(A, st, launches)
                     : launch_fused<64, 4, false>(A, st, launches);
