@@ -171,6 +171,12 @@ int rtf_forest_status(const rtf_forest *f, void *stream, rtf_header *headers_hos
 int rtf_sample(const rtf_forest *f, const uint32_t *xi, uint64_t count, int32_t *out,
                void *stream);
 
+/* rtf_sample for float xi in [0, 1): xi is first mapped exactly to the u32
+ * fixed point floor(xi 2^32) (reading R11); values outside [0, 1) saturate to
+ * 0 or 2^32 - 1 (NaN -> 0). */
+int rtf_sample_f32(const rtf_forest *f, const float *xi, uint64_t count, int32_t *out,
+                   void *stream);
+
 /* Measurement aid: loads[k] = number of memory loads rtf_sample performs for
  * xi[k] (1 guide-table entry + 1 per node visited), the load-count convention
  * of Table 1; gives E[visits], the maximum and average_32.

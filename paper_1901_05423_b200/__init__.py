@@ -106,6 +106,15 @@ class Forest:
 
     # ---------------------------------------------------------------- sampling
     def sample(self, xi: torch.Tensor, out: torch.Tensor | None = None, stream=None):
+        """xi: int32/uint32 fixed point xi/2^32, or float32 in [0, 1)."""
+        if xi.dtype == torch.float32:
+            if not xi.is_cuda or not xi.is_contiguous():
+                raise ValueError("xi must be a contiguous CUDA tensor")
+            if out is None:
+                out = torch.empty(xi.numel(), dtype=torch.int32, device=xi.device)
+            check(lib().rtf_sample_f32(ctypes.byref(self.view), _ptr(xi), xi.numel(), _ptr(out),
+                                       _stream(stream)), "rtf_sample_f32")
+            return out
         xi = _u32_view(xi)
         if out is None:
             out = torch.empty(xi.numel(), dtype=torch.int32, device=xi.device)

@@ -54,6 +54,7 @@ PROTOTYPES = {
     "rtf_forest_view": (_I32, [_P, _SZ, _U32, _U32, _U32, _F]),
     "rtf_forest_status": (_I32, [_F, _P, _H]),
     "rtf_sample": (_I32, [_F, _P, _U64, _P, _P]),
+    "rtf_sample_f32": (_I32, [_F, _P, _U64, _P, _P]),
     "rtf_sample_loads": (_I32, [_F, _P, _U64, _P, _P, _P]),
     "rtf_sample_rows": (_I32, [_F, _P, _P, _U64, _P, _P]),
     "rtf_build_cdf": (_I32, [_P, _U32, _P, _P, _P, _SZ, _P]),

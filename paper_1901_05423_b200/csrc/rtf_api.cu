@@ -176,6 +176,16 @@ int rtf_sample(const rtf_forest* f, const uint32_t* xi, uint64_t count, int32_t*
     return finish(e, launches);
 }
 
+int rtf_sample_f32(const rtf_forest* f, const float* xi, uint64_t count, int32_t* out,
+                   void* stream) {
+    if (!f || !f->nodes || !f->table || !f->header || f->rows != 1) return RTF_EINVAL;
+    if (count && (!xi || !out)) return RTF_EINVAL;
+    if ((((uintptr_t)xi | (uintptr_t)out) & 3u) != 0) return RTF_EINVAL;
+    int launches = 0;
+    cudaError_t e = rtf::launch_sample_f32(*f, xi, count, out, as_stream(stream), &launches);
+    return finish(e, launches);
+}
+
 int rtf_sample_loads(const rtf_forest* f, const uint32_t* xi, uint64_t count, int32_t* loads,
                      int32_t* loads_plain, void* stream) {
     if (!f || !f->nodes || !f->table || !f->header || f->rows != 1) return RTF_EINVAL;

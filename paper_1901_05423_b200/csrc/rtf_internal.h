@@ -76,6 +76,9 @@ cudaError_t launch_sample_2d(const rtf_forest2d& f, const uint32_t* xi1, const u
 cudaError_t launch_sample(const rtf_forest& f, const uint32_t* row, const uint32_t* xi,
                           uint64_t count, int32_t* out, cudaStream_t st, int* launches);
 
+cudaError_t launch_sample_f32(const rtf_forest& f, const float* xi, uint64_t count, int32_t* out,
+                              cudaStream_t st, int* launches);
+
 cudaError_t launch_sample_loads(const rtf_forest& f, const uint32_t* xi, uint64_t count,
                                 int32_t* loads, int32_t* loads_plain, cudaStream_t st,
                                 int* launches);

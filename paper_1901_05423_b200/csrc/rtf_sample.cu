@@ -47,7 +47,13 @@ __device__ __forceinline__ int32_t sample_one(const rtf_node* __restrict__ nodes
     return j >= 0 ? kCorrupt : ~j;
 }
 
-template <bool ROWS>
+// float xi in [0, 1) -> u32 fixed point floor(xi 2^32) (exact: a power-of-two
+// scaling, then truncation; reading R11); out-of-range values saturate
+__device__ __forceinline__ uint32_t xi_bits(uint32_t v, bool f32) {
+    return f32 ? __float2uint_rz(__uint_as_float(v) * 4294967296.0f) : v;
+}
+
+template <bool ROWS, bool F32 = false>
 __global__ void __launch_bounds__(kSampleThreads)
     k_sample(const rtf_node* __restrict__ nodes, const rtf_ref* __restrict__ table,
              const rtf_header* __restrict__ hdr, uint32_t n, uint32_t m,
@@ -65,7 +71,8 @@ __global__ void __launch_bounds__(kSampleThreads)
         const uint64_t nq = count >> 2;
         for (uint64_t q = gt; q < nq; q += gs) {
             const uint4 xv = ld_stream_u4(xi + 4 * q);
-            const uint32_t x[4] = {xv.x, xv.y, xv.z, xv.w};
+            const uint32_t x[4] = {xi_bits(xv.x, F32), xi_bits(xv.y, F32), xi_bits(xv.z, F32),
+                                   xi_bits(xv.w, F32)};
             int32_t j[4];
             const rtf_node* nb[4];
             uint64_t x63[4];
@@ -102,7 +109,7 @@ __global__ void __launch_bounds__(kSampleThreads)
     }
     for (uint64_t k = done + gt; k < count; k += gs) {
         const uint32_t r = ROWS ? row[k] : 0u;
-        out[k] = bad ? INT32_MAX : sample_one<ROWS>(nodes, table, hdr, n, m, r, xi[k]);
+        out[k] = bad ? INT32_MAX : sample_one<ROWS>(nodes, table, hdr, n, m, r, xi_bits(xi[k], F32));
     }
 }
 
@@ -280,6 +287,17 @@ cudaError_t launch_sample(const rtf_forest& f, const uint32_t* row, const uint32
     else
         k_sample<false><<<grid, kSampleThreads, 0, st>>>(f.nodes, f.table, f.header, f.n, f.m,
                                                          nullptr, xi, count, out, vec);
+    ++*launches;
+    return cudaGetLastError();
+}
+
+cudaError_t launch_sample_f32(const rtf_forest& f, const float* xi, uint64_t count, int32_t* out,
+                              cudaStream_t st, int* launches) {
+    if (count == 0) return cudaSuccess;
+    const bool vec = (((uintptr_t)xi | (uintptr_t)out) & 15u) == 0;
+    k_sample<false, true><<<grid_for(vec ? (count + 3) / 4 : count), kSampleThreads, 0, st>>>(
+        f.nodes, f.table, f.header, f.n, f.m, nullptr, reinterpret_cast<const uint32_t*>(xi), count,
+        out, vec);
     ++*launches;
     return cudaGetLastError();
 }

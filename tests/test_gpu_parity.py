@@ -354,3 +354,18 @@ def test_corrupted_forest_terminates(rtf):
     xi = dev_u32(np.arange(0, 2**32, 2**22, dtype=np.uint64).astype(np.uint32))
     out = f.sample(xi).cpu().numpy()
     assert np.all(out == np.iinfo(np.int32).min)
+
+
+def test_float_xi_entry(rtf):
+    """rtf_sample_f32: float xi in [0, 1) is mapped to floor(xi 2^32) exactly
+    (reading R11), then sampled as usual; out-of-range values saturate."""
+    rng = np.random.default_rng(17)
+    p = random_small(rng, 30000, zero_frac=0.2)
+    f = rtf.build(dev_f32(p), 4096)
+    ref = oracle.build(p, 4096)
+    xf = np.concatenate([rng.random(1 << 16).astype(np.float32),
+                         np.array([0.0, 0.5, np.nextafter(np.float32(1), np.float32(0)), 1.0, 7.5,
+                                   -0.25], np.float32)])
+    want_u = np.clip(np.floor(xf.astype(np.float64) * 2.0 ** 32), 0, 2**32 - 1).astype(np.uint32)
+    got = f.sample(torch.from_numpy(xf).cuda()).cpu().numpy()
+    assert np.array_equal(got, ref.sample(want_u))
