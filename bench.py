@@ -400,7 +400,10 @@ def run_gpu(args):
                      "traffic": (round(ncu_traffic("k_sample_per_sample", wl["name"]) * S)
                                  if ncu_traffic("k_sample_per_sample", wl["name"]) else None),
                      "algorithmic_bytes_per_unit": round(bytes_sample, 3),
-                     "unit_of_work": "sample", "peak_source": peak_src},
+                     "unit_of_work": "sample", "peak_source": peak_src,
+                     "limiter": "not HBM: scattered 8/16-B loads, one L1TEX->L2 request each; "
+                                "ncu l1tex__m_l1tex2xbar_req_cycles_active = 81% of peak "
+                                "(profiles/r01_summary.md, DESIGN.md 5.3)"},
         "roofline_build": {"kernel": "k_build (one cooperative kernel: scale, tile totals, "
                                      "spine scan, tiles + in-tile Alg. 1, cross-tile Alg. 1)",
                            "bound": "hbm",
@@ -408,6 +411,8 @@ def run_gpu(args):
                            "frac": round(ach_b / peak, 4),
                            "traffic": ncu_traffic("build", wl["name"]),
                            "algorithmic_bytes_per_launch": bytes_build,
+                           "limiter": "instruction issue (~285 thread-instructions per entry, "
+                                      "IPC 2.1; DRAM 16% of peak), profiles/r01_summary.md",
                            "peak_source": peak_src},
         "gpu_launches": launches,
         "clocks": sampler.summary(),
