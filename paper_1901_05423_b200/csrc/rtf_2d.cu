@@ -56,7 +56,7 @@ __device__ __forceinline__ double rel_pos(const rtf_node* __restrict__ nodes, in
     return __ddiv_rn(__ull2double_rn(((uint64_t)x << 31) - lo), __ull2double_rn(hi - lo));
 }
 
-__global__ void __launch_bounds__(k2dThreads)
+__global__ void __launch_bounds__(k2dThreads, 8)  // 32 registers: 2048 threads per SM
     k_sample_2d(rtf_forest2d f, const uint32_t* __restrict__ xi1, const uint32_t* __restrict__ xi2,
                 uint64_t count, int32_t* __restrict__ pixel, float* __restrict__ pos) {
     const uint64_t gs = (uint64_t)gridDim.x * blockDim.x;
