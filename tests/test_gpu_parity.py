@@ -369,3 +369,38 @@ def test_float_xi_entry(rtf):
     want_u = np.clip(np.floor(xf.astype(np.float64) * 2.0 ** 32), 0, 2**32 - 1).astype(np.uint32)
     got = f.sample(torch.from_numpy(xf).cuda()).cpu().numpy()
     assert np.array_equal(got, ref.sample(want_u))
+
+
+def test_concurrent_sampling_two_streams(rtf):
+    """rtf.h: sampling is read-only on the forest, so calls on two streams may
+    overlap; both give the oracle's indices."""
+    p = power_law(1 << 20, "B")
+    ref = oracle.build(p, 1 << 18)
+    f = rtf.build(dev_f32(p), 1 << 18)
+    torch.cuda.synchronize()
+    xa, xb = philox_xi(1 << 22, seed=31), philox_xi(1 << 22, seed=32)
+    da, db = dev_u32(xa), dev_u32(xb)
+    s1, s2 = torch.cuda.Stream(), torch.cuda.Stream()
+    oa = torch.empty_like(da)
+    ob = torch.empty_like(db)
+    for _ in range(3):
+        with torch.cuda.stream(s1):
+            f.sample(da, oa, stream=s1)
+        with torch.cuda.stream(s2):
+            f.sample(db, ob, stream=s2)
+    torch.cuda.synchronize()
+    assert np.array_equal(oa.cpu().numpy(), ref.sample(xa))
+    assert np.array_equal(ob.cpu().numpy(), ref.sample(xb))
+
+
+def test_rebuild_with_new_data(rtf):
+    """One Forest object rebuilt with different distributions of its size:
+    every build equals the oracle's (no state leaks between builds)."""
+    rng = np.random.default_rng(41)
+    n, m = 50000, 12345
+    f = rtf.Forest(n, m)
+    for t in range(6):
+        p = random_small(rng, n, zero_frac=float(rng.choice([0, 0.5, 0.95])),
+                         dyn=float(rng.choice([1, 10, 30])))
+        f.build(dev_f32(p))
+        assert_forest_equal(f, oracle.build(p, m), f"rebuild {t}")
