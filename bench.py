@@ -293,6 +293,22 @@ def run_gpu(args):
     cutbin_gs = world * S / (t_cb * 1e-3) / 1e9
     cutlin_gs = world * S_lin / (t_cl * 1e-3) / 1e9
 
+    # context only: torch.searchsorted on a float32 CDF -- a
+    # library binary search, not bit-exact with the fixed-point CDF
+    S_ts = min(S, 1 << 28)
+    cdf32 = torch.cumsum(p.double(), 0)
+    cdf32 = (cdf32 / cdf32[-1]).float()
+    xf = (xi[:S_ts].to(torch.int64) & 0xFFFFFFFF).to(torch.float64).mul_(2.0 ** -32).float()
+    ts_out = torch.searchsorted(cdf32, xf, right=True)
+    t_ts = time_call(lambda: torch.searchsorted(cdf32, xf, right=True, out=ts_out), 2)
+    ts_agree = float((ts_out.to(torch.int32) == out[:S_ts]).float().mean().item())
+    del cdf32, xf, ts_out
+    if world > 1:
+        t = torch.tensor([t_ts], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        t_ts = t.item()
+    torch_ss_gs = world * S_ts / (t_ts * 1e-3) / 1e9
+
     # ------------------------------------------------ load statistics (E[visits], avg_32)
     loads, loads_p = forest.sample_loads(xi[: 1 << 20], plain=True)
     loads, loads_p = loads.double(), loads_p.double()
@@ -389,6 +405,11 @@ def run_gpu(args):
                      "cutpoint_linear": {"value": round(cutlin_gs, 4), "unit": "G samples/s",
                                          "ms_per_batch": round(t_cl, 4), "samples": S_lin,
                                          "identical_indices": cl_eq},
+                     "torch_searchsorted_f32": {"value": round(torch_ss_gs, 4),
+                                                "unit": "G samples/s", "samples": S_ts,
+                                                "agreement": round(ts_agree, 6),
+                                                "note": "context only: float32 CDF, not "
+                                                        "bit-exact"},
                      "loads_per_sample": {"avg": round(e_loads, 4), "avg32": round(avg32, 4),
                                           "max": max_loads, "of": 1 << 20,
                                           "without_two_interval_flag": {
