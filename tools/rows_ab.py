@@ -1,0 +1,22 @@
+"""A/B of the config-5 rows build and rows sampling between library builds (child processes)."""
+import os, subprocess, sys
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+if os.environ.get("RTF_AB_LIB"):
+    sys.path.insert(0, ROOT)
+    import ctypes
+    from paper_1901_05423_b200 import _lib
+    _lib.LIB_PATH = os.environ["RTF_AB_LIB"]
+    import torch, bench, statistics
+    import paper_1901_05423_b200 as rtf
+    wl = bench.WORKLOADS["c5"]
+    p = torch.from_numpy(bench.make_p(wl)).cuda()
+    f = rtf.RowsForest(wl["rows"], wl["n_row"], wl["m"])
+    for _ in range(3): f.build(p)
+    ts = []
+    for _ in range(15):
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(); f.build(p); b.record(); torch.cuda.synchronize(); ts.append(a.elapsed_time(b))
+    print(f"{os.path.basename(_lib.LIB_PATH):22s} c5 build {statistics.median(ts):.4f} ms (min {min(ts):.4f})", flush=True)
+else:
+    for lib in sys.argv[1:]:
+        subprocess.run([sys.executable, os.path.abspath(__file__)], env=dict(os.environ, RTF_AB_LIB=os.path.abspath(lib)))
