@@ -21,14 +21,14 @@ struct RowsArgs {
     bool vec;
 };
 
-// 256-thread rows: at least 5 CTAs per SM (48 registers, shared carve-out at
+// 1024-entry rows (256 x 4): at least 5 CTAs per SM (48 registers, shared carve-out at
 // 100 %): measured 1.16 vs 1.18 ms for config 5 (6 CTAs: 40 registers with
 // spills, 1.17 ms)
-template <int THREADS>
-constexpr int rows_min_blocks() { return THREADS <= 256 ? 5 : 1; }
+template <int THREADS, int VPT>
+constexpr int rows_min_blocks() { return (THREADS == 256 && VPT == 4) ? 5 : 1; }
 
 template <int THREADS, int VPT>
-__global__ void __launch_bounds__(THREADS, rows_min_blocks<THREADS>()) k_build_rows(RowsArgs A) {
+__global__ void __launch_bounds__(THREADS, rows_min_blocks<THREADS, VPT>()) k_build_rows(RowsArgs A) {
     constexpr int NMAX = THREADS * VPT;
     extern __shared__ __align__(16) unsigned char smem[];
     struct __align__(16) SRec {
