@@ -444,7 +444,7 @@ def run_gpu(args):
         result["replication"] = replication
     if wl["name"] == "c3_powerlaw" and not args.no_c2:
         result["config2_envmap"] = c2_summary(args, dev, stream, flush, world)
-    if rank == 0 and not args.no_cpu_baseline:
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:  # the oracle baseline: N = 1 only
         result["cpu_baseline"] = cpu_baseline(p_host, m, xi[: 1 << 22].cpu().numpy().view(np.uint32),
                                               cdf.cdf.cpu().numpy().view(np.uint64))
     if world > 1:
