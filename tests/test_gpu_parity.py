@@ -404,3 +404,29 @@ def test_rebuild_with_new_data(rtf):
                          dyn=float(rng.choice([1, 10, 30])))
         f.build(dev_f32(p))
         assert_forest_equal(f, oracle.build(p, m), f"rebuild {t}")
+
+
+def test_maximum_size(rtf):
+    """n = 2^31 - 1, the largest n the leaf references allow (reading R3): the
+    build completes, n' and T match the oracle's exact CDF (O1-O6), and 2^20
+    samples equal the oracle's binary search over that CDF one by one."""
+    n, m = (1 << 31) - 1, 1 << 24
+    i = np.arange(n, dtype=np.int64)
+    p = ((i % 1000) + 1).astype(np.float32)  # a sawtooth: no zeros, n' = n
+    p[::7919] = 0.0                          # some zeros to compact
+    del i
+    K, T = oracle.cdf_all(p)
+    xi = philox_xi(1 << 20, seed=77)
+    want = oracle.sample_bsearch(K, xi)
+    del K
+    pd = torch.from_numpy(p).cuda()
+    n_pos = int(np.count_nonzero(p))
+    del p
+    f = rtf.build(pd, m)
+    h = f.header()
+    assert f.last_status == 0
+    assert h.n_pos == n_pos and h.total == T
+    got = f.sample(dev_u32(xi)).cpu().numpy()
+    assert np.array_equal(got, want)
+    del f, pd
+    torch.cuda.empty_cache()
