@@ -28,19 +28,29 @@ template <int THREADS, int VPT>
 constexpr int rows_min_blocks() { return (THREADS == 256 && VPT == 4) ? 5 : 1; }
 
 template <int THREADS, int VPT>
+__host__ __device__ constexpr int rows_padded() { return THREADS * VPT + THREADS; }
+
+template <int THREADS, int VPT>
+__host__ __device__ constexpr size_t rows_smem() { return (size_t)rows_padded<THREADS, VPT>() * (8 + 5 * 4) + THREADS * VPT; }
+
+template <int THREADS, int VPT>
 __global__ void __launch_bounds__(THREADS, rows_min_blocks<THREADS, VPT>()) k_build_rows(RowsArgs A) {
     constexpr int NMAX = THREADS * VPT;
+    constexpr int NP = rows_padded<THREADS, VPT>();
+    // Structure of arrays, each padded by one slot per VPT (Pd): a thread's VPT
+    // consecutive leaves (or cells) are VPT slots apart from its lane
+    // neighbour's, so the padded stride VPT + 1 is odd and the warp's blocked
+    // accesses fall into distinct banks.
     extern __shared__ __align__(16) unsigned char smem[];
-    struct __align__(16) SRec {
-        uint64_t key;
-        int32_t c0, c1;
-    };
-    SRec* s_rec = reinterpret_cast<SRec*>(smem);
-    int32_t* s_orig = reinterpret_cast<int32_t*>(s_rec + NMAX);
-    int32_t* s_ob = s_orig + NMAX;
-    int32_t* s_anc = s_ob + NMAX;     // [m_row] first leaf of the cell, -1 if empty
-    int32_t* s_lst = s_anc + NMAX;    // [m_row] last leaf of the cell, -1 if empty
-    uint8_t* s_lam = reinterpret_cast<uint8_t*>(s_lst + NMAX);
+    uint64_t* s_key = reinterpret_cast<uint64_t*>(smem);
+    int32_t* s_c0 = reinterpret_cast<int32_t*>(s_key + NP);
+    int32_t* s_c1 = s_c0 + NP;
+    int32_t* s_orig = s_c1 + NP;
+    int32_t* s_anc = s_orig + NP;   // [m_row] first leaf of the cell, -1 if empty
+    int32_t* s_lst = s_anc + NP;    // [m_row] last leaf of the cell, -1 if empty
+    int32_t* s_ob = s_anc;          // otherBounds (Alg. 1) replace the anchors after the table
+    uint8_t* s_lam = reinterpret_cast<uint8_t*>(s_lst + NP);
+    auto Pd = [](uint32_t j) { return j + j / VPT; };
     __shared__ uint64_t s_w[2 * (THREADS / 32)];
     __shared__ uint32_t s_c[2 * (THREADS / 32)];
     __shared__ uint32_t s_red[2 * (THREADS / 32)];
@@ -85,8 +95,8 @@ __global__ void __launch_bounds__(THREADS, rows_min_blocks<THREADS, VPT>()) k_bu
         s_red[2 * warp + 1] = fl;
     }
     for (uint32_t g = threadIdx.x; g < m; g += THREADS) {
-        s_anc[g] = -1;
-        s_lst[g] = -1;
+        s_anc[Pd(g)] = -1;
+        s_lst[Pd(g)] = -1;
     }
     __syncthreads();
     mx = 0;
@@ -145,19 +155,19 @@ __global__ void __launch_bounds__(THREADS, rows_min_blocks<THREADS, VPT>()) k_bu
             if (A.jmap) A.jmap[(size_t)r * n + first + k] = (int32_t)jl;
             const uint64_t Wn = W + w[k];
             w[k] = fixed_point(W, nm);
-            s_rec[jl].key = w[k];
-            s_orig[jl] = (int32_t)(first + k);
+            s_key[Pd(jl)] = w[k];
+            s_orig[Pd(jl)] = (int32_t)(first + k);
             W = Wn;
             ++jl;
         }
     }
-    if (threadIdx.x == 0 && cnt) s_anc[0] = 0;
+    if (threadIdx.x == 0 && cnt) s_anc[0] = 0;  // Pd(0) = 0
     __syncthreads();
     // cells and split levels of the own leaves (the row boundary is a wall);
     // the key after the thread's last leaf is its neighbour's (or "1")
     uint64_t lampack = 0;
     if (tc) {
-        uint64_t kn = (c_ex + tc < cnt) ? s_rec[c_ex + tc].key : kOne63;
+        uint64_t kn = (c_ex + tc < cnt) ? s_key[Pd(c_ex + tc)] : kOne63;
         uint32_t cn = (kn == kOne63) ? m : cell_of(kn, m);
 #pragma unroll
         for (int k = VPT - 1; k >= 0; --k) {
@@ -170,8 +180,8 @@ __global__ void __launch_bounds__(THREADS, rows_min_blocks<THREADS, VPT>()) k_bu
                 s_lam[jl] = (uint8_t)lam;
                 lampack |= (uint64_t)lam << (8 * rk);
                 if (lam == kLamBoundary) {
-                    s_lst[cell] = (int32_t)jl;
-                    if (cn < m) s_anc[cn] = (int32_t)(jl + 1);
+                    s_lst[Pd(cell)] = (int32_t)jl;
+                    if (cn < m) s_anc[Pd(cn)] = (int32_t)(jl + 1);
                 }
                 kn = key;
                 cn = cell;
@@ -180,9 +190,8 @@ __global__ void __launch_bounds__(THREADS, rows_min_blocks<THREADS, VPT>()) k_bu
     }
     __syncthreads();
     for (uint32_t l = threadIdx.x; l < cnt; l += THREADS) {
-        s_rec[l].c0 = ~s_orig[l ? l - 1 : 0];
-        s_rec[l].c1 = INT32_MIN;
-        s_ob[l] = -1;
+        s_c0[Pd(l)] = ~s_orig[Pd(l ? l - 1 : 0)];
+        s_c1[Pd(l)] = INT32_MIN;
     }
     // guide table: exclusive max-scan of the last leaf per cell (cells blocked per thread)
     {
@@ -191,7 +200,7 @@ __global__ void __launch_bounds__(THREADS, rows_min_blocks<THREADS, VPT>()) k_bu
         int32_t loc = -1;
 #pragma unroll
         for (int k = 0; k < MPT; ++k)
-            if (g0 + k < m) loc = max(loc, s_lst[g0 + k]);
+            if (g0 + k < m) loc = max(loc, s_lst[Pd(g0 + k)]);
         int32_t inc = loc;
 #pragma unroll
         for (int d = 1; d < 32; d <<= 1) {
@@ -211,18 +220,20 @@ __global__ void __launch_bounds__(THREADS, rows_min_blocks<THREADS, VPT>()) k_bu
         for (int k = 0; k < MPT; ++k) {
             const uint32_t g = g0 + k;
             if (g < m) {
-                const int32_t a = s_anc[g];
+                const int32_t a = s_anc[Pd(g)];
+                const int32_t lst = s_lst[Pd(g)];
                 if (a < 0) {
-                    st_cell(tab, g, 0u, ~s_orig[run]);
-                } else if (s_lst[g] == a) {  // one leaf: two intervals
-                    const uint2 e = single_leaf_cell(s_rec[a].key, s_orig[a],
-                                                     s_orig[a ? a - 1 : 0], a);
+                    st_cell(tab, g, 0u, ~s_orig[Pd(run)]);
+                } else if (lst == a) {  // one leaf: two intervals
+                    const uint2 e = single_leaf_cell(s_key[Pd(a)], s_orig[Pd(a)],
+                                                     s_orig[Pd(a ? a - 1 : 0)], a);
                     st_cell(tab, g, e.x, (int32_t)e.y);
                 } else {
                     st_cell(tab, g, 0u, a);
                 }
-                run = max(run, s_lst[g]);
+                run = max(run, lst);
             }
+            s_ob[Pd(g)] = -1;  // slot g's anchor is read (only by this thread)
         }
     }
     __syncthreads();
@@ -248,15 +259,15 @@ __global__ void __launch_bounds__(THREADS, rows_min_blocks<THREADS, VPT>()) k_bu
                     const bool right = lamL <= lamR;
                     const int32_t leaf = ~(int32_t)(first + k);
                     if ((lamL & lamR & kLamBoundary) != 0) {  // a cell root
-                        s_rec[l].c1 = leaf;
+                        s_c1[Pd(l)] = leaf;
                         continue;
                     }
                     const uint32_t q = right ? l : l + 1;
-                    if (right) s_rec[q].c1 = leaf;
-                    else s_rec[q].c0 = leaf;
-                    const int32_t other = atomicExch(&s_ob[q], (int32_t)((right ? lamR : lamL) << 16 | l));
+                    const uint32_t qp = Pd(q);
+                    (right ? s_c1 : s_c0)[qp] = leaf;
+                    const int32_t other = atomicExch(&s_ob[qp], (int32_t)((right ? lamR : lamL) << 16 | l));
                     if (other >= 0) {
-                        s_ob[q] = -1;
+                        s_ob[qp] = -1;
                         contw[rk] = (uint32_t)other;
                         pend |= 1u << rk;
                         rightbits |= (right ? 1u : 0u) << rk;
@@ -299,20 +310,20 @@ __global__ void __launch_bounds__(THREADS, rows_min_blocks<THREADS, VPT>()) k_bu
             if (!__any_sync(0xffffffffu, active)) break;
             if (active) {
                 if ((lamL & lamR & kLamBoundary) != 0) {  // a cell root: right child of its anchor
-                    s_rec[lo].c1 = node;
+                    s_c1[Pd(lo)] = node;
                     active = false;
                     continue;
                 }
                 const bool right = lamL <= lamR;
                 const int32_t parent = right ? lo : hi + 1;
-                if (right) s_rec[parent].c1 = node;
-                else s_rec[parent].c0 = node;
+                const uint32_t pp = Pd((uint32_t)parent);
+                (right ? s_c1 : s_c0)[pp] = node;
                 const int32_t dep = right ? (int32_t)(lamR << 16 | (uint32_t)hi)
                                           : (int32_t)(lamL << 16 | (uint32_t)lo);
-                const int32_t other = atomicExch(&s_ob[parent], dep);
+                const int32_t other = atomicExch(&s_ob[pp], dep);
                 active = other >= 0;
                 if (active) {
-                    s_ob[parent] = -1;
+                    s_ob[pp] = -1;
                     const int32_t bound = other & 0xffff;
                     const uint32_t lv = (uint32_t)other >> 16;
                     lo = right ? bound : lo;
@@ -326,8 +337,11 @@ __global__ void __launch_bounds__(THREADS, rows_min_blocks<THREADS, VPT>()) k_bu
     }
     __syncthreads();
     uint4* gnode = reinterpret_cast<uint4*>(A.nodes + (size_t)r * n);
-    const uint4* snode = reinterpret_cast<const uint4*>(s_rec);
-    for (uint32_t l = threadIdx.x; l < cnt; l += THREADS) gnode[l] = snode[l];
+    for (uint32_t l = threadIdx.x; l < cnt; l += THREADS) {
+        const uint32_t q = Pd(l);
+        const uint64_t key = s_key[q];
+        gnode[l] = make_uint4((uint32_t)key, (uint32_t)(key >> 32), (uint32_t)s_c0[q], (uint32_t)s_c1[q]);
+    }
     if (threadIdx.x == 0) {
         rtf_header h;
         h.total = T;
@@ -344,8 +358,7 @@ __global__ void __launch_bounds__(THREADS, rows_min_blocks<THREADS, VPT>()) k_bu
 
 template <int THREADS, int VPT>
 static cudaError_t launch_rows_t(const RowsArgs& A, cudaStream_t st) {
-    constexpr int NMAX = THREADS * VPT;
-    const size_t smem = (size_t)NMAX * (16 + 4 + 4 + 4 + 4 + 1);
+    const size_t smem = rows_smem<THREADS, VPT>();
     static bool attr = false;
     if (!attr) {
         cudaError_t e = cudaFuncSetAttribute(k_build_rows<THREADS, VPT>,
