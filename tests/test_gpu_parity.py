@@ -264,7 +264,9 @@ def assert_cells_equal(got, want, what=""):
 
 def test_rows_random_shapes(rtf):
     rng = np.random.default_rng(9)
-    for n_row, m_row in ((1, 1), (3, 7), (64, 16), (255, 256), (1000, 333), (1024, 4096),
+    # every kernel configuration: 64x4 (<= 256), 256x4 (<= 1024), 256x8 (<= 2048), 512x8
+    for n_row, m_row in ((1, 1), (3, 7), (64, 16), (255, 256), (256, 257), (1000, 333),
+                         (1024, 1024), (1025, 64), (1500, 700), (2048, 2048), (1024, 4096),
                          (4096, 4096), (2500, 100)):
         rows = 37
         p = np.stack([random_small(rng, n_row, zero_frac=0.3) for _ in range(rows)])
