@@ -472,14 +472,21 @@ __global__ void __launch_bounds__(THREADS, MINB) k_build(BuildArgs A) {
         constexpr int BATCH = F < 8 ? F : 8;
         const uint32_t t_beg = b * krng, t_end = min(nt, t_beg + krng);
         Pfx run{0ull, 0u, -1};  // thread 0: the range so far
-        for (uint32_t c0 = t_beg; c0 < t_end; c0 += CAP) {
-            const uint32_t c1 = min(t_end, c0 + CAP);
-            for (uint32_t t = c0 + warp; t < c1; t += NW) {
+        // short ranges (small n): up to F / BATCH warps share a tile, so every
+        // warp keeps loads in flight
+        constexpr uint32_t NCH = F / BATCH;
+        const uint32_t WPT = krng >= NW ? 1u : min(NCH, NW / krng >= 4 ? 4u : NW / krng >= 2 ? 2u : 1u);
+        const uint32_t CAPT = CAP / WPT;
+        for (uint32_t c0 = t_beg; c0 < t_end; c0 += CAPT) {
+            const uint32_t c1 = min(t_end, c0 + CAPT);
+            for (uint32_t u = warp; u < (c1 - c0) * WPT; u += NW) {
+                const uint32_t t = c0 + u / WPT, part = u % WPT;
                 Pfx acc{0ull, 0u, -1};
                 const uint32_t base = t * TILE;
                 if (A.vec && base + TILE <= n) {
+                    const int cb = (int)(part * (F / WPT)), ce = cb + (int)(F / WPT);
 #pragma unroll 1
-                    for (int c = 0; c < F; c += BATCH) {
+                    for (int c = cb; c < ce; c += BATCH) {
                         float4 v[BATCH];
 #pragma unroll
                         for (int u = 0; u < BATCH; ++u)
@@ -497,7 +504,7 @@ __global__ void __launch_bounds__(THREADS, MINB) k_build(BuildArgs A) {
                             }
                         }
                     }
-                } else {
+                } else if (part == 0) {
                     for (uint32_t e = base + lane; e < min(n, base + TILE); e += 32) {
                         const uint64_t w = quantize(A.p[e], scale);
                         acc.W += w;
@@ -506,13 +513,14 @@ __global__ void __launch_bounds__(THREADS, MINB) k_build(BuildArgs A) {
                     }
                 }
                 warp_sum_pfx(acc);
-                if (lane == 0) s_tagg[t - c0] = acc;
+                if (lane == 0) s_tagg[u] = acc;
             }
             __syncthreads();
             if (tid == 0)
                 for (uint32_t t = c0; t < c1; ++t) {
                     st_pfx(&A.excl[t], run);
-                    run = combine(run, s_tagg[t - c0]);
+                    for (uint32_t part = 0; part < WPT; ++part)
+                        run = combine(run, s_tagg[(t - c0) * WPT + part]);
                 }
             __syncthreads();
         }
