@@ -37,10 +37,11 @@ template <int THREADS, int VPT>
 __global__ void __launch_bounds__(THREADS, rows_min_blocks<THREADS, VPT>()) k_build_rows(RowsArgs A) {
     constexpr int NMAX = THREADS * VPT;
     constexpr int NP = rows_padded<THREADS, VPT>();
-    // Structure of arrays, each padded by one slot per VPT (Pd): a thread's VPT
-    // consecutive leaves (or cells) are VPT slots apart from its lane
-    // neighbour's, so the padded stride VPT + 1 is odd and the warp's blocked
-    // accesses fall into distinct banks.
+    // Structure of arrays with pad slots, so that both access patterns hit 32
+    // distinct banks: blocked (a thread's VPT consecutive leaves or cells, VPT
+    // slots apart from its lane neighbour's) and contiguous (one slot per
+    // lane).  4-B arrays: one pad per 32 slots (Pd).  The 8-B keys: one pad per
+    // VPT slots (PdK), an odd stride for the blocked stores.
     extern __shared__ __align__(16) unsigned char smem[];
     uint64_t* s_key = reinterpret_cast<uint64_t*>(smem);
     int32_t* s_c0 = reinterpret_cast<int32_t*>(s_key + NP);
@@ -50,7 +51,8 @@ __global__ void __launch_bounds__(THREADS, rows_min_blocks<THREADS, VPT>()) k_bu
     int32_t* s_lst = s_anc + NP;    // [m_row] last leaf of the cell, -1 if empty
     int32_t* s_ob = s_anc;          // otherBounds (Alg. 1) replace the anchors after the table
     uint8_t* s_lam = reinterpret_cast<uint8_t*>(s_lst + NP);
-    auto Pd = [](uint32_t j) { return j + j / VPT; };
+    auto Pd = [](uint32_t j) { return j + j / 32; };    // 4-B arrays
+    auto PdK = [](uint32_t j) { return j + j / VPT; };  // the 8-B keys
     __shared__ uint64_t s_w[2 * (THREADS / 32)];
     __shared__ uint32_t s_c[2 * (THREADS / 32)];
     __shared__ uint32_t s_red[2 * (THREADS / 32)];
@@ -155,7 +157,7 @@ __global__ void __launch_bounds__(THREADS, rows_min_blocks<THREADS, VPT>()) k_bu
             if (A.jmap) A.jmap[(size_t)r * n + first + k] = (int32_t)jl;
             const uint64_t Wn = W + w[k];
             w[k] = fixed_point(W, nm);
-            s_key[Pd(jl)] = w[k];
+            s_key[PdK(jl)] = w[k];
             s_orig[Pd(jl)] = (int32_t)(first + k);
             W = Wn;
             ++jl;
@@ -167,7 +169,7 @@ __global__ void __launch_bounds__(THREADS, rows_min_blocks<THREADS, VPT>()) k_bu
     // the key after the thread's last leaf is its neighbour's (or "1")
     uint64_t lampack = 0;
     if (tc) {
-        uint64_t kn = (c_ex + tc < cnt) ? s_key[Pd(c_ex + tc)] : kOne63;
+        uint64_t kn = (c_ex + tc < cnt) ? s_key[PdK(c_ex + tc)] : kOne63;
         uint32_t cn = (kn == kOne63) ? m : cell_of(kn, m);
 #pragma unroll
         for (int k = VPT - 1; k >= 0; --k) {
@@ -225,7 +227,7 @@ __global__ void __launch_bounds__(THREADS, rows_min_blocks<THREADS, VPT>()) k_bu
                 if (a < 0) {
                     st_cell(tab, g, 0u, ~s_orig[Pd(run)]);
                 } else if (lst == a) {  // one leaf: two intervals
-                    const uint2 e = single_leaf_cell(s_key[Pd(a)], s_orig[Pd(a)],
+                    const uint2 e = single_leaf_cell(s_key[PdK(a)], s_orig[Pd(a)],
                                                      s_orig[Pd(a ? a - 1 : 0)], a);
                     st_cell(tab, g, e.x, (int32_t)e.y);
                 } else {
@@ -339,7 +341,7 @@ __global__ void __launch_bounds__(THREADS, rows_min_blocks<THREADS, VPT>()) k_bu
     uint4* gnode = reinterpret_cast<uint4*>(A.nodes + (size_t)r * n);
     for (uint32_t l = threadIdx.x; l < cnt; l += THREADS) {
         const uint32_t q = Pd(l);
-        const uint64_t key = s_key[q];
+        const uint64_t key = s_key[PdK(l)];
         gnode[l] = make_uint4((uint32_t)key, (uint32_t)(key >> 32), (uint32_t)s_c0[q], (uint32_t)s_c1[q]);
     }
     if (threadIdx.x == 0) {
