@@ -23,9 +23,10 @@ struct RowsArgs {
 
 // 1024-entry rows (256 x 4): at least 5 CTAs per SM (48 registers, shared carve-out at
 // 100 %): measured 1.16 vs 1.18 ms for config 5 (6 CTAs: 40 registers with
-// spills, 1.17 ms)
+// spills, 1.17 ms).  2048-entry rows (256 x 8): 3 CTAs per SM (80 registers, no
+// spills; 96 registers allowed only 2): 1024 x 2048 rows in 44 vs 50 us.
 template <int THREADS, int VPT>
-constexpr int rows_min_blocks() { return (THREADS == 256 && VPT == 4) ? 5 : 1; }
+constexpr int rows_min_blocks() { return (THREADS == 256 && VPT == 4) ? 5 : (THREADS == 256 && VPT == 8) ? 3 : 1; }
 
 template <int THREADS, int VPT>
 __host__ __device__ constexpr int rows_padded() { return THREADS * VPT + THREADS; }
@@ -393,7 +394,7 @@ cudaError_t launch_build_rows(const float* p, uint32_t rows, uint32_t n_row, uin
     cudaError_t e;
     if (need <= 256) e = launch_rows_t<64, 4>(A, st);
     else if (need <= 1024) e = launch_rows_t<256, 4>(A, st);
-    else if (need <= 2048) e = launch_rows_t<256, 8>(A, st);  // 67 KB: 3 CTAs per SM
+    else if (need <= 2048) e = launch_rows_t<256, 8>(A, st);  // 65 KB, 80 registers: 3 CTAs per SM
     else e = launch_rows_t<512, 8>(A, st);
     ++*launches;
     return e;

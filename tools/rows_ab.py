@@ -17,6 +17,15 @@ if os.environ.get("RTF_AB_LIB"):
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         a.record(); f.build(p); b.record(); torch.cuda.synchronize(); ts.append(a.elapsed_time(b))
     print(f"{os.path.basename(_lib.LIB_PATH):22s} c5 build {statistics.median(ts):.4f} ms (min {min(ts):.4f})", flush=True)
+    # 2048-entry rows (the 2-D env map's conditionals): 1024 x 2048
+    p2 = torch.rand(1024 * 2048, generator=torch.Generator().manual_seed(3)).cuda()
+    f2 = rtf.RowsForest(1024, 2048, 2048)
+    for _ in range(3): f2.build(p2)
+    ts = []
+    for _ in range(15):
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(); f2.build(p2); b.record(); torch.cuda.synchronize(); ts.append(a.elapsed_time(b))
+    print(f"{os.path.basename(_lib.LIB_PATH):22s} 1024x2048 rows build {statistics.median(ts):.4f} ms (min {min(ts):.4f})", flush=True)
 else:
     for lib in sys.argv[1:]:
         subprocess.run([sys.executable, os.path.abspath(__file__)], env=dict(os.environ, RTF_AB_LIB=os.path.abspath(lib)))
