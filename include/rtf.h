@@ -100,7 +100,8 @@ typedef struct rtf_forest {
     uint32_t m;      /* guide-table cells per row                         */
     uint32_t rows;   /* 1, or the number of independent rows (batched)    */
     uint32_t flags;  /* build flags                                       */
-    rtf_node *nodes; /* rows * n records (the first n_pos of each row valid) */
+    rtf_node *nodes; /* rows * n records (the first n_pos of each row valid;
+                        rows_build: slot n_pos < n holds key 2^63, "1")   */
     rtf_ref *table;  /* rows * m guide-table cells (rtf_ref)              */
     rtf_header *header; /* rows headers                                  */
 } rtf_forest;

@@ -48,11 +48,14 @@ __device__ __forceinline__ int32_t descend_row(const rtf_node* __restrict__ node
     return j;
 }
 
-// relative position of x inside the interval of node j of a forest with n_pos leaves
+// relative position of x inside the interval of leaf j; last: the entry is the
+// row's last one (slot j + 1 is then past the row).  Otherwise slot j + 1 holds
+// the next leaf's key, or the key "1" that the row build stores after the last
+// leaf (no header read per sample).
 __device__ __forceinline__ double rel_pos(const rtf_node* __restrict__ nodes, int32_t j,
-                                          uint32_t n_pos, uint32_t x) {
+                                          bool last, uint32_t x) {
     const uint64_t lo = __ldg(&nodes[j].key);
-    const uint64_t hi = (uint32_t)(j + 1) < n_pos ? __ldg(&nodes[j + 1].key) : kOne63;
+    const uint64_t hi = last ? kOne63 : __ldg(&nodes[j + 1].key);
     return __ddiv_rn(__ull2double_rn(((uint64_t)x << 31) - lo), __ull2double_rn(hi - lo));
 }
 
@@ -77,9 +80,9 @@ __global__ void __launch_bounds__(k2dThreads, 8)  // 32 registers: 2048 threads 
                 out = y * (int32_t)f.W + x;
                 if (pos) {
                     const double u = rel_pos(f.marginal.nodes, __ldg(&f.marg_jmap[y]),
-                                             f.marginal.header->n_pos, a);
+                                             (uint32_t)y + 1 == f.H, a);
                     const double v = rel_pos(rn, __ldg(&f.rows_jmap[(size_t)y * f.W + x]),
-                                             f.rows.header[y].n_pos, b);
+                                             (uint32_t)x + 1 == f.W, b);
                     px = __double2float_rz(__ddiv_rn(__dadd_rn((double)x, v), (double)f.W));
                     py = __double2float_rz(__ddiv_rn(__dadd_rn((double)y, u), (double)f.H));
                 }

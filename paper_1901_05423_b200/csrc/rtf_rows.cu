@@ -345,6 +345,9 @@ __global__ void __launch_bounds__(THREADS, rows_min_blocks<THREADS, VPT>()) k_bu
         const uint64_t key = s_key[PdK(l)];
         gnode[l] = make_uint4((uint32_t)key, (uint32_t)(key >> 32), (uint32_t)s_c0[q], (uint32_t)s_c1[q]);
     }
+    // the free slot after the last leaf holds the key "1" (2^63), so the upper
+    // bound of any leaf's interval is the next slot's key (the 2-D sampler)
+    if (threadIdx.x == 0 && cnt < n) gnode[cnt] = make_uint4(0u, 0x80000000u, 0x80000000u, 0x80000000u);
     if (threadIdx.x == 0) {
         rtf_header h;
         h.total = T;
