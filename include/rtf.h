@@ -209,6 +209,8 @@ typedef struct rtf_forest2d {
     int32_t *rows_jmap;  /* H*W: row-local node index of entry (y, x), -1 for p = 0 */
     int32_t *marg_jmap;  /* H:   node index of row y in the marginal, -1 if q_y = 0 */
     float *weights;      /* H:   the row weights q_y (reading R19)                   */
+    uint32_t *rows_dense; /* H bits: bit y set if row y has no zero weight, so its
+                             rows_jmap is the identity (the sampler skips it)       */
 } rtf_forest2d;
 
 /* Bytes of a 2-D forest buffer (both forests, index maps, weights).  Host only. */

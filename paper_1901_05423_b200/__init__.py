@@ -256,6 +256,12 @@ class Forest2D:
         off = self.view.weights - self._buf.data_ptr()
         return self._buf[off: off + 4 * self.H].cpu().numpy().view(np.float32)
 
+    def dense_rows(self) -> np.ndarray:
+        """bool[H]: row y has no zero weight (rows_dense bit y)."""
+        off = self.view.rows_dense - self._buf.data_ptr()
+        words = self._buf[off: off + 4 * ((self.H + 31) // 32)].cpu().numpy().view(np.uint32)
+        return ((words[np.arange(self.H) // 32] >> (np.arange(self.H) % 32)) & 1).astype(bool)
+
 
 def build_2d(p: torch.Tensor, mx: int, my: int, stream=None) -> Forest2D:
     H, W = p.shape

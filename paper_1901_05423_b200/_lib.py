@@ -30,7 +30,7 @@ class rtf_forest2d(ctypes.Structure):
     _fields_ = [("W", ctypes.c_uint32), ("H", ctypes.c_uint32), ("mx", ctypes.c_uint32),
                 ("my", ctypes.c_uint32), ("rows", rtf_forest), ("marginal", rtf_forest),
                 ("rows_jmap", ctypes.c_void_p), ("marg_jmap", ctypes.c_void_p),
-                ("weights", ctypes.c_void_p)]
+                ("weights", ctypes.c_void_p), ("rows_dense", ctypes.c_void_p)]
 
 
 class rtf_shard_view(ctypes.Structure):

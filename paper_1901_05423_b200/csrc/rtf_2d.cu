@@ -12,9 +12,11 @@ constexpr int kMaxVisits2d = 64;
 
 // q_y = float32(float64(T_y) 2^(E_y - B_y - K)), K = max over non-empty rows of
 // E_y - B_y; an all-zero row gets 0, a row with NaN / Inf / negative data NaN
-// (so the marginal build reports the data error).  One CTA; H <= 4096.
+// (so the marginal build reports the data error).  dense: bit y set if row y
+// has W positive weights (its index map is the identity).  One CTA; H <= 4096.
 __global__ void __launch_bounds__(kRowWeightThreads)
-    k_row_weights(const rtf_header* __restrict__ hdr, uint32_t H, float* __restrict__ q) {
+    k_row_weights(const rtf_header* __restrict__ hdr, uint32_t H, uint32_t W, float* __restrict__ q,
+                  uint32_t* __restrict__ dense) {
     __shared__ int s_max[kRowWeightThreads / 32];
     int k = INT_MIN;
     for (uint32_t y = threadIdx.x; y < H; y += kRowWeightThreads)
@@ -24,8 +26,13 @@ __global__ void __launch_bounds__(kRowWeightThreads)
     __syncthreads();
     int K = INT_MIN;
     for (int w = 0; w < kRowWeightThreads / 32; ++w) K = max(K, s_max[w]);
-    for (uint32_t y = threadIdx.x; y < H; y += kRowWeightThreads) {
-        const rtf_header h = hdr[y];
+    for (uint32_t y0 = 0; y0 < H; y0 += kRowWeightThreads) {  // uniform trip count (ballot)
+        const uint32_t y = y0 + threadIdx.x;
+        const bool in = y < H;
+        const rtf_header h = in ? hdr[y] : rtf_header{};
+        const uint32_t bits = __ballot_sync(0xffffffffu, in && h.status == 0 && h.n_pos == W);
+        if (in && (threadIdx.x & 31) == 0) dense[y >> 5] = bits;
+        if (!in) continue;
         float v;
         if (h.status & (RTF_DATA_NAN | RTF_DATA_INF | RTF_DATA_NEG)) v = __int_as_float(0x7fc00000);
         else if (h.status) v = 0.0f;  // all-zero row
@@ -64,6 +71,7 @@ __global__ void __launch_bounds__(k2dThreads, 8)  // 32 registers: 2048 threads 
                 uint64_t count, int32_t* __restrict__ pixel, float* __restrict__ pos) {
     const uint64_t gs = (uint64_t)gridDim.x * blockDim.x;
     const bool bad = f.marginal.header->status != 0;
+    const bool marg_dense = f.marginal.header->n_pos == f.H;  // every row weight positive
     for (uint64_t k = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; k < count; k += gs) {
         const uint32_t a = xi1[k], b = xi2[k];
         int32_t out = INT32_MAX;
@@ -79,10 +87,12 @@ __global__ void __launch_bounds__(k2dThreads, 8)  // 32 registers: 2048 threads 
             } else {
                 out = y * (int32_t)f.W + x;
                 if (pos) {
-                    const double u = rel_pos(f.marginal.nodes, __ldg(&f.marg_jmap[y]),
-                                             (uint32_t)y + 1 == f.H, a);
-                    const double v = rel_pos(rn, __ldg(&f.rows_jmap[(size_t)y * f.W + x]),
-                                             (uint32_t)x + 1 == f.W, b);
+                    const int32_t jy_node = marg_dense ? y : __ldg(&f.marg_jmap[y]);
+                    const double u = rel_pos(f.marginal.nodes, jy_node, (uint32_t)y + 1 == f.H, a);
+                    const bool dense = (__ldg(&f.rows_dense[(uint32_t)y >> 5]) >> (y & 31)) & 1u;
+                    const int32_t jx_node =
+                        dense ? x : __ldg(&f.rows_jmap[(size_t)y * f.W + x]);
+                    const double v = rel_pos(rn, jx_node, (uint32_t)x + 1 == f.W, b);
                     px = __double2float_rz(__ddiv_rn(__dadd_rn((double)x, v), (double)f.W));
                     py = __double2float_rz(__ddiv_rn(__dadd_rn((double)y, u), (double)f.H));
                 }
@@ -94,9 +104,8 @@ __global__ void __launch_bounds__(k2dThreads, 8)  // 32 registers: 2048 threads 
 }
 
 cudaError_t launch_row_weights(const rtf_header* rows_hdr, uint32_t H, uint32_t W, float* q,
-                               cudaStream_t st, int* launches) {
-    (void)W;
-    k_row_weights<<<1, kRowWeightThreads, 0, st>>>(rows_hdr, H, q);
+                               uint32_t* dense, cudaStream_t st, int* launches) {
+    k_row_weights<<<1, kRowWeightThreads, 0, st>>>(rows_hdr, H, W, q, dense);
     ++*launches;
     return cudaGetLastError();
 }

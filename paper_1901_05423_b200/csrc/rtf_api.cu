@@ -212,7 +212,7 @@ int rtf_sample_rows(const rtf_forest* f, const uint32_t* row, const uint32_t* xi
 
 namespace {
 struct Layout2d {
-    size_t rows, marginal, rows_jmap, marg_jmap, weights, total;
+    size_t rows, marginal, rows_jmap, marg_jmap, weights, dense, total;
 };
 Layout2d layout_2d(uint32_t W, uint32_t H, uint32_t mx, uint32_t my) {
     Layout2d L;
@@ -227,6 +227,8 @@ Layout2d layout_2d(uint32_t W, uint32_t H, uint32_t mx, uint32_t my) {
     off += align_up(sizeof(int32_t) * (size_t)H);
     L.weights = off;
     off += align_up(sizeof(float) * (size_t)H);
+    L.dense = off;
+    off += align_up(sizeof(uint32_t) * (((size_t)H + 31) / 32));
     L.total = off;
     return L;
 }
@@ -260,12 +262,14 @@ int rtf_build_2d(const float* p, uint32_t W, uint32_t H, uint32_t mx, uint32_t m
     out->rows_jmap = reinterpret_cast<int32_t*>(b + L.rows_jmap);
     out->marg_jmap = reinterpret_cast<int32_t*>(b + L.marg_jmap);
     out->weights = reinterpret_cast<float*>(b + L.weights);
+    out->rows_dense = reinterpret_cast<uint32_t*>(b + L.dense);
     cudaStream_t st = as_stream(stream);
     int launches = 0;
     cudaError_t e = rtf::launch_build_rows(p, H, W, mx, out->rows.header, out->rows.nodes,
                                            out->rows.table, out->rows_jmap, st, &launches);
     if (e == cudaSuccess)
-        e = rtf::launch_row_weights(out->rows.header, H, W, out->weights, st, &launches);
+        e = rtf::launch_row_weights(out->rows.header, H, W, out->weights, out->rows_dense, st,
+                                    &launches);
     if (e == cudaSuccess)
         e = rtf::launch_build_rows(out->weights, 1, H, my, out->marginal.header,
                                    out->marginal.nodes, out->marginal.table, out->marg_jmap, st,
@@ -280,7 +284,8 @@ int rtf_forest2d_status(const rtf_forest2d* f, void* stream) {
 
 int rtf_sample_2d(const rtf_forest2d* f, const uint32_t* xi1, const uint32_t* xi2, uint64_t count,
                   int32_t* pixel, float* pos, void* stream) {
-    if (!f || !f->rows.nodes || !f->marginal.nodes || !f->rows_jmap || !f->marg_jmap)
+    if (!f || !f->rows.nodes || !f->marginal.nodes || !f->rows_jmap || !f->marg_jmap ||
+        !f->rows_dense)
         return RTF_EINVAL;
     if (count && (!xi1 || !xi2 || !pixel)) return RTF_EINVAL;
     if ((((uintptr_t)xi1 | (uintptr_t)xi2 | (uintptr_t)pixel) & 3u) || ((uintptr_t)pos & 7u))

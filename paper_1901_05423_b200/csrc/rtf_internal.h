@@ -68,7 +68,7 @@ cudaError_t launch_build_rows(const float* p, uint32_t rows, uint32_t n_row, uin
 
 // 2-D (Sec.6): row weights from the rows' headers, and the component-wise sampler
 cudaError_t launch_row_weights(const rtf_header* rows_hdr, uint32_t H, uint32_t W, float* q,
-                               cudaStream_t st, int* launches);
+                               uint32_t* dense, cudaStream_t st, int* launches);
 cudaError_t launch_sample_2d(const rtf_forest2d& f, const uint32_t* xi1, const uint32_t* xi2,
                              uint64_t count, int32_t* pixel, float* pos, cudaStream_t st,
                              int* launches);

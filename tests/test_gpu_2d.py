@@ -30,6 +30,7 @@ def check(rtf, p, mx, my, xi1, xi2, sample_all=True):
     assert f.status() == 0
     q = oracle.marginal_weights(p)
     assert f.weights().tobytes() == q.tobytes(), "row weights"
+    assert np.array_equal(f.dense_rows(), np.all(p > 0, axis=1)), "dense-row bits"
     pix, pos = f.sample(dev_u32(xi1), dev_u32(xi2))
     pix, pos = pix.cpu().numpy(), pos.cpu().numpy()
     ref = oracle.build_2d(p, mx, my)
@@ -48,7 +49,9 @@ def test_2d_random_small(rtf):
     rng = np.random.default_rng(11)
     for t in range(30):
         H, W = int(rng.integers(1, 40)), int(rng.integers(1, 70))
-        p = np.stack([random_small(rng, W, zero_frac=0.3) for _ in range(H)])
+        # zero-free rows (identity index maps) mixed with rows holding zeros
+        p = np.stack([random_small(rng, W, zero_frac=0.3 if (t + y) % 2 else 0.0)
+                      for y in range(H)])
         if t % 3 == 0:
             p[int(rng.integers(H))] = 0.0
             if not np.any(p > 0):
