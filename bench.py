@@ -36,6 +36,9 @@ METRIC = "forest build G entries/s; sampling G samples/s (vs binary search) at 1
 L2_FLUSH_BYTES = 512 << 20
 
 WORKLOADS = {
+    "c1": dict(name="c1_teaser", n=16, m=8, samples=1024,
+               desc="config 1 (teaser, Fig. 1): n=16 weights (2,4,10,24,3,1,1,2,1,1,1,2,3,1,4,4), "
+                    "m=8, 1024 Hammersley points (dim 0 = k/1024); latency-bound"),
     "c3": dict(name="c3_powerlaw", n=1 << 24, m=1 << 22, samples=1 << 30,
                desc="config 3: power law p_i ~ ((i+1)/n)^20 (family A), n=2^24, m=2^22, "
                     "2^30 Philox4x32-10 xi per GPU"),
@@ -714,6 +717,76 @@ def run_gpu_2d(args):
         print(json.dumps(result), flush=True)
 
 
+def run_gpu_c1(args):
+    """Config 1: the teaser distribution (16 weights, 8 cells, 1024 Hammersley
+    points).  Latency-bound: reports microseconds per build + sample step,
+    launched eagerly and as one replayed CUDA graph."""
+    import torch
+
+    import paper_1901_05423_b200 as rtf
+    from workloads import TEASER_WEIGHTS, hammersley_xi
+
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if int(os.environ.get("RANK", "0")) != 0:
+        return  # one GPU's latency: the other ranks have nothing to add
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    wl = WORKLOADS["c1"]
+    p = torch.tensor(TEASER_WEIGHTS, dtype=torch.float32, device=dev)
+    xi_host, _ = hammersley_xi(wl["samples"])
+    xi = torch.from_numpy(np.ascontiguousarray(xi_host, dtype=np.uint32).view(np.int32)).to(dev)
+    forest = rtf.Forest(wl["n"], wl["m"], device=dev)
+    out = torch.empty(wl["samples"], dtype=torch.int32, device=dev)
+    stream = torch.cuda.Stream(device=dev)
+    K = max(args.steps, 100)
+
+    def step():
+        forest.build(p, stream=stream)
+        forest.sample(xi, out, stream=stream)
+
+    def timed(fn):
+        with torch.cuda.stream(stream):
+            for _ in range(args.warmup):
+                fn()
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            stream.synchronize()
+            a.record(stream)
+            for _ in range(K):
+                fn()
+            b.record(stream)
+            b.synchronize()
+        return a.elapsed_time(b) * 1e3 / K
+
+    sampler = ClockSampler(local)
+    with sampler:
+        l0 = rtf.launch_count()
+        eager_us = timed(step)
+        launches = (rtf.launch_count() - l0) // (K + args.warmup)
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.stream(stream):
+            step()
+            stream.synchronize()
+            with torch.cuda.graph(g, stream=stream):
+                step()
+        graph_us = timed(g.replay)
+    torch.cuda.synchronize()
+    ok = np.array_equal(out.cpu().numpy(), np.searchsorted(
+        np.cumsum(np.array(TEASER_WEIGHTS, dtype=np.int64)) * (1 << 26), xi_host.astype(np.int64),
+        side="right"))
+    result = {
+        "metric": "config 1 latency: build + 1024 samples", "value": round(graph_us, 3),
+        "unit": "us per step (CUDA graph)", "n_gpus": 1, "steps": K, "warmup": args.warmup,
+        "ms_per_step": round(graph_us / 1e3, 6), "higher_is_better": False, "scaling": "weak",
+        "vs_baseline": None, "dtype": "u64", "data": "synthetic",
+        "config": {"workload": wl["desc"], "n": wl["n"], "m": wl["m"], "samples": wl["samples"],
+                   "l2": "not flushed (a 200-byte problem; latency is the quantity)"},
+        "eager_us_per_step": round(eager_us, 3), "graph_us_per_step": round(graph_us, 3),
+        "launches_per_step": launches, "indices_match_inverse_cdf": bool(ok),
+        "gpu_launches": launches * K, "clocks": sampler.summary(),
+    }
+    print(json.dumps(result), flush=True)
+
+
 def run_gpu_c5(args):
     """Config 5: batched rebuilds of 65536 independent rows (rtf_build_rows, one CTA
     per row, everything in shared memory) + sampling (row, xi) pairs.  Rows are
@@ -911,6 +984,8 @@ def main():
         run_gpu_c4(args)
     elif args.workload == "c5":
         run_gpu_c5(args)
+    elif args.workload == "c1":
+        run_gpu_c1(args)
     elif args.workload == "c2d":
         run_gpu_2d(args)
     else:

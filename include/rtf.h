@@ -138,9 +138,12 @@ int rtf_workspace_init(void *ws, size_t ws_bytes, uint32_t n, uint32_t m, uint32
  * Asynchronous: ONE cooperative kernel on `stream` whose phases are separated
  * by grid barriers (scale; tile totals; tiles: scan + exact normalisation +
  * cells/split levels/table + Alg. 1 in shared memory; cross-tile links from
- * the tiles' spines + long table runs).  The result bytes are independent of
- * the schedule and of `flags`.  Errors in the data (NaN, Inf, negative, all
- * zero) are reported in header->status (rtf_forest_status), not here. */
+ * the tiles' spines + long table runs).  With n <= 4096 and m <= 4096 (and no
+ * RTF_BUILD_SMALL_TILES) the row kernel of rtf_build_rows builds it instead,
+ * in one CTA without grid barriers.  The records [0, n_pos), the table and
+ * the header are independent of the schedule, of the kernel and of `flags`.
+ * Errors in the data (NaN, Inf, negative, all zero) are reported in
+ * header->status (rtf_forest_status), not here. */
 int rtf_build(const float *p, uint32_t n, uint32_t m, uint32_t flags, void *forest_buf,
               size_t forest_bytes, void *ws, size_t ws_bytes, void *stream, rtf_forest *out);
 

@@ -119,8 +119,16 @@ int rtf_build(const float* p, uint32_t n, uint32_t m, uint32_t flags, void* fore
     if (ws_bytes < rtf::build_workspace_layout(n, m, flags, &L)) return RTF_ENOSPACE;
     if (((uintptr_t)ws & (kAlign - 1)) != 0) return RTF_EINVAL;
     int launches = 0;
-    cudaError_t e = rtf::launch_build(p, n, m, flags, out->header, out->nodes, out->table,
-                                      nullptr, ws, L, as_stream(stream), &launches);
+    cudaError_t e;
+    if (!(flags & RTF_BUILD_SMALL_TILES) && n <= rtf::kRowsMax && m <= rtf::kRowsMax)
+        // one tile's worth: the row kernel builds the whole forest in one CTA's
+        // shared memory (the same layout and bytes as a one-row batched forest),
+        // without the cooperative kernel's grid barriers
+        e = rtf::launch_build_rows(p, 1, n, m, out->header, out->nodes, out->table, nullptr,
+                                   as_stream(stream), &launches);
+    else
+        e = rtf::launch_build(p, n, m, flags, out->header, out->nodes, out->table, nullptr, ws,
+                              L, as_stream(stream), &launches);
     return finish(e, launches);
 }
 

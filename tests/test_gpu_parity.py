@@ -109,6 +109,10 @@ def test_edge_cases(rtf):
     cases.append((g, 4))
     cases.append((np.ones(70000, np.float32), 1))                      # m = 1: one radix tree
     cases.append((random_small(rng, 5000), 40000))                     # m >> n
+    # one ragged tile in the cooperative kernel (n <= 4096 with m <= 4096 goes
+    # to the row kernel instead)
+    cases.append((random_small(rng, 3000), 5000))
+    cases.append((random_small(rng, 100), 8192))
     big = np.ones(6000, np.float32); big[::3] = 3e38; cases.append((big, 999))  # huge values
     for k, (p, m) in enumerate(cases):
         ref = oracle.build(p, m)
