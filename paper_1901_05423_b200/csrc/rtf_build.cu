@@ -344,6 +344,10 @@ __global__ void __launch_bounds__(THREADS, MINB) k_build(BuildArgs A) {
 #endif
     const bool sharded = A.shard_count > 0;
 
+    // the tiles form NRG ranges of krng consecutive tiles (phases A and B)
+    const uint32_t NRG = min(G, (uint32_t)THREADS);
+    const uint32_t krng = (nt + NRG - 1) / NRG;
+
     // ---------------------------------------------------------- A: scale
     if (b == 0 && tid == 0 && (ph & kPhTiles)) {
         A.counters[kCtrQueue] = 0;
@@ -374,14 +378,17 @@ __global__ void __launch_bounds__(THREADS, MINB) k_build(BuildArgs A) {
             else if (fabsf(x) == __int_as_float(0x7f800000)) f |= RTF_DATA_INF;
             else if (x < 0.0f) f |= RTF_DATA_NEG;
         };
-        const uint32_t gs = G * THREADS, gt = b * THREADS + tid;
+        // This CTA's share is the range of tiles it sums in phase B, so that
+        // phase B re-reads what this SM just pulled into its die's L2.
+        const uint32_t a_lo = (uint32_t)min((uint64_t)n, (uint64_t)b * krng * TILE);
+        const uint32_t a_hi = (uint32_t)min((uint64_t)n, ((uint64_t)b + 1) * krng * TILE);
         if (A.vec) {
-            const uint32_t n4 = n >> 2;
-            uint32_t q = gt;
-            for (; q + 7 * gs < n4; q += 8 * gs) {  // 8 independent 16-B loads in flight
+            const uint32_t lo4 = a_lo >> 2, hi4 = a_hi >> 2;  // a_lo is a multiple of TILE
+            uint32_t q = lo4 + tid;
+            for (; q + 7 * THREADS < hi4; q += 8 * THREADS) {  // 8 independent 16-B loads in flight
                 float4 v[8];
 #pragma unroll
-                for (int u = 0; u < 8; ++u) v[u] = ld_stream_f4(A.p + 4ull * (q + u * gs));
+                for (int u = 0; u < 8; ++u) v[u] = ld_stream_f4(A.p + 4ull * (q + u * THREADS));
 #pragma unroll
                 for (int u = 0; u < 8; ++u) {
                     visit(v[u].x);
@@ -390,34 +397,22 @@ __global__ void __launch_bounds__(THREADS, MINB) k_build(BuildArgs A) {
                     visit(v[u].w);
                 }
             }
-            for (; q < n4; q += gs) {
+            for (; q < hi4; q += THREADS) {
                 const float4 v = ld_stream_f4(A.p + 4ull * q);
                 visit(v.x);
                 visit(v.y);
                 visit(v.z);
                 visit(v.w);
             }
-            for (uint32_t i = 4 * n4 + gt; i < n; i += gs) visit(A.p[i]);
+            for (uint32_t i = 4 * hi4 + tid; i < a_hi; i += THREADS) visit(A.p[i]);
         } else {
-            for (uint32_t i = gt; i < n; i += gs) visit(A.p[i]);
+            for (uint32_t i = a_lo + tid; i < a_hi; i += THREADS) visit(A.p[i]);
         }
         uint32_t mx = (uint32_t)smax, fl = (smax >= 0x7f800000 || umax > 0x80000000u) ? 1u : 0u;
         block_max_or<THREADS>(mx, fl, s_red);
         if (fl) {  // invalid data somewhere in this CTA's share: exact flags
             fl = 0;
-            if (A.vec) {
-                const uint32_t n4 = n >> 2;
-                for (uint32_t q = gt; q < n4; q += gs) {
-                    const float4 v = ld_stream_f4(A.p + 4ull * q);
-                    classify(v.x, fl);
-                    classify(v.y, fl);
-                    classify(v.z, fl);
-                    classify(v.w, fl);
-                }
-                for (uint32_t i = 4 * n4 + gt; i < n; i += gs) classify(A.p[i], fl);
-            } else {
-                for (uint32_t i = gt; i < n; i += gs) classify(A.p[i], fl);
-            }
+            for (uint32_t i = a_lo + tid; i < a_hi; i += THREADS) classify(A.p[i], fl);
             uint32_t dummy = 0;
             block_max_or<THREADS>(dummy, fl, s_red);
         }
@@ -463,8 +458,6 @@ __global__ void __launch_bounds__(THREADS, MINB) k_build(BuildArgs A) {
     // barrier per tile), then writes each tile's exclusive prefix within its
     // range (excl) and the range total (rng).  Phase C scans only the NRG
     // range totals.
-    const uint32_t NRG = min(G, (uint32_t)THREADS);
-    const uint32_t krng = (nt + NRG - 1) / NRG;
     if ((ph & kPhTotals) && b < NRG) {
         Pfx* s_tagg = reinterpret_cast<Pfx*>(s_key);  // free until phase D
         constexpr uint32_t CAP = (uint32_t)(tile_padded<THREADS, VPT>() * 8 / sizeof(Pfx));
