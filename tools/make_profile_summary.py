@@ -37,16 +37,20 @@ for rep in (f"{R}_build.ncu-rep", f"{R}_sample.ncu-rep", f"{R}_full.ncu-rep"):
         rows = [h, units]
     idx = [rr[0].index(c) if c in rr[0] else None for c in h]
     sc = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
+    tsc = {"ns": 1e-3, "nsecond": 1e-3, "us": 1, "usecond": 1, "ms": 1e3, "msecond": 1e3}
     for r in rr[2:]:
         row = []
         for c, i in zip(h, idx):
             v = r[i] if i is not None else ""
             if c.startswith("dram__bytes_") and v:  # per-report units -> bytes
                 v = str(int(float(v.replace(",", "")) * sc.get(rr[1][i], 1)))
+            if c == "gpu__time_duration.sum" and v:  # per-report units -> us
+                v = f"{float(v.replace(',', '')) * tsc.get(rr[1][i], 1):.3f}"
             row.append(v)
         rows.append(row)
 for c in ("dram__bytes_read.sum", "dram__bytes_write.sum"):
     units[h.index(c)] = "byte"
+units[h.index("gpu__time_duration.sum")] = "us"
 want = ["Kernel Name", "gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum",
         "gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed", "lts__t_sector_hit_rate.pct",
         "sm__throughput.avg.pct_of_peak_sustained_elapsed", "sm__inst_executed.avg.per_cycle_elapsed",
@@ -65,12 +69,17 @@ with open(os.path.join(P, f"{R}_ncu_full.csv"), "w", newline="") as f:
         name = r[h.index("Kernel Name")].replace("void ", "").replace("rtf::", "")
         rd = float(r[h.index("dram__bytes_read.sum")].replace(",", "")) * scale.get(units[h.index("dram__bytes_read.sum")], 1)
         wr = float(r[h.index("dram__bytes_write.sum")].replace(",", "")) * scale.get(units[h.index("dram__bytes_write.sum")], 1)
-        key = "k_sample_2^28" if name.startswith("k_sample<0>") else \
-              "build" if name.startswith("k_build") else "k_bsearch" if name.startswith("k_bsearch") else None
+        if name.startswith("k_sample<0, 0>") or name.startswith("k_sample<0>"):
+            # the profiled launch is 2^28 config-3 samples (tools/gpu_ncu_main.sh)
+            tr.setdefault("k_sample_per_sample", round((rd + wr) / 2**28, 3))
+            continue
+        key = "build" if name.startswith("k_build<512, 8, 0") else \
+              "k_bsearch" if name.startswith("k_bsearch") else None
         if key and key not in tr:
             tr[key] = int(rd + wr)
-json.dump({"c3_powerlaw": tr, "note": f"dram read+write bytes per launch from ncu --set full ({R}); "
-           "k_sample traffic is for the profiled launch size (see profiles/" + f"{R}_ncu_full.csv)"},
+json.dump({"c3_powerlaw": tr, "note": f"dram read+write bytes from ncu --set full ({R}): per launch "
+           "for the build (n = 2^24) and k_bsearch (2^28 samples), per sample for k_sample "
+           "(measured on a 2^28-sample launch)"},
           open(os.path.join(P, "ncu_traffic.json"), "w"), indent=1)
 print(open(os.path.join(P, f"{R}_ncu_full.csv")).read())
 print(json.load(open(os.path.join(P, "ncu_traffic.json"))))
