@@ -94,3 +94,32 @@ def test_2d_data_errors(rtf):
     assert np.all(pix.cpu().numpy() == np.iinfo(np.int32).max)
     f = rtf.build_2d(torch.zeros((8, 16), dtype=torch.float32).cuda(), 16, 8)
     assert f.status() == rtf._lib.RTF_EALLZERO
+
+
+def test_2d_quadratic_error_qmc_vs_mc(rtf):
+    """The paper's convergence measure: e = sum_i (p_i - c_i/n)^2.
+    Pseudo-random pairs give E[e] = sum p_i (1 - p_i) / n; the Hammersley set
+    through the monotone inverse mapping keeps its stratification and lands
+    well below that (tools/convergence.py, profiles/r01_convergence.jsonl)."""
+    W, H, k = 2048, 1024, 20
+    n = 1 << k
+    img = env_map(W, H)
+    dev = torch.device("cuda", 0)
+    p = torch.from_numpy(img.astype(np.float64) / img.astype(np.float64).sum()).to(dev)
+    f = rtf.build_2d(torch.from_numpy(img).reshape(H, W).to(dev), W, H)
+    idx = np.arange(n, dtype=np.uint64)
+    rev = np.zeros(n, dtype=np.uint64)
+    for b in range(32):
+        rev |= ((idx >> np.uint64(b)) & np.uint64(1)) << np.uint64(31 - b)
+    qmc = (dev_u32((idx << np.uint64(32 - k)).astype(np.uint32)), dev_u32(rev.astype(np.uint32)))
+    mc = (dev_u32(philox_xi(n, seed=5)), dev_u32(philox_xi(n, seed=6)))
+
+    def err(x1, x2):
+        pix = f.sample(x1, x2, with_pos=False)
+        c = torch.bincount(pix.to(torch.int64), minlength=W * H).to(torch.float64)
+        return float(((p - c / n) ** 2).sum())
+
+    expected = float((p * (1 - p)).sum()) / n
+    e_mc, e_qmc = err(*mc), err(*qmc)
+    assert 0.8 * expected < e_mc < 1.2 * expected
+    assert e_qmc < e_mc / 3
