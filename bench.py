@@ -48,8 +48,8 @@ WORKLOADS = {
     # at random from DRAM: 39.6 G samples/s on one B200)
     "c4": dict(name="c4_spikes", n=1 << 28, m=1 << 22, samples=1 << 32,
                desc="config 4: n=2^28 spiky (4 spikes x 0.24 + uniform 0.04), m=2^22; sharded "
-                    "build (cross-GPU scan of shard totals) + replication; 2^32 Philox xi split "
-                    "over the GPUs"),
+                    "build (cross-GPU scan of shard totals), each rank keeping the cells of its "
+                    "xi stratum; 2^32 Philox xi split over the GPUs"),
     "c2d": dict(name="c2_envmap_2d", n=2048 * 1024, m=2048, W=2048, H=1024, my=1024,
                 samples=1 << 26,
                 desc="2-D (Sec.6 P:1523-1529): the 2048x1024 env map as marginal over rows "
