@@ -173,6 +173,20 @@ def test_repeat_builds_byte_identical(rtf):
             assert nodes == first, f"rep {rep} differs"
 
 
+def test_small_builds_same_bytes_from_both_kernels(rtf):
+    """n, m <= 4096 goes to the row kernel (one CTA); RTF_BUILD_SMALL_TILES keeps
+    the cooperative kernel.  Records [0, n'), table and header agree byte for byte."""
+    rng = np.random.default_rng(21)
+    for n, m in ((1, 1), (7, 3), (100, 4096), (1000, 17), (4096, 4096), (4096, 1)):
+        p = random_small(rng, n, zero_frac=0.2)
+        a, b = rtf.build(dev_f32(p), m, 0), rtf.build(dev_f32(p), m, 1)
+        ha, hb = a.header(), b.header()
+        assert bytes(ha) == bytes(hb), (n, m)
+        k = ha.n_pos
+        assert a.nodes_numpy()[:k].tobytes() == b.nodes_numpy()[:k].tobytes(), (n, m)
+        assert a.table_numpy().tobytes() == b.table_numpy().tobytes(), (n, m)
+
+
 # ---------------------------------------------------------------- workloads at scale
 
 @pytest.mark.parametrize("fam", ["A", "B", "C", "D"])
