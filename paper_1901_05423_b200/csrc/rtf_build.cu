@@ -1267,7 +1267,12 @@ template <int THREADS, int VPT, bool CDF, int MINB = 2, bool POW2 = false, bool 
 static cudaError_t launch_fused(BuildArgs& A, cudaStream_t st, int* launches) {
     auto kern = k_build<THREADS, VPT, CDF, MINB, POW2, FUSED>;
     const size_t smem = build_smem_bytes<THREADS, VPT>();  // phase B stages tile totals there
-    static int max_grid = 0;  // per instantiation: co-resident CTAs
+    // per instantiation and device: co-resident CTAs (the attribute is per device)
+    static int max_grid_dev[kMaxDevices] = {};
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= kMaxDevices)
+        return cudaErrorInvalidDevice;
+    int& max_grid = max_grid_dev[dev];
     if (!max_grid) {
         cudaError_t e = cudaSuccess;
         if (smem)

@@ -10,6 +10,7 @@
 namespace rtf {
 
 constexpr uint32_t kRowsMax = 4096;  // rtf_build_rows: n_row, m_row limit
+constexpr int kMaxDevices = 64;     // per-device launch attributes cached by the launchers
 
 // phases of the build kernel (bitmask); a single-GPU build runs kPhFull
 enum : uint32_t {

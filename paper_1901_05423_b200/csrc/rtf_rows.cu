@@ -365,7 +365,11 @@ __global__ void __launch_bounds__(THREADS, rows_min_blocks<THREADS, VPT>()) k_bu
 template <int THREADS, int VPT>
 static cudaError_t launch_rows_t(const RowsArgs& A, cudaStream_t st) {
     const size_t smem = rows_smem<THREADS, VPT>();
-    static bool attr = false;
+    static bool attr_dev[kMaxDevices] = {};  // the attributes are per device
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= kMaxDevices)
+        return cudaErrorInvalidDevice;
+    bool& attr = attr_dev[dev];
     if (!attr) {
         cudaError_t e = cudaFuncSetAttribute(k_build_rows<THREADS, VPT>,
                                              cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
