@@ -375,6 +375,7 @@ def run_gpu(args):
                             "path": "rtf_sample_host: pinned host xi -> 3-stream pipeline -> "
                                     "pinned host out"}}
 
+    quad = quad_summary(forest, xi, out, flush)
     result = {
         "metric": METRIC,
         "value": round(build_gs, 4),
@@ -413,6 +414,7 @@ def run_gpu(args):
                                                 "agreement": round(ts_agree, 6),
                                                 "note": "context only: float32 CDF, not "
                                                         "bit-exact"},
+                     "quad_records": quad,
                      "loads_per_sample": {"avg": round(e_loads, 4), "avg32": round(avg32, 4),
                                           "max": max_loads, "of": 1 << 20,
                                           "without_two_interval_flag": {
@@ -455,6 +457,36 @@ def run_gpu(args):
         dist.destroy_process_group()
     if rank == 0:
         print(json.dumps(result), flush=True)
+
+
+def quad_summary(forest, xi, out, flush, reps=3):
+    """The 4-ary collapsed records (rtf_build_quad / rtf_sample_quad)
+    on the same forest and xi: device time of the collapse and of one batch (L2
+    flushed before each launch, median of reps), and index equality with the
+    binary descent's out."""
+    import torch
+    out4 = torch.empty_like(out)
+
+    def timed(fn):
+        ts = []
+        for _ in range(reps):
+            flush.zero_()
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record()
+            fn()
+            b.record()
+            torch.cuda.synchronize()
+            ts.append(a.elapsed_time(b))
+        return statistics.median(ts)
+
+    t_q = timed(lambda: forest.build_quad())
+    t_s = timed(lambda: forest.sample_quad(xi, out4))
+    same = bool(torch.equal(out, out4))
+    del out4
+    return {"value": round(xi.numel() / (t_s * 1e-3) / 1e9, 4), "unit": "G samples/s",
+            "ms_per_batch": round(t_s, 4), "build_quad_ms": round(t_q, 4),
+            "identical_indices": same,
+            "what": "4-ary collapsed 32-B records: one load per two levels (P:1537-1539)"}
 
 
 def c2_summary(args, dev, stream, flush, world):
@@ -598,6 +630,7 @@ def run_gpu_c4(args):
     sample_gs = S * world * K / (ts * 1e-3) / 1e9
     peak, peak_src = peaks()
     bytes_build = 4 * n + 16 * forest.n_pos() + 8 * m
+    quad = quad_summary(forest, xi, out, flush) if world == 1 else None
     result = {
         "metric": METRIC, "value": round(build_gs, 4), "unit": "G entries/s", "n_gpus": world,
         "steps": K, "warmup": args.warmup, "ms_per_step": round((tb + ts) / K, 4),
@@ -615,7 +648,8 @@ def run_gpu_c4(args):
                                    f"sharded build over {world} GPU(s) + replicated forest; "
                                    "sampling split across GPUs")},
         "sampling": {"value": round(sample_gs, 4), "unit": "G samples/s",
-                     "ms_per_batch": round(ts / K, 4)},
+                     "ms_per_batch": round(ts / K, 4),
+                     "quad_records": quad if quad else "single-GPU forest only"},
         "roofline_build": {"kernel": "sharded build (all calls, incl. exchanges)",
                            "bound": "hbm", "achieved": round(bytes_build / (tb / K * 1e-3) / 1e9, 2),
                            "peak": peak, "unit": "GB/s",

@@ -190,6 +190,25 @@ int rtf_sample_f32(const rtf_forest *f, const float *xi, uint64_t count, int32_t
 int rtf_sample_loads(const rtf_forest *f, const uint32_t *xi, uint64_t count, int32_t *loads,
                      int32_t *loads_plain, void *stream);
 
+/* ------------------------------------ 4-ary collapsed records (Sec.5) */
+/*
+ * "Due to memory access granularity, it may be beneficial to construct 4-ary or
+ * even wider trees.  A higher branching factor simply results by just
+ * collapsing two (or more) levels of the binary trees."
+ * rtf_build_quad writes, for every node j < n_pos of a built single forest, a
+ * 32-B record {k0, k1, k2, flags, g0, g1, g2, g3}: k0 = ceil(key_j / 2^31),
+ * k1 / k2 the same for node j's children, g the four grandchildren (a leaf
+ * child stands for both of its slots), flags bit i: k_i = 2^32.  One 32-B load
+ * then decides two levels of Alg. 2.  rec4: device, 32-B aligned, >=
+ * rtf_quad_bytes(n) bytes, owned by the caller; valid until the forest is
+ * rebuilt.  rtf_sample_quad returns exactly rtf_sample's indices, reading the
+ * guide table and the quad records only.  Errors: RTF_EINVAL (NULL, rows != 1,
+ * misaligned), RTF_ENOSPACE (rec4 too small), RTF_ECUDA. */
+size_t rtf_quad_bytes(uint32_t n); /* host only */
+int rtf_build_quad(const rtf_forest *f, void *rec4, size_t rec4_bytes, void *stream);
+int rtf_sample_quad(const rtf_forest *f, const void *rec4, const uint32_t *xi, uint64_t count,
+                    int32_t *out, void *stream);
+
 /* Batched: sample k uses row[k] (< f->rows); out is row-local. */
 int rtf_sample_rows(const rtf_forest *f, const uint32_t *row, const uint32_t *xi,
                     uint64_t count, int32_t *out, void *stream);

@@ -122,6 +122,26 @@ class Forest:
                                _stream(stream)), "rtf_sample")
         return out
 
+    # ------------------------------------------- 4-ary collapsed records
+    def build_quad(self, stream=None) -> "Forest":
+        """32-B records deciding two levels per load (rtf_build_quad); call after build()."""
+        L = lib()
+        nb = L.rtf_quad_bytes(self.n)
+        if getattr(self, "_rec4", None) is None or self._rec4.numel() < nb:
+            self._rec4 = _bytes_tensor(nb, self._buf.forest.device)
+        check(L.rtf_build_quad(ctypes.byref(self.view), _ptr(self._rec4), self._rec4.numel(),
+                               _stream(stream)), "rtf_build_quad")
+        return self
+
+    def sample_quad(self, xi: torch.Tensor, out: torch.Tensor | None = None, stream=None):
+        """rtf_sample's indices through the quad records (build_quad() first)."""
+        xi = _u32_view(xi)
+        if out is None:
+            out = torch.empty(xi.numel(), dtype=torch.int32, device=xi.device)
+        check(lib().rtf_sample_quad(ctypes.byref(self.view), _ptr(self._rec4), _ptr(xi),
+                                    xi.numel(), _ptr(out), _stream(stream)), "rtf_sample_quad")
+        return out
+
     def sample_loads(self, xi: torch.Tensor, stream=None, plain: bool = False):
         """Per-sample memory loads of Alg. 2 (1 table cell + nodes visited);
         with plain=True also the count without the two-interval flag."""

@@ -56,6 +56,9 @@ PROTOTYPES = {
     "rtf_sample": (_I32, [_F, _P, _U64, _P, _P]),
     "rtf_sample_f32": (_I32, [_F, _P, _U64, _P, _P]),
     "rtf_sample_loads": (_I32, [_F, _P, _U64, _P, _P, _P]),
+    "rtf_quad_bytes": (_SZ, [_U32]),
+    "rtf_build_quad": (_I32, [_F, _P, _SZ, _P]),
+    "rtf_sample_quad": (_I32, [_F, _P, _P, _U64, _P, _P]),
     "rtf_sample_rows": (_I32, [_F, _P, _P, _U64, _P, _P]),
     "rtf_build_cdf": (_I32, [_P, _U32, _P, _P, _P, _SZ, _P]),
     "rtf_sample_bsearch": (_I32, [_P, _U32, _P, _P, _U64, _P, _P]),

@@ -184,6 +184,28 @@ int rtf_sample(const rtf_forest* f, const uint32_t* xi, uint64_t count, int32_t*
     return finish(e, launches);
 }
 
+size_t rtf_quad_bytes(uint32_t n) { return 32 * (size_t)(n ? n : 1); }
+
+int rtf_build_quad(const rtf_forest* f, void* rec4, size_t rec4_bytes, void* stream) {
+    if (!f || !f->nodes || !f->header || f->rows != 1 || !rec4) return RTF_EINVAL;
+    if (((uintptr_t)rec4 & 31u) != 0) return RTF_EINVAL;
+    if (rec4_bytes < rtf_quad_bytes(f->n)) return RTF_ENOSPACE;
+    int launches = 0;
+    cudaError_t e = rtf::launch_collapse4(*f, rec4, as_stream(stream), &launches);
+    return finish(e, launches);
+}
+
+int rtf_sample_quad(const rtf_forest* f, const void* rec4, const uint32_t* xi, uint64_t count,
+                    int32_t* out, void* stream) {
+    if (!f || !f->table || !f->header || f->rows != 1 || !rec4) return RTF_EINVAL;
+    if (((uintptr_t)rec4 & 31u) != 0) return RTF_EINVAL;
+    if (count && (!xi || !out)) return RTF_EINVAL;
+    if ((((uintptr_t)xi | (uintptr_t)out) & 3u) != 0) return RTF_EINVAL;
+    int launches = 0;
+    cudaError_t e = rtf::launch_sample4(*f, rec4, xi, count, out, as_stream(stream), &launches);
+    return finish(e, launches);
+}
+
 int rtf_sample_f32(const rtf_forest* f, const float* xi, uint64_t count, int32_t* out,
                    void* stream) {
     if (!f || !f->nodes || !f->table || !f->header || f->rows != 1) return RTF_EINVAL;

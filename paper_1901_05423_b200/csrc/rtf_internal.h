@@ -83,6 +83,10 @@ cudaError_t launch_sample_f32(const rtf_forest& f, const float* xi, uint64_t cou
 cudaError_t launch_sample_loads(const rtf_forest& f, const uint32_t* xi, uint64_t count,
                                 int32_t* loads, int32_t* loads_plain, cudaStream_t st,
                                 int* launches);
+// 4-ary collapsed records (rtf_quad.cu)
+cudaError_t launch_collapse4(const rtf_forest& f, void* rec4, cudaStream_t st, int* launches);
+cudaError_t launch_sample4(const rtf_forest& f, const void* rec4, const uint32_t* xi,
+                           uint64_t count, int32_t* out, cudaStream_t st, int* launches);
 
 cudaError_t launch_bsearch(const uint64_t* cdf, uint32_t n, const rtf_header* hdr,
                            const uint32_t* xi, uint64_t count, int32_t* out, cudaStream_t st,
