@@ -202,7 +202,10 @@ int rtf_sample_loads(const rtf_forest *f, const uint32_t *xi, uint64_t count, in
  * then decides two levels of Alg. 2.  rec4: device, 32-B aligned, >=
  * rtf_quad_bytes(n) bytes, owned by the caller; valid until the forest is
  * rebuilt.  rtf_sample_quad returns exactly rtf_sample's indices, reading the
- * guide table and the quad records only.  Errors: RTF_EINVAL (NULL, rows != 1,
+ * guide table and the quad records only.  On a ranged shard (rtf_shard_finish_range)
+ * only the records of the rank's own slots are valid, so only its own xi
+ * stratum may be sampled this way (child references are bounds-checked, never
+ * followed outside the forest).  Errors: RTF_EINVAL (NULL, rows != 1,
  * misaligned), RTF_ENOSPACE (rec4 too small), RTF_ECUDA. */
 size_t rtf_quad_bytes(uint32_t n); /* host only */
 int rtf_build_quad(const rtf_forest *f, void *rec4, size_t rec4_bytes, void *stream);

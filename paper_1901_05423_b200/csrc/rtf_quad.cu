@@ -39,7 +39,7 @@ __global__ void __launch_bounds__(kQuadThreads)
         key_ceil32(r.x, k[0], flags, 0);
 #pragma unroll
         for (int i = 0; i < 2; ++i) {
-            if (c[i] >= 0) {
+            if (c[i] >= 0 && (uint32_t)c[i] < n) {  // bounded: a ranged shard's foreign slots are stale
                 const ulonglong2 rc = __ldg(reinterpret_cast<const ulonglong2*>(nodes + c[i]));
                 key_ceil32(rc.x, k[1 + i], flags, 1 + i);
                 g[2 * i] = (int32_t)(uint32_t)rc.y;

@@ -53,6 +53,7 @@ def test_library_is_sm100a(L):
 
 
 def test_host_only_sizes(L):
+    c0 = L.rtf_launch_count()  # earlier tests in the same process may have launched
     fb = L.rtf_forest_bytes(1 << 24, 1 << 22, 1)
     assert fb >= 16 * (1 << 24) + 4 * (1 << 22) + 40
     assert fb % 256 == 0
@@ -63,11 +64,13 @@ def test_host_only_sizes(L):
     assert 4096 * (16 + 256) < wb < (1 << 24)
     assert L.rtf_status_string(0) == b"RTF_OK"
     assert b"sm_100a" in L.rtf_version()
-    assert L.rtf_launch_count() == 0
+    assert L.rtf_quad_bytes(1 << 24) == 32 << 24
+    assert L.rtf_launch_count() == c0
 
 
 def test_argument_validation_before_launch(L):
     from paper_1901_05423_b200 import _lib
+    c0 = L.rtf_launch_count()
     v = _lib.rtf_forest()
     EINVAL, ETOOLARGE = _lib.RTF_EINVAL, _lib.RTF_ETOOLARGE
     assert L.rtf_build(None, 10, 4, 0, None, 0, None, 0, None, ctypes.byref(v)) == EINVAL
@@ -82,7 +85,9 @@ def test_argument_validation_before_launch(L):
     assert L.rtf_sample(None, None, 0, None, None) == EINVAL
     assert L.rtf_build(fake, 10, 4, 7, fake, 1 << 30, fake, 1 << 30, None,
                        ctypes.byref(v)) == EINVAL  # unknown flag
-    assert L.rtf_launch_count() == 0
+    assert L.rtf_build_quad(None, fake, 1 << 30, None) == EINVAL
+    assert L.rtf_sample_quad(None, fake, None, 0, None, None) == EINVAL
+    assert L.rtf_launch_count() == c0
 
 
 def test_python_binding_fails_loudly_without_library(tmp_path, monkeypatch):
