@@ -538,13 +538,15 @@ def c2_summary(args, dev, stream, flush, world):
     loads = f.sample_loads(xi[: 1 << 20]).double().mean().item()
     bytes_b = 4 * n + 16 * f.n_pos() + 8 * m
     bytes_s = 4 + 4 + 8 + 16 * (loads - 1.0)
+    quad = quad_summary(f, xi, out, flush)
     return {"workload": wl["desc"],
             "build": {"value": round(world * n / (tb * 1e-3) / 1e9, 4), "unit": "G entries/s",
                       "ms_per_build": round(tb, 5),
                       "roofline_frac": round(bytes_b / (tb * 1e-3) / 1e9 / peak, 4)},
             "sampling": {"value": round(world * S / (ts * 1e-3) / 1e9, 4), "unit": "G samples/s",
                          "ms_per_batch": round(ts, 4),
-                         "roofline_frac": round(S * bytes_s / (ts * 1e-3) / 1e9 / peak, 4)},
+                         "roofline_frac": round(S * bytes_s / (ts * 1e-3) / 1e9 / peak, 4),
+                         "quad_records": quad},
             "bsearch": {"value": round(world * S / (tbs * 1e-3) / 1e9, 4), "unit": "G samples/s",
                         "identical_indices": eq},
             "timing": "median of >= 5 device-timed runs, L2 flushed before each"}
