@@ -135,6 +135,8 @@ class Forest:
 
     def sample_quad(self, xi: torch.Tensor, out: torch.Tensor | None = None, stream=None):
         """rtf_sample's indices through the quad records (build_quad() first)."""
+        if getattr(self, "_rec4", None) is None:
+            raise RuntimeError("sample_quad needs build_quad() after build()")
         xi = _u32_view(xi)
         if out is None:
             out = torch.empty(xi.numel(), dtype=torch.int32, device=xi.device)
