@@ -376,6 +376,17 @@ def run_gpu(args):
                                     "pinned host out"}}
 
     quad = quad_summary(forest, xi, out, flush)
+    xi_gen = None
+    if wl["name"] != "c2_envmap":  # the Philox input, timed apart from sampling
+        xi2 = torch.empty_like(xi)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        rtf.philox(S, seed=0x5EED, start=rank * S, out=xi2)
+        e1.record()
+        torch.cuda.synchronize()
+        xi_gen = {"kernel": "k_philox (Philox4x32-10)", "ms": round(e0.elapsed_time(e1), 4),
+                  "identical_to_timed_xi": bool(torch.equal(xi2, xi))}
+        del xi2
     result = {
         "metric": METRIC,
         "value": round(build_gs, 4),
@@ -415,6 +426,7 @@ def run_gpu(args):
                                                 "note": "context only: float32 CDF, not "
                                                         "bit-exact"},
                      "quad_records": quad,
+                     "xi_generation": xi_gen,
                      "loads_per_sample": {"avg": round(e_loads, 4), "avg32": round(avg32, 4),
                                           "max": max_loads, "of": 1 << 20,
                                           "without_two_interval_flag": {
