@@ -98,6 +98,7 @@ class Forest:
         if p.numel() != self.n:
             raise ValueError(f"p has {p.numel()} entries, forest was sized for {self.n}")
         self._p = p  # keep alive while kernels run
+        self._rec4_valid = False  # the 4-ary records describe the previous forest
         check(lib().rtf_build(_ptr(p), self.n, self.m, self.flags, _ptr(self._buf.forest),
                               self._buf.forest.numel(), _ptr(self._buf.ws),
                               self._buf.ws.numel(), _stream(stream), ctypes.byref(self.view)),
@@ -131,12 +132,13 @@ class Forest:
             self._rec4 = _bytes_tensor(nb, self._buf.forest.device)
         check(L.rtf_build_quad(ctypes.byref(self.view), _ptr(self._rec4), self._rec4.numel(),
                                _stream(stream)), "rtf_build_quad")
+        self._rec4_valid = True
         return self
 
     def sample_quad(self, xi: torch.Tensor, out: torch.Tensor | None = None, stream=None):
         """rtf_sample's indices through the quad records (build_quad() first)."""
-        if getattr(self, "_rec4", None) is None:
-            raise RuntimeError("sample_quad needs build_quad() after build()")
+        if getattr(self, "_rec4", None) is None or not getattr(self, "_rec4_valid", False):
+            raise RuntimeError("sample_quad needs build_quad() after the latest build()")
         xi = _u32_view(xi)
         if out is None:
             out = torch.empty(xi.numel(), dtype=torch.int32, device=xi.device)

@@ -115,7 +115,7 @@ cudaError_t launch_sample_2d(const rtf_forest2d& f, const uint32_t* xi1, const u
                              int* launches) {
     if (count == 0) return cudaSuccess;
     const uint64_t want = (count + k2dThreads - 1) / k2dThreads;
-    const uint32_t grid = (uint32_t)std::max<uint64_t>(1, std::min<uint64_t>(want, 148ull * 32ull));
+    const uint32_t grid = (uint32_t)std::max<uint64_t>(1, std::min<uint64_t>(want, (uint64_t)device_sms() * 32ull));
     k_sample_2d<<<grid, k2dThreads, 0, st>>>(f, xi1, xi2, count, pixel, pos);
     ++*launches;
     return cudaGetLastError();

@@ -394,62 +394,62 @@ int rtf_sample_host(const rtf_forest* f, const uint32_t* xi_host, uint64_t count
         return RTF_EINVAL;
     if (count == 0) return RTF_OK;
     if (chunk == 0) return RTF_EINVAL;
-    chunk = (chunk + 3) & ~3ull;
+    // The staging buffers hold 2 * chunk entries (rtf.h).  Round the chunk DOWN
+    // to a multiple of 4 (16-B aligned halves for the sampler's vector path);
+    // a chunk below 4 stays as given (launch_sample then uses scalar accesses).
+    if (chunk >= 4) chunk &= ~3ull;
     cudaStream_t user = as_stream(stream);
-    // three stages on three streams: H2D, sample, D2H; double-buffered staging
-    cudaStream_t s_in, s_run, s_out;
-    cudaEvent_t ev_ready[2], ev_in[2], ev_run[2], ev_out[2];
-    cudaError_t e = cudaSuccess;
-    bool ok = cudaStreamCreateWithFlags(&s_in, cudaStreamNonBlocking) == cudaSuccess;
-    ok = ok && cudaStreamCreateWithFlags(&s_run, cudaStreamNonBlocking) == cudaSuccess;
-    ok = ok && cudaStreamCreateWithFlags(&s_out, cudaStreamNonBlocking) == cudaSuccess;
-    for (int b = 0; b < 2 && ok; ++b) {
-        ok = ok && cudaEventCreateWithFlags(&ev_ready[b], cudaEventDisableTiming) == cudaSuccess;
-        ok = ok && cudaEventCreateWithFlags(&ev_in[b], cudaEventDisableTiming) == cudaSuccess;
-        ok = ok && cudaEventCreateWithFlags(&ev_run[b], cudaEventDisableTiming) == cudaSuccess;
-        ok = ok && cudaEventCreateWithFlags(&ev_out[b], cudaEventDisableTiming) == cudaSuccess;
+    // three stages on three streams: H2D, sample, D2H; double-buffered staging.
+    // Every handle starts null and every exit goes through the cleanup below,
+    // which destroys only what was created.
+    cudaStream_t s_in = nullptr, s_run = nullptr, s_out = nullptr;
+    cudaEvent_t ev_in[2] = {}, ev_run[2] = {}, ev_out[2] = {}, ev_user = nullptr;
+    cudaError_t e = cudaStreamCreateWithFlags(&s_in, cudaStreamNonBlocking);
+    if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&s_run, cudaStreamNonBlocking);
+    if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&s_out, cudaStreamNonBlocking);
+    for (int b = 0; b < 2 && e == cudaSuccess; ++b) {
+        e = cudaEventCreateWithFlags(&ev_in[b], cudaEventDisableTiming);
+        if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ev_run[b], cudaEventDisableTiming);
+        if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ev_out[b], cudaEventDisableTiming);
     }
-    if (!ok) return RTF_ECUDA;
-    // order after everything already enqueued on the caller's stream (the build)
-    cudaEvent_t ev_user;
-    cudaEventCreateWithFlags(&ev_user, cudaEventDisableTiming);
-    cudaEventRecord(ev_user, user);
-    cudaStreamWaitEvent(s_in, ev_user, 0);
-    cudaStreamWaitEvent(s_run, ev_user, 0);
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ev_user, cudaEventDisableTiming);
     int launches = 0;
-    uint64_t k = 0;
-    for (uint64_t c = 0; k < count && e == cudaSuccess; ++c) {
-        const int b = (int)(c & 1);
-        const uint64_t len = std::min<uint64_t>(chunk, count - k);
-        uint32_t* xd = xi_dev + (size_t)b * chunk;
-        int32_t* od = out_dev + (size_t)b * chunk;
-        if (c >= 2) cudaStreamWaitEvent(s_in, ev_run[b], 0);  // xi buffer b free
-        e = cudaMemcpyAsync(xd, xi_host + k, len * 4, cudaMemcpyHostToDevice, s_in);
-        cudaEventRecord(ev_in[b], s_in);
-        cudaStreamWaitEvent(s_run, ev_in[b], 0);
-        if (c >= 2) cudaStreamWaitEvent(s_run, ev_out[b], 0);  // out buffer b drained
-        if (e == cudaSuccess) e = rtf::launch_sample(*f, nullptr, xd, len, od, s_run, &launches);
-        cudaEventRecord(ev_run[b], s_run);
-        cudaStreamWaitEvent(s_out, ev_run[b], 0);
-        if (e == cudaSuccess)
-            e = cudaMemcpyAsync(out_host + k, od, len * 4, cudaMemcpyDeviceToHost, s_out);
-        cudaEventRecord(ev_out[b], s_out);
-        k += len;
+    if (e == cudaSuccess) {
+        // order after everything already enqueued on the caller's stream (the build)
+        e = cudaEventRecord(ev_user, user);
+        if (e == cudaSuccess) e = cudaStreamWaitEvent(s_in, ev_user, 0);
+        if (e == cudaSuccess) e = cudaStreamWaitEvent(s_run, ev_user, 0);
+        uint64_t k = 0;
+        for (uint64_t c = 0; k < count && e == cudaSuccess; ++c) {
+            const int b = (int)(c & 1);
+            const uint64_t len = std::min<uint64_t>(chunk, count - k);
+            uint32_t* xd = xi_dev + (size_t)b * chunk;
+            int32_t* od = out_dev + (size_t)b * chunk;
+            if (c >= 2) cudaStreamWaitEvent(s_in, ev_run[b], 0);  // xi buffer b free
+            e = cudaMemcpyAsync(xd, xi_host + k, len * 4, cudaMemcpyHostToDevice, s_in);
+            cudaEventRecord(ev_in[b], s_in);
+            cudaStreamWaitEvent(s_run, ev_in[b], 0);
+            if (c >= 2) cudaStreamWaitEvent(s_run, ev_out[b], 0);  // out buffer b drained
+            if (e == cudaSuccess) e = rtf::launch_sample(*f, nullptr, xd, len, od, s_run, &launches);
+            cudaEventRecord(ev_run[b], s_run);
+            cudaStreamWaitEvent(s_out, ev_run[b], 0);
+            if (e == cudaSuccess)
+                e = cudaMemcpyAsync(out_host + k, od, len * 4, cudaMemcpyDeviceToHost, s_out);
+            cudaEventRecord(ev_out[b], s_out);
+            k += len;
+        }
     }
-    cudaError_t e2 = cudaStreamSynchronize(s_out);
-    if (e == cudaSuccess) e = e2;
-    cudaStreamSynchronize(s_run);
-    cudaStreamSynchronize(s_in);
-    for (int b = 0; b < 2; ++b) {
-        cudaEventDestroy(ev_ready[b]);
-        cudaEventDestroy(ev_in[b]);
-        cudaEventDestroy(ev_run[b]);
-        cudaEventDestroy(ev_out[b]);
+    for (cudaStream_t s : {s_out, s_run, s_in}) {
+        if (!s) continue;
+        const cudaError_t e2 = cudaStreamSynchronize(s);
+        if (e == cudaSuccess) e = e2;
     }
-    cudaEventDestroy(ev_user);
-    cudaStreamDestroy(s_in);
-    cudaStreamDestroy(s_run);
-    cudaStreamDestroy(s_out);
+    for (int b = 0; b < 2; ++b)
+        for (cudaEvent_t ev : {ev_in[b], ev_run[b], ev_out[b]})
+            if (ev) cudaEventDestroy(ev);
+    if (ev_user) cudaEventDestroy(ev_user);
+    for (cudaStream_t s : {s_in, s_run, s_out})
+        if (s) cudaStreamDestroy(s);
     return finish(e, launches);
 }
 

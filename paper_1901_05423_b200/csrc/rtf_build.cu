@@ -6,24 +6,30 @@
 //                 last positive index (aggregates of the prefix sum).
 //   C  spine      CTA 0 turns the tile aggregates into exclusive prefixes and
 //                 publishes T, n' and the reciprocal of T (header).
-//   D  tiles      per tile (TMA-fed): block scan + tile prefix -> W_j,
-//                 compaction, one exact division per leaf (key_j); per owned
-//                 leaf: cell, split level lambda_j, guide-table anchors and
-//                 short runs; Alg. 1 for every leaf
-//                 of the tile except its first and last ("phase 1", shared-
-//                 memory atomicExch); coalesced flush of the 16-B records.
-//   E  cross      "phase 2": the <= 2 pending edge leaves per tile continue
-//                 Alg. 1 with global atomicExch, consuming the deposits the
-//                 tiles flushed; then the long empty-cell runs of the table.
+//   D  tiles      per tile (TMA-fed, dealt dynamically): block scan + tile
+//                 prefix -> W_j, compaction, one exact division per leaf
+//                 (key_j); per thread (8 entries): split levels lambda_j,
+//                 cells and guide-table entries, the 16-B records
+//                 {key_j, ~orig(j-1), ~orig(j)} staged in a 128-B-swizzled
+//                 shared-memory tile; then the radix forest of the tile:
+//                 every gap's parent is the nearer-in-level of its nearest
+//                 greater split levels on either side (the node Alg. 1,
+//                 P:1085-1121, merges it into), found in registers inside
+//                 the thread's 8 gaps and across threads from per-thread
+//                 spine summaries; one 4-B link per internal child into the
+//                 staged records; TMA tensor stores write the records out.
+//   E  cross      the links whose nearest greater split level lies in another
+//                 tile (each tile's spines), then the long empty-cell runs.
 //
-// A deposit in otherBounds carries the depositor's far bound AND the split
-// level beyond it, so the sibling that continues never re-reads lambda.
 // The result bytes do not depend on the schedule.
 
 #include "rtf_device.cuh"
 #include "rtf_internal.h"
 #include <atomic>
 #include <cstdlib>
+#include <cstring>
+#include <cuda.h>
+#include <cudaTypedefs.h>
 
 namespace rtf {
 
@@ -99,6 +105,7 @@ struct BuildArgs {
     uint32_t qcap;
     uint64_t* cdf;                // CDF mode only
     bool vec;
+    bool tma_store;               // records leave through the tensor maps (else plain stores)
 };
 
 // ------------------------------------------------------------ grid barrier
@@ -172,21 +179,49 @@ __device__ __forceinline__ void load_tile(const float* __restrict__ p, uint32_t 
     }
 }
 
-// Shared-memory arrays indexed by the local leaf index are padded with one slot
-// every 8 entries: with blocked ownership (lane L works on leaves ~8L + r) and
-// with strided access (consecutive leaves) both hit distinct banks.
-__device__ __forceinline__ uint32_t pad8(uint32_t j) { return j + (j >> 3); }
-
-template <int THREADS, int VPT>
-__host__ __device__ constexpr size_t tile_padded() {
-    return (size_t)THREADS * VPT + (size_t)THREADS * VPT / 8 + 4;  // + slot pad8(TILE)
-}
-
+// Dynamic shared memory of the build kernel (1024-B aligned base):
+//   stage   (TILE + 64) records of 16 B: the tile's node records, record l at
+//           row-swizzled position stage_pos(l + (j0 & 63)) (TMA SWIZZLE_128B)
+//   p       TILE floats: the tile's weights (1-D TMA target)
+//   per thread ("chunk" = its 8 entries): its packed split levels (u64, byte
+//           r = gap r), first leaf, last positive entry, 1 + max split level
 template <int THREADS, int VPT>
 constexpr size_t build_smem_bytes() {
-    // p tile / otherBounds (i32), keys (u64), child0, child1 (i32), split levels (u8)
-    return tile_padded<THREADS, VPT>() * (4 + 8 + 4 + 4) +
-           ((tile_padded<THREADS, VPT>() + 15) & ~(size_t)15);
+    return 1024 + (size_t)(THREADS * VPT + 64) * 16 + (size_t)THREADS * VPT * 4 +
+           (size_t)THREADS * (8 + 4 + 4 + 1);
+}
+
+// the 128-B swizzle of a TMA tensor store with 128-B rows: 16-B chunk c of
+// row r sits at chunk c ^ (r & 7).  A thread's 8 consecutive records then
+// spread over all 32 banks across 8 lanes (blocked 16-B stores conflict-free).
+__device__ __forceinline__ uint32_t stage_pos(uint32_t x) {
+    return (x & ~7u) | ((x ^ (x >> 3)) & 7u);
+}
+
+// split level (byte) i of a thread's 8 packed split levels
+__device__ __forceinline__ uint32_t lam_at(uint32_t lo, uint32_t hi, uint32_t i) {
+    return __byte_perm(lo, hi, i) & 0xffu;
+}
+
+// Byte masks (top bit per byte) over a thread's 8 packed split levels
+// (glo: bytes 0-3, ghi: bytes 4-7).  Highest marked byte below r / lowest
+// marked byte above r, -1 if none; r in [0, 7].
+__device__ __forceinline__ int byte_below(uint32_t glo, uint32_t ghi, uint32_t r) {
+    const uint32_t ml = r >= 4u ? 0xffffffffu : ((1u << (8u * r)) - 1u);
+    const uint32_t h = r <= 4u ? 0u : (ghi & ((1u << (8u * r - 32u)) - 1u));
+    return h ? 4 + ((31 - __clz(h)) >> 3) : (31 - __clz(glo & ml)) >> 3;
+}
+__device__ __forceinline__ int byte_above(uint32_t glo, uint32_t ghi, uint32_t r) {
+    const uint32_t l = r >= 3u ? 0u : (glo & (0xffffffffu << (8u * r + 8u)));
+    const uint32_t h = r == 7u ? 0u : (r < 4u ? ghi : (ghi & (0xffffffffu << (8u * r - 24u))));
+    return l ? (__ffs(l) - 1) >> 3 : (h ? 4 + ((__ffs(h) - 1) >> 3) : -1);
+}
+// first / last marked byte of a non-empty mask pair
+__device__ __forceinline__ uint32_t byte_first(uint32_t glo, uint32_t ghi) {
+    return glo ? (uint32_t)(__ffs(glo) - 1) >> 3 : 4u + ((uint32_t)(__ffs(ghi) - 1) >> 3);
+}
+__device__ __forceinline__ uint32_t byte_last(uint32_t glo, uint32_t ghi) {
+    return ghi ? 4u + ((uint32_t)(31 - __clz(ghi)) >> 3) : (uint32_t)(31 - __clz(glo)) >> 3;
 }
 
 // A long run of empty cells after the cell of leaf orig i: ~i for each, queued
@@ -296,32 +331,38 @@ __device__ unsigned long long g_phase_cycles[kMaxGrid][16];
 // ============================================================== the build kernel
 
 template <int THREADS, int VPT, bool CDF, int MINB = 2, bool POW2 = false, bool FUSED = false>
-__global__ void __launch_bounds__(THREADS, MINB) k_build(BuildArgs A) {
+__global__ void __launch_bounds__(THREADS, MINB)
+    k_build(BuildArgs A, const __grid_constant__ CUtensorMap tm_big,
+            const __grid_constant__ CUtensorMap tm_small) {
     constexpr int TILE = THREADS * VPT;
     constexpr int NW = THREADS / 32;
-    constexpr int P = (int)tile_padded<THREADS, VPT>();
-    extern __shared__ __align__(128) unsigned char smem[];
-    float* s_p = reinterpret_cast<float*>(smem);       // tile weights (TMA target)
-    int32_t* s_ob = reinterpret_cast<int32_t*>(smem);  // ... then otherBounds
-    uint64_t* s_key = reinterpret_cast<uint64_t*>(smem + 4 * P);
-    int32_t* s_c0 = reinterpret_cast<int32_t*>(s_key + P);
-    int32_t* s_c1 = s_c0 + P;
-    uint8_t* s_lam = reinterpret_cast<uint8_t*>(s_c1 + P);
+    extern __shared__ __align__(1024) unsigned char smem_raw[];
+    // 1024-B aligned (the TMA swizzle atom); derived from smem_raw so the
+    // compiler keeps shared-memory accesses (LDS/STS, not generic LD/ST)
+    unsigned char* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+    unsigned char* s_stage = smem;  // (TILE + 64) x 16-B staged records (swizzled)
+    const uint32_t a_stage = smem_u32(s_stage);
+    float* s_p = reinterpret_cast<float*>(smem + (size_t)(TILE + 64) * 16);  // TMA target
+    unsigned long long* s_clp = reinterpret_cast<unsigned long long*>(s_p + TILE);
+    uint32_t* s_ccex = reinterpret_cast<uint32_t*>(s_clp + THREADS);
+    int32_t* s_clast = reinterpret_cast<int32_t*>(s_ccex + THREADS);
+    uint8_t* s_cmax = reinterpret_cast<uint8_t*>(s_clast + THREADS);
     __shared__ __align__(8) uint64_t s_bar;
     __shared__ uint64_t s_w[2 * NW];
     __shared__ uint32_t s_c[2 * NW];
     __shared__ int32_t s_l[2 * NW];
-    __shared__ uint64_t s_key_after;
     __shared__ uint32_t s_red[2 * NW];
+    __shared__ uint32_t s_wmax[NW];  // per warp: max of its threads' 1 + max split level
+    __shared__ uint32_t s_B[NW * 64];  // per warp and level v: its threads with a level > v
+    __shared__ uint16_t s_task[NW * 256];  // per warp: its spine gaps (thread << 3 | gap)
     __shared__ __align__(16) Pfx s_rpre;  // the next tile's range prefix (issuer thread)
     __shared__ Pfx s_tot;
     __shared__ uint32_t s_next;
     __shared__ __align__(16) Pfx s_pin;  // TMA target: the next tile's prefix within its range
     __shared__ uint64_t s_recip;
     __shared__ unsigned long long s_mL, s_mR;  // this tile's spines (TileSpine)
-    __shared__ uint32_t s_walls;
-    __shared__ uint32_t s_fw, s_lw, s_mx;  // first / last wall, (max split level << 16 | gap)
-    __shared__ int32_t s_ref0;
+    __shared__ uint32_t s_fw, s_lw;            // first / last wall (lambda = 64) of the tile
+    __shared__ int32_t s_ref0, s_c0next;
     __shared__ uint16_t s_iL[65], s_iR[65];
 
     const uint32_t G = gridDim.x, b = blockIdx.x, tid = threadIdx.x;
@@ -459,8 +500,8 @@ __global__ void __launch_bounds__(THREADS, MINB) k_build(BuildArgs A) {
     // range (excl) and the range total (rng).  Phase C scans only the NRG
     // range totals.
     if ((ph & kPhTotals) && b < NRG) {
-        Pfx* s_tagg = reinterpret_cast<Pfx*>(s_key);  // free until phase D
-        constexpr uint32_t CAP = (uint32_t)(tile_padded<THREADS, VPT>() * 8 / sizeof(Pfx));
+        Pfx* s_tagg = reinterpret_cast<Pfx*>(s_stage);  // free until phase D
+        constexpr uint32_t CAP = (uint32_t)(TILE + 64);
         constexpr int F = TILE / 128;  // float4 per lane per tile
         constexpr int BATCH = F < 8 ? F : 8;
         const uint32_t t_beg = b * krng, t_end = min(nt, t_beg + krng);
@@ -650,24 +691,80 @@ __global__ void __launch_bounds__(THREADS, MINB) k_build(BuildArgs A) {
     // ---------------------------------------------------------- D: tiles
     // Tiles are dealt dynamically (their cost varies with the zero fraction
     // and the tree shape): CTA b starts with tile b, then takes G + tickets.
-    // Thread 0 draws each ticket one tile ahead, so the atomic's latency is
-    // hidden; the TMA copy of the next tile's weights also brings its prefix
-    // within its range (one mbarrier for both).
+    // The issuer thread draws each ticket one tile ahead, so the atomic's
+    // latency is hidden; the TMA copy of the next tile's weights also brings
+    // its prefix within its range (one mbarrier for both).  Three block
+    // barriers per tile: (1) scan, (2) records + per-thread summaries written,
+    // (3) every link written.
+    if constexpr (!CDF) {
+    static_assert(VPT == 8, "phase D packs a thread's 8 split levels into one 64-bit word");
+    constexpr uint32_t kIssuer = THREADS - 1;  // TMA, tickets, stores: the last warp
     uint32_t phase = 0;
-    uint32_t ticket = 0;  // issuer thread: the tile after the next one
+    uint32_t ticket = 0;      // issuer: the tile after the next one
+    bool store_pending = false;  // issuer: a TMA store group may still read the stage
     if (tid == 0) {
         s_mL = s_mR = 0ull;
-        s_walls = 0u;
         s_fw = 0xffffffffu;
         s_lw = 0u;
-        s_mx = 0u;
+        s_c0next = kNoLink;
     }
-    constexpr uint32_t kIssuer = THREADS - 1;  // TMA and tickets: the last warp (light duty)
     if (tid == kIssuer) {
         fence_proxy_async_global();  // phase B's prefixes, read by TMA below
         if (ph & kPhTiles) ticket = G + atomicAdd(&A.counters[kCtrTile], 1u);
     }
     if (ph & kPhTiles) wait_rpre();
+
+    // Gaps above level v in a thread's packed split levels: byte + 127 - v
+    // reaches bit 7 exactly when byte > v (bytes <= 64, so no carries).
+    auto above = [](uint32_t lo, uint32_t hi, uint32_t v, uint32_t& glo, uint32_t& ghi) {
+        const uint32_t c = __byte_perm(127u - v, 0u, 0u);  // 127 - v in every byte
+        glo = (lo + c) & 0x80808080u;
+        ghi = (hi + c) & 0x80808080u;
+    };
+    // The nearest greater split level of a gap at level v of thread c, to its
+    // right / left outside the thread: the first / last gap above v of the
+    // nearest thread whose largest level exceeds v (per-warp tables s_B).
+    auto search_right = [&](uint32_t c, uint32_t v, uint32_t& gap, uint32_t& lev) -> bool {
+        const uint32_t w = c >> 5, l = c & 31u;
+        uint32_t mk = s_B[w * 64 + v] & ~((2u << l) - 1u);
+        uint32_t u;
+        if (mk) {
+            u = (w << 5) + (uint32_t)__ffs(mk) - 1u;
+        } else {
+            uint32_t w2 = w + 1u;
+            while (w2 < (uint32_t)NW && s_wmax[w2] <= v + 1u) ++w2;
+            if (w2 >= (uint32_t)NW) return false;
+            u = (w2 << 5) + (uint32_t)__ffs(s_B[w2 * 64 + v]) - 1u;
+        }
+        const unsigned long long lp = s_clp[u];
+        uint32_t glo, ghi;
+        above((uint32_t)lp, (uint32_t)(lp >> 32), v, glo, ghi);
+        const uint32_t pos = byte_first(glo, ghi);
+        lev = lam_at((uint32_t)lp, (uint32_t)(lp >> 32), pos);
+        gap = s_ccex[u] + pos;
+        return true;
+    };
+    auto search_left = [&](uint32_t c, uint32_t v, uint32_t& gap, uint32_t& lev) -> bool {
+        const uint32_t w = c >> 5, l = c & 31u;
+        uint32_t mk = s_B[w * 64 + v] & ((1u << l) - 1u);
+        uint32_t u;
+        if (mk) {
+            u = (w << 5) + 31u - (uint32_t)__clz(mk);
+        } else {
+            int32_t w2 = (int32_t)w - 1;
+            while (w2 >= 0 && s_wmax[w2] <= v + 1u) --w2;
+            if (w2 < 0) return false;
+            u = ((uint32_t)w2 << 5) + 31u - (uint32_t)__clz(s_B[w2 * 64 + v]);
+        }
+        const unsigned long long lp = s_clp[u];
+        uint32_t glo, ghi;
+        above((uint32_t)lp, (uint32_t)(lp >> 32), v, glo, ghi);
+        const uint32_t pos = byte_last(glo, ghi);
+        lev = lam_at((uint32_t)lp, (uint32_t)(lp >> 32), pos);
+        gap = s_ccex[u] + pos;
+        return true;
+    };
+
     for (uint32_t t = b; (ph & kPhTiles) && t < nt; t = s_next) {
         const uint32_t first = t * TILE + tid * VPT;  // local index into p (global: + ib)
 
@@ -675,7 +772,13 @@ __global__ void __launch_bounds__(THREADS, MINB) k_build(BuildArgs A) {
         float x[VPT];
         Pfx pre;
         if (tma_tile(t)) {
+#ifdef RTF_PHASE_TIMING
+            const long long tw1_ = clock64();
             mbar_wait(&s_bar, phase);
+            if (tid == 0) g_phase_cycles[blockIdx.x][10] += (unsigned long long)(clock64() - tw1_);
+#else
+            mbar_wait(&s_bar, phase);
+#endif
             phase ^= 1u;
             pre = t == b ? tile_prefix(t) : combine(s_rpre, s_pin);
 #pragma unroll
@@ -690,311 +793,49 @@ __global__ void __launch_bounds__(THREADS, MINB) k_build(BuildArgs A) {
             load_tile<VPT>(A.p, first, n, A.vec, x);
             pre = tile_prefix(t);
         }
+        // (1) quantise; block scan of (W, positives) -- warp scans, one barrier,
+        // then every warp scans the warp totals itself
         uint64_t w[VPT];
         uint64_t tw = 0;
-        uint32_t tc = 0, posmask = 0;
-        int32_t tl = -1;
+        uint32_t posmask = 0;
 #pragma unroll
         for (int k = 0; k < VPT; ++k) {
             w[k] = quantize(x[k], scale);
             tw += w[k];
-            if (w[k]) {
-                ++tc;
-                posmask |= 1u << k;
-                tl = (int32_t)(first + k) + ib;
-            }
+            posmask |= (w[k] != 0ull ? 1u : 0u) << k;
         }
-        // (1) block scan (its barriers also retire every read of s_p);
-        // one exact division per positive entry
-        uint64_t w_ex, w_tot;
-        uint32_t c_ex, cnt;
-        int32_t l_ex;
-        block_scan3_excl<THREADS>(tw, tc, tl, w_ex, c_ex, l_ex, w_tot, cnt, s_w, s_c, s_l);
-        const uint32_t j0 = pre.cnt;  // global index of the tile's first leaf
-        {  // otherBounds start empty; the consumed weight tile becomes the array
-            int4* ob4 = reinterpret_cast<int4*>(s_ob);
-            for (uint32_t u = tid; u < (uint32_t)P / 4; u += THREADS)
-                ob4[u] = make_int4(-1, -1, -1, -1);
-        }
-        {
-            // Node records start as anchors: child0 = ~orig(j-1) (Fig. 6 caption
-            // P:1276-1277; j = 0 -> ~orig(0)); internal nodes overwrite it in
-            // Alg. 1.  child1 needs no initial value: every slot's right child
-            // is set by phase 1 here or by phase 2 afterwards.
-            int32_t prevo = l_ex >= 0 ? l_ex : (j0 ? pre.last : -1);
-            uint64_t W = pre.W + w_ex;
-            uint32_t jl = c_ex;
+        const uint32_t tc = __popc(posmask);
+        s_clast[tid] = posmask ? 31 - __clz((int)posmask) : -1;
+        uint64_t wi = tw;
+        uint32_t ci = tc;
 #pragma unroll
-            for (int k = 0; k < VPT; ++k) {
-                const uint64_t wk = w[k];
-                if (wk) {
-                    const int32_t i = (int32_t)(first + k) + ib;
-                    const uint32_t q = pad8(jl);
-                    w[k] = fixed_point(W, nm);  // w[k] holds key_j from here on
-                    s_key[q] = w[k];
-                    s_c0[q] = ~(prevo >= 0 ? prevo : i);
-                    prevo = i;
-                    ++jl;
-                }
-                W += wk;
+        for (int d = 1; d < 32; d <<= 1) {
+            const uint64_t tw2 = shfl_up_u64(wi, d);
+            const uint32_t tc2 = __shfl_up_sync(0xffffffffu, ci, d);
+            if (lane >= d) {
+                wi += tw2;
+                ci += tc2;
             }
         }
-        // the tile's first leaf is linked in phase E (its left split level
-        // belongs to the previous tile); the slot after the last leaf collects
-        // the left child of the last gap, if phase 1 links it
-        if (tc && c_ex == 0) s_ref0 = ~((int32_t)(first + __ffs(posmask) - 1) + ib);
-        if (tid == 0) s_c0[pad8(cnt)] = kNoLink;
-        if (tid == THREADS - 1) {  // key of the first leaf after the tile (or "1")
-            const uint64_t We = pre.W + w_tot;
-            s_key_after = (We == T) ? kOne63 : fixed_point(We, nm);
+        if (lane == 31) {
+            s_w[warp] = wi;
+            s_c[warp] = ci;
+        }
+        if (tid == kIssuer && store_pending) {  // the previous tile's records have left the stage
+#ifdef RTF_PHASE_TIMING
+            const long long tw0_ = clock64();
+            bulk_wait_read0();
+            g_phase_cycles[blockIdx.x][9] += (unsigned long long)(clock64() - tw0_);
+#else
+            bulk_wait_read0();
+#endif
+            store_pending = false;
         }
         __syncthreads();
-
         RTF_TICK(3);
-        // (2) own leaves: cell, split level, guide table; the
-        // thread's own split levels also stay in registers (byte r = rank r)
-        // keys come from registers (w[k]); only the key after the thread's last
-        // leaf is read back (its owner's, or the one after the tile)
-        uint64_t lampack = 0;
-        if (tc) {
-            uint64_t kn = (c_ex + tc < cnt) ? s_key[pad8(c_ex + tc)] : s_key_after;
-            uint32_t cn = POW2 ? 0u : ((kn == kOne63) ? m : cell_of(kn, m));
-            if (j0 == 0 && c_ex == 0) st_cell(table_at(0), 0, 0u, 0);  // leaf 0 (key 0): cell 0's anchor
-#pragma unroll
-            for (int k = VPT - 1; k >= 0; --k) {
-                if ((posmask >> k) & 1u) {
-                    const uint64_t key = w[k];
-                    const uint32_t r = __popc(posmask & ((1u << k) - 1u));  // rank
-                    const uint32_t jl = c_ex + r;
-                    uint32_t cell, lam;
-                    if (POW2) {  // a cell boundary lies between iff the keys differ at or
-                                 // above bit mshift (kn = 2^63 "1" differs at bit 63)
-                        const uint32_t d = split_level(key, kn);
-                        lam = d >= A.mshift ? kLamBoundary : d;
-                        cell = (uint32_t)(key >> A.mshift);
-                        cn = (uint32_t)(kn >> A.mshift);
-                    } else {
-                        cell = cell_of(key, m);
-                        lam = (cn != cell) ? kLamBoundary : split_level(key, kn);
-                    }
-                    s_lam[pad8(jl)] = (uint8_t)lam;
-                    lampack |= (uint64_t)lam << (8 * r);
-                    if (lam == kLamBoundary) {  // the table entries this leaf owes
-                        const int32_t i = (int32_t)(first + k) + ib;
-                        // the next cell's anchor (a one-leaf cell gets its
-                        // two-interval entry from the anchor's tile, below)
-                        if (cn < m) st_cell(table_at(cn), cn, 0u, (int32_t)(j0 + jl + 1));
-                        if (FUSED)  // the first leaf of every owner boundary k cpo in (cell, cn]
-                            for (uint32_t k = cell / A.cpo + 1; k <= min(A.npeer, cn / A.cpo); ++k)
-                                A.jbound[k] = j0 + jl + 1;
-                        const uint32_t len = cn - cell - 1;
-                        if (len <= kShortRun) {
-                            for (uint32_t g = cell + 1; g < cn; ++g) st_cell(table_at(g), g, 0u, ~i);
-                        } else {
-                            table_queue(A.counters, A.queue, A.qcap, i, cell, len);
-                        }
-                    }
-                    kn = key;
-                    cn = cell;
-                }
-            }
-        }
-        if (tc) {  // first / last wall and the largest other split level (byte SIMD)
-            const uint32_t h0 = (uint32_t)lampack, h1 = (uint32_t)(lampack >> 32);
-            const uint32_t w0 = __vcmpeq4(h0, 0x40404040u), w1 = __vcmpeq4(h1, 0x40404040u);
-            const uint32_t wm = (((w0 & 0x80808080u) * 0x00204081u) >> 28) |
-                                ((((w1 & 0x80808080u) * 0x00204081u) >> 28) << 4);
-            if (wm) {
-                atomicMin(&s_fw, c_ex + __ffs(wm) - 1);
-                atomicMax(&s_lw, c_ex + 31 - __clz(wm));
-            }
-            const uint32_t v0 = h0 & ~w0, v1 = h1 & ~w1;  // walls -> 0; bytes past tc are 0
-            uint32_t mv = __vmaxu4(v0, v1);
-            mv = __vmaxu4(mv, mv >> 16);
-            mv = max(mv & 0xffu, (mv >> 8) & 0xffu);
-            const uint32_t e0 = __vcmpeq4(v0, mv * 0x01010101u), e1 = __vcmpeq4(v1, mv * 0x01010101u);
-            const uint32_t em = (((e0 & 0x80808080u) * 0x00204081u) >> 28) |
-                                ((((e1 & 0x80808080u) * 0x00204081u) >> 28) << 4);
-            atomicMax(&s_mx, (mv + 1) << 16 | (c_ex + __ffs(em) - 1));
-        }
-        __syncthreads();
-
-        RTF_TICK(4);
-        // (3) phase 1: Alg. 1 for the tile's leaves 1..cnt-1 with shared-memory
-        // atomicExch.  A range containing leaf 0 (whose left split level is
-        // the previous tile's) never completes here; a range ending at the
-        // last leaf may still become the left child of the last gap, whose
-        // slot is cnt.  Every parent slot is in [1, cnt].  What stays open
-        // (first arrivals without a sibling in the tile) is exactly what the
-        // spines describe; those deposits are dropped.  Each lane walks its
-        // own leaves back to back.  A cell root (lambda = 64 on both sides) is
-        // the right child of its anchor lo and needs no exchange.  A deposit
-        // is (lambda beyond the bound) << 16 | bound.
-        {
-            // Stage A: the FIRST step of every own interior leaf, straight-line
-            // (half of all merge steps, without loop or divergence overhead).
-            // Leaf of rank r is l = c_ex + r; its split levels come from
-            // registers (lambda[l-1] of rank 0 from the previous thread).
-            const uint32_t lam_prev = c_ex ? (uint32_t)s_lam[pad8(c_ex - 1)] : kLamBoundary;
-            uint32_t contw[VPT];  // second arrivals: the sibling's packed deposit
-            uint32_t pend = 0, rightbits = 0;
-            {
-                uint32_t mask = posmask;
-#pragma unroll
-                for (int r = 0; r < VPT; ++r) {
-                    contw[r] = 0;
-                    if ((uint32_t)r < tc) {
-                        const uint32_t k = __ffs(mask) - 1;
-                        mask &= mask - 1;
-                        const uint32_t l = c_ex + r;
-                        if (l >= 1) {
-                            const uint32_t lamL =
-                                r ? (uint32_t)(lampack >> (8 * (r - 1))) & 0xffu : lam_prev;
-                            const uint32_t lamR = (uint32_t)(lampack >> (8 * r)) & 0xffu;
-                            const bool right = lamL <= lamR;
-                            const bool root = (lamL & lamR & kLamBoundary) != 0;
-                            const uint32_t q = pad8(right ? l : l + 1);
-                            s_c0[q + (right ? P : 0)] = ~((int32_t)(first + k) + ib);
-                            if (!root) {
-                                const int32_t other = atomicExch(
-                                    &s_ob[q], (int32_t)((right ? lamR : lamL) << 16 | l));
-                                if (other >= 0) {
-                                    s_ob[q] = -1;  // reset-on-consume
-                                    contw[r] = (uint32_t)other;
-                                    pend |= 1u << r;
-                                    rightbits |= (right ? 1u : 0u) << r;
-                                }
-                            } else {
-                                // a one-leaf cell: exactly two intervals overlap it
-                                // (P:1335-1338); slot q = l holds its key and the
-                                // anchor's left child ~orig(l-1)
-                                const uint64_t key = s_key[q];
-                                const int32_t a = (int32_t)(j0 + l);
-                                const uint2 e =
-                                    single_leaf_cell(key, (int32_t)(first + k) + ib, ~s_c0[q], a);
-                                if ((int32_t)e.y != a)
-                                    st_cell(table_at(cell_fn(key)), cell_fn(key), e.x,
-                                            (int32_t)e.y);
-                            }
-                        }
-                    }
-                }
-            }
-            // Stage B: the second arrivals climb on, one walker per lane at a time.
-            bool active = false;
-            int32_t lo = 0, hi = 0, node = 0;
-            uint32_t lamL = 0, lamR = 0;
-            while (true) {
-                if (!active && pend) {
-                    const uint32_t r = __ffs(pend) - 1;
-                    pend &= pend - 1;
-                    // select contw[r] by the bits of r (a 3-level tree of selects;
-                    // measured 1.5 % faster than a chain of compares)
-                    uint32_t sel[VPT];
-#pragma unroll
-                    for (int u = 0; u < VPT; ++u) sel[u] = contw[u];
-#pragma unroll
-                    for (int w = VPT / 2, bit = 1; w >= 1; w /= 2, bit <<= 1)
-#pragma unroll
-                        for (int u = 0; u < w; ++u) sel[u] = (r & bit) ? sel[2 * u + 1] : sel[2 * u];
-                    const uint32_t other = sel[0];
-                    const uint32_t l = c_ex + r;
-                    const uint32_t bound = other & 0xffffu, lv = other >> 16;
-                    const uint32_t own_lo = r ? (uint32_t)(lampack >> (8 * (r - 1))) & 0xffu
-                                              : lam_prev;
-                    const uint32_t own_hi = (uint32_t)(lampack >> (8 * r)) & 0xffu;
-                    active = true;
-                    if ((rightbits >> r) & 1u) {  // merged as the right child of node l
-                        lo = (int32_t)bound;
-                        hi = (int32_t)l;
-                        lamL = lv;
-                        lamR = own_hi;
-                        node = (int32_t)(j0 + l);
-                    } else {  // merged as the left child of node l + 1
-                        lo = (int32_t)l;
-                        hi = (int32_t)bound;
-                        lamL = own_lo;
-                        lamR = lv;
-                        node = (int32_t)(j0 + l + 1);
-                    }
-                }
-                if (!__any_sync(0xffffffffu, active)) break;
-                if (active) {
-                    const bool right = lamL <= lamR;  // Alg. 1: child 1 unless left is farther
-                    const bool root = (lamL & lamR & kLamBoundary) != 0;
-                    const int32_t parent = right ? lo : hi + 1;
-                    const uint32_t q = pad8((uint32_t)parent);
-                    s_c0[q + (right ? P : 0)] = node;
-                    const int32_t dep = right ? (int32_t)(lamR << 16 | (uint32_t)hi)
-                                              : (int32_t)(lamL << 16 | (uint32_t)lo);
-                    const int32_t other = root ? -1 : atomicExch(&s_ob[q], dep);
-                    active = other >= 0;  // first to arrive (or a root): stop
-                    if (active) {
-                        s_ob[q] = -1;  // reset-on-consume
-                        const int32_t bound = other & 0xffff;
-                        const uint32_t lv = (uint32_t)other >> 16;
-                        lo = right ? bound : lo;
-                        hi = right ? hi : bound;
-                        lamL = right ? lv : lamL;
-                        lamR = right ? lamR : lv;
-                        node = (int32_t)(j0 + parent);
-                    }
-                }
-            }
-        }
-        __syncthreads();
-
-        RTF_TICK(5);
-        // (4) the spines of the tile (TileSpine).  Every spine gap except the
-        // tile's maximum got exactly one arrival here that found no sibling:
-        // from its right (bound >= slot) on the left spine, from its left on
-        // the right spine -- so the leftover deposits name them.  The walls
-        // (first / last cell boundary) and, in a tile without walls, the
-        // maximum complete the two spines.
-        {
-            auto add = [&](bool left, uint32_t lv, uint32_t gap) {
-                if (left) {
-                    s_iL[lv] = (uint16_t)gap;
-                    atomicOr(&s_mL, 1ull << lv);
-                } else {
-                    s_iR[lv] = (uint16_t)gap;
-                    atomicOr(&s_mR, 1ull << lv);
-                }
-            };
-            auto leftover = [&](uint32_t e, int32_t o) {
-                if (o < 0) return;
-                const uint32_t q = e - e / 9;  // slot (gap q - 1)
-                add((uint32_t)(o & 0xffff) >= q, s_lam[pad8(q - 1)], q - 1);
-            };
-            const int4* ob4 = reinterpret_cast<const int4*>(s_ob);
-            const uint32_t n4 = cnt ? pad8(cnt) / 4 + 1 : 0u;
-            for (uint32_t u = tid; u < n4; u += THREADS) {
-                const int4 v = ob4[u];
-                if ((v.x & v.y & v.z & v.w) < 0) continue;  // four empty slots
-                leftover(4 * u, v.x);
-                leftover(4 * u + 1, v.y);
-                leftover(4 * u + 2, v.z);
-                leftover(4 * u + 3, v.w);
-            }
-            if (tid == THREADS - 33 && cnt) {  // another warp than the issuer's
-                if (s_fw != 0xffffffffu) {
-                    s_iL[64] = (uint16_t)s_fw;
-                    s_iR[64] = (uint16_t)s_lw;
-                    s_walls = 3u;
-                } else {  // no wall: the maximum heads both spines
-                    const uint32_t lv = (s_mx >> 16) - 1, gap = s_mx & 0xffffu;
-                    add(true, lv, gap);
-                    add(false, lv, gap);
-                }
-            }
-        }
-        // (5) the next tile's weights and prefix: TMA into the consumed weight
-        // buffer once every thread is done reading otherBounds; s_pin was read
-        // at step (0)
-        __syncthreads();
-        if (tid == kIssuer) {
+        if (tid == kIssuer) {  // every thread has its weights: the next tile can stream in
             const uint32_t nx = ticket;
-            s_next = nx;  // read after the barrier below
+            s_next = nx;  // read at the end of this tile
             if (tma_tile(nx)) {
                 fence_proxy_async_smem();
                 mbar_arrive_expect_tx(&s_bar, TILE * 4 + (uint32_t)sizeof(Pfx));
@@ -1006,49 +847,352 @@ __global__ void __launch_bounds__(THREADS, MINB) k_build(BuildArgs A) {
                 ticket = G + atomicAdd(&A.counters[kCtrTile], 1u);
             }
         }
-        // (6) node records, coalesced 16 B
+        uint64_t w_ex;
+        uint32_t c_ex, cnt;
         {
-            uint4* gnode = reinterpret_cast<uint4*>(A.nodes + j0);
-            for (uint32_t l = tid; l < cnt; l += THREADS) {
-                const uint32_t q = pad8(l);
-                const uint64_t key = s_key[q];
-                const uint4 rec = make_uint4((uint32_t)key, (uint32_t)(key >> 32),
-                                             (uint32_t)s_c0[q], (uint32_t)s_c1[q]);
-                if (FUSED)  // fused: to the rank owning the record's cell (peer memory)
-                    reinterpret_cast<uint4*>(A.peer_nodes[cell_fn(key) / A.cpo] + j0)[l] = rec;
-                else
-                    gnode[l] = rec;
+            uint64_t ww = lane < NW ? s_w[lane] : 0ull;
+            uint32_t cc = lane < NW ? s_c[lane] : 0u;
+#pragma unroll
+            for (int d = 1; d < NW; d <<= 1) {
+                const uint64_t tw2 = shfl_up_u64(ww, d);
+                const uint32_t tc2 = __shfl_up_sync(0xffffffffu, cc, d);
+                if (lane >= d) {
+                    ww += tw2;
+                    cc += tc2;
+                }
+            }
+            const uint64_t wb = __shfl_sync(0xffffffffu, ww, warp ? warp - 1 : 0);
+            const uint32_t cb = __shfl_sync(0xffffffffu, cc, warp ? warp - 1 : 0);
+            cnt = __shfl_sync(0xffffffffu, cc, NW - 1);
+            w_ex = (warp ? wb : 0ull) + wi - tw;
+            c_ex = (warp ? cb : 0u) + ci - tc;
+        }
+        const uint32_t j0 = pre.cnt;      // global index of the tile's first leaf
+        const uint32_t sh = j0 & 63u;     // record l is staged at stage_pos(l + sh)
+        // the previous positive entry (the first own leaf's left neighbour)
+        int32_t prevo = -1;
+        if (tc) {
+            int32_t u = (int32_t)tid - 1;
+            while (u >= 0 && s_clast[u] < 0) --u;
+            prevo = u >= 0 ? (int32_t)(t * TILE + (uint32_t)u * VPT) + s_clast[u] + ib
+                           : (j0 ? pre.last : -1);
+        }
+
+        // (2) one exact division per positive entry: w[k] holds key_j from here on;
+        // kn = the key of the first leaf after this thread's entries ("1" at the end)
+        uint64_t kn = kOne63;
+        {
+            uint64_t W = pre.W + w_ex;
+#pragma unroll
+            for (int k = 0; k < VPT; ++k) {
+                const uint64_t wk = w[k];
+                if (wk) w[k] = fixed_point(W, nm);
+                W += wk;
+            }
+            if (tc && W != T) kn = fixed_point(W, nm);
+        }
+
+        // (3) own gaps, last to first: split level lambda (byte r of lampack =
+        // gap c_ex + r, between leaves c_ex + r and c_ex + r + 1); at a cell
+        // boundary the guide-table entries the leaf owes: the
+        // next cell's anchor -- or, when the next leaf is alone in its cell,
+        // the two-interval entry (reading R18) -- and the empty cells between
+        uint64_t lampack = 0;
+        uint32_t lmax = 0;   // largest own split level
+        uint64_t key_f = 0;  // the first own leaf: key, original index
+        int32_t orig_f = 0;
+        if (tc) {
+            if (j0 == 0 && c_ex == 0) st_cell(table_at(0), 0, 0u, 0);  // leaf 0 (key 0) anchors cell 0
+            uint64_t nxt = kn;
+            uint32_t cn = POW2 ? (uint32_t)(kn >> A.mshift) : (kn == kOne63 ? m : cell_of(kn, m));
+            uint32_t lam_nx = 0xffu;  // split level after the next leaf (0xff: another thread's)
+            int32_t orig_nx = 0;
+            uint32_t r = tc;
+#pragma unroll
+            for (int k = VPT - 1; k >= 0; --k) {
+                if ((posmask >> k) & 1u) {
+                    --r;
+                    const uint64_t key = w[k];
+                    const int32_t i = (int32_t)(first + k) + ib;
+                    uint32_t cell, lam;
+                    if (POW2) {  // a cell boundary lies between iff the keys differ at or
+                                 // above bit mshift (kn = 2^63 "1" differs at bit 63)
+                        const uint32_t d = split_level(key, nxt);
+                        lam = d >= A.mshift ? kLamBoundary : d;
+                        cell = (uint32_t)(key >> A.mshift);
+                    } else {
+                        cell = cell_of(key, m);
+                        lam = (cn != cell) ? kLamBoundary : split_level(key, nxt);
+                    }
+                    lampack = (lampack << 8) | lam;
+                    lmax = max(lmax, lam);
+                    if (lam == kLamBoundary) {
+                        const int32_t anchor = (int32_t)(j0 + c_ex + r + 1u);
+                        if (cn < m) {
+                            uint2 e = make_uint2(0u, (uint32_t)anchor);
+                            if (lam_nx == kLamBoundary)  // the next leaf is alone in cell cn
+                                e = single_leaf_cell(nxt, orig_nx, i, anchor);
+                            st_cell(table_at(cn), cn, e.x, (int32_t)e.y);
+                        }
+                        if (FUSED)  // the first leaf of every owner boundary k cpo in (cell, cn]
+                            for (uint32_t q = cell / A.cpo + 1; q <= min(A.npeer, cn / A.cpo); ++q)
+                                A.jbound[q] = (uint32_t)anchor;
+                        const uint32_t len = cn - cell - 1;
+                        if (len <= kShortRun) {
+                            for (uint32_t g = cell + 1; g < cn; ++g) st_cell(table_at(g), g, 0u, ~i);
+                        } else {
+                            table_queue(A.counters, A.queue, A.qcap, i, cell, len);
+                        }
+                    }
+                    lam_nx = lam;
+                    orig_nx = i;
+                    nxt = key;
+                    cn = cell;
+                }
+            }
+            key_f = nxt;
+            orig_f = orig_nx;
+            if (c_ex == 0) s_ref0 = ~orig_f;  // the tile's first leaf: linked in phase E
+        }
+        const uint32_t lo32 = (uint32_t)lampack, hi32 = (uint32_t)(lampack >> 32);
+
+        // (4) the staged records {key_j, ~orig(j-1), ~orig(j)}: the left child
+        // of an anchor (Fig. 6 caption P:1276-1277) or of an internal node whose
+        // left child is the leaf j-1, the right child of a node whose right
+        // child is the leaf j.  Every other child is an internal node and is
+        // linked over it in (6).
+        {
+            int32_t po = prevo;
+            uint32_t l = c_ex + sh;
+#pragma unroll
+            for (int k = 0; k < VPT; ++k) {
+                if ((posmask >> k) & 1u) {
+                    const int32_t i = (int32_t)(first + k) + ib;
+                    const uint64_t key = w[k];
+                    sts_v4(a_stage + 16u * stage_pos(l),
+                           make_uint4((uint32_t)key, (uint32_t)(key >> 32),
+                                      (uint32_t)~(po >= 0 ? po : i), (uint32_t)~i));
+                    po = i;
+                    ++l;
+                }
             }
         }
-        __syncthreads();  // spines complete; keys and children are free
+
+        // (5) this thread's summary (its packed split levels, first leaf, 1 +
+        // its largest level) and the warp's level tables s_B[v] = the lanes
+        // whose largest level exceeds v; the tile's first and last wall
+        const uint32_t encmax = tc ? lmax + 1u : 0u;
+        s_clp[tid] = lampack;
+        s_ccex[tid] = c_ex;
+        s_cmax[tid] = (uint8_t)encmax;
+        {
+            const uint32_t wm = __reduce_max_sync(0xffffffffu, encmax);
+            if (lane == 0) s_wmax[warp] = wm;
+            if (lmax == kLamBoundary && tc) {
+                uint32_t glo, ghi;
+                above(lo32, hi32, kLamBoundary - 1u, glo, ghi);  // the walls
+                atomicMin(&s_fw, c_ex + byte_first(glo, ghi));
+                atomicMax(&s_lw, c_ex + byte_last(glo, ghi));
+            }
+            __syncwarp();
+            // lane L: the tables of levels L and L + 32 from the warp's 32 maxima
+            const uint4 m0 = *reinterpret_cast<const uint4*>(s_cmax + (warp << 5));
+            const uint4 m1 = *reinterpret_cast<const uint4*>(s_cmax + (warp << 5) + 16);
+            const uint32_t mw[8] = {m0.x, m0.y, m0.z, m0.w, m1.x, m1.y, m1.z, m1.w};
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                const uint32_t v = (uint32_t)lane + 32u * h;  // encodings > v + 1
+                const uint32_t c = __byte_perm(126u - v, 0u, 0u);
+                uint32_t bits = 0;
+#pragma unroll
+                for (int q = 0; q < 8; ++q)
+                    bits |= ((((mw[q] + c) & 0x80808080u) * 0x00204081u) >> 28) << (4 * q);
+                s_B[warp * 64 + v] = bits;
+            }
+        }
+        __syncthreads();
+        RTF_TICK(4);
+
+        // (6) the forest.  A gap's node hangs under the nearer-in-level of its
+        // nearest greater split levels on either side (Alg. 1's merge order,
+        // P:1101-1113; equal levels only between walls: the right child of the
+        // left wall's anchor) -- as the right child of the left one or the
+        // left child of the right one.  Found inside the thread's 8 gaps by
+        // byte arithmetic, otherwise from the other threads' summaries; a gap
+        // whose nearest greater level lies outside the tile is a spine gap of
+        // the tile (phase E).
+        // The first own leaf may close a one-leaf cell whose left wall is the
+        // previous thread's last gap (the two-interval entry, reading R18).
+        if (tc && c_ex > 0 && (lo32 & 0xffu) == kLamBoundary) {
+            int32_t u = (int32_t)tid - 1;
+            while (s_cmax[u] == 0) --u;  // c_ex > 0: some earlier thread has a leaf
+            const unsigned long long lpu = s_clp[u];
+            const uint32_t lastu = s_ccex[tid] - s_ccex[u] - 1u;  // its last gap
+            if (lam_at((uint32_t)lpu, (uint32_t)(lpu >> 32), lastu) == kLamBoundary) {
+                const int32_t a = (int32_t)(j0 + c_ex);
+                const uint2 e = single_leaf_cell(key_f, orig_f, prevo, a);
+                if ((int32_t)e.y != a) st_cell(table_at(cell_fn(key_f)), cell_fn(key_f), e.x, (int32_t)e.y);
+            }
+        }
+        {
+            // gap g's node under its parent: the right child of the left
+            // neighbour gl (slot gl + 1) if vl <= vr, else the left child of gr
+            auto link = [&](uint32_t g, uint32_t gl, uint32_t vl, uint32_t gr, uint32_t vr) {
+                const uint32_t node = j0 + g + 1u;
+                const bool right = vl <= vr;
+                const uint32_t slot = (right ? gl : gr) + 1u;
+                if (!right && slot == cnt) {  // left child of the tile's last gap (slot j0 + cnt)
+                    s_c0next = (int32_t)node;
+                } else {
+                    sts_u32(a_stage + 16u * stage_pos(slot + sh) + (right ? 12u : 8u), node);
+                }
+            };
+            // (a) both nearest greater levels inside the thread: link now; the
+            // others (about half) become tasks (thread << 5 | r << 2 | needs)
+            uint32_t ntask = 0, tasks[VPT];
+#pragma unroll
+            for (int r = 0; r < VPT; ++r) {
+                const uint32_t v = lam_at(lo32, hi32, (uint32_t)r);
+                tasks[r] = 0;
+                if ((uint32_t)r < tc && v < kLamBoundary) {
+                    uint32_t glo, ghi;
+                    above(lo32, hi32, v, glo, ghi);
+                    const int ngl = byte_below(glo, ghi, (uint32_t)r);
+                    const int ngr = byte_above(glo, ghi, (uint32_t)r);
+                    if (ngl >= 0 && ngr >= 0) {
+                        link(c_ex + r, c_ex + (uint32_t)ngl, lam_at(lo32, hi32, (uint32_t)ngl),
+                             c_ex + (uint32_t)ngr, lam_at(lo32, hi32, (uint32_t)ngr));
+                    } else {
+                        tasks[r] = tid << 5 | (uint32_t)r << 2 | (ngl < 0 ? 1u : 0u) | (ngr < 0 ? 2u : 0u);
+                        ++ntask;
+                    }
+                }
+            }
+            // (b) the tasks, compacted per warp so that every lane searches
+            uint32_t incl = ntask;
+#pragma unroll
+            for (int d = 1; d < 32; d <<= 1) {
+                const uint32_t t2 = __shfl_up_sync(0xffffffffu, incl, d);
+                if (lane >= d) incl += t2;
+            }
+            const uint32_t total = __shfl_sync(0xffffffffu, incl, 31);
+            uint16_t* q = s_task + warp * 256;
+            uint32_t qi = incl - ntask;
+#pragma unroll
+            for (int r = 0; r < VPT; ++r)
+                if (tasks[r]) q[qi++] = (uint16_t)tasks[r];
+            __syncwarp();
+            for (uint32_t k = lane; k < total; k += 32) {
+                const uint32_t task = q[k], o = task >> 5, r = (task >> 2) & 7u;
+                const unsigned long long lp = s_clp[o];
+                const uint32_t lo = (uint32_t)lp, hi = (uint32_t)(lp >> 32), ce = s_ccex[o];
+                const uint32_t v = lam_at(lo, hi, r), g = ce + r;
+                uint32_t glo, ghi;
+                above(lo, hi, v, glo, ghi);
+                uint32_t gl = 0, vl = 0, gr = 0, vr = 0;
+                bool hl = true, hr = true;
+                if (task & 1u) {
+                    hl = search_left(o, v, gl, vl);
+                } else {
+                    const uint32_t nl = (uint32_t)byte_below(glo, ghi, r);
+                    gl = ce + nl;
+                    vl = lam_at(lo, hi, nl);
+                }
+                if (task & 2u) {
+                    hr = search_right(o, v, gr, vr);
+                } else {
+                    const uint32_t nr = (uint32_t)byte_above(glo, ghi, r);
+                    gr = ce + nr;
+                    vr = lam_at(lo, hi, nr);
+                }
+                if (hl && hr) {
+                    link(g, gl, vl, gr, vr);
+                } else {  // a spine gap of the tile: phase E links it
+                    if (!hl) {
+                        s_iL[v] = (uint16_t)g;
+                        atomicOr(&s_mL, 1ull << v);
+                    }
+                    if (!hr) {
+                        s_iR[v] = (uint16_t)g;
+                        atomicOr(&s_mR, 1ull << v);
+                    }
+                }
+            }
+        }
+        fence_proxy_async_smem();  // the staged records are read by the TMA store below
+        __syncthreads();
+        RTF_TICK(5);
+
+        // (7) records out: whole 64-record blocks (1024-B aligned in the stage)
+        // by TMA tensor stores, the unaligned head and tail by the threads
+        {
+            const uint32_t e1 = j0 + cnt;
+            uint32_t a0 = (j0 + 63u) & ~63u, a1 = e1 & ~63u;
+            if (!A.tma_store || FUSED || a1 <= a0) a0 = a1 = e1;  // every record by the threads
+            if (tid == kIssuer && a1 > a0) {
+                const uint32_t base = j0 & ~63u;
+                for (uint32_t a = a0; a < a1;) {
+                    const unsigned char* src = s_stage + 16u * (a - base);
+                    if (a1 - a >= 256u) {
+                        tma_store_2d(&tm_big, 0, (int)(a >> 3), src);
+                        a += 256u;
+                    } else {
+                        tma_store_2d(&tm_small, 0, (int)(a >> 3), src);
+                        a += 64u;
+                    }
+                }
+                bulk_commit();
+                store_pending = true;
+            }
+            const uint32_t nhead = a0 - j0, ntot = nhead + (e1 - a1);
+            for (uint32_t q = tid; q < ntot; q += THREADS) {
+                const uint32_t l = q < nhead ? q : a1 - j0 + (q - nhead);
+                const uint4 rec = lds_v4(a_stage + 16u * stage_pos(l + sh));
+                if (FUSED) {  // to the rank owning the record's cell (peer memory)
+                    const uint64_t key = (uint64_t)rec.x | ((uint64_t)rec.y << 32);
+                    reinterpret_cast<uint4*>(A.peer_nodes[cell_fn(key) / A.cpo] + j0)[l] = rec;
+                } else {
+                    reinterpret_cast<uint4*>(A.nodes + j0)[l] = rec;
+                }
+            }
+        }
+        // (8) the tile's spine row for phase E
         {
             TileSpine* row = A.spine + t;
-            for (uint32_t u = tid; u < 65; u += THREADS) {
+            for (uint32_t u = tid; u < 64; u += THREADS) {
                 row->iL[u] = s_iL[u];
                 row->iR[u] = s_iR[u];
             }
             if (tid == 0) {
+                const uint32_t walls = s_fw != 0xffffffffu ? 3u : 0u;
                 row->mL = s_mL;
                 row->mR = s_mR;
                 row->j0 = j0;
                 row->cnt = cnt;
-                row->walls = s_walls;
-                row->c0_next = cnt ? s_c0[pad8(cnt)] : kNoLink;
+                row->walls = walls;
+                row->iL[64] = walls ? (uint16_t)s_fw : (uint16_t)0;
+                row->iR[64] = walls ? (uint16_t)s_lw : (uint16_t)0;
+                row->c0_next = cnt ? s_c0next : kNoLink;
                 row->ref0 = cnt ? s_ref0 : 0;
                 // phase E's row maxima: 1 + the largest split level, 0 if empty
-                const uint32_t enc = !cnt ? 0u : s_walls ? 65u : (s_mx >> 16);
+                const uint32_t enc = !cnt ? 0u
+                                     : walls ? kLamBoundary + 1u
+                                             : 64u - (uint32_t)__clzll((long long)s_mL);
                 A.tmax[t] = (uint8_t)enc;
                 if (enc) atomicMax(&A.bmax[t >> 6], enc);
-                s_mL = s_mR = 0ull;  // the next tile's atomics follow its scan barriers
-                s_walls = 0u;
+                s_mL = s_mR = 0ull;  // the next tile's writers follow its barriers
                 s_fw = 0xffffffffu;
                 s_lw = 0u;
-                s_mx = 0u;
+                s_c0next = kNoLink;
             }
         }
-        // no barrier here: the next tile writes shared memory only after its scan
         RTF_TICK(6);
     }
+    if (tid == kIssuer && store_pending) {  // every record written before the grid barrier
+        bulk_wait0();
+        fence_proxy_async_global();
+    }
+    }  // !CDF
     if (FUSED) __threadfence_system();  // peer stores visible before the next exchange
     grid_barrier(gbar);
     RTF_TICK(7);
@@ -1185,12 +1329,22 @@ __global__ void __launch_bounds__(THREADS, MINB) k_build(BuildArgs A) {
 
 // ============================================================== host-side launch
 
+// threads per CTA of the production tile (8 entries each), CTAs per SM
+#ifndef RTF_TILE_THREADS
+#define RTF_TILE_THREADS 512
+#endif
+constexpr int kTT = RTF_TILE_THREADS;
+#ifndef RTF_TILE_MINB
+#define RTF_TILE_MINB (1024 / RTF_TILE_THREADS)
+#endif
+constexpr int kTB = RTF_TILE_MINB;
+
 struct TileCfg {
     int threads, vpt;
 };
 
 static inline TileCfg tile_cfg(uint32_t flags) {
-    return (flags & RTF_BUILD_SMALL_TILES) ? TileCfg{64, 4} : TileCfg{512, 8};
+    return (flags & RTF_BUILD_SMALL_TILES) ? TileCfg{32, 8} : TileCfg{kTT, 8};
 }
 
 uint32_t build_tile_size(uint32_t flags) {
@@ -1251,28 +1405,57 @@ size_t build_workspace_layout(uint32_t n, uint32_t m, uint32_t flags, WsLayout* 
     return off;
 }
 
-static int num_sms() {
-    static int sms = 0;
-    if (!sms) {
-        int dev = 0;
-        cudaGetDevice(&dev);
-        if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess ||
-            sms <= 0)
-            sms = 148;
-    }
+// SMs of device `dev` (queried per device: a process may drive several GPUs)
+static int num_sms(int dev) {
+    int sms = 0;
+    if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || sms <= 0)
+        sms = 148;
     return sms;
 }
 
+// the node array as rows of 8 records (128 B) for the TMA tensor stores of
+// phase D: boxes of 32 rows (256 records) and 8 rows (64 records), 128-B
+// swizzle (the stage layout, stage_pos).  false: no tensor stores.
+static bool node_tensor_maps(rtf_node* nodes, uint64_t records, CUtensorMap* big,
+                             CUtensorMap* small) {
+    static std::atomic<PFN_cuTensorMapEncodeTiled_v12000> s_enc{nullptr};
+    static std::atomic<int> s_tried{0};
+    PFN_cuTensorMapEncodeTiled_v12000 enc = s_enc.load();
+    if (!enc && !s_tried.exchange(1)) {
+        void* fn = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) ==
+                cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            s_enc.store(reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn));
+        enc = s_enc.load();
+    }
+    const uint64_t rows = records / 8;
+    if (!enc || !nodes || rows == 0 || ((uintptr_t)nodes & 15u)) return false;
+    cuuint64_t dims[2] = {32, rows};
+    cuuint64_t strides[1] = {128};
+    cuuint32_t es[2] = {1, 1};
+    cuuint32_t bb[2] = {32, 32}, bs[2] = {32, 8};
+    return enc(big, CU_TENSOR_MAP_DATA_TYPE_UINT32, 2, nodes, dims, strides, bb, es,
+               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+               CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS &&
+           enc(small, CU_TENSOR_MAP_DATA_TYPE_UINT32, 2, nodes, dims, strides, bs, es,
+               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+               CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 template <int THREADS, int VPT, bool CDF, int MINB = 2, bool POW2 = false, bool FUSED = false>
-static cudaError_t launch_fused(BuildArgs& A, cudaStream_t st, int* launches) {
+static cudaError_t launch_fused(BuildArgs& A, const CUtensorMap* tmb, const CUtensorMap* tms,
+                                cudaStream_t st, int* launches) {
     auto kern = k_build<THREADS, VPT, CDF, MINB, POW2, FUSED>;
     const size_t smem = build_smem_bytes<THREADS, VPT>();  // phase B stages tile totals there
     // per instantiation and device: co-resident CTAs (the attribute is per device)
-    static int max_grid_dev[kMaxDevices] = {};
+    // (atomic: host threads may launch on several devices concurrently)
+    static std::atomic<int> max_grid_dev[kMaxDevices] = {};
     int dev = 0;
     if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= kMaxDevices)
         return cudaErrorInvalidDevice;
-    int& max_grid = max_grid_dev[dev];
+    int max_grid = max_grid_dev[dev].load(std::memory_order_relaxed);
     if (!max_grid) {
         cudaError_t e = cudaSuccess;
         if (smem)
@@ -1282,10 +1465,11 @@ static cudaError_t launch_fused(BuildArgs& A, cudaStream_t st, int* launches) {
         e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, THREADS, smem);
         if (e != cudaSuccess) return e;
         if (per_sm < 1) return cudaErrorCooperativeLaunchTooLarge;
-        max_grid = std::min<int>(per_sm * num_sms(), (int)kMaxGrid);
+        max_grid = std::min<int>(per_sm * num_sms(dev), (int)kMaxGrid);
+        max_grid_dev[dev].store(max_grid, std::memory_order_relaxed);
     }
     const uint32_t grid = std::max<uint32_t>(1u, std::min<uint32_t>(A.nt, (uint32_t)max_grid));
-    void* args[] = {&A};
+    void* args[] = {&A, const_cast<CUtensorMap*>(tmb), const_cast<CUtensorMap*>(tms)};
     const cudaError_t e =
         cudaLaunchCooperativeKernel((const void*)kern, dim3(grid), dim3(THREADS), args, smem, st);
     ++*launches;
@@ -1338,24 +1522,29 @@ cudaError_t launch_build(const float* p, uint32_t n, uint32_t m, uint32_t flags,
     A.qcap = L.qcap;
     A.cdf = cdf;
     A.vec = ((uintptr_t)p & 15u) == 0;
+    // phase D's record stores: tensor maps over the caller's node array
+    // (sharded calls address the whole forest with global leaf indices)
+    alignas(64) CUtensorMap tmb, tms;
+    std::memset(&tmb, 0, sizeof(tmb));
+    std::memset(&tms, 0, sizeof(tms));
+    A.tma_store = !cdf && (A.phases & kPhTiles) &&
+                  node_tensor_maps(nodes, sc ? sc->n_global : n, &tmb, &tms);
     const bool small = flags & RTF_BUILD_SMALL_TILES;
     if (cdf)
-        return small ? launch_fused<64, 4, true>(A, st, launches)
-                     : launch_fused<512, 8, true>(A, st, launches);
-    // 512 x 8 at 2 CTAs/SM measured best on B200 (vs 512x8 @1, 256x16 @2,
-    // 1024x4 @1: 336 vs 399 / 352 / 403 us for config 3)
-    // (2048-entry tiles at 4 or 3 CTAs/SM and 1024-entry tiles at 8 CTAs/SM
-    // were measured again with the fused kernel: 293 / 315 / 399 us for c3)
+        return small ? launch_fused<64, 4, true>(A, &tmb, &tms, st, launches)
+                     : launch_fused<kTT, 8, true, kTB>(A, &tmb, &tms, st, launches);
+    // 512 x 8 at 2 CTAs/SM (4096-entry tiles); RTF_BUILD_SMALL_TILES: 32 x 8
+    // (256-entry tiles, most links cross tiles: a test schedule)
     const bool pow2 = (m & (m - 1)) == 0;
     A.mshift = 63u - (uint32_t)ceil_log2_u32(m);
     if (A.npeer)  // fused ranged sharding (rtf_shard_build_peers)
-        return small ? launch_fused<64, 4, false, 2, false, true>(A, st, launches)
-                     : launch_fused<512, 8, false, 2, false, true>(A, st, launches);
+        return small ? launch_fused<32, 8, false, 2, false, true>(A, &tmb, &tms, st, launches)
+                     : launch_fused<kTT, 8, false, kTB, false, true>(A, &tmb, &tms, st, launches);
     if (small)
-        return pow2 ? launch_fused<64, 4, false, 2, true>(A, st, launches)
-                    : launch_fused<64, 4, false>(A, st, launches);
-    return pow2 ? launch_fused<512, 8, false, 2, true>(A, st, launches)
-                : launch_fused<512, 8, false>(A, st, launches);
+        return pow2 ? launch_fused<32, 8, false, 2, true>(A, &tmb, &tms, st, launches)
+                    : launch_fused<32, 8, false>(A, &tmb, &tms, st, launches);
+    return pow2 ? launch_fused<kTT, 8, false, kTB, true>(A, &tmb, &tms, st, launches)
+                : launch_fused<kTT, 8, false, kTB>(A, &tmb, &tms, st, launches);
 }
 
 }  // namespace rtf

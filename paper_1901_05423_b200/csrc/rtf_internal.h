@@ -1,6 +1,7 @@
 // rtf_internal.h -- declarations shared between librtf translation units (not installed).
 #pragma once
 #include <algorithm>
+#include <atomic>
 #include <cstddef>
 #include <cstdint>
 #include <cuda_runtime.h>
@@ -24,6 +25,21 @@ enum : uint32_t {
 };
 constexpr uint32_t kBuildShardedLayout = 0x100;  // internal flag: room for all shards' rows
 constexpr uint32_t kMaxShards = 1024;
+
+// SM count of the current device, cached per device (grid-stride launchers
+// size their grids in multiples of it)
+inline int device_sms() {
+    static std::atomic<int> cache[kMaxDevices] = {};
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= kMaxDevices) return 148;
+    int s = cache[dev].load(std::memory_order_relaxed);
+    if (!s) {
+        if (cudaDeviceGetAttribute(&s, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || s <= 0)
+            s = 148;
+        cache[dev].store(s, std::memory_order_relaxed);
+    }
+    return s;
+}
 
 inline int ceil_log2_u32(uint32_t n) {
     int c = 0;

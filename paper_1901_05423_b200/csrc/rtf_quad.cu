@@ -114,7 +114,7 @@ __global__ void __launch_bounds__(kQuadThreads)
 
 static inline uint32_t quad_grid(uint64_t items) {
     const uint64_t want = (items + kQuadThreads - 1) / kQuadThreads;
-    return (uint32_t)std::max<uint64_t>(1, std::min<uint64_t>(want, 148ull * 64ull));
+    return (uint32_t)std::max<uint64_t>(1, std::min<uint64_t>(want, (uint64_t)device_sms() * 64ull));
 }
 
 cudaError_t launch_collapse4(const rtf_forest& f, void* rec4, cudaStream_t st, int* launches) {

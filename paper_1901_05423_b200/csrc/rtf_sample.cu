@@ -272,7 +272,7 @@ __global__ void k_philox(uint64_t seed, uint64_t start, uint64_t count, uint32_t
 
 static inline uint32_t grid_for(uint64_t work_items) {
     const uint64_t want = (work_items + kSampleThreads - 1) / kSampleThreads;
-    return (uint32_t)std::max<uint64_t>(1, std::min<uint64_t>(want, 148ull * 64ull));
+    return (uint32_t)std::max<uint64_t>(1, std::min<uint64_t>(want, (uint64_t)device_sms() * 64ull));
 }
 
 cudaError_t launch_sample(const rtf_forest& f, const uint32_t* row, const uint32_t* xi,

@@ -368,6 +368,10 @@ def ranged_xi(xi: torch.Tensor, rank: int, count: int, m: int) -> torch.Tensor:
     stratified split of the unit interval (input generation, not the method)."""
     if count & (count - 1):
         raise ValueError("ranged sampling needs a power-of-two shard count")
+    if m % count:
+        # the strata [g_r 2^32 / m, g_{r+1} 2^32 / m) are 2^32 / count wide only
+        # when count divides m; otherwise xi would land in another rank's cells
+        raise ValueError("ranged sampling needs m divisible by the shard count")
     lo = (rank * m // count) * (1 << 32) // m
     v = (xi.to(torch.int64) & 0xFFFFFFFF) >> (count.bit_length() - 1)
     return ((v + lo) & 0xFFFFFFFF).to(torch.int32)

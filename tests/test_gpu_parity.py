@@ -450,3 +450,24 @@ def test_maximum_size(rtf):
     assert np.array_equal(got, want)
     del f, pd
     torch.cuda.empty_cache()
+
+
+def test_host_sampling_ragged_chunk_stays_in_staging(rtf):
+    """rtf_sample_host with a chunk that is not a multiple of 4: the staging
+    buffers hold exactly 2 * chunk entries (rtf.h) and nothing past them is
+    written; indices still equal the oracle's."""
+    p = env_map(256, 128, seed=11)
+    m = p.size // 2
+    ref = oracle.build(p, m)
+    f = rtf.Forest(p.size, m).build(dev_f32(p))
+    xi = philox_xi(100_003, seed=12)
+    xi_host = torch.from_numpy(xi.view(np.int32)).pin_memory()
+    out_host = torch.empty(xi.size, dtype=torch.int32).pin_memory()
+    chunk = 1001
+    guard = 64
+    xi_big = torch.full((2 * chunk + guard,), 0x55AA55AA, dtype=torch.int32, device=DEV)
+    out_big = torch.full((2 * chunk + guard,), 0x55AA55AA, dtype=torch.int32, device=DEV)
+    rtf.sample_host(f, xi_host, out_host, xi_big[: 2 * chunk], out_big[: 2 * chunk])
+    assert np.array_equal(out_host.numpy(), ref.sample(xi))
+    assert bool((xi_big[2 * chunk:] == 0x55AA55AA).all()), "xi staging overrun"
+    assert bool((out_big[2 * chunk:] == 0x55AA55AA).all()), "out staging overrun"

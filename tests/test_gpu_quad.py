@@ -91,3 +91,20 @@ def test_quad_poisoned_and_deep(rtf):
     g = np.exp2(-np.arange(120, dtype=np.float64)).astype(np.float32)  # a deep chain
     check(rtf, g, 2, np.concatenate([philox_xi(4096, seed=2), boundary_xi(oracle.build(g, 2),
                                                                            np.random.default_rng(0), 256)]))
+
+
+def test_quad_records_invalidated_by_rebuild(rtf):
+    """After build(p1); build_quad(); build(p2) the 4-ary records describe p1:
+    sample_quad must refuse until build_quad() runs again, then match p2."""
+    p1 = power_law(1 << 14, "A")
+    p2 = env_map(128, 128, seed=4)
+    m = 1 << 12
+    f = rtf.Forest(p1.size, m).build(dev_f32(p1)).build_quad()
+    xi = dev_u32(philox_xi(1 << 14, seed=3))
+    f.build(dev_f32(p2))
+    with pytest.raises(RuntimeError):
+        f.sample_quad(xi)
+    f.build_quad()
+    assert torch.equal(f.sample_quad(xi), f.sample(xi))
+    ref = oracle.build(p2, m)
+    assert np.array_equal(f.sample(xi).cpu().numpy(), ref.sample(xi.cpu().numpy().view(np.uint32)))

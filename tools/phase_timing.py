@@ -17,8 +17,9 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 LIB = os.path.join(ROOT, "tools", "librtf_timing.so")
 SLOTS = ["A scale (+barrier)", "B totals (+barrier)", "C spine (+barrier)",
-         "D0 load+quantise+scan+keys", "D2 cells/lambda/table", "D3 Alg.1 phase 1",
-         "D4 flush", "D tail (barrier wait)", "E cross-tile + runs"]
+         "D1 wait+quantise+warp scan (+bar 1)", "D2 scan/keys/lambda/table/records (+bar 2)",
+         "D3 forest links (+bar 3)", "D4 record stores + spine row", "D tail (barrier wait)",
+         "E cross-tile + runs"]
 
 
 def build():
@@ -53,6 +54,7 @@ def run(reps, workload):
     torch.cuda.synchronize()
     print(f"{workload}: {start.elapsed_time(stop) / reps * 1e3:.1f} us per build ({reps} builds)")
     fn(buf.ctypes.data, rows, 0)
+    extra = buf[:, 9:11].astype(np.float64) / reps
     used = buf[:, :9].sum(axis=1) > 0
     per = buf[used, :9].astype(np.float64) / reps
     tot = per.sum(axis=1)
@@ -62,6 +64,9 @@ def run(reps, workload):
         col = per[:, s]
         print(f"  {name:30s} mean {col.mean():9.0f}  max {col.max():9.0f}  "
               f"{100 * col.mean() / tot.mean():5.1f} %")
+    ex = extra[used]
+    print(f"  (issuer waiting for the TMA store to read the stage: mean {ex[:, 0].mean():.0f}; "
+          f"thread 0 waiting for the weights' TMA load: mean {ex[:, 1].mean():.0f} cycles per CTA)")
 
 
 if __name__ == "__main__":
