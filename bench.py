@@ -324,10 +324,17 @@ def run_gpu(args):
     # ------------------------------------------------ roofline
     peak, peak_src = peaks()
     n_pos = forest.n_pos()
-    bytes_sample = 4 + 4 + 8 + 16 * (e_loads - 1.0)   # xi, out, table cell, visited records
+    # SURVEY.md 8(d)'s algorithmic bytes (a 4-B table reference): per sample
+    # 4 (xi) + 4 (out) + 4 (table) + 16 E[v], E[v] = node records visited after
+    # the table (e_loads counts the table load too); per build entry 4 (p) +
+    # 16 (record) + 4 m / n (table).  The implementation's own 8-B table cell
+    # and n' records are reported beside them ("implementation_bytes").
+    bytes_sample = 4 + 4 + 4 + 16 * (e_loads - 1.0)
+    bytes_sample_impl = 4 + 4 + 8 + 16 * (e_loads - 1.0)
     t_sample_launch = ts / K * 1e-3
     ach_s = S * bytes_sample / t_sample_launch / 1e9
-    bytes_build = 4 * n + 16 * n_pos + 8 * m          # read p, write records, write table
+    bytes_build = 4 * n + 16 * n + 4 * m
+    bytes_build_impl = 4 * n + 16 * n_pos + 8 * m
     t_build = tb / K * 1e-3
     ach_b = bytes_build / t_build / 1e9
 
@@ -438,19 +445,25 @@ def run_gpu(args):
                      "traffic": (round(ncu_traffic("k_sample_per_sample", wl["name"]) * S)
                                  if ncu_traffic("k_sample_per_sample", wl["name"]) else None),
                      "algorithmic_bytes_per_unit": round(bytes_sample, 3),
+                     "bytes_definition": "SURVEY.md 8(d): 4 xi + 4 out + 4 table + 16 E[v]",
+                     "implementation_bytes_per_unit": round(bytes_sample_impl, 3),
                      "unit_of_work": "sample", "peak_source": peak_src,
                      "limiter": "not HBM: scattered 8/16-B loads, one L1TEX->L2 request each; "
                                 "ncu l1tex__m_l1tex2xbar_req_cycles_active = 81% of peak "
                                 "(profiles/r01_summary.md, DESIGN.md 5.3)"},
         "roofline_build": {"kernel": "k_build (one cooperative kernel: scale, tile totals, "
-                                     "spine scan, tiles + in-tile Alg. 1, cross-tile Alg. 1)",
+                                     "spine scan, tiles + in-tile forest, cross-tile links)",
                            "bound": "hbm",
                            "achieved": round(ach_b, 2), "peak": peak, "unit": "GB/s",
                            "frac": round(ach_b / peak, 4),
                            "traffic": ncu_traffic("build", wl["name"]),
                            "algorithmic_bytes_per_launch": bytes_build,
-                           "limiter": "instruction issue (~285 thread-instructions per entry, "
-                                      "IPC 2.1; DRAM 16% of peak), profiles/r01_summary.md",
+                           "bytes_definition": "SURVEY.md 8(d): 4 p + 16 record + 4 m/n table "
+                                               "per entry",
+                           "implementation_bytes_per_launch": bytes_build_impl,
+                           "limiter": "issue latency: ~290 thread-instructions per entry at "
+                                      "IPC 2.2, 32 warps/SM, block-barrier stalls; DRAM far "
+                                      "below peak (profiles/, DESIGN.md 5.2)",
                            "peak_source": peak_src},
         "gpu_launches": launches,
         "clocks": sampler.summary(),
@@ -548,8 +561,8 @@ def c2_summary(args, dev, stream, flush, world):
         tb, ts, tbs = t.tolist()
     peak, _ = peaks()
     loads = f.sample_loads(xi[: 1 << 20]).double().mean().item()
-    bytes_b = 4 * n + 16 * f.n_pos() + 8 * m
-    bytes_s = 4 + 4 + 8 + 16 * (loads - 1.0)
+    bytes_b = 4 * n + 16 * n + 4 * m
+    bytes_s = 4 + 4 + 4 + 16 * (loads - 1.0)
     quad = quad_summary(f, xi, out, flush)
     return {"workload": wl["desc"],
             "build": {"value": round(world * n / (tb * 1e-3) / 1e9, 4), "unit": "G entries/s",
@@ -643,7 +656,7 @@ def run_gpu_c4(args):
     build_gs = n * K / (tb * 1e-3) / 1e9
     sample_gs = S * world * K / (ts * 1e-3) / 1e9
     peak, peak_src = peaks()
-    bytes_build = 4 * n + 16 * forest.n_pos() + 8 * m
+    bytes_build = 4 * n + 16 * n + 4 * m
     quad = quad_summary(forest, xi, out, flush) if world == 1 else None
     result = {
         "metric": METRIC, "value": round(build_gs, 4), "unit": "G entries/s", "n_gpus": world,
@@ -904,7 +917,7 @@ def run_gpu_c5(args):
     sample_gs = world * S * K / (ts * 1e-3) / 1e9
     peak, peak_src = peaks()
     n_pos = int(forest.headers()["n_pos"].astype(np.int64).sum())
-    bytes_build = 4 * N + 16 * n_pos + 8 * m_row * rows
+    bytes_build = 4 * N + 16 * N + 4 * m_row * rows
     ach_b = bytes_build / (tb / K * 1e-3) / 1e9
     result = {
         "metric": METRIC, "value": round(build_gs, 4), "unit": "G entries/s", "n_gpus": world,
@@ -931,6 +944,22 @@ def run_gpu_c5(args):
         print(json.dumps(result), flush=True)
 
 
+def host_cpu():
+    """The host CPU model and its logical CPU count."""
+    model = "unknown"
+    try:
+        with open("/proc/cpuinfo") as fh:
+            for line in fh:
+                if line.startswith("model name"):
+                    model = line.split(":", 1)[1].strip()
+                    break
+    except OSError:
+        pass
+    return {"model": model, "nproc": os.cpu_count(),
+            "affinity": len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity")
+            else os.cpu_count()}
+
+
 def cpu_baseline(p_host, m, xi_sample, cdf_host):
     """The CPU oracle as it stands (single thread), on a bounded sample; plus
     the OpenMP binary search (baselines/cpu_bsearch.c) on the same CDF."""
@@ -952,7 +981,7 @@ def cpu_baseline(p_host, m, xi_sample, cdf_host):
     baselines.bsearch(cdf_host, xs)
     tbs = time.perf_counter() - t0
     return {"value": round(n * reps / tb / 1e9, 6), "unit": "G entries/s", "cores": 1,
-            "kind": "oracle",
+            "kind": "oracle", "host": host_cpu(),
             "sample": f"{reps} full oracle builds of the same n={n} input; sampling "
                       f"{xi_sample.size} of the same xi",
             "sampling": {"value": round(xi_sample.size / tsm / 1e9, 6), "unit": "G samples/s"},
@@ -997,7 +1026,7 @@ def run_reference(args):
                    "note": "CPU oracle (oracle/rtf_oracle.c, serial, 1 thread): each step = one "
                            "full build of the same input + a bounded sample of 2^20 xi"},
         "cpu_baseline": {"value": round(value, 6), "unit": "G entries/s", "cores": 1,
-                         "kind": "oracle",
+                         "kind": "oracle", "host": host_cpu(),
                          "sample": f"full n={n} build per step; sampling {S_ref} xi per step",
                          "sampling": {"value": round(S_ref * args.steps / ts / 1e9, 6),
                                       "unit": "G samples/s"}},

@@ -384,12 +384,28 @@ int rtf_shard_finish_range(uint32_t n_local, uint32_t n_global, uint32_t m,
  * MAX-reduce of jbound gives every rank its slots [J_r, J_{r+1}).  After the
  * spine rows are gathered (which also orders every rank's peer stores before
  * the finish), rtf_shard_finish_range completes each rank's cells.  Blocks
- * the host until the pointer upload is done. */
+ * the host until the pointer upload is done -- unless peer_forest_bufs is
+ * NULL: then the pointers rtf_shard_set_peers stored in the workspace are
+ * used and the call only enqueues work (no host synchronisation). */
 int rtf_shard_build_peers(const float *p, uint32_t n_local, uint32_t n_global, uint32_t m,
                           uint32_t index_base, uint32_t rank, uint32_t count, const void *totals,
                           void *const *peer_forest_bufs, uint32_t npeer, void *forest_buf,
                           size_t forest_bytes, void *ws, size_t ws_bytes, void *stream,
                           rtf_forest *out);
+
+/* Set-up for repeated fused builds: stores the npeer peer forest pointers in
+ * this shard's workspace once (blocks the host until the upload is done), so
+ * that rtf_shard_build_peers(.., peer_forest_bufs = NULL, npeer, ..) needs no
+ * host round trip.  Valid until the workspace is re-initialised. */
+int rtf_shard_set_peers(void *ws, size_t ws_bytes, uint32_t n_local, uint32_t n_global,
+                        uint32_t m, void *const *peer_forest_bufs, uint32_t npeer,
+                        size_t forest_bytes, void *stream);
+/* rtf_shard_finish_range with the slot range read on the device: after the
+ * MAX-reduce of view.jbound, [J_rank, J_{rank+1}) = [jbound[rank],
+ * jbound[rank + 1]) -- no copy of J to the host between build and finish. */
+int rtf_shard_finish_own(uint32_t n_local, uint32_t n_global, uint32_t m, const void *spine_all,
+                         uint32_t nt_all, uint32_t rank, void *forest_buf, size_t forest_bytes,
+                         void *ws, size_t ws_bytes, void *stream, rtf_forest *out);
 
 /* ---------------------------------------------------------- utilities */
 

@@ -85,6 +85,8 @@ PROTOTYPES = {
     "rtf_shard_build_peers": (_I32, [_P, _U32, _U32, _U32, _U32, _U32, _U32, _P, _P, _U32, _P,
                                      _SZ, _P, _SZ, _P, _F]),
     "rtf_shard_count_cells": (_I32, [_P, _SZ, _U32, _U32, _U32, _U32, _P, _U32, _P, _P]),
+    "rtf_shard_set_peers": (_I32, [_P, _SZ, _U32, _U32, _U32, _P, _U32, _SZ, _P]),
+    "rtf_shard_finish_own": (_I32, [_U32, _U32, _U32, _P, _U32, _U32, _P, _SZ, _P, _SZ, _P, _F]),
     "rtf_launch_count": (_U64, []),
     "rtf_status_string": (ctypes.c_char_p, [_I32]),
     "rtf_version": (ctypes.c_char_p, []),

@@ -557,10 +557,35 @@ int rtf_shard_build_peers(const float* p, uint32_t n_local, uint32_t n_global, u
                           rtf_forest* out) {
     rtf::WsLayout L;
     if (!p || !totals || ((uintptr_t)p & 3u) || count == 0 || rank >= count) return RTF_EINVAL;
-    if (!peer_forest_bufs || npeer == 0 || npeer > rtf::kMaxShards || m % npeer) return RTF_EINVAL;
+    if (npeer == 0 || npeer > rtf::kMaxShards || m % npeer) return RTF_EINVAL;
     if (int s = shard_layout(ws, ws_bytes, n_local, n_global, m, &L)) return s;
     if ((uint64_t)index_base + n_local > n_global) return RTF_EINVAL;
     if (int s = rtf_forest_view(forest_buf, forest_bytes, n_global, m, 1, out)) return s;
+    unsigned char* w = static_cast<unsigned char*>(ws);
+    cudaStream_t st = as_stream(stream);
+    if (peer_forest_bufs) {  // upload now (else: rtf_shard_set_peers stored them)
+        if (int s = rtf_shard_set_peers(ws, ws_bytes, n_local, n_global, m, peer_forest_bufs,
+                                        npeer, forest_bytes, stream))
+            return s;
+    }
+    if (cudaMemsetAsync(w + L.jbound, 0, sizeof(uint32_t) * (rtf::kMaxShards + 1), st))
+        return RTF_ECUDA;
+    rtf::ShardCall sc{rtf::kPhTiles | rtf::kPhRuns, n_global, index_base, rank, count, 0,
+                      totals, nullptr};
+    sc.npeer = npeer;
+    int launches = 0;
+    cudaError_t e =
+        rtf::launch_build(p, n_local, m, rtf::kBuildShardedLayout, out->header, out->nodes,
+                          out->table, nullptr, ws, L, st, &launches, &sc);
+    return finish(e, launches);
+}
+
+int rtf_shard_set_peers(void* ws, size_t ws_bytes, uint32_t n_local, uint32_t n_global,
+                        uint32_t m, void* const* peer_forest_bufs, uint32_t npeer,
+                        size_t forest_bytes, void* stream) {
+    rtf::WsLayout L;
+    if (!peer_forest_bufs || npeer == 0 || npeer > rtf::kMaxShards || m % npeer) return RTF_EINVAL;
+    if (int s = shard_layout(ws, ws_bytes, n_local, n_global, m, &L)) return s;
     // the peers' record and table sections (every forest buffer has this layout)
     void* ptrs[2 * rtf::kMaxShards];
     for (uint32_t r = 0; r < npeer; ++r) {
@@ -573,17 +598,27 @@ int rtf_shard_build_peers(const float* p, uint32_t n_local, uint32_t n_global, u
     cudaStream_t st = as_stream(stream);
     if (cudaMemcpyAsync(w + L.peers, ptrs, sizeof(void*) * npeer, cudaMemcpyHostToDevice, st) ||
         cudaMemcpyAsync(w + L.peers + sizeof(void*) * rtf::kMaxShards, ptrs + rtf::kMaxShards,
-                        sizeof(void*) * npeer, cudaMemcpyHostToDevice, st) ||
-        cudaMemsetAsync(w + L.jbound, 0, sizeof(uint32_t) * (rtf::kMaxShards + 1), st))
+                        sizeof(void*) * npeer, cudaMemcpyHostToDevice, st))
         return RTF_ECUDA;
-    cudaStreamSynchronize(st);  // the host pointer array is a stack buffer
-    rtf::ShardCall sc{rtf::kPhTiles | rtf::kPhRuns, n_global, index_base, rank, count, 0,
-                      totals, nullptr};
-    sc.npeer = npeer;
+    // the host pointer array is a stack buffer: wait for the copies
+    return cudaStreamSynchronize(st) == cudaSuccess ? RTF_OK : RTF_ECUDA;
+}
+
+int rtf_shard_finish_own(uint32_t n_local, uint32_t n_global, uint32_t m, const void* spine_all,
+                         uint32_t nt_all, uint32_t rank, void* forest_buf, size_t forest_bytes,
+                         void* ws, size_t ws_bytes, void* stream, rtf_forest* out) {
+    rtf::WsLayout L;
+    if (!spine_all || ((uintptr_t)spine_all & 15u) || rank >= rtf::kMaxShards) return RTF_EINVAL;
+    if (int s = shard_layout(ws, ws_bytes, n_local, n_global, m, &L)) return s;
+    if (nt_all > L.nt_cap) return RTF_EINVAL;
+    if (int s = rtf_forest_view(forest_buf, forest_bytes, n_global, m, 1, out)) return s;
+    rtf::ShardCall sc{rtf::kPhCross, n_global, 0, 0, 1, nt_all, nullptr, spine_all};
+    sc.j_rank = (int32_t)rank;
     int launches = 0;
+    const float* dummy = reinterpret_cast<const float*>(ws);  // phases A-D do not run
     cudaError_t e =
-        rtf::launch_build(p, n_local, m, rtf::kBuildShardedLayout, out->header, out->nodes,
-                          out->table, nullptr, ws, L, st, &launches, &sc);
+        rtf::launch_build(dummy, n_local, m, rtf::kBuildShardedLayout, out->header, out->nodes,
+                          out->table, nullptr, ws, L, as_stream(stream), &launches, &sc);
     return finish(e, launches);
 }
 

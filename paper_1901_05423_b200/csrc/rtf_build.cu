@@ -91,6 +91,7 @@ struct BuildArgs {
     uint32_t epoch;     // this launch's number: CTA 0 publishes rpre with it
     uint32_t mshift;    // m a power of two: cell = key >> mshift (63 - log2 m)
     uint32_t j_lo, j_hi;  // phase E writes only node slots in [j_lo, j_hi) (a ranged finish)
+    int32_t j_rank;       // >= 0: [j_lo, j_hi) = [jbound[j_rank], jbound[j_rank + 1]) (device)
     // fused ranged sharding: records and table cells are stored straight into
     // the buffer of the rank owning their cell (cells [r cpo, (r + 1) cpo)),
     // over NVLink peer memory; jbound[k] receives the first leaf of cell k cpo
@@ -1229,7 +1230,9 @@ __global__ void __launch_bounds__(THREADS, MINB)
         if (gathered) grid_barrier(gbar);
         // a ranged finish (sharded.py, ranged=True) holds only the records of
         // its cell range [j_lo, j_hi): the other links are other ranks'
-        auto local = [&](uint32_t slot) { return slot >= A.j_lo && slot < A.j_hi; };
+        const uint32_t jlo = A.j_rank >= 0 ? __ldcg(&A.jbound[A.j_rank]) : A.j_lo;
+        const uint32_t jhi = A.j_rank >= 0 ? __ldcg(&A.jbound[A.j_rank + 1]) : A.j_hi;
+        auto local = [&](uint32_t slot) { return slot >= jlo && slot < jhi; };
         // E1: one warp per row; lane e links entry e
         auto far_left = [&](uint32_t t, uint32_t v, uint32_t& lam, int32_t& gap) {
             const int32_t u = row_left(A.tmax, A.bmax, t, v + 1);
@@ -1491,6 +1494,7 @@ cudaError_t launch_build(const float* p, uint32_t n, uint32_t m, uint32_t flags,
     A.index_base = sc ? sc->index_base : 0;
     A.j_lo = sc ? sc->j_lo : 0u;
     A.j_hi = sc ? sc->j_hi : 0xffffffffu;
+    A.j_rank = sc ? sc->j_rank : -1;
     A.npeer = sc ? sc->npeer : 0u;
     A.cpo = A.npeer ? m / A.npeer : 0u;
     A.peer_nodes = A.npeer ? reinterpret_cast<rtf_node* const*>(w + L.peers) : nullptr;

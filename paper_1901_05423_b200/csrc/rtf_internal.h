@@ -62,6 +62,7 @@ struct ShardCall {
     const void* spine_in;      // device: finish -- all shards' tile spines (nt_in rows)
     uint32_t j_lo = 0, j_hi = 0xffffffffu;  // finish: node slots this rank holds
     uint32_t npeer = 0;  // fused ranged build: peer pointers already in the workspace
+    int32_t j_rank = -1;  // >= 0: finish reads [j_lo, j_hi) = jbound[j_rank .. j_rank + 1]
 };
 
 // leaves of nodes[j0, j0 + cnt) whose cell is below bound[k]: counts[k], k < nb

@@ -88,40 +88,80 @@ def _local_peers(shards):
 
 
 class DistComm:
-    """One shard per process (torch.distributed); lists hold the local tensor."""
+    """One shard per process (torch.distributed); lists hold the local tensor.
+
+    NCCL (one process per GPU): device tensors go straight into the
+    collectives, and the fused build's peer pointers come from CUDA symmetric
+    memory (NVLink).  gloo (CPU tests, or several processes sharing one GPU in
+    the single-GPU multi-process tests): device tensors are staged through host
+    memory, and peer pointers are CUDA IPC mappings of the other processes'
+    forest buffers (valid when the processes share the device)."""
 
     def __init__(self, group=None):
         import torch.distributed as dist
         self.dist = dist
         self.group = group
+        self.host = dist.get_backend(group) == "gloo"
+        self._ipc_keep = []  # opened IPC storages stay mapped while the comm lives
+
+    def _run(self, t, fn):
+        """fn(tensor) on t, or on a host copy of it (gloo), written back."""
+        if self.host and t.is_cuda:
+            h = t.cpu()
+            fn(h)
+            t.copy_(h)
+        else:
+            fn(t)
 
     def allreduce_max(self, ts):
-        self.dist.all_reduce(ts[0], op=self.dist.ReduceOp.MAX, group=self.group)
+        self._run(ts[0], lambda t: self.dist.all_reduce(t, op=self.dist.ReduceOp.MAX,
+                                                        group=self.group))
 
     def allgather(self, ts):
         t = ts[0].reshape(-1).contiguous()
         world = self.dist.get_world_size(self.group)
-        if t.is_cuda:  # NCCL: one fused all-gather
+        if t.is_cuda and not self.host:  # NCCL: one fused all-gather
             out = torch.empty(world * t.numel(), dtype=t.dtype, device=t.device)
             self.dist.all_gather_into_tensor(out, t, group=self.group)
             return [out]
-        parts = [torch.empty_like(t) for _ in range(world)]  # gloo
-        self.dist.all_gather(parts, t, group=self.group)
-        return [torch.cat(parts)]
+        src = t.cpu() if t.is_cuda else t
+        parts = [torch.empty_like(src) for _ in range(world)]  # gloo
+        self.dist.all_gather(parts, src, group=self.group)
+        return [torch.cat(parts).to(t.device)]
 
     def broadcast(self, ts, src):
-        self.dist.broadcast(ts[0], src=src, group=self.group)
+        self._run(ts[0], lambda t: self.dist.broadcast(t, src=src, group=self.group))
 
     def allreduce_sum(self, ts):
-        self.dist.all_reduce(ts[0], op=self.dist.ReduceOp.SUM, group=self.group)
+        self._run(ts[0], lambda t: self.dist.all_reduce(t, op=self.dist.ReduceOp.SUM,
+                                                        group=self.group))
 
     # fused ranged sharding: forest buffers in CUDA symmetric memory, so every
     # rank's kernels can store into every peer's buffer over NVLink
     def alloc(self, nbytes, device):
+        if self.host:
+            return torch.empty(nbytes, dtype=torch.uint8, device=device)
         import torch.distributed._symmetric_memory as symm_mem
         return symm_mem.empty(nbytes, dtype=torch.uint8, device=device)
 
     def peer_ptrs(self, buf):
+        if self.host:  # processes sharing one device: CUDA IPC handles
+            st = buf.untyped_storage()
+            handle = st._share_cuda_()
+            off = buf.data_ptr() - st.data_ptr()
+            world = self.dist.get_world_size(self.group)
+            allh = [None] * world
+            self.dist.all_gather_object(allh, (handle, off), group=self.group)
+            me = self.dist.get_rank(self.group)
+            ptrs = []
+            for r, (h, o) in enumerate(allh):
+                if r == me:
+                    ptrs.append(buf.data_ptr())
+                    continue
+                peer = torch.UntypedStorage._new_shared_cuda(*h)
+                self._ipc_keep.append(peer)
+                ptrs.append(peer.data_ptr() + o)
+            return ptrs
         import torch.distributed._symmetric_memory as symm_mem
         group = self.group if self.group is not None else self.dist.group.WORLD
         hdl = symm_mem.rendezvous(buf, group)
@@ -129,8 +169,26 @@ class DistComm:
 
     def alltoallv(self, sends, recvs):
         """Grouped point-to-point transfers of the local pieces (sends[0][r] to
-        rank r, recvs[0][q] from rank q) straight between their final places."""
+        rank r, recvs[0][q] from rank q) straight between their final places
+        (gloo: through host copies)."""
         me = self.dist.get_rank(self.group)
+        if self.host:
+            hs = [None if t is None else t.cpu() for t in sends[0]]
+            hr = [None if t is None else torch.empty(t.shape, dtype=t.dtype) for t in recvs[0]]
+            ops = []
+            for r, t in enumerate(hs):
+                if r != me and t is not None and t.numel():
+                    ops.append(self.dist.P2POp(self.dist.isend, t, r, group=self.group))
+            for q, t in enumerate(hr):
+                if q != me and t is not None and t.numel():
+                    ops.append(self.dist.P2POp(self.dist.irecv, t, q, group=self.group))
+            if ops:
+                for w in self.dist.batch_isend_irecv(ops):
+                    w.wait()
+            for q, t in enumerate(hr):
+                if q != me and t is not None and t.numel():
+                    recvs[0][q].copy_(t)
+            return
         ops = []
         for r, t in enumerate(sends[0]):
             if r != me and t is not None and t.numel():
@@ -146,6 +204,9 @@ class DistComm:
         me = self.dist.get_rank(self.group)
         t = full[0]
         equal = len(set(int(h) - int(l) for l, h in zip(lo, hi))) == 1 and int(lo[0]) == 0
+        if self.host:  # gloo (no reduce-scatter): the all-reduce covers the slice
+            self.allreduce_max([t])
+            return
         if t.is_cuda and equal and int(hi[-1]) == t.numel():  # NCCL: one reduce-scatter
             out = torch.empty(int(hi[me]) - int(lo[me]), dtype=t.dtype, device=t.device)
             self.dist.reduce_scatter_tensor(out, t, op=self.dist.ReduceOp.MAX, group=self.group)
@@ -277,11 +338,7 @@ def build_sharded(shards: list[Shard], comm, ranged: bool = False, fused: bool =
         if cnt:
             comm.broadcast([s.node_bytes(j0, cnt) for s in shards], src=r)
     comm.allreduce_max([s.table_words() for s in shards])
-    nt_max = max(s.view.nt_local for s in shards)
-    if hasattr(comm, "dist"):  # shards of other processes may have more tiles
-        t = torch.tensor([nt_max], dtype=torch.int64, device=sh0.p.device)
-        comm.allreduce_max([t])
-        nt_max = int(t.item())
+    nt_max = _nt_max(shards, comm)
     row = sh0.view.spine_row_bytes
     spine_all = comm.allgather([_padded(s.spine_bytes(), row * nt_max, 0) for s in shards])
     # 5. cross-tile links over all shards' spine rows, on every shard
@@ -344,11 +401,7 @@ def _redistribute_and_finish(shards, comm, starts, counts, st) -> None:
     comm.alltoallv(sends, recvs)
     # table: each rank's cell slice, MAX over the shards' partial tables
     comm.reduce_scatter_max([s.table_words() for s in shards], g[:-1], g[1:])
-    nt_max = max(s.view.nt_local for s in shards)
-    if hasattr(comm, "dist"):
-        t = torch.tensor([nt_max], dtype=torch.int64, device=dev)
-        comm.allreduce_max([t])
-        nt_max = int(t.item())
+    nt_max = _nt_max(shards, comm)
     row = sh0.view.spine_row_bytes
     spine_all = comm.allgather([_padded(s.spine_bytes(), row * nt_max, 0) for s in shards])
     args = lambda s: (s.n_local, s.n_global, s.m)  # noqa: E731
@@ -377,38 +430,65 @@ def ranged_xi(xi: torch.Tensor, rank: int, count: int, m: int) -> torch.Tensor:
     return ((v + lo) & 0xFFFFFFFF).to(torch.int32)
 
 
+def _nt_max(shards, comm) -> int:
+    """The most tile rows any shard has (the spine gather pads to it); fixed by
+    the shard sizes, so computed once and cached on the shards."""
+    sh0 = shards[0]
+    if getattr(sh0, "_nt_max", None) is None:
+        nt_max = max(s.view.nt_local for s in shards)
+        if hasattr(comm, "dist"):  # shards of other processes may have more tiles
+            t = torch.tensor([nt_max], dtype=torch.int64, device=sh0.p.device)
+            comm.allreduce_max([t])
+            nt_max = int(t.item())
+        for s in shards:
+            s._nt_max = nt_max
+    return sh0._nt_max
+
+
 def _build_fused(shards, comm, totals, st) -> None:
     """Fused ranged build: step 3 writes each record / table cell into the
     buffer of the rank owning its cell; then the boundaries J and the spine
-    rows are exchanged and each rank finishes its own cells."""
+    rows are exchanged and each rank finishes its own cells.  The peer
+    pointers are uploaded once (rtf_shard_set_peers) and J stays on the device
+    (rtf_shard_finish_own), so repeated builds enqueue work without any host
+    round trip (s.slots is read back lazily, after the build)."""
     L = _lib.load()
     sh0 = shards[0]
-    N, m, dev = sh0.count, sh0.m, sh0.p.device
+    N, m = sh0.count, sh0.m
     if m % N:
         raise ValueError("fused ranged sharding needs m divisible by the shard count")
     args = lambda s: (s.n_local, s.n_global, s.m)  # noqa: E731
     for s, tot in zip(shards, totals):
-        peers = _local_peers(shards) if isinstance(comm, LocalComm) else comm.peer_ptrs(s.forest)
-        arr = (ctypes.c_void_p * N)(*peers)
+        if not getattr(s, "_peers_set", False):
+            peers = _local_peers(shards) if isinstance(comm, LocalComm) else comm.peer_ptrs(s.forest)
+            arr = (ctypes.c_void_p * N)(*peers)
+            check(L.rtf_shard_set_peers(_ptr(s.ws), s.ws.numel(), *args(s), arr, N,
+                                        s.forest.numel(), st), "shard peers")
+            s._peers_set = True
         check(L.rtf_shard_build_peers(_ptr(s.p), *args(s), s.base, s.rank, s.count, _ptr(tot),
-                                      arr, N, _ptr(s.forest), s.forest.numel(), _ptr(s.ws),
+                                      None, N, _ptr(s.forest), s.forest.numel(), _ptr(s.ws),
                                       s.ws.numel(), st, ctypes.byref(s.fview)),
               "shard build (fused)")
     jb = [s._ws_slice(s.view.jbound, 4 * (N + 1)).view(torch.int32) for s in shards]
     comm.allreduce_max(jb)
-    J = jb[0].cpu().numpy().astype(np.int64)
-    nt_max = max(s.view.nt_local for s in shards)
-    if hasattr(comm, "dist"):
-        t = torch.tensor([nt_max], dtype=torch.int64, device=dev)
-        comm.allreduce_max([t])
-        nt_max = int(t.item())
+    nt_max = _nt_max(shards, comm)
     row = sh0.view.spine_row_bytes
-    spine_all = comm.allgather([_padded(s.spine_bytes(), row * nt_max, 0) for s in shards])
+    spine_all = comm.allgather([s.spine_bytes() if s.view.nt_local == nt_max
+                                else _padded(s.spine_bytes(), row * nt_max, 0) for s in shards])
     for s, sa in zip(shards, spine_all):
-        lo, hi = int(J[s.rank]), int(J[s.rank + 1])
-        check(L.rtf_shard_finish_range(*args(s), _ptr(sa), s.count * nt_max, lo, hi,
-                                       _ptr(s.forest), s.forest.numel(), _ptr(s.ws),
-                                       s.ws.numel(), st, ctypes.byref(s.fview)),
+        check(L.rtf_shard_finish_own(*args(s), _ptr(sa), s.count * nt_max, s.rank,
+                                     _ptr(s.forest), s.forest.numel(), _ptr(s.ws),
+                                     s.ws.numel(), st, ctypes.byref(s.fview)),
               "shard finish (fused)")
         s.cells = (s.rank * m // N, (s.rank + 1) * m // N)
-        s.slots = (lo, hi)
+        s._jb = jb[shards.index(s)]
+        s.slots = None  # [J_r, J_{r+1}) read back on demand: slots_of(s)
+
+
+def slots_of(s) -> tuple[int, int]:
+    """The node slots [J_r, J_{r+1}) a ranged shard holds (a host read of the
+    device boundaries after a fused build)."""
+    if s.slots is None:
+        J = s._jb.cpu().numpy().astype(np.int64)
+        s.slots = (int(J[s.rank]), int(J[s.rank + 1]))
+    return s.slots

@@ -104,7 +104,7 @@ def _check_ranged(rtf, p, m, count, fused=False):
     covered = 0
     for s in shards:
         f = rtf.Forest.from_buffer(s.n_global, m, s.forest)
-        (j0, j1), (g0, g1) = s.slots, s.cells
+        (j0, j1), (g0, g1) = sharded.slots_of(s), s.cells
         covered += j1 - j0
         allrec = f._section(f.view.nodes, 16 * ref.n_pos).cpu().numpy().view(rtf.NODE_DTYPE)
         assert allrec[j0:j1].tobytes() == nodes[j0:j1].tobytes(), f"shard {s.rank} records"
