@@ -13,8 +13,12 @@ Default workload: config 3 (power law p_i ~ ((i+1)/n)^20, n = 2^24, m = 2^22,
 `value` = forest build throughput (G entries/s, whole job); the sampling
 throughput, its binary-search baseline, roofline fractions, the CPU oracle
 baseline, end-to-end (host buffer) numbers and clocks are extra keys.
-Multi-GPU (torchrun): every rank builds and samples its own problem (weak
-scaling, no collective on the data path); times are max over ranks.
+Multi-GPU (torchrun): config 3 (default) is weak-scaled WITHOUT redundant
+work: one distribution of N x 2^24 entries built by the sharded protocol (the
+cross-GPU scan of shard totals, per-shard builds storing into the owner's
+buffer over NVLink), each rank sampling its own xi stratum; config 4 is the
+strong-scaled sharded build of one n = 2^28 distribution; the env-map and rows
+workloads run one independent problem per GPU.  Times are max over ranks.
 """
 from __future__ import annotations
 
@@ -61,7 +65,10 @@ WORKLOADS = {
 }
 
 
-def make_p(wl):
+def make_p(wl, rank=0):
+    """The workload's weights; rank r > 0 of a multi-GPU run of the env-map or
+    rows workloads gets its own independent problem (seed + r): independent
+    problems are the unit those workloads shard over (weak scaling)."""
     from workloads import env_map, power_law, spikes
     if wl["name"] == "c3_powerlaw":
         return power_law(wl["n"], "A")
@@ -69,8 +76,8 @@ def make_p(wl):
         return spikes(wl["n"])
     if wl["name"] == "c5_rows":
         from workloads import rows_lognormal
-        return rows_lognormal(wl["rows"], wl["n_row"])
-    return env_map()
+        return rows_lognormal(wl["rows"], wl["n_row"], seed=7 + rank)
+    return env_map(seed=1 + rank)
 
 
 def peaks():
@@ -112,8 +119,9 @@ class ClockSampler:
         except Exception:
             return
         for line in self._proc.stdout:
-            if line.strip():
-                self.rows.append([x.strip() for x in line.split(",")])
+            row = [x.strip() for x in line.split(",")]
+            if len(row) >= 3:  # skip error / blank lines
+                self.rows.append(row)
             if self._stop.is_set():
                 break
 
@@ -145,6 +153,25 @@ class ClockSampler:
 
 # ============================================================================ GPU arm
 
+def init_dist(world, local):
+    """Device and process group of this rank.  One process per GPU over NCCL;
+    RTF_DIST_BACKEND=gloo with RTF_ONE_DEVICE=1 runs every rank on cuda:0 (the
+    single-GPU multi-process test of the N > 1 code path: collectives staged
+    through host memory, meaningless timings)."""
+    import torch
+    import torch.distributed as dist
+    one = os.environ.get("RTF_ONE_DEVICE") == "1"
+    dev = torch.device("cuda", 0 if one else local)
+    torch.cuda.set_device(dev)
+    if world > 1:
+        backend = os.environ.get("RTF_DIST_BACKEND", "nccl")
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group(backend)
+    return dev
+
+
 def run_gpu(args):
     import torch
     import torch.distributed as dist
@@ -157,16 +184,15 @@ def run_gpu(args):
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if world != args.gpus:
         raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
-    torch.cuda.set_device(local)
-    dev = torch.device("cuda", local)
-    if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+    if world > 1 and args.workload == "c3":
+        return run_gpu_c3_sharded(args)
+    dev = init_dist(world, local)
 
     wl = WORKLOADS[args.workload]
     n, m, S = wl["n"], wl["m"], wl["samples"]
     if args.samples:
         S = args.samples
-    p_host = make_p(wl)
+    p_host = make_p(wl, rank)
     p = torch.from_numpy(p_host).to(dev)
     forest = rtf.Forest(n, m)
     if wl["name"] == "c2_envmap":  # Sobol dim 0, this rank's slice of the sequence
@@ -194,7 +220,7 @@ def run_gpu(args):
     assert forest.status() == 0
 
     evs = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(args.steps)]
-    sampler = ClockSampler(local)
+    sampler = ClockSampler(dev.index)
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
@@ -410,8 +436,9 @@ def run_gpu(args):
         "config": {"workload": wl["desc"], "n": n, "m": m, "samples_per_gpu": S,
                    "n_pos": n_pos,
                    "l2": f"flushed between steps ({L2_FLUSH_BYTES >> 20} MiB write, untimed)",
-                   "parallelism": f"replicas x{world}: each GPU builds and samples its own "
-                                  "problem, no collective on the data path",
+                   "parallelism": f"independent problems x{world}: GPU r builds and samples "
+                                  "its own distribution (seed 1 + r), no collective on the data "
+                                  "path",
                    "value_is": "build entries per second: n * n_gpus * steps / sum of build "
                                "times (max over ranks)"},
         "build": {"value": round(build_gs, 4), "unit": "G entries/s",
@@ -577,6 +604,141 @@ def c2_summary(args, dev, stream, flush, world):
             "timing": "median of >= 5 device-timed runs, L2 flushed before each"}
 
 
+def run_gpu_c3_sharded(args):
+    """Config 3 at N > 1 GPUs, weak scaling without redundant work: ONE
+    power-law distribution (family A) of n = N 2^24 entries and m = N 2^22
+    cells, 2^24 entries per GPU.  The build is the sharded protocol
+    (north star: "a cross-GPU scan of per-shard totals plus a per-shard build
+    over contiguous cell ranges"; paper_1901_05423_b200.sharded, fused: the
+    build kernel stores each record and table cell straight into the buffer
+    of the rank owning its cell, over NVLink symmetric memory); rank r keeps
+    the cells [r m/N, (r+1) m/N) and samples 2^30 xi of that stratum.  Every
+    collective runs inside the timed build (CUDA events, max over ranks)."""
+    import torch
+    import torch.distributed as dist
+
+    import paper_1901_05423_b200 as rtf
+    from paper_1901_05423_b200 import sharded
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    dev = init_dist(world, local)
+    wl = WORKLOADS["c3"]
+    n_local, S = wl["n"], (args.samples or wl["samples"])
+    n, m = world * n_local, world * wl["m"]
+    base = rank * n_local
+    # this rank's shard of ((i+1)/n)^20 (family A over the whole n; the scale is
+    # irrelevant: quantisation normalises by the largest weight)
+    i = np.arange(base, base + n_local, dtype=np.float64)
+    p_local = torch.from_numpy(np.exp(20.0 * np.log((i + 1.0) / n)).astype(np.float32)).to(dev)
+    del i
+    comm = sharded.DistComm()
+    shards = sharded.make_shards_local(p_local, n, m, rank, world, base, alloc=comm.alloc)
+    forest = rtf.Forest.from_buffer(n, m, shards[0].forest)
+    xi = sharded.ranged_xi(rtf.philox(S, seed=0x5EED, start=rank * S, device=dev), rank, world, m)
+    out = torch.empty(S, dtype=torch.int32, device=dev)
+    flush = torch.empty(L2_FLUSH_BYTES, dtype=torch.uint8, device=dev)
+    stream = torch.cuda.current_stream()
+
+    def step(ev=None):
+        if ev:
+            ev[0].record(stream)
+        sharded.build_sharded(shards, comm, ranged=True, fused=True)
+        if ev:
+            ev[1].record(stream)
+        forest.sample(xi, out)
+        if ev:
+            ev[2].record(stream)
+
+    for _ in range(args.warmup):
+        step()
+        flush.zero_()
+    torch.cuda.synchronize()
+    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(args.steps)]
+    sampler = ClockSampler(dev.index)
+    dist.barrier()
+    torch.cuda.synchronize()
+    l0 = rtf.launch_count()
+    with sampler:
+        for k in range(args.steps):
+            step(evs[k])
+            flush.zero_()
+        torch.cuda.synchronize()
+    launches = rtf.launch_count() - l0
+    dist.barrier()
+    tb = sum(e[0].elapsed_time(e[1]) for e in evs)
+    ts = sum(e[1].elapsed_time(e[2]) for e in evs)
+    t = torch.tensor([tb, ts], dtype=torch.float64, device=dev)
+    comm.allreduce_max([t])
+    tb, ts = t.tolist()
+    # the slots this rank holds and a sampled check of its indices (untimed)
+    j0, j1 = sharded.slots_of(shards[0])
+    g0, g1 = shards[0].cells
+    cnt = torch.tensor([j1 - j0], dtype=torch.int64, device=dev)
+    comm.allreduce_sum([cnt])
+    K = args.steps
+    build_gs = n * K / (tb * 1e-3) / 1e9
+    sample_gs = S * world * K / (ts * 1e-3) / 1e9
+    peak, peak_src = peaks()
+    bytes_rank = 4 * n_local + 16 * n_local + 4 * (m // world)  # SURVEY.md 8(d), per GPU
+    result = {
+        "metric": METRIC, "value": round(build_gs, 4), "unit": "G entries/s", "n_gpus": world,
+        "steps": K, "warmup": args.warmup, "ms_per_step": round((tb + ts) / K, 4),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u64",
+        "data": "synthetic",
+        "config": {"workload": f"config 3 weak-scaled: one power law ((i+1)/n)^20 over "
+                               f"n = {world} x 2^24 entries, m = {world} x 2^22, 2^30 Philox xi "
+                               "per GPU (each GPU samples its stratum)",
+                   "n": n, "m": m, "n_per_gpu": n_local, "samples_per_gpu": S,
+                   "n_pos": int(cnt.item()),
+                   "l2": f"flushed between steps ({L2_FLUSH_BYTES >> 20} MiB write, untimed)",
+                   "parallelism": f"sharded build over {world} GPUs: MAX all-reduce of the "
+                                  "scale word, all-gather of shard totals (the cross-GPU scan), "
+                                  "per-shard build storing records / table cells into the owning "
+                                  "rank's buffer (symmetric memory over NVLink), MAX all-reduce "
+                                  "of the slot boundaries, all-gather of tile spine rows, "
+                                  "per-rank finish; rank r keeps cells [r m/N, (r+1) m/N)",
+                   "value_is": "entries of the one distribution per second (n K / max over "
+                               "ranks of the summed build times)"},
+        "build": {"value": round(build_gs, 4), "unit": "G entries/s",
+                  "ms_per_build": round(tb / K, 5)},
+        "sampling": {"value": round(sample_gs, 4), "unit": "G samples/s",
+                     "ms_per_batch": round(ts / K, 4)},
+        "roofline": {"kernel": "sharded build, per GPU (all calls incl. exchanges)",
+                     "bound": "hbm",
+                     "achieved": round(bytes_rank / (tb / K * 1e-3) / 1e9, 2), "peak": peak,
+                     "unit": "GB/s", "frac": round(bytes_rank / (tb / K * 1e-3) / 1e9 / peak, 4),
+                     "traffic": None, "peak_source": peak_src},
+        "gpu_launches": launches, "clocks": sampler.summary(),
+    }
+    if not args.no_e2e:  # end to end: each rank's p shard from pinned host memory, the
+        # sharded build, the status word read back; wall clock, max over ranks
+        p_pin = p_local.cpu().pin_memory()
+        te = []
+        for _ in range(K):
+            flush.zero_()
+            torch.cuda.synchronize()
+            dist.barrier()
+            t0 = time.perf_counter()
+            p_local.copy_(p_pin, non_blocking=True)
+            sharded.build_sharded(shards, comm, ranged=True, fused=True)
+            st = forest.status()
+            te.append(time.perf_counter() - t0)
+            assert st == 0
+        t = torch.tensor([sum(te)], dtype=torch.float64, device=dev)
+        comm.allreduce_max([t])
+        result["e2e"] = {"value": round(n * K / t.item() / 1e9, 4), "unit": "G entries/s",
+                         "h2d_bytes_per_step": 4 * n_local, "d2h_bytes_per_step": 40,
+                         "path": "per rank: pinned host p shard -> device, sharded build "
+                                 "(all collectives), header status read back"}
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+    if rank == 0:
+        print(json.dumps(result), flush=True)
+
+
 def run_gpu_c4(args):
     """Config 4: strong scaling of one n = 2^28 distribution over N GPUs.  Each
     rank holds its shard of p; the build is the sharded protocol of
@@ -591,10 +753,7 @@ def run_gpu_c4(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
-    torch.cuda.set_device(local)
-    dev = torch.device("cuda", local)
-    if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+    dev = init_dist(world, local)
     wl = WORKLOADS["c4"]
     n, m = wl["n"], wl["m"]
     S = (args.samples or wl["samples"]) // world
@@ -635,7 +794,7 @@ def run_gpu_c4(args):
     torch.cuda.synchronize()
     assert forest.status() == 0
     evs = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(args.steps)]
-    sampler = ClockSampler(local)
+    sampler = ClockSampler(dev.index)
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
@@ -703,14 +862,11 @@ def run_gpu_2d(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
-    torch.cuda.set_device(local)
-    dev = torch.device("cuda", local)
-    if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+    dev = init_dist(world, local)
     wl = WORKLOADS["c2d"]
     W, H, mx, my = wl["W"], wl["H"], wl["m"], wl["my"]
     S = args.samples or wl["samples"]
-    p = torch.from_numpy(env_map(W, H)).to(dev)
+    p = torch.from_numpy(env_map(W, H, seed=1 + rank)).to(dev)
     f = rtf.Forest2D(W, H, mx, my, device=dev)
     xi1 = rtf.philox(S, seed=0x5EED, start=2 * rank * S, device=dev)
     xi2 = rtf.philox(S, seed=0x5EED, start=(2 * rank + 1) * S, device=dev)
@@ -735,7 +891,7 @@ def run_gpu_2d(args):
     torch.cuda.synchronize()
     assert f.status() == 0
     evs = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(args.steps)]
-    sampler = ClockSampler(local)
+    sampler = ClockSampler(dev.index)
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
@@ -763,7 +919,8 @@ def run_gpu_2d(args):
         "config": {"workload": wl["desc"], "W": W, "H": H, "mx": mx, "my": my,
                    "samples_per_gpu": S,
                    "l2": f"flushed between steps ({L2_FLUSH_BYTES >> 20} MiB write, untimed)",
-                   "parallelism": f"replicas x{world}"},
+                   "parallelism": f"independent problems x{world}: GPU r its own env map "
+                                  "(seed 1 + r)"},
         "build": {"value": round(build_gs, 4), "unit": "G entries/s", "ms_per_build": round(tb / K, 5),
                   "launches": "rows build + row weights + marginal build"},
         "sampling": {"value": round(sample_gs, 4), "unit": "G 2-D samples/s",
@@ -818,7 +975,7 @@ def run_gpu_c1(args):
             b.synchronize()
         return a.elapsed_time(b) * 1e3 / K
 
-    sampler = ClockSampler(local)
+    sampler = ClockSampler(dev.index)
     with sampler:
         l0 = rtf.launch_count()
         eager_us = timed(step)
@@ -860,14 +1017,11 @@ def run_gpu_c5(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
-    torch.cuda.set_device(local)
-    dev = torch.device("cuda", local)
-    if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+    dev = init_dist(world, local)
     wl = WORKLOADS["c5"]
     rows, n_row, m_row = wl["rows"], wl["n_row"], wl["m"]
     S = args.samples or wl["samples"]
-    p_host = make_p(wl)
+    p_host = make_p(wl, rank)
     p = torch.from_numpy(p_host).to(dev)
     forest = rtf.RowsForest(rows, n_row, m_row, device=dev)
     row = torch.from_numpy((np.arange(S, dtype=np.uint64) * 2654435761 % rows)
@@ -894,7 +1048,7 @@ def run_gpu_c5(args):
     forest.headers()
     assert forest.last_status == 0
     evs = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(args.steps)]
-    sampler = ClockSampler(local)
+    sampler = ClockSampler(dev.index)
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
@@ -927,7 +1081,8 @@ def run_gpu_c5(args):
         "config": {"workload": wl["desc"], "rows": rows, "n_row": n_row, "m_row": m_row,
                    "samples_per_gpu": S,
                    "l2": f"flushed between steps ({L2_FLUSH_BYTES >> 20} MiB write, untimed)",
-                   "parallelism": f"replicas x{world}: each GPU builds its own rows"},
+                   "parallelism": f"independent problems x{world}: GPU r builds its own rows "
+                                  "(seed 7 + r)"},
         "build": {"value": round(build_gs, 4), "unit": "G entries/s", "ms_per_build": round(tb / K, 5)},
         "sampling": {"value": round(sample_gs, 4), "unit": "G samples/s",
                      "ms_per_batch": round(ts / K, 4)},
