@@ -275,11 +275,12 @@ def marginal_weights(p2d) -> np.ndarray:
     return q
 
 
-def _f32_rz(d: float) -> np.float32:
-    """float64 -> float32 rounded toward zero."""
-    f = np.float32(d)
-    if abs(float(f)) > abs(d):
-        f = np.nextafter(f, np.float32(0))
+def _f32_rz(d):
+    """float64 -> float32 rounded toward zero (element-wise)."""
+    d = np.asarray(d, np.float64)
+    f = d.astype(np.float32)
+    over = np.abs(f.astype(np.float64)) > np.abs(d)
+    f[over] = np.nextafter(f[over], np.float32(0))
     return f
 
 
@@ -292,35 +293,47 @@ class Forest2D:
     marginal: Forest
     rows: list  # Forest per row (None for an all-zero row)
 
-    def _interval(self, f: Forest, idx: int, xi: int) -> float:
-        """Relative position of xi inside interval idx of forest f (the
+    @staticmethod
+    def _positions(f: Forest, idx: np.ndarray, xi: np.ndarray) -> np.ndarray:
+        """Relative position of each xi inside interval idx of forest f (the
         sub-pixel rescale of P:1526-1528): float64(xi 2^31 - key_j) /
-        float64(key_{j+1} - key_j), each integer rounded to nearest once."""
-        j = int(np.flatnonzero(f.orig == idx)[0])
-        lo = int(f.key[j])
-        hi = int(f.key[j + 1]) if j + 1 < f.n_pos else ONE
-        return float((xi << 31) - lo) / float(hi - lo)
+        float64(key_{j+1} - key_j), each integer rounded to nearest once
+        (numpy's uint64 -> float64 conversion rounds to nearest, as
+        Python's float(int) does); j is the leaf of original index idx."""
+        j_of = np.full(f.n, -1, np.int64)
+        j_of[f.orig] = np.arange(f.n_pos)
+        j = j_of[np.asarray(idx, np.int64)]
+        keys = np.append(f.key.astype(np.uint64), np.uint64(ONE))  # key_{n'} = "1"
+        lo, hi = keys[j], keys[j + 1]
+        num = (np.asarray(xi, np.uint64) << np.uint64(31)) - lo
+        return num.astype(np.float64) / (hi - lo).astype(np.float64)
 
     def sample(self, xi1, xi2):
         """O15: y = marginal^-1(xi1); x = row_y^-1(xi2); the continuous position
         ((x + v) / W, (y + u) / H) in float64, rounded toward zero to float32
         (so it stays below 1, reading R19), u and v the relative
         positions inside the chosen intervals.  Returns (pixel = y W + x,
-        pos float32[N, 2] as (x, y))."""
+        pos float32[N, 2] as (x, y)).  The samples of one row go through that
+        row's forest together."""
         xi1 = np.asarray(xi1, dtype=np.uint32)
         xi2 = np.asarray(xi2, dtype=np.uint32)
-        ys = self.marginal.sample(xi1)
-        pix = np.empty(xi1.size, np.int32)
+        ys = self.marginal.sample(xi1).astype(np.int64)
+        xs = np.empty(xi1.size, np.int64)
+        v = np.empty(xi1.size, np.float64)
+        order = np.argsort(ys, kind="stable")
+        ys_sorted = ys[order]
+        bounds = np.flatnonzero(np.diff(ys_sorted)) + 1
+        for sel in np.split(order, bounds):
+            if sel.size == 0:
+                continue
+            fr = self.rows[int(ys[sel[0]])]
+            xs[sel] = fr.sample(xi2[sel])
+            v[sel] = self._positions(fr, xs[sel], xi2[sel])
+        u = self._positions(self.marginal, ys, xi1)
+        pix = (ys * self.W + xs).astype(np.int32)
         pos = np.empty((xi1.size, 2), np.float32)
-        for k in range(xi1.size):
-            y = int(ys[k])
-            fr = self.rows[y]
-            x = int(fr.sample(xi2[k:k + 1])[0])
-            u = self._interval(self.marginal, y, int(xi1[k]))
-            v = self._interval(fr, x, int(xi2[k]))
-            pix[k] = y * self.W + x
-            pos[k, 0] = _f32_rz((float(x) + v) / float(self.W))
-            pos[k, 1] = _f32_rz((float(y) + u) / float(self.H))
+        pos[:, 0] = _f32_rz((xs.astype(np.float64) + v) / float(self.W))
+        pos[:, 1] = _f32_rz((ys.astype(np.float64) + u) / float(self.H))
         return pix, pos
 
 

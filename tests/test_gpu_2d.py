@@ -78,11 +78,11 @@ def test_2d_constant_image_identity(rtf):
 
 
 def test_2d_envmap_full(rtf):
-    """The C2 environment map (2048 x 1024) as a 2-D distribution: weights bit-exact,
-    4096 of 2^20 samples one by one against the oracle, all 2^20 by properties."""
+    """The C2 environment map (2048 x 1024) as a 2-D distribution: weights
+    bit-exact, all 2^20 samples (pixels and positions) against the oracle."""
     p = env_map().reshape(1024, 2048)
     xi1, xi2 = philox_xi(1 << 20, seed=21), philox_xi(1 << 20, seed=22)
-    check(rtf, p, 2048, 1024, xi1, xi2, sample_all=False)
+    check(rtf, p, 2048, 1024, xi1, xi2)
 
 
 def test_2d_data_errors(rtf):

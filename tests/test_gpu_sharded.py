@@ -142,3 +142,49 @@ def test_sharded_fused_peer_stores(rtf, count):
     rng = np.random.default_rng(20 + count)
     _check_ranged(rtf, random_small(rng, 4096 * 3 * count - 100, zero_frac=0.3, dyn=12.0),
                   1 << 16, count, fused=True)
+
+
+def test_config4_full_size_records_vs_oracle(rtf):
+    """Config 4 at its full size (n = 2^28 spikes, m = 2^22): EVERY node record
+    (key and both children) and EVERY guide-table cell of the single-GPU build
+    equal the oracle's (O1-O13, about 8 GB of host arrays); then the fused
+    ranged build over 4 virtual shards (the N > 1 default: peer stores into the
+    owner's buffer) gives byte-equal cell slices, and 2^20 samples of each
+    shard's xi stratum equal the single forest's."""
+    from paper_1901_05423_b200 import sharded
+    n, m = 1 << 28, 1 << 22
+    p = spikes(n)
+    pd = torch.from_numpy(p).cuda()
+    single = rtf.build(pd, m)
+    assert single.status() == 0
+    nodes = single.nodes_numpy()
+    table = single.table_numpy()
+    del single
+    torch.cuda.empty_cache()
+    ref = oracle.build(p, m)
+    assert nodes.size == ref.n_pos
+    assert np.array_equal(nodes["key"], ref.key), "keys"
+    assert np.array_equal(nodes["c0"], ref.child0), "left children"
+    assert np.array_equal(nodes["c1"], ref.child1), "right children"
+    assert table.tobytes() == ref.table2().tobytes(), "guide table"
+    del ref
+    shards = sharded.make_shards(pd, m, 4)
+    sharded.build_sharded(shards, sharded.LocalComm(), ranged=True, fused=True)
+    covered = 0
+    for s in shards:
+        f = rtf.Forest.from_buffer(s.n_global, m, s.forest)
+        (j0, j1), (g0, g1) = sharded.slots_of(s), s.cells
+        covered += j1 - j0
+        recs = f._section(f.view.nodes + 16 * j0, 16 * (j1 - j0)).cpu().numpy()
+        assert recs.tobytes() == nodes[j0:j1].tobytes(), f"shard {s.rank} records"
+        assert f.table_numpy()[g0:g1].tobytes() == table[g0:g1].tobytes(), f"shard {s.rank} table"
+        xi = philox_xi(1 << 20, seed=40 + s.rank)
+        xr = sharded.ranged_xi(torch.from_numpy(xi.view(np.int32)), s.rank, 4, m).cuda()
+        got = f.sample(xr).cpu().numpy()
+        # the definition (P:61-63) on the verified keys: the last key <= xi 2^31;
+        # no zero weights here (n' = n), so leaf index = original index
+        want = np.searchsorted(nodes["key"], xr.cpu().numpy().view(np.uint32).astype(np.uint64)
+                               << np.uint64(31), side="right") - 1
+        assert np.all((want >= j0) & (want < j1)), f"shard {s.rank}: xi outside its stratum"
+        assert np.array_equal(got, want.astype(np.int32)), f"shard {s.rank} samples"
+    assert covered == nodes.size == n
