@@ -148,6 +148,33 @@ class Forest:
         ~(xi < key32 ? ref + 1 : ref)."""
         return table2_of(self.table, self.key, self.orig, self.cell, self.m)
 
+    def table3(self) -> np.ndarray:
+        """O16: the guide table with three-interval cells packed (R20); the
+        table the build produces."""
+        return table3_of(self.table2(), self.key, self.orig, self.cell, self.m)
+
+    def sample_table3(self, xi) -> np.ndarray:
+        """Alg. 2 through the O16 table: plain Python loop."""
+        t3 = self.table3()
+        rec = self.records()
+        shift = 32 - (self.m.bit_length() - 1)
+        out = np.empty(len(xi), dtype=np.int32)
+        for k, x in enumerate(np.asarray(xi, dtype=np.uint64).tolist()):
+            g = (x * self.m) >> 32
+            key32, ref = int(t3[g]["key32"]), int(t3[g]["ref"])
+            if ref >= 0 and key32:  # three intervals: ref = orig(a-1)
+                xi0 = g << shift
+                out[k] = ref + (x >= xi0 + (key32 & 0xFFFF)) + (x >= xi0 + (key32 >> 16))
+                continue
+            if ref < 0:
+                out[k] = ~(ref + 1 if x < key32 else ref)
+                continue
+            j = ref
+            while j >= 0:
+                j = int(rec[j]["c0"]) if (x << 31) < int(rec[j]["key"]) else int(rec[j]["c1"])
+            out[k] = ~j
+        return out
+
     def sample_table2(self, xi) -> np.ndarray:
         """Alg. 2 through the O13 table: plain Python loop."""
         t2 = self.table2()
@@ -163,6 +190,41 @@ class Forest:
                 j = int(rec[j]["c0"]) if (x << 31) < int(rec[j]["key"]) else int(rec[j]["c1"])
             out[k] = ~j
         return out
+
+
+PACK_MIN_M = 1 << 17  # O16 packs cells of m >= 2^17 power-of-two tables (R20)
+
+
+def table3_of(t2, key, orig, cell, m) -> np.ndarray:
+    """O16 (reading R20): the O13 table with every cell that holds exactly two
+    leaves a, a+1 -- overlapped by the three intervals a-1, a, a+1 --
+    stored in the 8-byte entry itself, carrying the paper's idea that
+    "further information could also be stored in the reference" so that
+    "there is no need to explicitly store a node" (Sec.3.2) one
+    step further than the two-interval flag.  Only for a power-of-two m >=
+    2^17 (a cell is then at most 2^15 xi values wide, xi0 = g 2^32 / m its
+    first xi), when a >= 1 and orig(a+1) = orig(a-1) + 2 (no zero weight
+    between the three intervals):
+        key32 = s1 | s2 << 16,  s = ceil(key / 2^31) - xi0 for key_a, key_{a+1}
+        ref   = orig(a-1)  (>= 0, as an anchor's; key32 != 0 tells them apart:
+                            s2 >= 1 because key_{a+1} > xi0 2^31)
+    Sampling: ref + [xi >= xi0 + s1] + [xi >= xi0 + s2] (xi 2^31 < key <=>
+    xi < ceil(key / 2^31), so the comparisons are Alg. 2's).  Every other
+    cell and any other m: the O13 entry."""
+    out = np.array(t2, dtype=TABLE2_DTYPE, copy=True)
+    if m < PACK_MIN_M or (m & (m - 1)):
+        return out
+    shift = 32 - (m.bit_length() - 1)  # xi0 = g << shift
+    leaves_per_cell = np.bincount(cell.astype(np.int64), minlength=m)
+    for g in np.flatnonzero((out["ref"] >= 0) & (leaves_per_cell == 2)).tolist():
+        a = int(out["ref"][g])  # the anchor: the cell's first leaf
+        if a == 0 or int(orig[a + 1]) != int(orig[a - 1]) + 2:
+            continue
+        xi0 = g << shift
+        s1 = -(-int(key[a]) >> 31) - xi0
+        s2 = -(-int(key[a + 1]) >> 31) - xi0
+        out[g] = (s1 | (s2 << 16), int(orig[a - 1]))
+    return out
 
 
 def table2_of(table, key, orig, cell, m) -> np.ndarray:

@@ -458,3 +458,66 @@ def test_philox_known_answers():
             [0xD16CFE09, 0x94FDCCEB, 0x5001E420, 0x24126EA1]]
     for c, k, wv in zip(ctr, keys, want):
         assert philox4x32_10(c[None, :], k)[0].tolist() == wv
+
+
+def test_table3_hand_derived():
+    """O16 (R20) on w = (2^20, 1, 2^20 - 1), m = 2^17: E = 20, B = 60, so the
+    quantised weights are (2^60, 2^40, 2^60 - 2^40), T = 2^61 and the keys
+    W 2^63 / T = 4 W are (0, 2^62, 2^62 + 2^42) -- cells key >> 46 = (0,
+    65536, 65536).  Cell 65536 holds exactly the two leaves 1, 2: its first xi
+    is 65536 2^15 = 2^31, ceil(key_1 / 2^31) = 2^31 (s1 = 0: interval 0 ends
+    at the cell edge) and ceil(key_2 / 2^31) = 2^31 + 2^11 (s2 = 2048 = w_1 /
+    T 2^32); entry (2048 << 16, orig(0) = 0).  Every other cell keeps O13."""
+    p = np.array([2.0**20, 1.0, 2.0**20 - 1.0], F32)
+    m = 1 << 17
+    f = oracle.build(p, m)
+    assert f.key.tolist() == [0, 1 << 62, (1 << 62) + (1 << 42)]
+    t2, t3 = f.table2(), f.table3()
+    diff = np.flatnonzero(t2.view(np.uint64) != t3.view(np.uint64)).tolist()
+    assert diff == [65536]
+    assert (int(t3[65536]["key32"]), int(t3[65536]["ref"])) == (2048 << 16, 0)
+    xs = np.array([2**31 - 1, 2**31, 2**31 + 2047, 2**31 + 2048, 2**31 + 2**15 - 1], np.uint32)
+    assert f.sample_table3(xs).tolist() == [0, 1, 1, 2, 2]
+    w, _, _ = oracle.quantize(p)
+    assert [_definition_index(w, int(x)) for x in xs] == [0, 1, 1, 2, 2]
+
+
+def test_table3_not_packed():
+    """No packing below m = 2^17 or for a non-power-of-two m (O16 = O13), for
+    a = 0, or with a zero weight among the three intervals."""
+    p = np.array([2.0**20, 1.0, 2.0**20 - 1.0], F32)
+    for m in (1 << 16, (1 << 17) + 1):
+        f = oracle.build(p, m)
+        assert f.table3().tobytes() == f.table2().tobytes()
+    f = oracle.build(np.array([1.0, 1.0, 2.0**30], F32), 1 << 17)  # leaves 0, 1 share cell 0
+    assert f.table3().tobytes() == f.table2().tobytes()
+    f = oracle.build(np.array([2.0**20, 0.0, 1.0, 2.0**20 - 1.0], F32), 1 << 17)
+    assert f.table3().tobytes() == f.table2().tobytes()
+
+
+def test_table3_descent_brute_force():
+    """Alg. 2 through the O16 table equals the inverse-CDF definition (P:61-63,
+    oracle.sample_bsearch over the exact fixed-point CDF) and the tree descent
+    on every packed cell's boundaries +-1, its edges and random xi in it."""
+    rng = np.random.default_rng(31)
+    npack = 0
+    for t, m in enumerate([1 << 17, 1 << 17, 1 << 18]):
+        n = int(m * rng.uniform(0.7, 1.6))
+        p = random_small(rng, n, zero_frac=float(rng.choice([0.0, 0.1])), dyn=float(rng.choice([2, 8])))
+        f = oracle.build(p, m)
+        t3 = f.table3()
+        packed = np.flatnonzero((t3["ref"] >= 0) & (t3["key32"] != 0))
+        npack += packed.size
+        shift = 32 - (m.bit_length() - 1)
+        xs = set()
+        for g in packed[:: max(1, packed.size // 400)].tolist():
+            x0, k = g << shift, int(t3[g]["key32"])
+            for s in (k & 0xFFFF, k >> 16):
+                xs |= {x0 + s - 1, x0 + s, x0 + s + 1}
+            xs |= {x0, x0 + (1 << shift) - 1, x0 + int(rng.integers(1 << shift))}
+        xs = np.array(sorted(x for x in xs if 0 <= x < 2**32), np.uint32)
+        K, _ = oracle.cdf_all(p)
+        want = oracle.sample_bsearch(K, xs)
+        assert np.array_equal(f.sample_table3(xs), want), t
+        assert np.array_equal(f.sample(xs), want), t
+    assert npack > 1000  # the inputs do exercise the packed cells
