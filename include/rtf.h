@@ -273,6 +273,19 @@ int rtf_build_cdf(const float *p, uint32_t n, uint64_t *cdf, rtf_header *header,
 int rtf_sample_bsearch(const uint64_t *cdf, uint32_t n, const rtf_header *header,
                        const uint32_t *xi, uint64_t count, int32_t *out, void *stream);
 
+/* Eytzinger binary-search baseline (Sec.2.2 P:114-127 laid out for a GPU):
+ * rtf_build_eytzinger writes the keys cdf[1..n-1] as a complete binary
+ * search tree in breadth-first order, eyt[k] for 1 <= k < 2^H,
+ * H = ceil(log2 n) (u64[2^H], device, caller-owned; rtf_eytzinger_slots(n)
+ * = 2^H entries; missing ranks hold UINT64_MAX).  rtf_sample_eytzinger:
+ * out[k] as rtf_sample_bsearch (identical results), descending H levels, the
+ * top 13 from a shared-memory copy per CTA.  Asynchronous on `stream`;
+ * RTF_EINVAL on NULL or misaligned pointers. */
+uint64_t rtf_eytzinger_slots(uint32_t n);
+int rtf_build_eytzinger(const uint64_t *cdf, uint32_t n, uint64_t *eyt, void *stream);
+int rtf_sample_eytzinger(const uint64_t *eyt, uint32_t n, const rtf_header *header,
+                         const uint32_t *xi, uint64_t count, int32_t *out, void *stream);
+
 /* Cutpoint baselines (guide table of the classic cutpoint method, Sec.2.3
  * P:168-232; the "cutpoint + linear / binary" rows of Table 1) on
  * the same full CDF.  rtf_build_cutpoint: cut[g] (u32[m + 1], device) = the

@@ -340,9 +340,34 @@ class Cdf:
         return out
 
 
+    def eytzinger(self, stream=None) -> "Eytzinger":
+        """The same CDF as a breadth-first search tree (the Eytzinger baseline)."""
+        return Eytzinger(self, stream)
+
     def cutpoint(self, m: int, stream=None) -> "Cutpoint":
         """The cutpoint table (m cells) over this CDF, for the cutpoint baselines."""
         return Cutpoint(self, m, stream)
+
+
+class Eytzinger:
+    """Binary search over a Cdf in breadth-first (Eytzinger) order, top levels
+    in shared memory: the competent GPU binary-search baseline."""
+
+    def __init__(self, cdf: Cdf, stream=None):
+        self.cdf = cdf
+        slots = int(lib().rtf_eytzinger_slots(cdf.n))
+        self.eyt = torch.empty(slots, dtype=torch.int64, device=cdf.cdf.device)
+        check(lib().rtf_build_eytzinger(_ptr(cdf.cdf), cdf.n, _ptr(self.eyt), _stream(stream)),
+              "rtf_build_eytzinger")
+
+    def sample(self, xi: torch.Tensor, out=None, stream=None) -> torch.Tensor:
+        xi = _u32_view(xi)
+        if out is None:
+            out = torch.empty(xi.numel(), dtype=torch.int32, device=xi.device)
+        check(lib().rtf_sample_eytzinger(_ptr(self.eyt), self.cdf.n, _ptr(self.cdf.header),
+                                         _ptr(xi), xi.numel(), _ptr(out), _stream(stream)),
+              "rtf_sample_eytzinger")
+        return out
 
 
 class Cutpoint:

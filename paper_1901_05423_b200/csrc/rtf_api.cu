@@ -352,6 +352,30 @@ int rtf_sample_bsearch(const uint64_t* cdf, uint32_t n, const rtf_header* header
     return finish(e, launches);
 }
 
+uint64_t rtf_eytzinger_slots(uint32_t n) { return 1ull << rtf::ceil_log2_u32(n); }
+
+int rtf_build_eytzinger(const uint64_t* cdf, uint32_t n, uint64_t* eyt, void* stream) {
+    if (!cdf || !eyt) return RTF_EINVAL;
+    if (int s = check_nm(n, 1)) return s;
+    if ((((uintptr_t)cdf | (uintptr_t)eyt) & 7u) != 0) return RTF_EINVAL;
+    int launches = 0;
+    cudaError_t e = rtf::launch_eytzinger_build(cdf, n, eyt, as_stream(stream), &launches);
+    return finish(e, launches);
+}
+
+int rtf_sample_eytzinger(const uint64_t* eyt, uint32_t n, const rtf_header* header,
+                         const uint32_t* xi, uint64_t count, int32_t* out, void* stream) {
+    if (!eyt || !header) return RTF_EINVAL;
+    if (int s = check_nm(n, 1)) return s;
+    if (count && (!xi || !out)) return RTF_EINVAL;
+    if ((((uintptr_t)xi | (uintptr_t)out) & 3u) != 0 || ((uintptr_t)eyt & 7u) != 0)
+        return RTF_EINVAL;
+    int launches = 0;
+    cudaError_t e = rtf::launch_eytzinger(eyt, n, header, xi, count, out, as_stream(stream),
+                                          &launches);
+    return finish(e, launches);
+}
+
 int rtf_build_cutpoint(const uint64_t* cdf, uint32_t n, uint32_t m, uint32_t* cut, void* stream) {
     if (!cdf || !cut) return RTF_EINVAL;
     if (int s = check_nm(n, m)) return s;

@@ -70,7 +70,7 @@ cudaError_t launch_count_cells(const rtf_node* nodes, uint32_t j0, uint32_t cnt,
                                const uint32_t* bounds, uint32_t nb, uint32_t* counts,
                                cudaStream_t st, int* launches);
 
-uint32_t build_tile_size(uint32_t flags);
+uint32_t build_rows(uint32_t n, uint32_t flags);  // warp ranges (spine rows) of a build
 size_t build_workspace_layout(uint32_t n, uint32_t m, uint32_t flags, WsLayout* L,
                               uint32_t n_global = 0);
 size_t spine_row_bytes();       // bytes of one tile-spine row
@@ -108,6 +108,12 @@ cudaError_t launch_sample4(const rtf_forest& f, const void* rec4, const uint32_t
 cudaError_t launch_bsearch(const uint64_t* cdf, uint32_t n, const rtf_header* hdr,
                            const uint32_t* xi, uint64_t count, int32_t* out, cudaStream_t st,
                            int* launches);
+
+cudaError_t launch_eytzinger_build(const uint64_t* cdf, uint32_t n, uint64_t* eyt,
+                                   cudaStream_t st, int* launches);
+cudaError_t launch_eytzinger(const uint64_t* eyt, uint32_t n, const rtf_header* hdr,
+                             const uint32_t* xi, uint64_t count, int32_t* out, cudaStream_t st,
+                             int* launches);
 
 cudaError_t launch_cutpoint_build(const uint64_t* cdf, uint32_t n, uint32_t m, uint32_t* cut,
                                   cudaStream_t st, int* launches);

@@ -179,6 +179,75 @@ __global__ void __launch_bounds__(kSampleThreads)
     }
 }
 
+// ------------------------------------------------------------ Eytzinger binary-search baseline
+// The binary search of Sec.2.2 laid out for a GPU: the keys
+// cdf[1..n-1] (cdf[0] = 0 is below every xi) as a complete binary search tree
+// of height H = ceil(log2 n) in breadth-first order (node k at depth d holds the
+// key of in-order rank (2 (k - 2^d) + 1) 2^(H-1-d) - 1, ranks >= n - 1 hold
+// +inf).  After H comparisons "go right iff key <= x" the node index minus 2^H
+// is the number of keys <= x, i.e. the last i with cdf[i] <= x: no index array.
+// The top levels (up to 2^13 - 1 keys, 64 KB) sit in shared memory per CTA,
+// so only the lower levels are global (L2 / HBM) loads.
+
+constexpr int kEytThreads = 256;
+constexpr int kEytSmemLevels = 13;
+
+__global__ void k_eytzinger_build(const uint64_t* __restrict__ cdf, uint32_t n, uint32_t H,
+                                  uint64_t* __restrict__ eyt) {
+    const uint64_t slots = 1ull << H;  // index 0 unused
+    const uint64_t gs = (uint64_t)gridDim.x * blockDim.x;
+    for (uint64_t k = 1 + (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; k < slots; k += gs) {
+        const uint32_t d = 63u - (uint32_t)__clzll((long long)k);
+        const uint64_t rank = ((2ull * (k - (1ull << d)) + 1ull) << (H - 1u - d)) - 1ull;
+        eyt[k] = rank + 1 < n ? cdf[rank + 1] : ~0ull;
+    }
+}
+
+__global__ void __launch_bounds__(kEytThreads, 3)
+    k_eytzinger(const uint64_t* __restrict__ eyt, uint32_t H, const rtf_header* __restrict__ hdr,
+                const uint32_t* __restrict__ xi, uint64_t count, int32_t* __restrict__ out,
+                bool vec) {
+    extern __shared__ uint64_t s_top[];  // s_top[k] = eyt[k], k < 2^L
+    const uint32_t L = H < (uint32_t)kEytSmemLevels ? H : (uint32_t)kEytSmemLevels;
+    for (uint32_t k = threadIdx.x; k < (1u << L); k += blockDim.x) s_top[k] = eyt[k];
+    __syncthreads();
+    const bool bad = hdr->status != 0;
+    const uint64_t gt = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const uint64_t gs = (uint64_t)gridDim.x * blockDim.x;
+    const uint64_t top = 1ull << H;
+    uint64_t done = 0;
+    if (vec) {
+        const uint64_t nq = count >> 2;
+        for (uint64_t q = gt; q < nq; q += gs) {
+            const uint4 xv = ld_stream_u4(xi + 4 * q);
+            const uint64_t x63[4] = {(uint64_t)xv.x << 31, (uint64_t)xv.y << 31,
+                                     (uint64_t)xv.z << 31, (uint64_t)xv.w << 31};
+            uint64_t k[4] = {1, 1, 1, 1};
+            for (uint32_t d = 0; d < L; ++d) {
+#pragma unroll
+                for (int s = 0; s < 4; ++s) k[s] = 2 * k[s] + (s_top[k[s]] <= x63[s] ? 1 : 0);
+            }
+            for (uint32_t d = L; d < H; ++d) {
+#pragma unroll
+                for (int s = 0; s < 4; ++s) k[s] = 2 * k[s] + (__ldg(eyt + k[s]) <= x63[s] ? 1 : 0);
+            }
+            int4 o;
+            o.x = bad ? INT32_MAX : (int32_t)(k[0] - top);
+            o.y = bad ? INT32_MAX : (int32_t)(k[1] - top);
+            o.z = bad ? INT32_MAX : (int32_t)(k[2] - top);
+            o.w = bad ? INT32_MAX : (int32_t)(k[3] - top);
+            __stcs(reinterpret_cast<int4*>(out + 4 * q), o);
+        }
+        done = nq << 2;
+    }
+    for (uint64_t i = done + gt; i < count; i += gs) {
+        const uint64_t x63 = (uint64_t)xi[i] << 31;
+        uint64_t k = 1;
+        for (uint32_t d = 0; d < H; ++d) k = 2 * k + ((d < L ? s_top[k] : __ldg(eyt + k)) <= x63 ? 1 : 0);
+        out[i] = bad ? INT32_MAX : (int32_t)(k - top);
+    }
+}
+
 // ------------------------------------------------------------ cutpoint baselines
 // The guide-table methods the paper compares against (Sec.2.3, Table 1
 // P:1458-1482): cut[g] = the answer for the smallest xi of cell g (an index
@@ -319,6 +388,40 @@ cudaError_t launch_bsearch(const uint64_t* cdf, uint32_t n, const rtf_header* hd
     const bool vec = (((uintptr_t)xi | (uintptr_t)out) & 15u) == 0;
     k_bsearch<<<grid_for(vec ? (count + 3) / 4 : count), kSampleThreads, 0, st>>>(cdf, n, hdr, xi,
                                                                                   count, out, vec);
+    ++*launches;
+    return cudaGetLastError();
+}
+
+cudaError_t launch_eytzinger_build(const uint64_t* cdf, uint32_t n, uint64_t* eyt,
+                                   cudaStream_t st, int* launches) {
+    const uint32_t H = (uint32_t)ceil_log2_u32(n);
+    if (H == 0) return cudaSuccess;
+    k_eytzinger_build<<<grid_for(1ull << H), kSampleThreads, 0, st>>>(cdf, n, H, eyt);
+    ++*launches;
+    return cudaGetLastError();
+}
+
+cudaError_t launch_eytzinger(const uint64_t* eyt, uint32_t n, const rtf_header* hdr,
+                             const uint32_t* xi, uint64_t count, int32_t* out, cudaStream_t st,
+                             int* launches) {
+    if (count == 0) return cudaSuccess;
+    const uint32_t H = (uint32_t)ceil_log2_u32(n);
+    const uint32_t L = std::min<uint32_t>(H, kEytSmemLevels);
+    const size_t smem = sizeof(uint64_t) << L;
+    static std::atomic<bool> attr_set[kMaxDevices] = {};
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (dev >= 0 && dev < kMaxDevices && !attr_set[dev].load(std::memory_order_relaxed)) {
+        cudaError_t e = cudaFuncSetAttribute(k_eytzinger, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             (int)(sizeof(uint64_t) << kEytSmemLevels));
+        if (e != cudaSuccess) return e;
+        attr_set[dev].store(true, std::memory_order_relaxed);
+    }
+    const bool vec = (((uintptr_t)xi | (uintptr_t)out) & 15u) == 0;
+    const uint64_t items = vec ? (count + 3) / 4 : count;
+    const uint64_t want = (items + kEytThreads - 1) / kEytThreads;
+    const uint32_t grid = (uint32_t)std::max<uint64_t>(1, std::min<uint64_t>(want, 3ull * device_sms()));
+    k_eytzinger<<<grid, kEytThreads, smem, st>>>(eyt, H, hdr, xi, count, out, vec);
     ++*launches;
     return cudaGetLastError();
 }

@@ -39,3 +39,31 @@ def test_gpu_cutpoint_baselines_match_oracle():
         for binary in (True, False):
             got = cut.sample(xd, binary=binary).cpu().numpy()
             assert np.array_equal(got, want), (p.size, m, binary)
+
+
+@pytest.mark.gpu
+def test_gpu_eytzinger_baseline_matches_oracle():
+    """The Eytzinger-layout binary search returns the oracle's inverse CDF:
+    trees of height 0 (n = 1) to 20, shallower and deeper than the 13
+    shared-memory levels, ragged sample counts (scalar tail), zero weights."""
+    torch = pytest.importorskip("torch")
+    if not torch.cuda.is_available():
+        pytest.fail("CUDA device required for -m gpu tests")
+    import paper_1901_05423_b200 as rtf
+    rng = np.random.default_rng(33)
+    cases = [random_small(rng, n, zero_frac=z, dyn=8.0)
+             for n, z in ((1, 0.0), (2, 0.0), (3, 0.3), (4096, 0.5), (8193, 0.2), (70001, 0.3))]
+    cases.append(power_law(1 << 20, "A"))
+    for p in cases:
+        ref = oracle.build(p, 64)
+        cdf = rtf.build_cdf(torch.from_numpy(p).cuda())
+        ey = cdf.eytzinger()
+        K, _ = oracle.cdf_all(p)
+        edges = np.clip(np.concatenate([K[:64] >> 31, (K[:64] >> 31) + 1, (K[-64:] >> 31) - 1,
+                                        K[-64:] >> 31]), 0, 2**32 - 1).astype(np.uint32)
+        xi = np.concatenate([philox_xi((1 << 16) + 3, seed=p.size), edges,
+                             np.array([0, 2**32 - 1], np.uint32)])
+        want = ref.sample(xi)
+        for xs, w in ((xi, want), (xi[1:], want[1:])):  # aligned, then misaligned (scalar path)
+            got = ey.sample(torch.from_numpy(xs.view(np.int32)).cuda()).cpu().numpy()
+            assert np.array_equal(got, w), p.size
