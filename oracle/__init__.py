@@ -175,6 +175,73 @@ class Forest:
             out[k] = ~j
         return out
 
+    def cell_depths(self) -> tuple[np.ndarray, np.ndarray]:
+        """O17 helper: per cell g, (D_g, k_g).  k_g = leaves whose cell is g;
+        D_g = the most node records Alg. 2 (through the O10 table)
+        visits for any 32-bit xi of cell g: 1 for the anchor's left child
+        (interval a-1), else the visits to the leaf j that xi_j =
+        ceil(key_j / 2^31) reaches, over the leaves j reachable by a 32-bit xi
+        (ceil(key_j / 2^31) < ceil(key_{j+1} / 2^31), key_{n'} = 2^63), each
+        counted in the cell of xi_j (every xi mapping to leaf j follows the
+        same path, and xi_j is the first of them).  D_g = 0 for cells without
+        an anchor."""
+        kc = np.array([-(-int(k) >> 31) for k in self.key] + [1 << 32], dtype=np.uint64)
+        reach = np.flatnonzero(kc[:-1] < kc[1:])
+        xs = kc[reach].astype(np.uint32)
+        _, loads = self.sample(xs, with_loads=True)
+        cells = ((xs.astype(np.uint64) * np.uint64(self.m)) >> np.uint64(32)).astype(np.int64)
+        D = np.zeros(self.m, dtype=np.int64)
+        np.maximum.at(D, cells, loads.astype(np.int64) - 1)
+        D[self.table >= 0] = np.maximum(D[self.table >= 0], 1)
+        k = np.bincount(self.cell.astype(np.int64), minlength=self.m)
+        return D, k
+
+    def table4(self) -> np.ndarray:
+        """O17: the O16 table with degenerate cells marked for bisection (R21)."""
+        D, k = self.cell_depths()
+        return table4_of(self.table3(), D, k)
+
+    def sample_table4(self, xi, with_loads: bool = False):
+        """Alg. 2 through the O17 table: a marked cell is searched by bisection
+        of the index interval [a-1, a+k) of the intervals overlapping it (Sec.6
+        P:1545-1548: "the implicit balanced tree is traversed by consecutive
+        bisection of the index interval"); every other cell as sample_table3.
+        with_loads: also the node records read after the table (bisection:
+        one per probe)."""
+        t4 = self.table4()
+        rec = self.records()
+        shift = 32 - (self.m.bit_length() - 1)
+        out = np.empty(len(xi), dtype=np.int32)
+        visits = np.zeros(len(xi), dtype=np.int32)
+        for q, x in enumerate(np.asarray(xi, dtype=np.uint64).tolist()):
+            g = (x * self.m) >> 32
+            key32, ref = int(t4[g]["key32"]), int(t4[g]["ref"])
+            if ref >= 0 and key32 >> 31:  # bisection over the intervals a-1 .. a+k-1
+                a, kk = ref, key32 & 0x7FFFFFFF
+                lo, hi = a - 1, a + kk  # key_lo <= x 2^31 < key_hi
+                while hi - lo > 1:
+                    mid = (lo + hi) // 2
+                    visits[q] += 1
+                    if int(self.key[mid]) <= (x << 31):
+                        lo = mid
+                    else:
+                        hi = mid
+                out[q] = int(self.orig[lo])
+                continue
+            if ref >= 0 and key32:  # three intervals (O16)
+                xi0 = g << shift
+                out[q] = ref + (x >= xi0 + (key32 & 0xFFFF)) + (x >= xi0 + (key32 >> 16))
+                continue
+            if ref < 0:
+                out[q] = ~(ref + 1 if x < key32 else ref)
+                continue
+            j = ref
+            while j >= 0:
+                visits[q] += 1
+                j = int(rec[j]["c0"]) if (x << 31) < int(rec[j]["key"]) else int(rec[j]["c1"])
+            out[q] = ~j
+        return (out, visits) if with_loads else out
+
     def sample_table2(self, xi) -> np.ndarray:
         """Alg. 2 through the O13 table: plain Python loop."""
         t2 = self.table2()
@@ -224,6 +291,36 @@ def table3_of(t2, key, orig, cell, m) -> np.ndarray:
         s1 = -(-int(key[a]) >> 31) - xi0
         s2 = -(-int(key[a + 1]) >> 31) - xi0
         out[g] = (s1 | (s2 << 16), int(orig[a - 1]))
+    return out
+
+
+FALLBACK_SLACK = 4  # O17 (reading R21): the depth allowed above binary search
+
+
+def bisect_visits(k: int) -> int:
+    """Node records a bisection of the k + 1 intervals overlapping a cell with
+    k leaves reads at most: ceil(log2(k + 1))."""
+    return (k).bit_length() if k > 0 else 0  # ceil(log2(k + 1)) for k >= 0
+
+
+def table4_of(t3, D, k) -> np.ndarray:
+    """O17 (reading R21): the fallback of Sec.3 P:983-984 ("for degenerate
+    hierarchical structures the worst case may increase ... a fallback method
+    constructs such a structure upon detection to guarantee logarithmic
+    complexity"), with the balanced tree of Sec.6 P:1545-1548 that "does not
+    need to be built" (bisection of the index interval) and the criterion of
+    Sec.4 P:1516-1518 (an explicit tree only pays "if the maximum depth does
+    not exceed the number of comparisons required for binary search").  A cell
+    whose O16 entry is an anchor (key32 = 0, ref = a >= 0) is marked when its
+    radix depth D_g exceeds the bisection's ceil(log2(k_g + 1)) node reads by
+    more than FALLBACK_SLACK:
+        key32 = 2^31 | k_g,  ref = a  (O16 entries have key32 < 2^31)
+    Every other entry: the O16 entry."""
+    out = np.array(t3, dtype=TABLE2_DTYPE, copy=True)
+    for g in np.flatnonzero((out["ref"] >= 0) & (out["key32"] == 0)).tolist():
+        kk = int(k[g])
+        if int(D[g]) > bisect_visits(kk) + FALLBACK_SLACK:
+            out[g] = ((1 << 31) | kk, int(out["ref"][g]))
     return out
 
 

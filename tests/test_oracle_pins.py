@@ -521,3 +521,99 @@ def test_table3_descent_brute_force():
         assert np.array_equal(f.sample_table3(xs), want), t
         assert np.array_equal(f.sample(xs), want), t
     assert npack > 1000  # the inputs do exercise the packed cells
+
+
+# ---------------------------------------------------------------- O17 (reading R21): fallback
+
+def test_table4_geometric_chain_hand_derived():
+    """O17 on p_i = 2^-i (i < 20), m = 1: every split level is below the one
+    before it (the keys halve their distance to the top), so Alg. 1 builds a
+    chain -- the deepest leaf 19 sits under 19 internal nodes, 20 visits with
+    the anchor -- while bisection of the 21 intervals needs ceil(log2 21) = 5:
+    20 > 5 + 4, so the cell is marked (2^31 | 20, anchor 0), every xi is
+    answered in at most 5 reads, and the answers are the definition's."""
+    L = 20
+    p = np.exp2(-np.arange(L, dtype=np.float64)).astype(F32)
+    f = oracle.build(p, 1)
+    assert np.all(np.diff(f.lam[:-1].astype(np.int64)) < 0)  # a strictly falling chain
+    D, k = f.cell_depths()
+    assert (int(D[0]), int(k[0])) == (L, L)
+    assert oracle.bisect_visits(L) == 5
+    t4 = f.table4()
+    assert (int(t4[0]["key32"]), int(t4[0]["ref"])) == ((1 << 31) | L, 0)
+    w, _, _ = oracle.quantize(p)
+    xs = {0, 2**32 - 1}
+    for key in f.key.tolist():
+        b = -(-int(key) >> 31)
+        xs |= {b - 1, b, b + 1}
+    xs = np.array(sorted(x for x in xs if 0 <= x < 2**32), np.uint32)
+    got, visits = f.sample_table4(xs, with_loads=True)
+    assert [int(g) for g in got] == [_definition_index(w, int(x)) for x in xs]
+    assert int(visits.max()) <= 5
+
+
+def test_table4_balanced_not_marked():
+    """Equal weights (n = 1024, m = 1): keys j 2^53, a perfect radix tree of
+    10 internal levels -- 11 visits with the anchor, exactly the bisection's
+    ceil(log2 1025) = 11 -- so nothing is marked (O17 = O16)."""
+    f = oracle.build(np.ones(1024, F32), 1)
+    D, k = f.cell_depths()
+    assert (int(D[0]), int(k[0])) == (11, 1024)
+    assert oracle.bisect_visits(1024) == 11
+    assert f.table4().tobytes() == f.table3().tobytes()
+
+
+def test_cell_depths_brute_force():
+    """D_g from the reachable leaves equals the most visits over EVERY 32-bit
+    xi of the cell (m = 2^20: cells of 4096 xi, enumerated)."""
+    rng = np.random.default_rng(41)
+    m = 1 << 20
+    p = np.concatenate([np.exp2(-np.arange(30, dtype=np.float64)) * 1e-3,
+                        random_small(rng, 3000, zero_frac=0.2, dyn=30.0)]).astype(F32)
+    f = oracle.build(p, m)
+    D, _ = f.cell_depths()
+    cells = np.unique(f.cell)[:40].tolist() + np.flatnonzero(D == D.max())[:3].tolist()
+    for g in cells:
+        xs = np.arange(g << 12, (g + 1) << 12, dtype=np.uint64).astype(np.uint32)
+        _, loads = f.sample(xs, with_loads=True)
+        assert int(loads.max()) - 1 == int(D[g]), g
+
+
+def test_table4_descent_brute_force():
+    """Alg. 2 through the O17 table equals the inverse-CDF definition on
+    distributions with degenerate cells (geometric runs) and ordinary ones;
+    a marked cell never reads more than ceil(log2(k + 1)) records."""
+    rng = np.random.default_rng(43)
+    marked = 0
+    for t in range(24):
+        parts = []
+        for _ in range(int(rng.integers(1, 4))):
+            if rng.random() < 0.6:
+                L = int(rng.integers(8, 40))
+                parts.append(np.exp2(-np.arange(L, dtype=np.float64) * rng.uniform(0.7, 1.5))
+                             * rng.uniform(1e-6, 1.0))
+            else:
+                parts.append(random_small(rng, int(rng.integers(1, 60)), zero_frac=0.2, dyn=8.0))
+        p = np.concatenate(parts).astype(F32)
+        if not np.any(p > 0):
+            continue
+        m = int(rng.choice([1, 2, 3, 7, 64]))
+        f = oracle.build(p, m)
+        w, _, _ = oracle.quantize(p)
+        t4 = f.table4()
+        mk = np.flatnonzero((t4["ref"] >= 0) & (t4["key32"] >> 31 == 1))
+        marked += mk.size
+        xs = set(rng.integers(0, 2**32, 64).tolist()) | {0, 2**32 - 1}
+        for key in f.key.tolist():
+            b = -(-int(key) >> 31)
+            xs |= {b - 1, b, b + 1}
+        xs = np.array(sorted(x for x in xs if 0 <= x < 2**32), np.uint32)
+        got, visits = f.sample_table4(xs, with_loads=True)
+        for x, g in zip(xs.tolist(), got.tolist()):
+            assert g == _definition_index(w, x), (t, x)
+        cells = (xs.astype(np.uint64) * np.uint64(m)) >> np.uint64(32)
+        for g in mk.tolist():
+            sel = cells == g
+            if np.any(sel):
+                assert int(visits[sel].max()) <= oracle.bisect_visits(int(t4[g]["key32"]) & 0x7FFFFFFF)
+    assert marked > 5
