@@ -216,8 +216,8 @@ class Forest:
         for q, x in enumerate(np.asarray(xi, dtype=np.uint64).tolist()):
             g = (x * self.m) >> 32
             key32, ref = int(t4[g]["key32"]), int(t4[g]["ref"])
-            if ref >= 0 and key32 >> 31:  # bisection over the intervals a-1 .. a+k-1
-                a, kk = ref, key32 & 0x7FFFFFFF
+            if ref >= 0 and key32 >> 30 == 3:  # bisection over the intervals a-1 .. a+k-1
+                a, kk = ref, key32 & 0x3FFFFFFF
                 lo, hi = a - 1, a + kk  # key_lo <= x 2^31 < key_hi
                 while hi - lo > 1:
                     mid = (lo + hi) // 2
@@ -311,17 +311,23 @@ def table4_of(t3, D, k) -> np.ndarray:
     need to be built" (bisection of the index interval) and the criterion of
     Sec.4 P:1516-1518 (an explicit tree only pays "if the maximum depth does
     not exceed the number of comparisons required for binary search").  A cell
-    whose O16 entry is an anchor (key32 = 0, ref = a >= 0) is marked when its
-    radix depth D_g exceeds the bisection's ceil(log2(k_g + 1)) node reads by
-    more than FALLBACK_SLACK:
-        key32 = 2^31 | k_g,  ref = a  (O16 entries have key32 < 2^31)
-    Every other entry: the O16 entry."""
+    whose O16 entry is an anchor (key32 = 0, ref = a >= 0) and that holds k_g <
+    2^30 leaves is marked when its radix depth D_g exceeds the bisection's
+    ceil(log2(k_g + 1)) node reads by more than FALLBACK_SLACK:
+        key32 = 3 << 30 | k_g,  ref = a
+    (an O16 packed entry never has both top bits set: s2 <= 2^15, and s2 =
+    2^15 leaves s1 < 2^15 in the low bits).  Every other entry: the O16 entry."""
     out = np.array(t3, dtype=TABLE2_DTYPE, copy=True)
     for g in np.flatnonzero((out["ref"] >= 0) & (out["key32"] == 0)).tolist():
         kk = int(k[g])
-        if int(D[g]) > bisect_visits(kk) + FALLBACK_SLACK:
-            out[g] = ((1 << 31) | kk, int(out["ref"][g]))
+        if kk < (1 << 30) and int(D[g]) > bisect_visits(kk) + FALLBACK_SLACK:
+            out[g] = ((3 << 30) | kk, int(out["ref"][g]))
     return out
+
+
+def is_bisect(t4) -> np.ndarray:
+    """O17 marks: ref >= 0 and both top bits of key32 set."""
+    return (t4["ref"] >= 0) & ((t4["key32"] >> 30) == 3)
 
 
 def table2_of(table, key, orig, cell, m) -> np.ndarray:

@@ -530,7 +530,7 @@ def test_table4_geometric_chain_hand_derived():
     before it (the keys halve their distance to the top), so Alg. 1 builds a
     chain -- the deepest leaf 19 sits under 19 internal nodes, 20 visits with
     the anchor -- while bisection of the 21 intervals needs ceil(log2 21) = 5:
-    20 > 5 + 4, so the cell is marked (2^31 | 20, anchor 0), every xi is
+    20 > 5 + 4, so the cell is marked (3 << 30 | 20, anchor 0), every xi is
     answered in at most 5 reads, and the answers are the definition's."""
     L = 20
     p = np.exp2(-np.arange(L, dtype=np.float64)).astype(F32)
@@ -540,7 +540,7 @@ def test_table4_geometric_chain_hand_derived():
     assert (int(D[0]), int(k[0])) == (L, L)
     assert oracle.bisect_visits(L) == 5
     t4 = f.table4()
-    assert (int(t4[0]["key32"]), int(t4[0]["ref"])) == ((1 << 31) | L, 0)
+    assert (int(t4[0]["key32"]), int(t4[0]["ref"])) == ((3 << 30) | L, 0)
     w, _, _ = oracle.quantize(p)
     xs = {0, 2**32 - 1}
     for key in f.key.tolist():
@@ -601,7 +601,7 @@ def test_table4_descent_brute_force():
         f = oracle.build(p, m)
         w, _, _ = oracle.quantize(p)
         t4 = f.table4()
-        mk = np.flatnonzero((t4["ref"] >= 0) & (t4["key32"] >> 31 == 1))
+        mk = np.flatnonzero(oracle.is_bisect(t4))
         marked += mk.size
         xs = set(rng.integers(0, 2**32, 64).tolist()) | {0, 2**32 - 1}
         for key in f.key.tolist():
@@ -615,5 +615,27 @@ def test_table4_descent_brute_force():
         for g in mk.tolist():
             sel = cells == g
             if np.any(sel):
-                assert int(visits[sel].max()) <= oracle.bisect_visits(int(t4[g]["key32"]) & 0x7FFFFFFF)
+                assert int(visits[sel].max()) <= oracle.bisect_visits(int(t4[g]["key32"]) & 0x3FFFFFFF)
     assert marked > 5
+
+
+def test_table4_marks_never_collide_with_packed():
+    """An O16 packed entry can carry bit 31 but never both top bits: p = (2^46,
+    2^46 - 2^30, 2^30, 2^63 - 2^47) gives E = 62, B = 60, w = p / 4, T = 2^61
+    and keys 4 W = (0, 2^46, 2^47 - 2^30, 2^47); with m = 2^17 (cells key >>
+    46) cell 1 holds leaves 1, 2 and starts at xi0 = 2^15: s1 = 2^15 - xi0 =
+    0, s2 = ceil(2^16 - 1/2) - xi0 = 2^15 -- entry (2^31, orig(0) = 0).  O17's
+    marks are 3 << 30 | k, so this entry is no mark, and through the O17 table
+    cell 1 still answers as O16 and the definition do."""
+    p = np.array([2.0**46, 2.0**46 - 2.0**30, 2.0**30, 2.0**63 - 2.0**47], F32)
+    f = oracle.build(p, 1 << 17)
+    assert f.key.tolist() == [0, 1 << 46, (1 << 47) - (1 << 30), 1 << 47]
+    t3, t4 = f.table3(), f.table4()
+    assert (int(t3[1]["key32"]), int(t3[1]["ref"])) == (1 << 31, 0)
+    assert not np.any(oracle.is_bisect(t4))
+    xs = np.array([1 << 15, (1 << 16) - 2, (1 << 16) - 1], np.uint32)
+    w, _, _ = oracle.quantize(p)
+    want = [_definition_index(w, int(x)) for x in xs]
+    assert want == [1, 1, 1]
+    assert f.sample_table3(xs).tolist() == want
+    assert f.sample_table4(xs).tolist() == want
