@@ -424,6 +424,8 @@ def run_gpu(args):
                                     "pinned host out"}}
 
     quad = quad_summary(forest, xi, out, flush)
+    fallback = fallback_summary(forest, p, xi, out, flush)
+    forest.build(p)  # unmarked again
     xi_gen = None
     if wl["name"] != "c2_envmap":  # the Philox input, timed apart from sampling
         xi2 = torch.empty_like(xi)
@@ -481,6 +483,7 @@ def run_gpu(args):
                                                 "note": "context only: float32 CDF, not "
                                                         "bit-exact"},
                      "quad_records": quad,
+                     "fallback": fallback,
                      "xi_generation": xi_gen,
                      "loads_per_sample": {"avg": round(e_loads, 4), "avg32": round(avg32, 4),
                                           "max": max_loads, "of": 1 << 20,
@@ -560,6 +563,57 @@ def quad_summary(forest, xi, out, flush, reps=3):
             "ms_per_batch": round(t_s, 4), "build_quad_ms": round(t_q, 4),
             "identical_indices": same,
             "what": "4-ary collapsed 32-B records: one load per two levels (P:1537-1539)"}
+
+
+def fallback_summary(forest, p, xi, out, flush, reps=3):
+    """The degenerate-cell fallback (reading R21; rtf_build_fallback): device
+    time of the marking pass and of one batch through the marked table (L2
+    flushed before each launch, median of reps), index equality with out, and
+    the worst case over EVERY 32-bit xi (the per-cell depths the pass
+    measures): node reads + 1 table read with the radix trees alone and with
+    the marked cells bisected.  The forest is rebuilt afterwards by the caller
+    if it is sampled again unmarked."""
+    import numpy as np
+    import torch
+    out_f = torch.empty_like(out)
+
+    def timed(fn, reps=reps):
+        ts = []
+        for _ in range(reps):
+            flush.zero_()
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record()
+            fn()
+            b.record()
+            torch.cuda.synchronize()
+            ts.append(a.elapsed_time(b))
+        return statistics.median(ts)
+
+    def fb_once():
+        forest.build(p)  # untimed: an unmarked table for every measured pass
+        torch.cuda.synchronize()
+        return timed(lambda: forest.build_fallback(), reps=1)
+
+    t_f = statistics.median(fb_once() for _ in range(reps))
+    depth, last = forest.cell_depths()  # of the last pass, on an unmarked table
+    tab = forest.table_numpy()
+    marked = (tab["ref"] >= 0) & (tab["key32"] >> 30 == 3)
+    k = (tab["key32"].astype(np.int64) & 0x3FFFFFFF)
+    bis = np.where(marked, np.ceil(np.log2(k + 1)).astype(np.int64), 0)
+    worst_radix = int(depth.max()) + 1
+    worst_fb = int(np.where(marked, bis, depth).max()) + 1
+    t_s = timed(lambda: forest.sample(xi, out_f))
+    same = bool(torch.equal(out, out_f))
+    loads = forest.sample_loads(xi[: 1 << 20]).double()
+    del out_f
+    return {"value": round(xi.numel() / (t_s * 1e-3) / 1e9, 4), "unit": "G samples/s",
+            "ms_per_batch": round(t_s, 4), "build_fallback_ms": round(t_f, 4),
+            "cells_marked": int(marked.sum()), "identical_indices": same,
+            "worst_case_loads_all_xi": {"radix": worst_radix, "with_fallback": worst_fb},
+            "loads_per_sample": {"avg": round(loads.mean().item(), 4),
+                                 "max": int(loads.max().item()), "of": 1 << 20},
+            "what": "cells deeper than bisection + 4 reads searched by bisection "
+                    "(P:983-984, P:1516-1518, P:1545-1548)"}
 
 
 def c2_summary(args, dev, stream, flush, world):

@@ -99,7 +99,7 @@ typedef struct rtf_forest {
     uint32_t n;      /* entries per row                                   */
     uint32_t m;      /* guide-table cells per row                         */
     uint32_t rows;   /* 1, or the number of independent rows (batched)    */
-    uint32_t flags;  /* build flags                                       */
+    uint32_t flags;  /* build flags; RTF_FOREST_MARKED after rtf_build_fallback */
     rtf_node *nodes; /* rows * n records (the first n_pos of each row valid;
                         rows_build: slot n_pos < n holds key 2^63, "1")   */
     rtf_ref *table;  /* rows * m guide-table cells (rtf_ref)              */
@@ -108,6 +108,7 @@ typedef struct rtf_forest {
 
 /* rtf_build flags */
 #define RTF_BUILD_DEFAULT 0u
+#define RTF_FOREST_MARKED 0x100u /* set in rtf_forest.flags by rtf_build_fallback */
 #define RTF_BUILD_SMALL_TILES 1u /* 256-entry tiles: a test/debug schedule that moves most
                                     links into the cross-tile phase; same result bytes */
 
@@ -272,6 +273,25 @@ int rtf_build_cdf(const float *p, uint32_t n, uint64_t *cdf, rtf_header *header,
  * (identical results to rtf_sample on the same p). */
 int rtf_sample_bsearch(const uint64_t *cdf, uint32_t n, const rtf_header *header,
                        const uint32_t *xi, uint64_t count, int32_t *out, void *stream);
+
+/* Degenerate-cell fallback (reading R21; "for degenerate hierarchical
+ * structures the worst case may increase ... a fallback method constructs such
+ * a structure upon detection to guarantee logarithmic complexity", Sec.3
+ * P:983-984; criterion Sec.4).  Marks in f's guide table every
+ * anchor cell holding k < 2^30 leaves whose radix tree makes some 32-bit xi
+ * read more than ceil(log2(k + 1)) + 4 node records: key32 = 3 << 30 | k,
+ * ref = the cell's first leaf (a packed cell never has both top bits set).  rtf_sample and rtf_sample_loads then search
+ * such cells by bisection of their index interval (the implicit balanced tree
+ * of Sec.6): at most ceil(log2(k + 1)) reads.  Sampled indices are
+ * unchanged.  ws: >= rtf_fallback_bytes(m) bytes of device scratch; afterwards
+ * it holds per cell the radix depth (u32[m]) and the cell's last leaf (u32[m]).
+ * Sets RTF_FOREST_MARKED in f->flags (rtf_sample then launches its
+ * bisecting variant; the unmarked sampler carries no code for it).
+ * Asynchronous on `stream`; run it after rtf_build (a rebuild clears the
+ * marks and the flag); rtf_sample_quad does not read marked tables
+ * (RTF_EINVAL).  RTF_EINVAL for a rows forest or NULL pointers. */
+size_t rtf_fallback_bytes(uint32_t m);
+int rtf_build_fallback(rtf_forest *f, void *ws, size_t ws_bytes, void *stream);
 
 /* Eytzinger binary-search baseline (Sec.2.2 P:114-127 laid out for a GPU):
  * rtf_build_eytzinger writes the keys cdf[1..n-1] as a complete binary

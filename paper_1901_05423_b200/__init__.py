@@ -99,6 +99,7 @@ class Forest:
             raise ValueError(f"p has {p.numel()} entries, forest was sized for {self.n}")
         self._p = p  # keep alive while kernels run
         self._rec4_valid = False  # the 4-ary records describe the previous forest
+        self._marked = False      # a rebuild writes an unmarked table
         check(lib().rtf_build(_ptr(p), self.n, self.m, self.flags, _ptr(self._buf.forest),
                               self._buf.forest.numel(), _ptr(self._buf.ws),
                               self._buf.ws.numel(), _stream(stream), ctypes.byref(self.view)),
@@ -139,12 +140,36 @@ class Forest:
         """rtf_sample's indices through the quad records (build_quad() first)."""
         if getattr(self, "_rec4", None) is None or not getattr(self, "_rec4_valid", False):
             raise RuntimeError("sample_quad needs build_quad() after the latest build()")
+        if getattr(self, "_marked", False):
+            raise RuntimeError("sample_quad does not read tables marked by build_fallback()")
         xi = _u32_view(xi)
         if out is None:
             out = torch.empty(xi.numel(), dtype=torch.int32, device=xi.device)
         check(lib().rtf_sample_quad(ctypes.byref(self.view), _ptr(self._rec4), _ptr(xi),
                                     xi.numel(), _ptr(out), _stream(stream)), "rtf_sample_quad")
         return out
+
+    # ------------------------------------------- degenerate-cell fallback (R21)
+    def build_fallback(self, stream=None) -> "Forest":
+        """Mark the cells whose radix trees are deeper than bisection + 4 reads
+        (rtf_build_fallback); rtf_sample then bisects them.  Call after build()."""
+        L = lib()
+        nb = L.rtf_fallback_bytes(self.m)
+        if getattr(self, "_fb_ws", None) is None or self._fb_ws.numel() < nb:
+            self._fb_ws = _bytes_tensor(nb, self._buf.forest.device)
+        check(L.rtf_build_fallback(ctypes.byref(self.view), _ptr(self._fb_ws), self._fb_ws.numel(),
+                                   _stream(stream)), "rtf_build_fallback")
+        self._marked = True
+        return self
+
+    def cell_depths(self):
+        """After build_fallback(): per cell the radix depth (node reads of the
+        deepest xi, anchor cells; else 0) and the cell's last leaf, as int64 numpy."""
+        if getattr(self, "_fb_ws", None) is None:
+            raise RuntimeError("cell_depths needs build_fallback()")
+        torch.cuda.synchronize(self._buf.forest.device)
+        w = self._fb_ws[: 8 * self.m].view(torch.int32).cpu().numpy().astype(np.int64)
+        return w[: self.m], w[self.m: 2 * self.m]
 
     def sample_loads(self, xi: torch.Tensor, stream=None, plain: bool = False):
         """Per-sample memory loads of Alg. 2 (1 table cell + nodes visited);

@@ -13,7 +13,7 @@ constexpr int kMaxVisits2d = 64;
 // q_y = float32(float64(T_y) 2^(E_y - B_y - K)), K = max over non-empty rows of
 // E_y - B_y; an all-zero row gets 0, a row with NaN / Inf / negative data NaN
 // (so the marginal build reports the data error).  dense: bit y set if row y
-// has W positive weights (its index map is the identity).  One CTA; H <= 4096.
+// has W positive weights (its index map is the identity).  One CTA.
 __global__ void __launch_bounds__(kRowWeightThreads)
     k_row_weights(const rtf_header* __restrict__ hdr, uint32_t H, uint32_t W, float* __restrict__ q,
                   uint32_t* __restrict__ dense) {
@@ -44,9 +44,9 @@ __global__ void __launch_bounds__(kRowWeightThreads)
 // one Alg. 2 descent in a row forest (nodes + table of that row); returns ~leaf
 __device__ __forceinline__ int32_t descend_row(const rtf_node* __restrict__ nodes,
                                                const rtf_ref* __restrict__ table, uint32_t m,
-                                               uint32_t x) {
+                                               uint32_t xmask, uint32_t x) {
     const int2 e = __ldg(reinterpret_cast<const int2*>(table) + (uint32_t)(((uint64_t)x * m) >> 32));
-    int32_t j = (e.y >= 0 || x >= (uint32_t)e.x) ? e.y : e.y + 1;
+    int32_t j = table_step(e, x, x & xmask);
     const uint64_t x63 = (uint64_t)x << 31;
     for (int d = 0; j >= 0 && d < kMaxVisits2d; ++d) {
         const ulonglong2 r = __ldg(reinterpret_cast<const ulonglong2*>(nodes + j));
@@ -67,8 +67,9 @@ __device__ __forceinline__ double rel_pos(const rtf_node* __restrict__ nodes, in
 }
 
 __global__ void __launch_bounds__(k2dThreads, 8)  // 32 registers: 2048 threads per SM
-    k_sample_2d(rtf_forest2d f, const uint32_t* __restrict__ xi1, const uint32_t* __restrict__ xi2,
-                uint64_t count, int32_t* __restrict__ pixel, float* __restrict__ pos) {
+    k_sample_2d(rtf_forest2d f, uint32_t xmask_x, uint32_t xmask_y, const uint32_t* __restrict__ xi1,
+                const uint32_t* __restrict__ xi2, uint64_t count, int32_t* __restrict__ pixel,
+                float* __restrict__ pos) {
     const uint64_t gs = (uint64_t)gridDim.x * blockDim.x;
     const bool bad = f.marginal.header->status != 0;
     const bool marg_dense = f.marginal.header->n_pos == f.H;  // every row weight positive
@@ -77,10 +78,10 @@ __global__ void __launch_bounds__(k2dThreads, 8)  // 32 registers: 2048 threads 
         int32_t out = INT32_MAX;
         float px = __int_as_float(0x7fc00000), py = px;
         if (!bad) {
-            const int32_t jy = descend_row(f.marginal.nodes, f.marginal.table, f.my, a);
+            const int32_t jy = descend_row(f.marginal.nodes, f.marginal.table, f.my, xmask_y, a);
             const int32_t y = ~jy;
             const rtf_node* rn = f.rows.nodes + (size_t)y * f.W;
-            const int32_t jx = descend_row(rn, f.rows.table + (size_t)y * f.mx, f.mx, b);
+            const int32_t jx = descend_row(rn, f.rows.table + (size_t)y * f.mx, f.mx, xmask_x, b);
             const int32_t x = ~jx;
             if (jy >= 0 || jx >= 0) {
                 out = INT32_MIN;  // corrupted forest (a descent did not end in a leaf)
@@ -103,6 +104,46 @@ __global__ void __launch_bounds__(k2dThreads, 8)  // 32 registers: 2048 threads 
     }
 }
 
+// Rows built by the cooperative kernel (wider than the row kernel's 4096
+// entries, or a marginal of more than 4096 rows): the row-local compacted
+// leaf index of every entry (-1 for a zero weight) by a block scan per row,
+// and the key "1" after the row's last leaf when the row has zero weights
+// (what the row kernel stores there; rel_pos reads it).  One CTA per row.
+constexpr int kJmapThreads = 1024;
+__global__ void __launch_bounds__(kJmapThreads)
+    k_rows_jmap(const float* __restrict__ p, uint32_t W, const rtf_header* __restrict__ hdr,
+                rtf_node* __restrict__ nodes, int32_t* __restrict__ jmap) {
+    __shared__ uint32_t s_cnt[kJmapThreads / 32];
+    const uint32_t y = blockIdx.x, lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const float* row = p + (size_t)y * W;
+    int32_t* jm = jmap + (size_t)y * W;
+    uint32_t base = 0;
+    for (uint32_t x0 = 0; x0 < W; x0 += kJmapThreads) {
+        const uint32_t x = x0 + threadIdx.x;
+        const bool pos = x < W && row[x] > 0.0f;
+        const uint32_t bal = __ballot_sync(0xffffffffu, pos);
+        if (lane == 0) s_cnt[warp] = __popc(bal);
+        __syncthreads();
+        uint32_t before = base, total = 0;
+        for (uint32_t w = 0; w < kJmapThreads / 32; ++w) {
+            if (w < warp) before += s_cnt[w];
+            total += s_cnt[w];
+        }
+        if (x < W) jm[x] = pos ? (int32_t)(before + __popc(bal & ((1u << lane) - 1u))) : -1;
+        base += total;
+        __syncthreads();
+    }
+    if (threadIdx.x == 0 && hdr[y].status == 0 && hdr[y].n_pos < W)
+        nodes[(size_t)y * W + hdr[y].n_pos].key = kOne63;
+}
+
+cudaError_t launch_rows_jmap(const float* p, uint32_t W, uint32_t H, const rtf_header* hdr,
+                             rtf_node* nodes, int32_t* jmap, cudaStream_t st, int* launches) {
+    k_rows_jmap<<<H, kJmapThreads, 0, st>>>(p, W, hdr, nodes, jmap);
+    ++*launches;
+    return cudaGetLastError();
+}
+
 cudaError_t launch_row_weights(const rtf_header* rows_hdr, uint32_t H, uint32_t W, float* q,
                                uint32_t* dense, cudaStream_t st, int* launches) {
     k_row_weights<<<1, kRowWeightThreads, 0, st>>>(rows_hdr, H, W, q, dense);
@@ -116,7 +157,8 @@ cudaError_t launch_sample_2d(const rtf_forest2d& f, const uint32_t* xi1, const u
     if (count == 0) return cudaSuccess;
     const uint64_t want = (count + k2dThreads - 1) / k2dThreads;
     const uint32_t grid = (uint32_t)std::max<uint64_t>(1, std::min<uint64_t>(want, (uint64_t)device_sms() * 32ull));
-    k_sample_2d<<<grid, k2dThreads, 0, st>>>(f, xi1, xi2, count, pixel, pos);
+    k_sample_2d<<<grid, k2dThreads, 0, st>>>(f, xoff_mask(f.mx), xoff_mask(f.my), xi1, xi2, count,
+                                             pixel, pos);
     ++*launches;
     return cudaGetLastError();
 }

@@ -198,6 +198,7 @@ int rtf_build_quad(const rtf_forest* f, void* rec4, size_t rec4_bytes, void* str
 int rtf_sample_quad(const rtf_forest* f, const void* rec4, const uint32_t* xi, uint64_t count,
                     int32_t* out, void* stream) {
     if (!f || !f->table || !f->header || f->rows != 1 || !rec4) return RTF_EINVAL;
+    if (f->flags & RTF_FOREST_MARKED) return RTF_EINVAL;  // the quad sampler does not bisect
     if (((uintptr_t)rec4 & 31u) != 0) return RTF_EINVAL;
     if (count && (!xi || !out)) return RTF_EINVAL;
     if ((((uintptr_t)xi | (uintptr_t)out) & 3u) != 0) return RTF_EINVAL;
@@ -242,8 +243,12 @@ int rtf_sample_rows(const rtf_forest* f, const uint32_t* row, const uint32_t* xi
 
 namespace {
 struct Layout2d {
-    size_t rows, marginal, rows_jmap, marg_jmap, weights, dense, total;
+    size_t rows, marginal, rows_jmap, marg_jmap, weights, dense, ws, ws_bytes, total;
 };
+// rows wider than the row kernel's 4096 entries (or with more than 4096
+// cells), and a marginal of more than 4096 rows, are built one distribution at
+// a time by the cooperative kernel, which needs a build workspace
+bool rows_big(uint32_t W, uint32_t mx) { return W > rtf::kRowsMax || mx > rtf::kRowsMax; }
 Layout2d layout_2d(uint32_t W, uint32_t H, uint32_t mx, uint32_t my) {
     Layout2d L;
     size_t off = 0;
@@ -259,14 +264,22 @@ Layout2d layout_2d(uint32_t W, uint32_t H, uint32_t mx, uint32_t my) {
     off += align_up(sizeof(float) * (size_t)H);
     L.dense = off;
     off += align_up(sizeof(uint32_t) * (((size_t)H + 31) / 32));
+    L.ws = off;
+    L.ws_bytes = 0;
+    if (rows_big(W, mx) || rows_big(H, my)) {
+        rtf::WsLayout wl;
+        L.ws_bytes = std::max(rows_big(W, mx) ? rtf::build_workspace_layout(W, mx, 0, &wl) : 0,
+                              rows_big(H, my) ? rtf::build_workspace_layout(H, my, 0, &wl) : 0);
+        off += align_up(L.ws_bytes);
+    }
     L.total = off;
     return L;
 }
 int check_2d(uint32_t W, uint32_t H, uint32_t mx, uint32_t my) {
     if (W == 0 || H == 0 || mx == 0 || my == 0) return RTF_EINVAL;
-    if (W > rtf::kRowsMax || H > rtf::kRowsMax || mx > rtf::kRowsMax || my > rtf::kRowsMax)
-        return RTF_ETOOLARGE;
-    return RTF_OK;
+    if ((uint64_t)W * H > 0x7fffffffull) return RTF_ETOOLARGE;  // pixel indices are int32
+    if (int s = check_nm(W, mx)) return s;
+    return check_nm(H, my);
 }
 }  // namespace
 
@@ -295,15 +308,28 @@ int rtf_build_2d(const float* p, uint32_t W, uint32_t H, uint32_t mx, uint32_t m
     out->rows_dense = reinterpret_cast<uint32_t*>(b + L.dense);
     cudaStream_t st = as_stream(stream);
     int launches = 0;
-    cudaError_t e = rtf::launch_build_rows(p, H, W, mx, out->rows.header, out->rows.nodes,
-                                           out->rows.table, out->rows_jmap, st, &launches);
+    // one distribution of n entries and m cells per row of `rows` (the row
+    // kernel, or one cooperative build per row, then the index maps)
+    auto build = [&](const float* q, uint32_t rows, uint32_t n, uint32_t m, rtf_forest& f,
+                     int32_t* jmap) -> cudaError_t {
+        if (!rows_big(n, m))
+            return rtf::launch_build_rows(q, rows, n, m, f.header, f.nodes, f.table, jmap, st,
+                                          &launches);
+        rtf::WsLayout wl;
+        rtf::build_workspace_layout(n, m, 0, &wl);
+        void* ws = b + L.ws;
+        cudaError_t e = cudaMemsetAsync(ws, 0, wl.spine, st);  // rtf_workspace_init
+        for (uint32_t y = 0; y < rows && e == cudaSuccess; ++y)
+            e = rtf::launch_build(q + (size_t)y * n, n, m, 0, f.header + y, f.nodes + (size_t)y * n,
+                                  f.table + (size_t)y * m, nullptr, ws, wl, st, &launches);
+        if (e == cudaSuccess) e = rtf::launch_rows_jmap(q, n, rows, f.header, f.nodes, jmap, st, &launches);
+        return e;
+    };
+    cudaError_t e = build(p, H, W, mx, out->rows, out->rows_jmap);
     if (e == cudaSuccess)
         e = rtf::launch_row_weights(out->rows.header, H, W, out->weights, out->rows_dense, st,
                                     &launches);
-    if (e == cudaSuccess)
-        e = rtf::launch_build_rows(out->weights, 1, H, my, out->marginal.header,
-                                   out->marginal.nodes, out->marginal.table, out->marg_jmap, st,
-                                   &launches);
+    if (e == cudaSuccess) e = build(out->weights, 1, H, my, out->marginal, out->marg_jmap);
     return finish(e, launches);
 }
 
@@ -349,6 +375,19 @@ int rtf_sample_bsearch(const uint64_t* cdf, uint32_t n, const rtf_header* header
     int launches = 0;
     cudaError_t e = rtf::launch_bsearch(cdf, n, header, xi, count, out, as_stream(stream),
                                         &launches);
+    return finish(e, launches);
+}
+
+size_t rtf_fallback_bytes(uint32_t m) { return 2 * sizeof(uint32_t) * (size_t)(m ? m : 1); }
+
+int rtf_build_fallback(rtf_forest* f, void* ws, size_t ws_bytes, void* stream) {
+    if (!f || !f->nodes || !f->table || !f->header || f->rows != 1 || !ws) return RTF_EINVAL;
+    if (((uintptr_t)ws & 3u) != 0) return RTF_EINVAL;
+    if (ws_bytes < rtf_fallback_bytes(f->m)) return RTF_ENOSPACE;
+    uint32_t* depth = static_cast<uint32_t*>(ws);
+    int launches = 0;
+    cudaError_t e = rtf::launch_fallback(*f, depth, depth + f->m, as_stream(stream), &launches);
+    if (e == cudaSuccess) f->flags |= RTF_FOREST_MARKED;
     return finish(e, launches);
 }
 

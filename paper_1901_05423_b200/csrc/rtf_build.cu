@@ -26,6 +26,7 @@
 #include "rtf_device.cuh"
 #include "rtf_internal.h"
 #include <atomic>
+#include <type_traits>
 #include <cstdlib>
 #include <cstring>
 #include <cuda.h>
@@ -107,6 +108,7 @@ struct BuildArgs {
     uint64_t* cdf;                // CDF mode only
     bool vec;
     bool tma_store;               // records leave through the tensor maps (else plain stores)
+    bool pack2;                   // two-leaf cells packed into the table (R20, pack2_possible(m))
 };
 
 // ------------------------------------------------------------ grid barrier
@@ -798,17 +800,17 @@ __global__ void __launch_bounds__(THREADS, MINB)
         // then every warp scans the warp totals itself
         uint64_t w[VPT];
         uint64_t tw = 0;
-        uint32_t posmask = 0;
+        uint32_t posmask_in = 0;
 #pragma unroll
         for (int k = 0; k < VPT; ++k) {
             w[k] = quantize(x[k], scale);
             tw += w[k];
-            posmask |= (w[k] != 0ull ? 1u : 0u) << k;
+            posmask_in |= (w[k] != 0ull ? 1u : 0u) << k;
         }
-        const uint32_t tc = __popc(posmask);
-        s_clast[tid] = posmask ? 31 - __clz((int)posmask) : -1;
+        const uint32_t tc_in = __popc(posmask_in);
+        s_clast[tid] = posmask_in ? 31 - __clz((int)posmask_in) : -1;
         uint64_t wi = tw;
-        uint32_t ci = tc;
+        uint32_t ci = tc_in;
 #pragma unroll
         for (int d = 1; d < 32; d <<= 1) {
             const uint64_t tw2 = shfl_up_u64(wi, d);
@@ -849,7 +851,7 @@ __global__ void __launch_bounds__(THREADS, MINB)
             }
         }
         uint64_t w_ex;
-        uint32_t c_ex, cnt;
+        uint32_t c_ex_in, cnt;
         {
             uint64_t ww = lane < NW ? s_w[lane] : 0ull;
             uint32_t cc = lane < NW ? s_c[lane] : 0u;
@@ -866,13 +868,24 @@ __global__ void __launch_bounds__(THREADS, MINB)
             const uint32_t cb = __shfl_sync(0xffffffffu, cc, warp ? warp - 1 : 0);
             cnt = __shfl_sync(0xffffffffu, cc, NW - 1);
             w_ex = (warp ? wb : 0ull) + wi - tw;
-            c_ex = (warp ? cb : 0u) + ci - tc;
+            c_ex_in = (warp ? cb : 0u) + ci - tc_in;
         }
+        // The rest of the tile, specialised for tiles whose TILE entries are
+        // all positive (ALLPOS: leaves = entries, every test on the positive
+        // mask folds away) and for the general case; the choice is uniform
+        // across the CTA (cnt), so the barriers inside stay CTA-wide.
+        auto tile_body = [&](auto allpos) {
+        constexpr bool ALLPOS = decltype(allpos)::value;
+        const uint32_t posmask = ALLPOS ? 0xffu : posmask_in;
+        const uint32_t tc = ALLPOS ? (uint32_t)VPT : tc_in;
+        const uint32_t c_ex = ALLPOS ? tid * (uint32_t)VPT : c_ex_in;
         const uint32_t j0 = pre.cnt;      // global index of the tile's first leaf
         const uint32_t sh = j0 & 63u;     // record l is staged at stage_pos(l + sh)
         // the previous positive entry (the first own leaf's left neighbour)
         int32_t prevo = -1;
-        if (tc) {
+        if (ALLPOS) {
+            prevo = tid ? (int32_t)(first - 1u) + ib : (j0 ? pre.last : -1);
+        } else if (tc) {
             int32_t u = (int32_t)tid - 1;
             while (u >= 0 && s_clast[u] < 0) --u;
             prevo = u >= 0 ? (int32_t)(t * TILE + (uint32_t)u * VPT) + s_clast[u] + ib
@@ -887,7 +900,7 @@ __global__ void __launch_bounds__(THREADS, MINB)
 #pragma unroll
             for (int k = 0; k < VPT; ++k) {
                 const uint64_t wk = w[k];
-                if (wk) w[k] = fixed_point(W, nm);
+                if (ALLPOS || wk) w[k] = fixed_point(W, nm);
                 W += wk;
             }
             if (tc && W != T) kn = fixed_point(W, nm);
@@ -1013,6 +1026,55 @@ __global__ void __launch_bounds__(THREADS, MINB)
         }
         __syncthreads();
         RTF_TICK(4);
+
+        // (5b) cells holding exactly two leaves a, a+1 (reading R20) with
+        // leaf a-1 in this tile (the rest: phase E): packed into the table by
+        // the owner of leaf a+1, replacing the anchor written in (3), from
+        // the walls (split level 64) after leaves a+1 and a-1 and none after
+        // leaf a, and the staged records of leaves a, a+1 (keys; as prefilled,
+        // ~orig(a-1) = the anchor's child0 and ~orig(a+1) = child1 of the
+        // cell root)
+        if (A.pack2 && tc) {
+            uint32_t glo, ghi;
+            above(lo32, hi32, kLamBoundary - 1u, glo, ghi);  // the walls
+            const uint32_t wm = (((glo * 0x00204081u) >> 28) & 0xfu) | ((((ghi * 0x00204081u) >> 28) & 0xfu) << 4);
+            // bit r + 2: a wall after own leaf r; bits 1, 0: after the two
+            // leaves before own leaf 0 (earlier threads of the tile)
+            uint32_t ext = wm << 2;
+            if ((wm & 3u) && c_ex > 0) {
+                int32_t u = (int32_t)tid - 1;
+                while (s_cmax[u] == 0) --u;
+                const unsigned long long lpu = s_clp[u];
+                const uint32_t cu = c_ex - s_ccex[u];  // leaves of thread u
+                ext |= (lam_at((uint32_t)lpu, (uint32_t)(lpu >> 32), cu - 1u) == kLamBoundary) ? 2u : 0u;
+                uint32_t lb = 0xffu;
+                if (cu >= 2) {
+                    lb = lam_at((uint32_t)lpu, (uint32_t)(lpu >> 32), cu - 2u);
+                } else {
+                    int32_t u2 = u - 1;
+                    while (u2 >= 0 && s_cmax[u2] == 0) --u2;
+                    if (u2 >= 0) {
+                        const unsigned long long lp2 = s_clp[u2];
+                        lb = lam_at((uint32_t)lp2, (uint32_t)(lp2 >> 32), s_ccex[u] - s_ccex[u2] - 1u);
+                    }
+                }
+                ext |= lb == kLamBoundary ? 1u : 0u;
+            }
+            // own leaf r ends a two-leaf cell: walls after r and r - 2, none after r - 1
+            uint32_t pat = (ext >> 2) & ~(ext >> 1) & ext & ((1u << tc) - 1u);
+            pat &= c_ex >= 2 ? 0xffu : (c_ex == 1 ? 0xfeu : 0xfcu);  // leaf a-1 in this tile
+            while (pat) {
+                const uint32_t q = c_ex + (uint32_t)__ffs(pat) - 1u;  // local index of leaf a+1
+                pat &= pat - 1u;
+                const uint4 ra = lds_v4(a_stage + 16u * stage_pos(q - 1u + sh));
+                const uint4 rb = lds_v4(a_stage + 16u * stage_pos(q + sh));
+                const uint64_t kb = (uint64_t)rb.x | ((uint64_t)rb.y << 32);
+                const uint32_t g = cell_fn(kb);
+                const uint2 e = pack2_cell(g, A.mshift - 31u, (uint64_t)ra.x | ((uint64_t)ra.y << 32),
+                                           kb, ~(int32_t)ra.z, ~(int32_t)rb.w);
+                if (e.x) st_cell(table_at(g), g, e.x, (int32_t)e.y);
+            }
+        }
 
         // (6) the forest.  A gap's node hangs under the nearer-in-level of its
         // nearest greater split levels on either side (Alg. 1's merge order,
@@ -1187,6 +1249,9 @@ __global__ void __launch_bounds__(THREADS, MINB)
                 s_c0next = kNoLink;
             }
         }
+        };
+        if (cnt == (uint32_t)TILE) tile_body(std::true_type{});
+        else tile_body(std::false_type{});
         RTF_TICK(6);
     }
     if (tid == kIssuer && store_pending) {  // every record written before the grid barrier
@@ -1285,6 +1350,39 @@ __global__ void __launch_bounds__(THREADS, MINB)
                                                          (int32_t)j0);
                         if ((int32_t)e.y != (int32_t)j0)
                             st_cell(A.table, cell_fn(key), e.x, (int32_t)e.y);
+                    }
+                    // two-leaf cells across the row boundary (R20; (5b) packs the rest):
+                    // leaves {j0, j0+1} (the row's first gap inside the cell, its
+                    // second a wall) or {j0-1, j0} (the previous row's last gap
+                    // inside the cell, the one before it a wall); the records hold
+                    // the keys and, as prefilled, ~orig(a-1) (anchor child0) and
+                    // ~orig(a+1) (child1 of the cell root)
+                    if (A.pack2) {
+                        uint32_t a = 0xffffffffu;
+                        if (lamp == kLamBoundary && lam0 < kLamBoundary && wL &&
+                            __ldcg(&S->iL[64]) == 1u && j0 >= 1) {
+                            a = j0;
+                        } else if (lam0 == kLamBoundary && lamp < kLamBoundary && u >= 0 && j0 >= 2) {
+                            const TileSpine* U = SP + u;
+                            const uint32_t cu = __ldcg(&U->cnt);
+                            bool wall2;  // the gap before leaf j0-1 is a wall
+                            if (cu >= 2) {
+                                wall2 = (__ldcg(&U->walls) & 2u) && __ldcg(&U->iR[64]) == cu - 2u;
+                            } else {
+                                const int32_t u2 = row_left(A.tmax, A.bmax, (uint32_t)u, 0u);
+                                wall2 = u2 < 0 || spine_lowest(__ldcg(&SP[u2].mR),
+                                                               __ldcg(&SP[u2].walls) & 2u) == kLamBoundary;
+                            }
+                            if (wall2) a = j0 - 1;
+                        }
+                        if (a != 0xffffffffu && local(a)) {
+                            const uint64_t ka = __ldcg(&A.nodes[a].key), kb = __ldcg(&A.nodes[a + 1].key);
+                            const uint32_t g = cell_fn(kb);
+                            const uint2 e = pack2_cell(g, A.mshift - 31u, ka, kb,
+                                                       ~__ldcg(&A.nodes[a].child[0]),
+                                                       ~__ldcg(&A.nodes[a + 1].child[1]));
+                            if (e.x) st_cell(A.table, g, e.x, (int32_t)e.y);
+                        }
                     }
                 } else if (e == 1) {  // left child of the last gap, linked in the tile
                     const int32_t c = __ldcg(&S->c0_next);
@@ -1531,6 +1629,12 @@ cudaError_t launch_build(const float* p, uint32_t n, uint32_t m, uint32_t flags,
     alignas(64) CUtensorMap tmb, tms;
     std::memset(&tmb, 0, sizeof(tmb));
     std::memset(&tms, 0, sizeof(tms));
+    A.mshift = 63u - (uint32_t)ceil_log2_u32(m);
+#ifdef RTF_NO_PACK2
+    A.pack2 = false;
+#else
+    A.pack2 = !cdf && pack2_possible(m);
+#endif
     A.tma_store = !cdf && (A.phases & kPhTiles) &&
                   node_tensor_maps(nodes, sc ? sc->n_global : n, &tmb, &tms);
     const bool small = flags & RTF_BUILD_SMALL_TILES;

@@ -329,6 +329,56 @@ __device__ __forceinline__ uint2 single_leaf_cell(uint64_t key_a, int32_t orig_a
     return make_uint2(0u, (uint32_t)anchor);
 }
 
+// Packed three-interval cells (reading R20, oracle O16): a cell of a
+// power-of-two table with m >= 2^17 (so a cell spans at most 2^15 xi values,
+// its first xi being xi0 = g 2^32 / m) that holds exactly the two leaves a,
+// a+1 -- overlapped by the intervals a-1, a, a+1 with orig(a+1) = orig(a-1) + 2
+// and a >= 1 -- stores both split points as offsets from xi0 next to
+// orig(a-1): key32 = s1 | s2 << 16 (s = ceil(key / 2^31) - xi0, s2 >= 1),
+// ref = orig(a-1) >= 0.  "Further information could also be stored in the
+// reference": no node is read for such a cell.
+constexpr uint32_t kPackMinLog2M = 17;
+
+__host__ __device__ __forceinline__ bool pack2_possible(uint32_t m) {
+    return m >= (1u << kPackMinLog2M) && (m & (m - 1)) == 0;
+}
+
+// the packed entry of the two-leaf cell g (leaves a, a+1 with keys ka, kb and
+// original indices orig(a-1) = op, orig(a+1) = oq), or {0, 0} when the three
+// intervals are not consecutive (a zero weight between: the anchor stays).
+// shift = 32 - log2 m.
+__device__ __forceinline__ uint2 pack2_cell(uint32_t g, uint32_t shift, uint64_t ka, uint64_t kb,
+                                            int32_t op, int32_t oq) {
+    if (oq != op + 2) return make_uint2(0u, 0u);
+    const uint64_t xi0 = (uint64_t)g << shift;
+    const uint32_t s1 = (uint32_t)(((ka + 0x7fffffffull) >> 31) - xi0);
+    const uint32_t s2 = (uint32_t)(((kb + 0x7fffffffull) >> 31) - xi0);
+    return make_uint2(s1 | s2 << 16, (uint32_t)op);
+}
+
+// Alg. 2's first step on a guide-table cell e (rtf_ref as int2) for xi = x:
+// a node reference (anchor: key32 = 0, ref >= 0), a packed three-interval
+// cell (key32 != 0, ref >= 0; xoff = x mod (2^32 / m)), or a leaf that a
+// two-interval cell (key32 != 0, ref < 0; reading R18) splits with one
+// comparison (key32 = 0, ref < 0: one interval).  Returns a node index >= 0
+// or ~leaf.
+__device__ __forceinline__ int32_t table_step(int2 e, uint32_t x, uint32_t xoff) {
+    if (e.y >= 0) {
+        if (e.x == 0) return e.y;
+        const uint32_t s1 = (uint32_t)e.x & 0xffffu, s2 = (uint32_t)e.x >> 16;
+        return ~(e.y + (xoff >= s1 ? 1 : 0) + (xoff >= s2 ? 1 : 0));
+    }
+    return x >= (uint32_t)e.x ? e.y : e.y + 1;
+}
+
+// x mod (2^32 / m) for a power-of-two m (the offset table_step needs), else 0
+__host__ __device__ __forceinline__ uint32_t xoff_mask(uint32_t m) {
+    if (m & (m - 1)) return 0u;
+    uint32_t lg = 0;
+    while ((1u << lg) < m) ++lg;
+    return lg == 0 ? 0xffffffffu : ((1u << (32u - lg)) - 1u);
+}
+
 __device__ __forceinline__ void st_cell(rtf_ref* table, uint32_t g, uint32_t key32, int32_t ref) {
     *reinterpret_cast<uint2*>(table + g) = make_uint2(key32, (uint32_t)ref);
 }

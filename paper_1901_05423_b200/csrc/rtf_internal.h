@@ -85,6 +85,8 @@ cudaError_t launch_build_rows(const float* p, uint32_t rows, uint32_t n_row, uin
                               cudaStream_t st, int* launches);
 
 // 2-D (Sec.6): row weights from the rows' headers, and the component-wise sampler
+cudaError_t launch_rows_jmap(const float* p, uint32_t W, uint32_t H, const rtf_header* hdr,
+                             rtf_node* nodes, int32_t* jmap, cudaStream_t st, int* launches);
 cudaError_t launch_row_weights(const rtf_header* rows_hdr, uint32_t H, uint32_t W, float* q,
                                uint32_t* dense, cudaStream_t st, int* launches);
 cudaError_t launch_sample_2d(const rtf_forest2d& f, const uint32_t* xi1, const uint32_t* xi2,
@@ -100,6 +102,8 @@ cudaError_t launch_sample_f32(const rtf_forest& f, const float* xi, uint64_t cou
 cudaError_t launch_sample_loads(const rtf_forest& f, const uint32_t* xi, uint64_t count,
                                 int32_t* loads, int32_t* loads_plain, cudaStream_t st,
                                 int* launches);
+cudaError_t launch_fallback(const rtf_forest& f, uint32_t* depth, uint32_t* last, cudaStream_t st,
+                            int* launches);
 // 4-ary collapsed records (rtf_quad.cu)
 cudaError_t launch_collapse4(const rtf_forest& f, void* rec4, cudaStream_t st, int* launches);
 cudaError_t launch_sample4(const rtf_forest& f, const void* rec4, const uint32_t* xi,

@@ -68,15 +68,16 @@ __device__ __forceinline__ int32_t quad_step(const uint4* __restrict__ rec4, int
 }
 
 __device__ __forceinline__ int32_t cell_ref(const rtf_ref* __restrict__ table, uint32_t m,
-                                            uint32_t x) {
+                                            uint32_t xmask, uint32_t x) {
     const int2 e = __ldg(reinterpret_cast<const int2*>(table) + (uint32_t)(((uint64_t)x * m) >> 32));
-    return (e.y >= 0 || x >= (uint32_t)e.x) ? e.y : e.y + 1;
+    return table_step(e, x, x & xmask);
 }
 
 // four samples per thread in lock-step, as k_sample
 __global__ void __launch_bounds__(kQuadThreads)
     k_sample4(const uint4* __restrict__ rec4, const rtf_ref* __restrict__ table,
-              const rtf_header* __restrict__ hdr, uint32_t m, const uint32_t* __restrict__ xi,
+              const rtf_header* __restrict__ hdr, uint32_t m, uint32_t xmask,
+              const uint32_t* __restrict__ xi,
               uint64_t count, int32_t* __restrict__ out, bool vec) {
     const uint64_t gt = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
     const uint64_t gs = (uint64_t)gridDim.x * blockDim.x;
@@ -89,7 +90,7 @@ __global__ void __launch_bounds__(kQuadThreads)
             const uint32_t x[4] = {xv.x, xv.y, xv.z, xv.w};
             int32_t j[4];
 #pragma unroll
-            for (int k = 0; k < 4; ++k) j[k] = bad ? -1 : cell_ref(table, m, x[k]);
+            for (int k = 0; k < 4; ++k) j[k] = bad ? -1 : cell_ref(table, m, xmask, x[k]);
             for (int it = 0; (j[0] & j[1] & j[2] & j[3]) >= 0 && it < kMaxQuadVisits; ++it) {
 #pragma unroll
                 for (int k = 0; k < 4; ++k)
@@ -106,7 +107,7 @@ __global__ void __launch_bounds__(kQuadThreads)
     }
     for (uint64_t k = done + gt; k < count; k += gs) {
         const uint32_t x = xi[k];
-        int32_t j = bad ? -1 : cell_ref(table, m, x);
+        int32_t j = bad ? -1 : cell_ref(table, m, xmask, x);
         for (int it = 0; j >= 0 && it < kMaxQuadVisits; ++it) j = quad_step(rec4, j, x);
         out[k] = bad ? INT32_MAX : (j >= 0 ? INT32_MIN : ~j);
     }
@@ -129,7 +130,7 @@ cudaError_t launch_sample4(const rtf_forest& f, const void* rec4, const uint32_t
     if (count == 0) return cudaSuccess;
     const bool vec = (((uintptr_t)xi | (uintptr_t)out) & 15u) == 0;
     k_sample4<<<quad_grid(vec ? (count + 3) / 4 : count), kQuadThreads, 0, st>>>(
-        static_cast<const uint4*>(rec4), f.table, f.header, f.m, xi, count, out, vec);
+        static_cast<const uint4*>(rec4), f.table, f.header, f.m, xoff_mask(f.m), xi, count, out, vec);
     ++*launches;
     return cudaGetLastError();
 }

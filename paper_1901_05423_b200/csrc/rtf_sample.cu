@@ -24,24 +24,70 @@ __device__ __forceinline__ int32_t descend_step(const rtf_node* __restrict__ nod
     return (int32_t)(x63 < r.x ? (uint32_t)r.y : (uint32_t)(r.y >> 32));
 }
 
-// Alg. 2's first step on a guide-table cell (rtf_ref): a node reference, or a
-// leaf that a two-interval cell (key32 != 0) splits with one comparison.
-__device__ __forceinline__ int32_t cell_step(const rtf_ref* __restrict__ table, uint32_t m,
-                                             uint32_t x) {
-    const int2 e = __ldg(reinterpret_cast<const int2*>(table) + (uint32_t)(((uint64_t)x * m) >> 32));
-    return (e.y >= 0 || x >= (uint32_t)e.x) ? e.y : e.y + 1;
+// Degenerate-cell fallback (reading R21): a marked cell (key32 = 3 << 30 | k,
+// ref = its first leaf a) is searched by bisection of the index interval
+// [a-1, a+k) of the intervals overlapping it (Sec.6), at most
+// ceil(log2(k + 1)) record reads.  The answer's leaf reference comes from the
+// probed records as prefilled by the build: ~orig(a-1) is the anchor's child0,
+// ~orig(j) the child1 of record j when leaf j hangs right of gap j-1, else
+// the child0 of record j+1 (then probed as the upper bound).
+constexpr uint32_t kBisectFlag = 0xC0000000u;  // both top bits: never a packed cell's
+constexpr uint32_t kFallbackSlack = 4;
+
+__device__ __forceinline__ int32_t bisect_cell(const rtf_node* __restrict__ nodes, int32_t a,
+                                               uint32_t k, uint64_t x63, int32_t* visits) {
+    int32_t lo = a - 1, hi = a + (int32_t)k;  // key_lo <= x63 < key_hi
+    int32_t c1_lo = 0, c0_hi = 0;
+    while (hi - lo > 1) {
+        const int32_t mid = (lo + hi) >> 1;  // lo >= -1 and hi < 2^31: no overflow
+        const ulonglong2 r = __ldg(reinterpret_cast<const ulonglong2*>(nodes + mid));
+        if (r.x <= x63) {
+            lo = mid;
+            c1_lo = (int32_t)(uint32_t)(r.y >> 32);
+        } else {
+            hi = mid;
+            c0_hi = (int32_t)(uint32_t)r.y;
+        }
+        if (visits) ++*visits;
+    }
+    return (lo == a - 1 || c1_lo >= 0) ? c0_hi : c1_lo;
 }
 
-template <bool ROWS>
+// Alg. 2's first step on a guide-table cell (rtf_ref): a node reference, a
+// packed three-interval cell (R20) or a leaf that a two-interval cell (R18)
+// splits with one comparison (table_step, rtf_device.cuh).  A marked cell
+// (R21) returns kBisect: the caller bisects it after its lock-step descents,
+// so the bisection adds no registers to them.  (kBisect = INT32_MIN is no leaf
+// reference: ~orig >= INT32_MIN + 1 for orig < 2^31 - 1.)
+constexpr int32_t kBisect = INT32_MIN;
+
+template <bool FB = true>
+__device__ __forceinline__ int32_t cell_step(const rtf_ref* __restrict__ table, uint32_t m,
+                                             uint32_t xmask, uint32_t x) {
+    const int2 e = __ldg(reinterpret_cast<const int2*>(table) + (uint32_t)(((uint64_t)x * m) >> 32));
+    if (FB && e.y >= 0 && ((uint32_t)e.x & kBisectFlag) == kBisectFlag) return kBisect;
+    return table_step(e, x, x & xmask);
+}
+
+// the answer for xi = x in a marked cell (a leaf reference)
+__device__ __noinline__ int32_t bisect_xi(const rtf_ref* __restrict__ table,
+                                          const rtf_node* __restrict__ nodes, uint32_t m, uint32_t x,
+                                          int32_t* visits) {
+    const int2 e = __ldg(reinterpret_cast<const int2*>(table) + (uint32_t)(((uint64_t)x * m) >> 32));
+    return bisect_cell(nodes, e.y, (uint32_t)e.x & ~kBisectFlag, (uint64_t)x << 31, visits);
+}
+
+template <bool ROWS, bool FB>
 __device__ __forceinline__ int32_t sample_one(const rtf_node* __restrict__ nodes,
                                               const rtf_ref* __restrict__ table,
                                               const rtf_header* __restrict__ hdr, uint32_t n,
-                                              uint32_t m, uint32_t r, uint32_t x) {
+                                              uint32_t m, uint32_t xmask, uint32_t r, uint32_t x) {
     if (ROWS) {  // a poisoned row's cells are {0, INT32_MIN}: the answer is INT32_MAX
         nodes += (size_t)r * n;
         table += (size_t)r * m;
     }
-    int32_t j = cell_step(table, m, x);
+    int32_t j = cell_step<FB>(table, m, xmask, x);
+    if (FB && j == kBisect) return ~bisect_xi(table, nodes, m, x, nullptr);
     const uint64_t x63 = (uint64_t)x << 31;
     for (int d = 0; j >= 0 && d < kMaxVisits; ++d) j = descend_step(nodes, j, x63);
     return j >= 0 ? kCorrupt : ~j;
@@ -53,10 +99,12 @@ __device__ __forceinline__ uint32_t xi_bits(uint32_t v, bool f32) {
     return f32 ? __float2uint_rz(__uint_as_float(v) * 4294967296.0f) : v;
 }
 
-template <bool ROWS, bool F32 = false>
-__global__ void __launch_bounds__(kSampleThreads)
+// FB: the table may hold cells marked by rtf_build_fallback (R21); the
+// unmarked sampler carries no code for them (registers stay at 32).
+template <bool ROWS, bool F32 = false, bool FB = false>
+__global__ void __launch_bounds__(kSampleThreads, FB ? 8 : 0)
     k_sample(const rtf_node* __restrict__ nodes, const rtf_ref* __restrict__ table,
-             const rtf_header* __restrict__ hdr, uint32_t n, uint32_t m,
+             const rtf_header* __restrict__ hdr, uint32_t n, uint32_t m, uint32_t xmask,
              const uint32_t* __restrict__ row, const uint32_t* __restrict__ xi, uint64_t count,
              int32_t* __restrict__ out, bool vec) {
     const uint64_t gt = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -91,12 +139,18 @@ __global__ void __launch_bounds__(kSampleThreads)
                 }
                 nb[k] = nk;
                 x63[k] = (uint64_t)x[k] << 31;
-                j[k] = dead[k] ? -1 : cell_step(tk, m, x[k]);
+                j[k] = dead[k] ? -1 : cell_step<FB>(tk, m, xmask, x[k]);
             }
             for (int it = 0; (j[0] & j[1] & j[2] & j[3]) >= 0 && it < kMaxVisits; ++it) {
 #pragma unroll
                 for (int k = 0; k < 4; ++k)
                     if (j[k] >= 0) j[k] = descend_step(nb[k], j[k], x63[k]);
+            }
+            if (FB && ((j[0] == kBisect) | (j[1] == kBisect) | (j[2] == kBisect) | (j[3] == kBisect))) {
+#pragma unroll
+                for (int k = 0; k < 4; ++k)  // marked cells (R21), after the lock-step descents
+                    if (j[k] == kBisect)
+                        j[k] = bisect_xi(ROWS ? table + (size_t)rr[k] * m : table, nb[k], m, x[k], nullptr);
             }
             int4 o;
             o.x = dead[0] ? INT32_MAX : (j[0] >= 0 ? kCorrupt : ~j[0]);
@@ -109,29 +163,84 @@ __global__ void __launch_bounds__(kSampleThreads)
     }
     for (uint64_t k = done + gt; k < count; k += gs) {
         const uint32_t r = ROWS ? row[k] : 0u;
-        out[k] = bad ? INT32_MAX : sample_one<ROWS>(nodes, table, hdr, n, m, r, xi_bits(xi[k], F32));
+        out[k] = bad ? INT32_MAX : sample_one<ROWS, FB>(nodes, table, hdr, n, m, xmask, r, xi_bits(xi[k], F32));
     }
 }
 
 // Load counts (a measurement aid, not the sampler): 1 table cell + 1 per node
 // visited (Table 1's convention); loads_plain: the same without
-// the two-interval flag, where a flagged cell costs its anchor visit too.
+// the two-interval and packed-cell flags (a flagged cell costs its anchor
+// visit, a packed one its anchor and root visits too).
 __global__ void __launch_bounds__(kSampleThreads)
     k_sample_loads(const rtf_node* __restrict__ nodes, const rtf_ref* __restrict__ table,
-                   uint32_t m, const uint32_t* __restrict__ xi, uint64_t count,
+                   uint32_t m, uint32_t xmask, const uint32_t* __restrict__ xi, uint64_t count,
                    int32_t* __restrict__ loads, int32_t* __restrict__ loads_plain) {
     const uint64_t gs = (uint64_t)gridDim.x * blockDim.x;
     for (uint64_t k = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; k < count; k += gs) {
         const uint32_t x = xi[k];
         const uint32_t g = (uint32_t)(((uint64_t)x * m) >> 32);
-        const bool flagged = table[g].key32 != 0;
-        int32_t j = cell_step(table, m, x);
+        // without the flags a two-interval cell costs its anchor visit too,
+        // a packed cell its anchor and root visits
+        const rtf_ref e = table[g];
+        const int32_t extra =
+            (e.key32 == 0 || (e.ref >= 0 && (e.key32 & kBisectFlag) == kBisectFlag)) ? 0 : (e.ref < 0 ? 1 : 2);
         int32_t l = 1;
+        int32_t j = cell_step(table, m, xmask, x);
+        if (j == kBisect) j = bisect_xi(table, nodes, m, x, &l);
         for (; j >= 0 && l <= kMaxVisits; ++l) j = descend_step(nodes, j, (uint64_t)x << 31);
         loads[k] = l;
-        if (loads_plain) loads_plain[k] = l + (flagged ? 1 : 0);
+        if (loads_plain) loads_plain[k] = l + extra;
     }
 }
+
+// ------------------------------------------------------------ degenerate-cell fallback pass (R21)
+// K1, one thread per leaf j: the last leaf of each cell (last[cell]); for a
+// leaf reachable by a 32-bit xi (ceil(key_j / 2^31) < ceil(key_{j+1} / 2^31))
+// the node visits Alg. 2 makes for xi_j = ceil(key_j / 2^31) through an
+// anchor cell, maximised per cell of xi_j (depth[]).  Every xi reaching leaf j
+// follows the same path, so depth[g] is the most visits of any xi of cell g
+// (but the anchor's left child: 1).
+__global__ void __launch_bounds__(kSampleThreads)
+    k_fallback_depth(const rtf_node* __restrict__ nodes, const rtf_ref* __restrict__ table,
+                     const rtf_header* __restrict__ hdr, uint32_t n, uint32_t m,
+                     uint32_t* __restrict__ depth, uint32_t* __restrict__ last) {
+    const uint32_t n_pos = hdr->status ? 0u : min(hdr->n_pos, n);
+    const uint32_t gs = gridDim.x * blockDim.x;
+    for (uint32_t j = blockIdx.x * blockDim.x + threadIdx.x; j < n_pos; j += gs) {
+        const uint64_t key = __ldg(&nodes[j].key);
+        const uint64_t kn = j + 1 < n_pos ? __ldg(&nodes[j + 1].key) : kOne63;
+        const uint32_t c = cell_of(key, m);
+        if (j + 1 == n_pos || cell_of(kn, m) != c) last[c] = j;
+        const uint64_t x = (key + 0x7fffffffull) >> 31, xn = (kn + 0x7fffffffull) >> 31;
+        if (x >= xn) continue;  // no 32-bit xi reaches leaf j
+        const uint32_t g = (uint32_t)((x * m) >> 32);
+        const int2 e = __ldg(reinterpret_cast<const int2*>(table) + g);
+        if (e.y < 0 || e.x != 0) continue;  // not an anchor cell
+        const uint64_t x63 = x << 31;
+        int32_t v = 0, node = e.y;
+        for (; node >= 0 && v < kMaxVisits; ++v) {
+            const ulonglong2 r = __ldg(reinterpret_cast<const ulonglong2*>(nodes + node));
+            node = (int32_t)(x63 < r.x ? (uint32_t)r.y : (uint32_t)(r.y >> 32));
+        }
+        atomicMax(&depth[g], (uint32_t)v);
+    }
+}
+
+// K2, one thread per cell: an anchor cell (key32 = 0, ref = a) with k leaves
+// is marked when it holds k < 2^30 leaves and its depth exceeds
+// ceil(log2(k + 1)) + kFallbackSlack.
+__global__ void k_fallback_mark(rtf_ref* __restrict__ table, uint32_t m,
+                                const uint32_t* __restrict__ depth, const uint32_t* __restrict__ last) {
+    const uint32_t gs = gridDim.x * blockDim.x;
+    for (uint32_t g = blockIdx.x * blockDim.x + threadIdx.x; g < m; g += gs) {
+        const rtf_ref e = table[g];
+        if (e.ref < 0 || e.key32 != 0) continue;
+        const uint32_t k = last[g] - (uint32_t)e.ref + 1u;
+        const uint32_t bis = 32u - (uint32_t)__clz((int)k);  // ceil(log2(k + 1))
+        if (k < (1u << 30) && depth[g] > bis + kFallbackSlack) st_cell(table, g, kBisectFlag | k, e.ref);
+    }
+}
+
 
 // ------------------------------------------------------------ binary-search baseline
 
@@ -344,6 +453,18 @@ static inline uint32_t grid_for(uint64_t work_items) {
     return (uint32_t)std::max<uint64_t>(1, std::min<uint64_t>(want, (uint64_t)device_sms() * 64ull));
 }
 
+cudaError_t launch_fallback(const rtf_forest& f, uint32_t* depth, uint32_t* last, cudaStream_t st,
+                            int* launches) {
+    cudaError_t e = cudaMemsetAsync(depth, 0, sizeof(uint32_t) * (size_t)f.m, st);
+    if (e != cudaSuccess) return e;
+    k_fallback_depth<<<grid_for(f.n), kSampleThreads, 0, st>>>(f.nodes, f.table, f.header, f.n,
+                                                               f.m, depth, last);
+    ++*launches;
+    k_fallback_mark<<<grid_for(f.m), kSampleThreads, 0, st>>>(f.table, f.m, depth, last);
+    ++*launches;
+    return cudaGetLastError();
+}
+
 cudaError_t launch_sample(const rtf_forest& f, const uint32_t* row, const uint32_t* xi,
                           uint64_t count, int32_t* out, cudaStream_t st, int* launches) {
     if (count == 0) return cudaSuccess;
@@ -351,11 +472,15 @@ cudaError_t launch_sample(const rtf_forest& f, const uint32_t* row, const uint32
     if (row) vec = vec && (((uintptr_t)row & 15u) == 0);
     const uint32_t grid = grid_for(vec ? (count + 3) / 4 : count);
     if (row)
-        k_sample<true><<<grid, kSampleThreads, 0, st>>>(f.nodes, f.table, f.header, f.n, f.m, row,
-                                                        xi, count, out, vec);
+        k_sample<true><<<grid, kSampleThreads, 0, st>>>(f.nodes, f.table, f.header, f.n, f.m,
+                                                        xoff_mask(f.m), row, xi, count, out, vec);
+    else if (f.flags & RTF_FOREST_MARKED)
+        k_sample<false, false, true><<<grid, kSampleThreads, 0, st>>>(
+            f.nodes, f.table, f.header, f.n, f.m, xoff_mask(f.m), nullptr, xi, count, out, vec);
     else
         k_sample<false><<<grid, kSampleThreads, 0, st>>>(f.nodes, f.table, f.header, f.n, f.m,
-                                                         nullptr, xi, count, out, vec);
+                                                         xoff_mask(f.m), nullptr, xi, count, out,
+                                                         vec);
     ++*launches;
     return cudaGetLastError();
 }
@@ -364,9 +489,16 @@ cudaError_t launch_sample_f32(const rtf_forest& f, const float* xi, uint64_t cou
                               cudaStream_t st, int* launches) {
     if (count == 0) return cudaSuccess;
     const bool vec = (((uintptr_t)xi | (uintptr_t)out) & 15u) == 0;
+    if (f.flags & RTF_FOREST_MARKED) {
+        k_sample<false, true, true><<<grid_for(vec ? (count + 3) / 4 : count), kSampleThreads, 0, st>>>(
+            f.nodes, f.table, f.header, f.n, f.m, xoff_mask(f.m), nullptr,
+            reinterpret_cast<const uint32_t*>(xi), count, out, vec);
+        ++*launches;
+        return cudaGetLastError();
+    }
     k_sample<false, true><<<grid_for(vec ? (count + 3) / 4 : count), kSampleThreads, 0, st>>>(
-        f.nodes, f.table, f.header, f.n, f.m, nullptr, reinterpret_cast<const uint32_t*>(xi), count,
-        out, vec);
+        f.nodes, f.table, f.header, f.n, f.m, xoff_mask(f.m), nullptr,
+        reinterpret_cast<const uint32_t*>(xi), count, out, vec);
     ++*launches;
     return cudaGetLastError();
 }
@@ -375,8 +507,9 @@ cudaError_t launch_sample_loads(const rtf_forest& f, const uint32_t* xi, uint64_
                                 int32_t* loads, int32_t* loads_plain, cudaStream_t st,
                                 int* launches) {
     if (count == 0) return cudaSuccess;
-    k_sample_loads<<<grid_for(count), kSampleThreads, 0, st>>>(f.nodes, f.table, f.m, xi, count,
-                                                              loads, loads_plain);
+    k_sample_loads<<<grid_for(count), kSampleThreads, 0, st>>>(f.nodes, f.table, f.m,
+                                                              xoff_mask(f.m), xi, count, loads,
+                                                              loads_plain);
     ++*launches;
     return cudaGetLastError();
 }

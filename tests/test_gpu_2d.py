@@ -123,3 +123,22 @@ def test_2d_quadratic_error_qmc_vs_mc(rtf):
     e_mc, e_qmc = err(*mc), err(*qmc)
     assert 0.8 * expected < e_mc < 1.2 * expected
     assert e_qmc < e_mc / 3
+
+
+def test_2d_beyond_row_kernel(rtf):
+    """Maps beyond the row kernel's 4096 entries / cells (Sec.6
+    sets no size limit): rows of 8192 pixels (the 8192 x 4096 lat-long map,
+    rows built by the cooperative kernel), more than 4096 rows (a cooperative
+    marginal), and more than 4096 cells per row, with zeros and an all-zero
+    row; weights, pixels and positions bit-exact vs oracle O14/O15."""
+    rng = np.random.default_rng(12)
+    cases = [(env_map(8192, 4096, seed=4).reshape(4096, 8192), 8192, 4096, 1 << 18)]
+    p = np.stack([random_small(rng, 700, zero_frac=0.2 * (y % 3 == 0)) for y in range(5000)])
+    p[17] = 0.0
+    cases.append((p, 700, 6000, 1 << 16))
+    p = np.stack([random_small(rng, 3000, zero_frac=0.5 * (y % 2)) for y in range(40)])
+    cases.append((p, 5000, 40, 1 << 16))
+    for k, (p, mx, my, ns) in enumerate(cases):
+        xi1 = np.concatenate([philox_xi(ns, seed=30 + k), [0, 2**32 - 1]]).astype(np.uint32)
+        xi2 = np.concatenate([philox_xi(ns, seed=40 + k), [2**32 - 1, 0]]).astype(np.uint32)
+        check(rtf, p.astype(np.float32), mx, my, xi1, xi2)

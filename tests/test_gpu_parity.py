@@ -42,7 +42,7 @@ def assert_forest_equal(f, ref, what=""):
     bad = np.flatnonzero((nodes["c0"] != ref.child0) | (nodes["c1"] != ref.child1))
     assert bad.size == 0, f"{what}: {bad.size} node records differ, first at {bad[:5]}"
     tab = f.table_numpy()
-    want = ref.table2()
+    want = ref.table3()  # the table the build produces (O16: packed two-leaf cells)
     badt = np.flatnonzero((tab["ref"] != want["ref"]) | (tab["key32"] != want["key32"]))
     assert badt.size == 0, f"{what}: {badt.size} table cells differ, first at {badt[:5]}"
 
@@ -95,6 +95,26 @@ def test_random_small(rtf, flags):
         f = rtf.build(dev_f32(p), m, flags)
         assert_forest_equal(f, ref, f"case {t} n={n} m={m}")
         check_sampling(f, ref, boundary_xi(ref, rng, 512))
+
+
+@pytest.mark.parametrize("flags", [0, 1])
+def test_packed_two_leaf_cells(rtf, flags):
+    """Power-of-two tables with m >= 2^17 hold the packed three-interval cells
+    of reading R20 (oracle O16): many two-leaf cells (m near n), zero weights
+    between them (no packing then), cells across tile boundaries (small tiles
+    put most of them there), the packing threshold m = 2^17 and below it."""
+    rng = np.random.default_rng(11 + flags)
+    for t, (n, m, z) in enumerate(((70000, 1 << 17, 0.0), (70000, 1 << 16, 0.0),
+                                   (150000, 1 << 17, 0.3), (200000, 1 << 18, 0.05),
+                                   (300000, 1 << 17, 0.0), (1 << 20, 1 << 19, 0.1))):
+        p = random_small(rng, n, zero_frac=z, dyn=float(rng.choice([0.5, 4])))
+        ref = oracle.build(p, m)
+        f = rtf.build(dev_f32(p), m, flags)
+        assert_forest_equal(f, ref, f"case {t} n={n} m={m}")
+        t3 = ref.table3()
+        packed = int(np.count_nonzero((t3["ref"] >= 0) & (t3["key32"] != 0)))
+        assert (packed > 0) == (m >= 1 << 17), (t, packed)
+        check_sampling(f, ref, boundary_xi(ref, rng, 4096))
 
 
 def test_edge_cases(rtf):

@@ -32,7 +32,7 @@ def _check(rtf, p, m, count):
     want_nodes = single.nodes_numpy().tobytes()
     want_table = single.table_numpy().tobytes()
     assert np.array_equal(single.nodes_numpy()["c1"], ref.child1)
-    assert want_table == ref.table2().tobytes()
+    assert want_table == ref.table3().tobytes()
     for s in shards:
         f = rtf.Forest.from_buffer(s.n_global, m, s.forest)
         assert f.status() == 0
@@ -166,7 +166,7 @@ def test_config4_full_size_records_vs_oracle(rtf):
     assert np.array_equal(nodes["key"], ref.key), "keys"
     assert np.array_equal(nodes["c0"], ref.child0), "left children"
     assert np.array_equal(nodes["c1"], ref.child1), "right children"
-    assert table.tobytes() == ref.table2().tobytes(), "guide table"
+    assert table.tobytes() == ref.table3().tobytes(), "guide table"
     del ref
     shards = sharded.make_shards(pd, m, 4)
     sharded.build_sharded(shards, sharded.LocalComm(), ranged=True, fused=True)
