@@ -365,7 +365,7 @@ __global__ void __launch_bounds__(THREADS, MINB)
     __shared__ uint64_t s_recip;
     __shared__ unsigned long long s_mL, s_mR;  // this tile's spines (TileSpine)
     __shared__ uint32_t s_fw, s_lw;            // first / last wall (lambda = 64) of the tile
-    __shared__ int32_t s_ref0, s_c0next;
+    __shared__ int32_t s_ref0;
     __shared__ uint16_t s_iL[65], s_iR[65];
 
     const uint32_t G = gridDim.x, b = blockIdx.x, tid = threadIdx.x;
@@ -709,7 +709,6 @@ __global__ void __launch_bounds__(THREADS, MINB)
         s_mL = s_mR = 0ull;
         s_fw = 0xffffffffu;
         s_lw = 0u;
-        s_c0next = kNoLink;
     }
     if (tid == kIssuer) {
         fence_proxy_async_global();  // phase B's prefixes, read by TMA below
@@ -970,6 +969,7 @@ __global__ void __launch_bounds__(THREADS, MINB)
         }
         const uint32_t lo32 = (uint32_t)lampack, hi32 = (uint32_t)(lampack >> 32);
 
+        if (tid == 0) sts_u32(a_stage + 16u * stage_pos(cnt + sh) + 8u, (uint32_t)kNoLink);
         // (4) the staged records {key_j, ~orig(j-1), ~orig(j)}: the left child
         // of an anchor (Fig. 6 caption P:1276-1277) or of an internal node whose
         // left child is the leaf j-1, the right child of a node whose right
@@ -1100,15 +1100,14 @@ __global__ void __launch_bounds__(THREADS, MINB)
         {
             // gap g's node under its parent: the right child of the left
             // neighbour gl (slot gl + 1) if vl <= vr, else the left child of gr
+            // (slot cnt, the next tile's first record, has a stage row too: only
+            // its child0 -- the left child of the tile's last gap -- is written,
+            // and it goes to the tile's spine row, not to the records)
             auto link = [&](uint32_t g, uint32_t gl, uint32_t vl, uint32_t gr, uint32_t vr) {
                 const uint32_t node = j0 + g + 1u;
                 const bool right = vl <= vr;
                 const uint32_t slot = (right ? gl : gr) + 1u;
-                if (!right && slot == cnt) {  // left child of the tile's last gap (slot j0 + cnt)
-                    s_c0next = (int32_t)node;
-                } else {
-                    sts_u32(a_stage + 16u * stage_pos(slot + sh) + (right ? 12u : 8u), node);
-                }
+                sts_u32(a_stage + 16u * stage_pos(slot + sh) + (right ? 12u : 8u), node);
             };
             // (a) both nearest greater levels inside the thread: link now; the
             // others (about half) become tasks (thread << 5 | r << 2 | needs)
@@ -1235,7 +1234,7 @@ __global__ void __launch_bounds__(THREADS, MINB)
                 row->walls = walls;
                 row->iL[64] = walls ? (uint16_t)s_fw : (uint16_t)0;
                 row->iR[64] = walls ? (uint16_t)s_lw : (uint16_t)0;
-                row->c0_next = cnt ? s_c0next : kNoLink;
+                row->c0_next = cnt ? (int32_t)lds_u32(a_stage + 16u * stage_pos(cnt + sh) + 8u) : kNoLink;
                 row->ref0 = cnt ? s_ref0 : 0;
                 // phase E's row maxima: 1 + the largest split level, 0 if empty
                 const uint32_t enc = !cnt ? 0u
@@ -1246,7 +1245,6 @@ __global__ void __launch_bounds__(THREADS, MINB)
                 s_mL = s_mR = 0ull;  // the next tile's writers follow its barriers
                 s_fw = 0xffffffffu;
                 s_lw = 0u;
-                s_c0next = kNoLink;
             }
         }
         };
