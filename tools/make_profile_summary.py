@@ -26,7 +26,10 @@ with open(os.path.join(P, f"{R}_launches.csv"), "w", newline="") as f:
 # full captures: the main-path kernels (tools/gpu_ncu_main.sh) and the baselines
 # (tools/gpu_round_profile.sh)
 rows, h, units = [], None, None
-for rep in (f"{R}_build.ncu-rep", f"{R}_sample.ncu-rep", f"{R}_full.ncu-rep"):
+import glob as _glob
+_reps = [f"{R}_build.ncu-rep", f"{R}_sample.ncu-rep", f"{R}_full.ncu-rep"] + sorted(
+    os.path.basename(x) for x in _glob.glob(os.path.join(G, f"{R}_k_*.ncu-rep")))
+for rep in _reps:
     if not os.path.exists(os.path.join(G, rep)):
         continue
     out = subprocess.run(["ncu", "-i", os.path.join(G, rep), "--page", "raw", "--csv"],
