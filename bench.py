@@ -900,6 +900,7 @@ def run_gpu_c4(args):
     peak, peak_src = peaks()
     bytes_build = 4 * n + 16 * n + 4 * m
     quad = quad_summary(forest, xi, out, flush) if world == 1 else None
+    m26 = c4_m26_summary(p_local, n, flush) if world == 1 and not args.no_m26 else None
     result = {
         "metric": METRIC, "value": round(build_gs, 4), "unit": "G entries/s", "n_gpus": world,
         "steps": K, "warmup": args.warmup, "ms_per_step": round((tb + ts) / K, 4),
@@ -919,6 +920,7 @@ def run_gpu_c4(args):
         "sampling": {"value": round(sample_gs, 4), "unit": "G samples/s",
                      "ms_per_batch": round(ts / K, 4),
                      "quad_records": quad if quad else "single-GPU forest only"},
+        "m_2_26": m26 if m26 else "single GPU only (or --no-m26)",
         "roofline_build": {"kernel": "sharded build (all calls, incl. exchanges)",
                            "bound": "hbm", "achieved": round(bytes_build / (tb / K * 1e-3) / 1e9, 2),
                            "peak": peak, "unit": "GB/s",
@@ -931,6 +933,46 @@ def run_gpu_c4(args):
         dist.destroy_process_group()
     if rank == 0:
         print(json.dumps(result), flush=True)
+
+
+def c4_m26_summary(p, n, flush, S=1 << 30, reps=3):
+    """Config 4's distribution with the table size SURVEY.md proposes, m =
+    2^26 (a 512 MB table that no longer stays in L2), built once by rtf_build
+    on one GPU: build time, 2^30 Philox samples through the binary records,
+    the 4-ary records and the fallback-marked table (each median of reps, L2
+    flushed before every launch), identical indices."""
+    import torch
+
+    import paper_1901_05423_b200 as rtf
+    m = 1 << 26
+
+    def timed(fn):
+        ts = []
+        for _ in range(reps):
+            flush.zero_()
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record()
+            fn()
+            b.record()
+            torch.cuda.synchronize()
+            ts.append(a.elapsed_time(b))
+        return statistics.median(ts)
+
+    f = rtf.Forest(n, m, device=p.device)
+    tb = timed(lambda: f.build(p))
+    xi = rtf.philox(S, seed=0x5EED, device=p.device)
+    out = torch.empty_like(xi)
+    ts = timed(lambda: f.sample(xi, out))
+    quad = quad_summary(f, xi, out, flush, reps)
+    fb = fallback_summary(f, p, xi, out, flush, reps)
+    del f, xi, out
+    torch.cuda.empty_cache()
+    return {"m": m, "build": {"ms": round(tb, 4), "value": round(n / (tb * 1e-3) / 1e9, 4),
+                              "unit": "G entries/s"},
+            "sampling": {"value": round(S / (ts * 1e-3) / 1e9, 4), "unit": "G samples/s",
+                         "ms_per_batch": round(ts, 4), "samples": S},
+            "quad_records": quad, "fallback": fb,
+            "note": "one forest (rtf_build), not the sharded protocol; 512 MB table"}
 
 
 def run_gpu_2d(args):
@@ -1287,6 +1329,8 @@ def main():
     ap.add_argument("--no-c2", action="store_true", help="skip the config-2 summary")
     ap.add_argument("--c4-replicate", action="store_true",
                     help="config 4: replicate the whole forest instead of ranged sharding")
+    ap.add_argument("--no-m26", action="store_true",
+                    help="config 4: skip the m = 2^26 single-forest summary")
     ap.add_argument("--c4-nccl", action="store_true",
                     help="config 4 ranged: move records with NCCL send/recv instead of the "
                          "fused peer stores")

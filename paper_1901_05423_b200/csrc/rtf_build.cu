@@ -34,7 +34,10 @@
 
 namespace rtf {
 
-constexpr uint32_t kShortRun = 32;  // empty-cell runs up to this length: written in place
+#ifndef RTF_SHORT_RUN
+#define RTF_SHORT_RUN 32
+#endif
+constexpr uint32_t kShortRun = RTF_SHORT_RUN;  // empty-cell runs up to this length: written in place
 constexpr uint32_t kChunk = 2048;   // longer runs: queued in chunks of this many cells
 constexpr uint32_t kMaxGrid = 8192; // partials capacity (CTAs of the cooperative grid)
 
@@ -1451,7 +1454,7 @@ uint32_t build_tile_size(uint32_t flags) {
     return (uint32_t)(c.threads * c.vpt);
 }
 
-uint32_t build_queue_capacity(uint32_t m) { return m / 32u + m / kChunk + 64u; }
+uint32_t build_queue_capacity(uint32_t m) { return m / (kShortRun + 1u) + m / kChunk + 64u; }
 
 size_t spine_row_bytes() { return sizeof(TileSpine); }
 

@@ -368,12 +368,12 @@ __device__ __forceinline__ uint2 pack2_cell(uint32_t g, uint32_t shift, uint64_t
 // comparison (key32 = 0, ref < 0: one interval).  Returns a node index >= 0
 // or ~leaf.
 __device__ __forceinline__ int32_t table_step(int2 e, uint32_t x, uint32_t xoff) {
-    if (e.y >= 0) {
-        if (e.x == 0) return e.y;
-        const uint32_t s1 = (uint32_t)e.x & 0xffffu, s2 = (uint32_t)e.x >> 16;
-        return ~(e.y + (xoff >= s1 ? 1 : 0) + (xoff >= s2 ? 1 : 0));
-    }
-    return x >= (uint32_t)e.x ? e.y : e.y + 1;
+    // branch-free (selects): the samplers issue their next loads without waiting
+    // on a divergent branch per sample
+    const uint32_t s1 = (uint32_t)e.x & 0xffffu, s2 = (uint32_t)e.x >> 16;
+    const int32_t packed = ~(e.y + (xoff >= s1 ? 1 : 0) + (xoff >= s2 ? 1 : 0));
+    const int32_t plain = (e.y >= 0 || x >= (uint32_t)e.x) ? e.y : e.y + 1;
+    return (e.y >= 0 && e.x != 0) ? packed : plain;
 }
 
 // x mod (2^32 / m) for a power-of-two m (the offset table_step needs), else 0
