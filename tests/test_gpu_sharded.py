@@ -188,3 +188,19 @@ def test_config4_full_size_records_vs_oracle(rtf):
         assert np.all((want >= j0) & (want < j1)), f"shard {s.rank}: xi outside its stratum"
         assert np.array_equal(got, want.astype(np.int32)), f"shard {s.rank} samples"
     assert covered == nodes.size == n
+
+
+@pytest.mark.parametrize("count", [2, 3, 8])
+def test_sharded_packed_cells(rtf, count):
+    """Packed three-interval cells (R20, m = 2^17 and 2^18 power-of-two
+    tables with m near n) across shard boundaries, in the replicated, ranged
+    and fused builds: every shard's table equals the single build's (and the
+    oracle's O16 table), including cells whose two leaves sit on two shards."""
+    rng = np.random.default_rng(60 + count)
+    p = random_small(rng, 4096 * 40 * count + 77, zero_frac=0.05, dyn=3.0)
+    _check(rtf, p, 1 << 17, count)
+    if (1 << 17) % count == 0:  # ranged shards own m / count cells each
+        _check_ranged(rtf, p, 1 << 17, count)
+    if (1 << 18) % count == 0:
+        _check_ranged(rtf, random_small(rng, 4096 * 70 * count, zero_frac=0.0, dyn=2.0),
+                      1 << 18, count, fused=True)
