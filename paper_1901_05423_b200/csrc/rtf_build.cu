@@ -366,6 +366,7 @@ __global__ void __launch_bounds__(THREADS, MINB)
     __shared__ uint32_t s_next;
     __shared__ __align__(16) Pfx s_pin;  // TMA target: the next tile's prefix within its range
     __shared__ uint64_t s_recip;
+    __shared__ Recip128 s_rc;
     __shared__ unsigned long long s_mL, s_mR;  // this tile's spines (TileSpine)
     __shared__ uint32_t s_fw, s_lw;            // first / last wall (lambda = 64) of the tile
     __shared__ int32_t s_ref0;
@@ -642,6 +643,7 @@ __global__ void __launch_bounds__(THREADS, MINB)
     nm.s = (uint32_t)__clzll((long long)T);
     nm.d = T << nm.s;
     if (ph & kPhTiles) {
+        if (tid == 0) s_rc = recip128(T);  // the keys' reciprocal (fixed_point_r)
         if (tid == THREADS - 1) {
             s_recip = reciprocal_fast(nm.d);
             if (b == 0) {
@@ -660,6 +662,7 @@ __global__ void __launch_bounds__(THREADS, MINB)
         __syncthreads();
     }
     nm.v = s_recip;
+    const Recip128 rc = s_rc;
 
     // exclusive prefix of tile t: its range's, then its own within the range
     auto tile_prefix = [&](uint32_t t) -> Pfx {
@@ -686,7 +689,7 @@ __global__ void __launch_bounds__(THREADS, MINB)
             uint64_t W = pre.W + w_ex;
 #pragma unroll
             for (int k = 0; k < VPT; ++k) {
-                if (first + k < n) A.cdf[first + k] = (W == T) ? kOne63 : fixed_point(W, nm);
+                if (first + k < n) A.cdf[first + k] = (W == T) ? kOne63 : fixed_point_r(W, rc, T);
                 W += w[k];
             }
             __syncthreads();
@@ -902,10 +905,10 @@ __global__ void __launch_bounds__(THREADS, MINB)
 #pragma unroll
             for (int k = 0; k < VPT; ++k) {
                 const uint64_t wk = w[k];
-                if (ALLPOS || wk) w[k] = fixed_point(W, nm);
+                if (ALLPOS || wk) w[k] = fixed_point_r(W, rc, T);
                 W += wk;
             }
-            if (tc && W != T) kn = fixed_point(W, nm);
+            if (tc && W != T) kn = fixed_point_r(W, rc, T);
         }
 
         // (3) own gaps, last to first: split level lambda (byte r of lampack =
