@@ -337,6 +337,32 @@ def run_gpu(args):
     eyt_gs = world * S / (t_ey * 1e-3) / 1e9
     del ey, ey_out
 
+    # ------------------------------------------------ baseline: the alias method (Sec.2.6)
+    # host-built table over the same xi grid (baselines/alias.c); every item
+    # receives exactly its inverse-CDF xi count (checked here), not the same xi
+    import numpy as np
+    import baselines
+    K_host = cdf.cdf.cpu().numpy().view(np.uint64)
+    prob, alias, ak = baselines.alias_table(K_host)
+    kc = (K_host + np.uint64((1 << 31) - 1)) >> np.uint64(31)
+    want_cnt = np.diff(np.append(kc, np.uint64(1 << 32)).astype(np.int64))
+    s_b = float(1 << (32 - ak))
+    got_cnt = (np.bincount(np.arange(prob.size), weights=prob.astype(np.float64), minlength=prob.size)
+               + np.bincount(alias, weights=s_b - prob.astype(np.float64), minlength=prob.size))
+    alias_exact = bool(np.array_equal(got_cnt[:n].astype(np.int64), want_cnt)
+                       and not np.any(got_cnt[n:]))
+    al = rtf.Alias(prob, alias, ak, device=dev)
+    al_out = torch.empty_like(out)
+    al.sample(xi, al_out)
+    t_al = time_call(lambda: al.sample(xi, al_out), max(2, min(3, K)))
+    if world > 1:
+        t = torch.tensor([t_al], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        t_al = t.item()
+    alias_gs = world * S / (t_al * 1e-3) / 1e9
+    alias_same = float((al_out == out).float().mean().item())
+    del al, al_out, K_host
+
     # context only: torch.searchsorted on a float32 CDF -- a
     # library binary search, not bit-exact with the fixed-point CDF
     S_ts = min(S, 1 << 28)
@@ -469,6 +495,13 @@ def run_gpu(args):
                                            "identical_indices": ey_eq,
                                            "what": "binary search in breadth-first key order, "
                                                    "top 13 levels in shared memory"},
+                     "alias_method": {"value": round(alias_gs, 4), "unit": "G samples/s",
+                                      "ms_per_batch": round(t_al, 4), "buckets": 1 << ak,
+                                      "exact_counts": alias_exact,
+                                      "same_index_fraction": round(alias_same, 6),
+                                      "what": "Walker/Vose alias table over the same 32-bit xi "
+                                              "grid (host-built): exact per-item xi counts, "
+                                              "but not monotone (Sec.2.6 P:203-239)"},
                      "speedup_vs_bsearch": round(sample_gs / max(bsearch_gs, eyt_gs), 3),
                      "speedup_vs_bsearch_plain": round(sample_gs / bsearch_gs, 3),
                      "cutpoint_binary": {"value": round(cutbin_gs, 4), "unit": "G samples/s",

@@ -306,6 +306,16 @@ int rtf_build_eytzinger(const uint64_t *cdf, uint32_t n, uint64_t *eyt, void *st
 int rtf_sample_eytzinger(const uint64_t *eyt, uint32_t n, const rtf_header *header,
                          const uint32_t *xi, uint64_t count, int32_t *out, void *stream);
 
+/* Alias-method baseline (Walker / Vose, Sec.2.6; a comparison
+ * system of the paper): table = 2^k entries {u32 prob, i32 alias} (device,
+ * 8-B aligned, built on the host by baselines/alias.c over the same 32-bit
+ * xi grid, so item i receives exactly the xi count the inverse mapping gives
+ * it); out[i] = b if (xi mod 2^(32-k)) < prob[b] else alias[b], b = xi >>
+ * (32-k).  Not monotone in xi (the property the forest keeps).  1 <= k <= 31;
+ * RTF_EINVAL otherwise or on NULL / misaligned pointers. */
+int rtf_sample_alias(const void *table, uint32_t k, const uint32_t *xi, uint64_t count,
+                     int32_t *out, void *stream);
+
 /* Cutpoint baselines (guide table of the classic cutpoint method, Sec.2.3
  * P:168-232; the "cutpoint + linear / binary" rows of Table 1) on
  * the same full CDF.  rtf_build_cutpoint: cut[g] (u32[m + 1], device) = the

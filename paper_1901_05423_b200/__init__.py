@@ -395,6 +395,25 @@ class Eytzinger:
         return out
 
 
+class Alias:
+    """The alias-method baseline (rtf_sample_alias) over a host-built table
+    {prob, alias} of 2^k buckets (baselines.alias_table): argument marshalling."""
+
+    def __init__(self, prob: np.ndarray, alias: np.ndarray, k: int, device="cuda"):
+        tab = np.empty((prob.size, 2), np.uint32)
+        tab[:, 0], tab[:, 1] = prob, alias.view(np.uint32)
+        self.k = int(k)
+        self.table = torch.from_numpy(tab.view(np.int32)).to(device)
+
+    def sample(self, xi: torch.Tensor, out=None, stream=None) -> torch.Tensor:
+        xi = _u32_view(xi)
+        if out is None:
+            out = torch.empty(xi.numel(), dtype=torch.int32, device=xi.device)
+        check(lib().rtf_sample_alias(_ptr(self.table), self.k, _ptr(xi), xi.numel(), _ptr(out),
+                                     _stream(stream)), "rtf_sample_alias")
+        return out
+
+
 class Cutpoint:
     """Classic cutpoint guide table over a Cdf (baselines of Sec.2.3 / Table 1)."""
 

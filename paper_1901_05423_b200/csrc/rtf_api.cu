@@ -415,6 +415,18 @@ int rtf_sample_eytzinger(const uint64_t* eyt, uint32_t n, const rtf_header* head
     return finish(e, launches);
 }
 
+int rtf_sample_alias(const void* table, uint32_t k, const uint32_t* xi, uint64_t count,
+                     int32_t* out, void* stream) {
+    if (!table || k < 1 || k > 31) return RTF_EINVAL;
+    if (count && (!xi || !out)) return RTF_EINVAL;
+    if ((((uintptr_t)xi | (uintptr_t)out) & 3u) != 0 || ((uintptr_t)table & 7u) != 0)
+        return RTF_EINVAL;
+    int launches = 0;
+    cudaError_t e = rtf::launch_alias(static_cast<const uint2*>(table), k, xi, count, out,
+                                      as_stream(stream), &launches);
+    return finish(e, launches);
+}
+
 int rtf_build_cutpoint(const uint64_t* cdf, uint32_t n, uint32_t m, uint32_t* cut, void* stream) {
     if (!cdf || !cut) return RTF_EINVAL;
     if (int s = check_nm(n, m)) return s;

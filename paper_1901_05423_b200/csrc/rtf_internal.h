@@ -119,6 +119,8 @@ cudaError_t launch_eytzinger(const uint64_t* eyt, uint32_t n, const rtf_header* 
                              const uint32_t* xi, uint64_t count, int32_t* out, cudaStream_t st,
                              int* launches);
 
+cudaError_t launch_alias(const uint2* tab, uint32_t k, const uint32_t* xi, uint64_t count,
+                         int32_t* out, cudaStream_t st, int* launches);
 cudaError_t launch_cutpoint_build(const uint64_t* cdf, uint32_t n, uint32_t m, uint32_t* cut,
                                   cudaStream_t st, int* launches);
 

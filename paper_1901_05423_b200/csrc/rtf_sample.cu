@@ -357,6 +357,40 @@ __global__ void __launch_bounds__(kEytThreads, 3)
     }
 }
 
+// ------------------------------------------------------------ alias baseline
+// The alias method (Walker, Vose; Sec.2.6, a comparison system of
+// the paper) over the same 32-bit xi grid: 2^k buckets of 2^(32-k) xi each,
+// entry {prob, alias} (host-built, baselines/alias.c); xi -> bucket b = xi >>
+// (32-k), offset o = xi mod 2^(32-k), answer o < prob ? b : alias.  Each
+// item receives exactly the xi count the inverse mapping gives it, but not
+// the same xi: the mapping is not monotone.  One 8-B load per xi.
+__global__ void __launch_bounds__(kSampleThreads)
+    k_alias(const uint2* __restrict__ tab, uint32_t k, const uint32_t* __restrict__ xi,
+            uint64_t count, int32_t* __restrict__ out, bool vec) {
+    const uint64_t gt = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const uint64_t gs = (uint64_t)gridDim.x * blockDim.x;
+    const uint32_t sh = 32u - k, om = (uint32_t)((1ull << sh) - 1ull);
+    auto one = [&](uint32_t x) -> int32_t {
+        const uint2 e = __ldg(tab + (x >> sh));
+        return (x & om) < e.x ? (int32_t)(x >> sh) : (int32_t)e.y;
+    };
+    uint64_t done = 0;
+    if (vec) {
+        const uint64_t nq = count >> 2;
+        for (uint64_t q = gt; q < nq; q += gs) {
+            const uint4 xv = ld_stream_u4(xi + 4 * q);
+            int4 o;
+            o.x = one(xv.x);
+            o.y = one(xv.y);
+            o.z = one(xv.z);
+            o.w = one(xv.w);
+            __stcs(reinterpret_cast<int4*>(out + 4 * q), o);
+        }
+        done = nq << 2;
+    }
+    for (uint64_t i = done + gt; i < count; i += gs) out[i] = one(xi[i]);
+}
+
 // ------------------------------------------------------------ cutpoint baselines
 // The guide-table methods the paper compares against (Sec.2.3, Table 1
 // P:1458-1482): cut[g] = the answer for the smallest xi of cell g (an index
@@ -555,6 +589,16 @@ cudaError_t launch_eytzinger(const uint64_t* eyt, uint32_t n, const rtf_header* 
     const uint64_t want = (items + kEytThreads - 1) / kEytThreads;
     const uint32_t grid = (uint32_t)std::max<uint64_t>(1, std::min<uint64_t>(want, 3ull * device_sms()));
     k_eytzinger<<<grid, kEytThreads, smem, st>>>(eyt, H, hdr, xi, count, out, vec);
+    ++*launches;
+    return cudaGetLastError();
+}
+
+cudaError_t launch_alias(const uint2* tab, uint32_t k, const uint32_t* xi, uint64_t count,
+                         int32_t* out, cudaStream_t st, int* launches) {
+    if (count == 0) return cudaSuccess;
+    const bool vec = (((uintptr_t)xi | (uintptr_t)out) & 15u) == 0;
+    k_alias<<<grid_for(vec ? (count + 3) / 4 : count), kSampleThreads, 0, st>>>(tab, k, xi, count,
+                                                                                out, vec);
     ++*launches;
     return cudaGetLastError();
 }

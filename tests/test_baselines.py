@@ -67,3 +67,57 @@ def test_gpu_eytzinger_baseline_matches_oracle():
         for xs, w in ((xi, want), (xi[1:], want[1:])):  # aligned, then misaligned (scalar path)
             got = ey.sample(torch.from_numpy(xs.view(np.int32)).cuda()).cpu().numpy()
             assert np.array_equal(got, w), p.size
+
+
+def _alias_counts(prob, alias, k):
+    """xi count per item that the table realises (bucket b keeps prob[b] of its
+    2^(32-k) values for item b and gives the rest to alias[b])."""
+    s = 1 << (32 - k)
+    cnt = np.zeros(prob.size, np.int64)
+    np.add.at(cnt, np.arange(prob.size), prob.astype(np.int64))
+    np.add.at(cnt, alias.astype(np.int64), s - prob.astype(np.int64))
+    return cnt
+
+
+def test_alias_table_realises_the_inverse_cdf_counts():
+    """The alias table (baselines/alias.c, the comparison system of Sec.2.6
+    P:203-239) gives every item exactly the number of 32-bit xi the inverse
+    mapping gives it (ceil(K_{i+1}/2^31) - ceil(K_i/2^31), from the oracle's
+    CDF); padding buckets own nothing; brute force over all xi of a few
+    buckets agrees with the counts."""
+    rng = np.random.default_rng(71)
+    for n in (1, 2, 3, 17, 1000, 4097, 70000):
+        p = random_small(rng, n, zero_frac=0.3, dyn=10.0)
+        K, _ = oracle.cdf_all(p)
+        prob, alias, k = baselines.alias_table(K)
+        kc = np.array([-(-int(x) >> 31) for x in K] + [1 << 32], dtype=np.int64)
+        cnt = _alias_counts(prob, alias, k)
+        assert np.array_equal(cnt[:n], np.diff(kc)), n
+        assert int(cnt[n:].sum()) == 0
+    # every xi of 8 buckets, item by item
+    p = random_small(rng, 300, zero_frac=0.2, dyn=6.0)
+    K, _ = oracle.cdf_all(p)
+    prob, alias, k = baselines.alias_table(K)
+    for b in (0, 1, 7, 100, 255, 299, 300, 511):
+        xs = np.arange(b << (32 - k), (b + 1) << (32 - k), dtype=np.uint64).astype(np.uint32)
+        got = baselines.alias_sample(prob, alias, k, xs)
+        want = np.where(np.arange(xs.size) < prob[b], b, alias[b])
+        assert np.array_equal(got, want), b
+
+
+@pytest.mark.gpu
+def test_gpu_alias_sampler_matches_table():
+    torch = pytest.importorskip("torch")
+    if not torch.cuda.is_available():
+        pytest.fail("CUDA device required for -m gpu tests")
+    import paper_1901_05423_b200 as rtf
+    rng = np.random.default_rng(72)
+    for n in (2, 1000, 70001, 1 << 20):
+        p = random_small(rng, n, zero_frac=0.3, dyn=10.0)
+        K, _ = oracle.cdf_all(p)
+        prob, alias, k = baselines.alias_table(K)
+        a = rtf.Alias(prob, alias, k)
+        xi = np.concatenate([philox_xi((1 << 18) + 3, seed=n), np.array([0, 2**32 - 1], np.uint32)])
+        for xs in (xi, xi[1:]):  # vector and scalar paths
+            got = a.sample(torch.from_numpy(xs.view(np.int32)).cuda()).cpu().numpy()
+            assert np.array_equal(got, baselines.alias_sample(prob, alias, k, xs)), n
