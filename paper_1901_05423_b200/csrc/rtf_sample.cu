@@ -482,9 +482,13 @@ __global__ void k_philox(uint64_t seed, uint64_t start, uint64_t count, uint32_t
 
 // ------------------------------------------------------------ launchers
 
+#ifndef RTF_SAMPLE_GRID_PER_SM
+#define RTF_SAMPLE_GRID_PER_SM 64
+#endif
 static inline uint32_t grid_for(uint64_t work_items) {
     const uint64_t want = (work_items + kSampleThreads - 1) / kSampleThreads;
-    return (uint32_t)std::max<uint64_t>(1, std::min<uint64_t>(want, (uint64_t)device_sms() * 64ull));
+    return (uint32_t)std::max<uint64_t>(
+        1, std::min<uint64_t>(want, (uint64_t)device_sms() * RTF_SAMPLE_GRID_PER_SM));
 }
 
 cudaError_t launch_fallback(const rtf_forest& f, uint32_t* depth, uint32_t* last, cudaStream_t st,

@@ -34,6 +34,17 @@ def child():
             ts.append(a.elapsed_time(b))
         ts.sort()
         res.append(f"{wlname} build {ts[15]*1e3:7.1f} us (min {ts[0]*1e3:7.1f})")
+        if wlname == "c2":
+            xi = rtf.philox(1 << 26, seed=0x5EED)
+            out = torch.empty_like(xi)
+            f.sample(xi, out)
+            ts = []
+            for _ in range(7):
+                a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                a.record(); f.sample(xi, out); b.record(); torch.cuda.synchronize()
+                ts.append(a.elapsed_time(b))
+            ts.sort()
+            res.append(f"c2 sample 2^26 {ts[3]*1e3:.1f} us")
         if wlname == "c3":
             xi = rtf.philox(1 << 28, seed=0x5EED)
             out = torch.empty_like(xi)

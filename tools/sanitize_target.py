@@ -47,6 +47,39 @@ def main():
     f2.sample(xi_d[: 1 << 12], xi_d[1 << 12: 2 << 12], pix, pos)
     torch.cuda.synchronize()
     del rf
+    # round 2: packed three-interval cells (m = 2^17) in both tile configurations,
+    # the degenerate-cell fallback and its bisecting sampler
+    pk = random_small(rng, 150000, zero_frac=0.05, dyn=3.0)
+    refp = oracle.build(pk, 1 << 17)
+    for flags in (rtf.RTF_BUILD_DEFAULT, rtf.RTF_BUILD_SMALL_TILES):
+        fp = rtf.build(dev(pk), 1 << 17, flags)
+        assert np.array_equal(fp.table_numpy().view(np.uint64), refp.table3().view(np.uint64))
+        assert np.array_equal(fp.sample(xi_d).cpu().numpy(), refp.sample(xi)), "packed samples"
+    chain = np.concatenate([np.exp2(-np.arange(40, dtype=np.float64)), np.ones(5000)])
+    chain = chain.astype(np.float32)
+    refc = oracle.build(chain, 3)
+    fc = rtf.build(dev(chain), 3).build_fallback()
+    assert np.array_equal(fc.table_numpy().view(np.uint64), refc.table4().view(np.uint64))
+    assert np.array_equal(fc.sample(xi_d).cpu().numpy(), refc.sample(xi)), "fallback samples"
+    fc.sample_loads(xi_d)
+    # baselines: Eytzinger and alias
+    import baselines
+    q = power_law(20000, "A")
+    cdf = rtf.build_cdf(dev(q))
+    assert np.array_equal(cdf.eytzinger().sample(xi_d).cpu().numpy(), oracle.build(q, 64).sample(xi))
+    K, _ = oracle.cdf_all(q)
+    prob, alias, ak = baselines.alias_table(K)
+    got = rtf.Alias(prob, alias, ak).sample(xi_d).cpu().numpy()
+    assert np.array_equal(got, baselines.alias_sample(prob, alias, ak, xi)), "alias"
+    # 2-D rows wider than the row kernel (cooperative per-row builds + index maps)
+    wide = np.stack([random_small(rng, 4200, zero_frac=0.2 * (y % 2)) for y in range(3)])
+    f2w = rtf.build_2d(dev(wide), 5000, 3)
+    pw = torch.empty(1 << 12, dtype=torch.int32, device="cuda")
+    qw = torch.empty((1 << 12, 2), dtype=torch.float32, device="cuda")
+    f2w.sample(xi_d[: 1 << 12], xi_d[1 << 12: 2 << 12], pw, qw)
+    rp, _ = oracle.build_2d(wide, 5000, 3).sample(xi[: 1 << 12], xi[1 << 12: 2 << 12])
+    assert np.array_equal(pw.cpu().numpy(), rp), "2-D wide rows"
+    torch.cuda.synchronize()
     print("sanitize target ok")
 
 
