@@ -1125,8 +1125,12 @@ __global__ void __launch_bounds__(THREADS, MINB)
                 if ((uint32_t)r < tc && v < kLamBoundary) {
                     uint32_t glo, ghi;
                     above(lo32, hi32, v, glo, ghi);
-                    const int ngl = byte_below(glo, ghi, (uint32_t)r);
-                    const int ngr = byte_above(glo, ghi, (uint32_t)r);
+                    // the 8 byte flags as 8 bits, then the nearest set bit on
+                    // either side of r (-1 if none)
+                    const uint32_t m8 = ((glo * 0x00204081u) >> 28) | (((ghi * 0x00204081u) >> 28) << 4);
+                    const int ngl = r == 0 ? -1 : 31 - __clz(m8 & ((1u << r) - 1u));
+                    const uint32_t up = m8 & (0xffu << (r + 1));
+                    const int ngr = up ? __ffs(up) - 1 : -1;
                     if (ngl >= 0 && ngr >= 0) {
                         link(c_ex + r, c_ex + (uint32_t)ngl, lam_at(lo32, hi32, (uint32_t)ngl),
                              c_ex + (uint32_t)ngr, lam_at(lo32, hi32, (uint32_t)ngr));
