@@ -570,12 +570,20 @@ __global__ void __launch_bounds__(THREADS, MINB)
     // the tile weights of phase D can stream in while the spine scan runs
     const bool tma = !CDF && A.vec && (ph & kPhTiles);
     auto tma_tile = [&](uint32_t t) { return tma && t < nt && (t + 1) * TILE <= n; };
+    // the order tiles are dealt in: a dealing index maps to a tile (RTF_TILE_REVERSE:
+    // from the end of p; indices >= nt stay out of range)
+#ifdef RTF_TILE_REVERSE
+    auto tmap = [&](uint32_t x) -> uint32_t { return x < nt ? nt - 1u - x : x; };
+#else
+    auto tmap = [&](uint32_t x) -> uint32_t { return x; };
+#endif
+    const uint32_t t_first = tmap(b);
     if (tma && tid == 0) {
         mbar_init(&s_bar, 1);
         fence_proxy_async_smem();
-        if (tma_tile(b)) {
+        if (tma_tile(t_first)) {
             mbar_arrive_expect_tx(&s_bar, TILE * 4);
-            tma_load_1d(s_p, A.p + (size_t)b * TILE, TILE * 4, &s_bar);
+            tma_load_1d(s_p, A.p + (size_t)t_first * TILE, TILE * 4, &s_bar);
         }
     }
     // sharded: this shard writes only the table cells its leaves own; the rest
@@ -773,7 +781,7 @@ __global__ void __launch_bounds__(THREADS, MINB)
         return true;
     };
 
-    for (uint32_t t = b; (ph & kPhTiles) && t < nt; t = s_next) {
+    for (uint32_t t = t_first; (ph & kPhTiles) && t < nt; t = s_next) {
         const uint32_t first = t * TILE + tid * VPT;  // local index into p (global: + ib)
 
         // (0) weights of this thread's VPT consecutive entries
@@ -788,7 +796,7 @@ __global__ void __launch_bounds__(THREADS, MINB)
             mbar_wait(&s_bar, phase);
 #endif
             phase ^= 1u;
-            pre = t == b ? tile_prefix(t) : combine(s_rpre, s_pin);
+            pre = t == t_first ? tile_prefix(t) : combine(s_rpre, s_pin);
 #pragma unroll
             for (int k = 0; k < VPT; k += 4) {
                 const float4 v = *reinterpret_cast<const float4*>(s_p + tid * VPT + k);
@@ -842,7 +850,7 @@ __global__ void __launch_bounds__(THREADS, MINB)
         __syncthreads();
         RTF_TICK(3);
         if (tid == kIssuer) {  // every thread has its weights: the next tile can stream in
-            const uint32_t nx = ticket;
+            const uint32_t nx = tmap(ticket);
             s_next = nx;  // read at the end of this tile
             if (tma_tile(nx)) {
                 fence_proxy_async_smem();
