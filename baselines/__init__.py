@@ -36,6 +36,9 @@ def _load():
         lib.alias_build.argtypes = [ctypes.c_void_p, ctypes.c_uint32, ctypes.c_void_p,
                                     ctypes.c_void_p]
         lib.alias_build.restype = ctypes.c_int
+        lib.alias_build_counts.argtypes = [ctypes.c_void_p, ctypes.c_uint32, ctypes.c_int,
+                                           ctypes.c_void_p, ctypes.c_void_p]
+        lib.alias_build_counts.restype = ctypes.c_int
         _lib = lib
     return _lib
 
@@ -73,3 +76,46 @@ def alias_sample(prob: np.ndarray, alias: np.ndarray, k: int, xi: np.ndarray) ->
     b = (x >> np.uint64(32 - k)).astype(np.int64)
     o = x & np.uint64((1 << (32 - k)) - 1)
     return np.where(o < prob[b].astype(np.uint64), b, alias[b]).astype(np.int32)
+
+
+def alias_from_counts(counts: np.ndarray):
+    """Alias table realising per-item xi counts (summing to 2^32): (prob, alias, k)."""
+    c = np.ascontiguousarray(counts, dtype=np.uint64)
+    k = 1
+    while (1 << k) < c.size:
+        k += 1
+    prob = np.empty(1 << k, np.uint32)
+    alias = np.empty(1 << k, np.int32)
+    if _load().alias_build_counts(c.ctypes.data, c.size, k, prob.ctypes.data, alias.ctypes.data):
+        raise MemoryError("alias_build_counts")
+    return prob, alias, k
+
+
+def counts_from_cdf(K: np.ndarray) -> np.ndarray:
+    """Exact xi counts the inverse mapping gives each item of a full fixed-point
+    CDF K[0..n) (K_n = 2^63): c_i = ceil(K_{i+1}/2^31) - ceil(K_i/2^31)."""
+    kc = (np.asarray(K, np.uint64) + np.uint64((1 << 31) - 1)) >> np.uint64(31)
+    return np.diff(np.append(kc, np.uint64(1 << 32)).astype(np.int64)).astype(np.uint64)
+
+
+def alias_2d(K_marg: np.ndarray, K_rows):
+    """Tables of the 2-D alias baseline: the marginal over the rows' fixed-point
+    CDF K_marg and one table per row (K_rows[y], or None for a zero-weight row,
+    which the marginal never selects: uniform filler).  Returns ((prob, alias,
+    ky), (prob[H, 2^kx], alias[H, 2^kx], kx))."""
+    marg = alias_from_counts(counts_from_cdf(K_marg))
+    W = max(len(K) for K in K_rows if K is not None)
+    kx = 1
+    while (1 << kx) < W:
+        kx += 1
+    H = len(K_rows)
+    prob = np.empty((H, 1 << kx), np.uint32)
+    alias = np.empty((H, 1 << kx), np.int32)
+    for y, K in enumerate(K_rows):
+        if K is None:
+            prob[y], alias[y] = np.uint32(1 << (32 - kx)), np.arange(1 << kx, dtype=np.int32)
+            continue
+        c = counts_from_cdf(K)
+        c = np.concatenate([c, np.zeros((1 << kx) - c.size, np.uint64)])
+        prob[y], alias[y], _ = alias_from_counts(c)
+    return marg, (prob, alias, kx)

@@ -12,10 +12,9 @@
 #include <stdint.h>
 #include <stdlib.h>
 
-/* returns k (log2 of the bucket count), or -1 on allocation failure */
-int alias_build(const uint64_t *K, uint32_t n, uint32_t *prob, int32_t *alias) {
-    int k = 1;
-    while ((1ull << k) < (uint64_t)n) ++k;
+/* From per-item xi counts c[0..n) (summing to 2^32) into 2^k >= n buckets;
+ * returns 0, or -1 on allocation failure. */
+int alias_build_counts(const uint64_t *cnt, uint32_t n, int k, uint32_t *prob, int32_t *alias) {
     const uint64_t nb = 1ull << k, s = 1ull << (32 - k);
     uint64_t *c = (uint64_t *)malloc(sizeof(uint64_t) * nb);
     uint32_t *small = (uint32_t *)malloc(sizeof(uint32_t) * nb);
@@ -24,15 +23,7 @@ int alias_build(const uint64_t *K, uint32_t n, uint32_t *prob, int32_t *alias) {
         free(c); free(small); free(large);
         return -1;
     }
-    for (uint64_t b = 0; b < nb; ++b) {
-        if (b < n) {
-            const uint64_t lo = (K[b] + 0x7fffffffull) >> 31;
-            const uint64_t hi = b + 1 < n ? (K[b + 1] + 0x7fffffffull) >> 31 : (1ull << 32);
-            c[b] = hi - lo;
-        } else {
-            c[b] = 0;
-        }
-    }
+    for (uint64_t b = 0; b < nb; ++b) c[b] = b < n ? cnt[b] : 0;
     uint64_t ns = 0, nl = 0;
     for (uint64_t b = nb; b-- > 0;) {  /* worklists as stacks, lowest index on top */
         if (c[b] < s) small[ns++] = (uint32_t)b;
@@ -58,5 +49,22 @@ int alias_build(const uint64_t *K, uint32_t n, uint32_t *prob, int32_t *alias) {
         alias[l] = (int32_t)l;
     }
     free(c); free(small); free(large);
-    return k;
+    return 0;
+}
+
+/* From the full fixed-point CDF K[0..n): c_i = ceil(K_{i+1}/2^31) -
+ * ceil(K_i/2^31) (K_n = 2^63).  Returns k (log2 of the bucket count), or -1. */
+int alias_build(const uint64_t *K, uint32_t n, uint32_t *prob, int32_t *alias) {
+    int k = 1;
+    while ((1ull << k) < (uint64_t)n) ++k;
+    uint64_t *c = (uint64_t *)malloc(sizeof(uint64_t) * (n ? n : 1));
+    if (!c) return -1;
+    for (uint32_t b = 0; b < n; ++b) {
+        const uint64_t lo = (K[b] + 0x7fffffffull) >> 31;
+        const uint64_t hi = b + 1 < n ? (K[b + 1] + 0x7fffffffull) >> 31 : (1ull << 32);
+        c[b] = hi - lo;
+    }
+    const int r = alias_build_counts(c, n, k, prob, alias);
+    free(c);
+    return r ? -1 : k;
 }

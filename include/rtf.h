@@ -316,6 +316,18 @@ int rtf_sample_eytzinger(const uint64_t *eyt, uint32_t n, const rtf_header *head
 int rtf_sample_alias(const void *table, uint32_t k, const uint32_t *xi, uint64_t count,
                      int32_t *out, void *stream);
 
+/* 2-D alias baseline (the alias-method curve of the paper's convergence
+ * figure): marg = 2^ky entries {u32 prob, i32 alias} over the H
+ * rows, rows = H x 2^kx entries (row y's table at rows + y 2^kx) over its W
+ * columns, all built on the host (baselines.alias_2d) from the same exact
+ * 32-bit xi counts the 2-D forest realises.  pixel[i] = y W + x with y =
+ * alias(marg, xi1[i]), x = alias(row y, xi2[i]) (rule of rtf_sample_alias).
+ * RTF_EINVAL on NULL / misaligned pointers, k outside [1, 31], W > 2^kx or H
+ * > 2^ky; RTF_ETOOLARGE if W H >= 2^31. */
+int rtf_sample_alias_2d(const void *marg, uint32_t ky, const void *rows, uint32_t kx,
+                        uint32_t W, uint32_t H, const uint32_t *xi1, const uint32_t *xi2,
+                        uint64_t count, int32_t *pixel, void *stream);
+
 /* Cutpoint baselines (guide table of the classic cutpoint method, Sec.2.3
  * P:168-232; the "cutpoint + linear / binary" rows of Table 1) on
  * the same full CDF.  rtf_build_cutpoint: cut[g] (u32[m + 1], device) = the

@@ -414,6 +414,32 @@ class Alias:
         return out
 
 
+class Alias2D:
+    """The 2-D alias baseline (rtf_sample_alias_2d) over host-built tables
+    (baselines.alias_2d): marginal {prob, alias} of 2^ky buckets, H row
+    tables of 2^kx buckets each.  Argument marshalling."""
+
+    def __init__(self, marg, rows, W: int, H: int, device="cuda"):
+        (mp, ma, ky), (rp, ra, kx) = marg, rows
+        def pack(prob, alias):
+            t = np.empty(prob.shape + (2,), np.uint32)
+            t[..., 0], t[..., 1] = prob, alias.view(np.uint32)
+            return torch.from_numpy(t.view(np.int32)).to(device)
+        self.W, self.H, self.ky, self.kx = int(W), int(H), int(ky), int(kx)
+        self.marg, self.rows = pack(mp, ma), pack(rp, ra)
+
+    def sample(self, xi1: torch.Tensor, xi2: torch.Tensor, pixel=None, stream=None):
+        xi1, xi2 = _u32_view(xi1), _u32_view(xi2)
+        if xi1.numel() != xi2.numel():
+            raise ValueError("xi1 and xi2 must have the same length")
+        if pixel is None:
+            pixel = torch.empty(xi1.numel(), dtype=torch.int32, device=xi1.device)
+        check(lib().rtf_sample_alias_2d(_ptr(self.marg), self.ky, _ptr(self.rows), self.kx,
+                                        self.W, self.H, _ptr(xi1), _ptr(xi2), xi1.numel(),
+                                        _ptr(pixel), _stream(stream)), "rtf_sample_alias_2d")
+        return pixel
+
+
 class Cutpoint:
     """Classic cutpoint guide table over a Cdf (baselines of Sec.2.3 / Table 1)."""
 

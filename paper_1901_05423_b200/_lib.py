@@ -63,6 +63,7 @@ PROTOTYPES = {
     "rtf_build_cdf": (_I32, [_P, _U32, _P, _P, _P, _SZ, _P]),
     "rtf_sample_bsearch": (_I32, [_P, _U32, _P, _P, _U64, _P, _P]),
     "rtf_sample_alias": (_I32, [_P, _U32, _P, _U64, _P, _P]),
+    "rtf_sample_alias_2d": (_I32, [_P, _U32, _P, _U32, _U32, _U32, _P, _P, _U64, _P, _P]),
     "rtf_fallback_bytes": (_SZ, [_U32]),
     "rtf_build_fallback": (_I32, [_F, _P, _SZ, _P]),
     "rtf_eytzinger_slots": (_U64, [_U32]),

@@ -427,6 +427,23 @@ int rtf_sample_alias(const void* table, uint32_t k, const uint32_t* xi, uint64_t
     return finish(e, launches);
 }
 
+int rtf_sample_alias_2d(const void* marg, uint32_t ky, const void* rows, uint32_t kx,
+                        uint32_t W, uint32_t H, const uint32_t* xi1, const uint32_t* xi2,
+                        uint64_t count, int32_t* pixel, void* stream) {
+    if (!marg || !rows || ky < 1 || ky > 31 || kx < 1 || kx > 31) return RTF_EINVAL;
+    if (W == 0 || H == 0 || W > (1u << kx) || H > (1u << ky)) return RTF_EINVAL;
+    if ((uint64_t)W * H > 0x7fffffffull) return RTF_ETOOLARGE;
+    if (count && (!xi1 || !xi2 || !pixel)) return RTF_EINVAL;
+    if ((((uintptr_t)xi1 | (uintptr_t)xi2 | (uintptr_t)pixel) & 3u) != 0 ||
+        (((uintptr_t)marg | (uintptr_t)rows) & 7u) != 0)
+        return RTF_EINVAL;
+    int launches = 0;
+    cudaError_t e = rtf::launch_alias_2d(static_cast<const uint2*>(marg), ky,
+                                         static_cast<const uint2*>(rows), kx, W, xi1, xi2, count,
+                                         pixel, as_stream(stream), &launches);
+    return finish(e, launches);
+}
+
 int rtf_build_cutpoint(const uint64_t* cdf, uint32_t n, uint32_t m, uint32_t* cut, void* stream) {
     if (!cdf || !cut) return RTF_EINVAL;
     if (int s = check_nm(n, m)) return s;

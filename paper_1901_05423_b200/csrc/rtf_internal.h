@@ -119,6 +119,9 @@ cudaError_t launch_eytzinger(const uint64_t* eyt, uint32_t n, const rtf_header* 
                              const uint32_t* xi, uint64_t count, int32_t* out, cudaStream_t st,
                              int* launches);
 
+cudaError_t launch_alias_2d(const uint2* marg, uint32_t ky, const uint2* rows, uint32_t kx,
+                            uint32_t W, const uint32_t* xi1, const uint32_t* xi2, uint64_t count,
+                            int32_t* pixel, cudaStream_t st, int* launches);
 cudaError_t launch_alias(const uint2* tab, uint32_t k, const uint32_t* xi, uint64_t count,
                          int32_t* out, cudaStream_t st, int* launches);
 cudaError_t launch_cutpoint_build(const uint64_t* cdf, uint32_t n, uint32_t m, uint32_t* cut,

@@ -607,6 +607,37 @@ cudaError_t launch_alias(const uint2* tab, uint32_t k, const uint32_t* xi, uint6
     return cudaGetLastError();
 }
 
+// 2-D alias baseline (the comparison of the paper's convergence figure,
+// P:900-970): xi1 through the marginal table picks the row y, xi2 through row
+// y's table (2^kx buckets at rows + y 2^kx) picks the column x.  Two dependent
+// 8-B loads per pair.
+__global__ void __launch_bounds__(kSampleThreads)
+    k_alias_2d(const uint2* __restrict__ marg, uint32_t ky, const uint2* __restrict__ rows,
+               uint32_t kx, uint32_t W, const uint32_t* __restrict__ xi1,
+               const uint32_t* __restrict__ xi2, uint64_t count, int32_t* __restrict__ pixel) {
+    const uint64_t gs = (uint64_t)gridDim.x * blockDim.x;
+    const uint32_t shy = 32u - ky, omy = (uint32_t)((1ull << shy) - 1ull);
+    const uint32_t shx = 32u - kx, omx = (uint32_t)((1ull << shx) - 1ull);
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < count; i += gs) {
+        const uint32_t a = __ldcs(xi1 + i), b = __ldcs(xi2 + i);
+        const uint2 ey = __ldg(marg + (a >> shy));
+        const uint32_t y = (a & omy) < ey.x ? (a >> shy) : ey.y;
+        const uint2 ex = __ldg(rows + ((uint64_t)y << kx) + (b >> shx));
+        const uint32_t x = (b & omx) < ex.x ? (b >> shx) : ex.y;
+        __stcs(pixel + i, (int32_t)(y * W + x));
+    }
+}
+
+cudaError_t launch_alias_2d(const uint2* marg, uint32_t ky, const uint2* rows, uint32_t kx,
+                            uint32_t W, const uint32_t* xi1, const uint32_t* xi2, uint64_t count,
+                            int32_t* pixel, cudaStream_t st, int* launches) {
+    if (count == 0) return cudaSuccess;
+    k_alias_2d<<<grid_for(count), kSampleThreads, 0, st>>>(marg, ky, rows, kx, W, xi1, xi2, count,
+                                                           pixel);
+    ++*launches;
+    return cudaGetLastError();
+}
+
 cudaError_t launch_cutpoint_build(const uint64_t* cdf, uint32_t n, uint32_t m, uint32_t* cut,
                                   cudaStream_t st, int* launches) {
     k_cutpoint_build<<<grid_for((uint64_t)m + 1), kSampleThreads, 0, st>>>(cdf, n, m, cut);

@@ -121,3 +121,58 @@ def test_gpu_alias_sampler_matches_table():
         for xs in (xi, xi[1:]):  # vector and scalar paths
             got = a.sample(torch.from_numpy(xs.view(np.int32)).cuda()).cpu().numpy()
             assert np.array_equal(got, baselines.alias_sample(prob, alias, k, xs)), n
+
+
+def _alias_2d_case(rng, W=37, H=11):
+    p2d = np.stack([random_small(rng, W, zero_frac=0.3, dyn=8.0) for _ in range(H)])
+    p2d[3] = 0.0  # a zero row: the marginal never selects it
+    q = oracle.marginal_weights(p2d)
+    K_marg, _ = oracle.cdf_all(q)
+    K_rows = [oracle.cdf_all(p2d[y])[0] if np.any(p2d[y] > 0) else None for y in range(H)]
+    return p2d, K_marg, K_rows
+
+
+def test_alias_2d_tables_realise_the_inverse_counts():
+    """The 2-D alias baseline's tables (baselines.alias_2d): the marginal table
+    gives row y exactly the xi1 count the marginal inverse mapping gives it, and
+    row y's table gives column x exactly the xi2 count of row y's inverse
+    mapping (both from the oracle's fixed-point CDFs, P:61-63 and Sec.6
+    P:1523-1529); padding buckets own nothing."""
+    rng = np.random.default_rng(73)
+    p2d, K_marg, K_rows = _alias_2d_case(rng)
+    H, W = p2d.shape
+    (mp, ma, ky), (rp, ra, kx) = baselines.alias_2d(K_marg, K_rows)
+    want_m = np.diff(np.array([-(-int(x) >> 31) for x in K_marg] + [1 << 32], dtype=np.int64))
+    cm = _alias_counts(mp, ma, ky)
+    assert np.array_equal(cm[:H], want_m) and cm[3] == 0 and int(cm[H:].sum()) == 0
+    for y in range(H):
+        if K_rows[y] is None:
+            continue
+        want = np.diff(np.array([-(-int(x) >> 31) for x in K_rows[y]] + [1 << 32], dtype=np.int64))
+        c = _alias_counts(rp[y], ra[y], kx)
+        assert np.array_equal(c[:W], want), y
+        assert int(c[W:].sum()) == 0
+
+
+@pytest.mark.gpu
+def test_gpu_alias_2d_sampler_matches_tables():
+    torch = pytest.importorskip("torch")
+    if not torch.cuda.is_available():
+        pytest.fail("CUDA device required for -m gpu tests")
+    import paper_1901_05423_b200 as rtf
+    rng = np.random.default_rng(74)
+    p2d, K_marg, K_rows = _alias_2d_case(rng, W=300, H=70)
+    H, W = p2d.shape
+    marg, rows = baselines.alias_2d(K_marg, K_rows)
+    a = rtf.Alias2D(marg, rows, W, H)
+    x1 = np.concatenate([philox_xi(1 << 18, seed=1), np.array([0, 2**32 - 1], np.uint32)])
+    x2 = np.concatenate([philox_xi(1 << 18, seed=2), np.array([2**32 - 1, 0], np.uint32)])
+    got = a.sample(torch.from_numpy(x1.view(np.int32)).cuda(),
+                   torch.from_numpy(x2.view(np.int32)).cuda()).cpu().numpy()
+    y = baselines.alias_sample(*marg, x1)
+    (rp, ra, kx) = rows
+    b = (x2 >> np.uint32(32 - kx)).astype(np.int64)
+    frac = x2.astype(np.int64) & ((1 << (32 - kx)) - 1)
+    x = np.where(frac < rp[y, b], b, ra[y, b])
+    assert np.array_equal(got, (y * W + x).astype(np.int32))
+    assert not np.any(y == 3)

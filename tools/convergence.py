@@ -9,8 +9,12 @@ Two point sets per n = 2^k:
     P:1523-1529).  The inverse mapping is monotone, so the set's stratification
     survives (the paper's argument for inversion over the alias method);
   * mc: Philox4x32-10 pseudo-random pairs.
-The alias method of the paper's figure is a comparison system and is not
-built here.
+  * qmc_alias / mc_alias: the same two point sets through the 2-D alias
+    baseline (rtf_sample_alias_2d), whose tables give every row and pixel
+    exactly the xi counts the inverse mapping gives it (baselines.alias_2d
+    over the same fixed-point CDFs): the difference is the mapping alone.
+    The paper's figure shows the alias method losing the Hammersley set's
+    advantage.
 
   python tools/convergence.py [--kmin 14] [--kmax 26] [--out profiles/r01_convergence.jsonl]
 """
@@ -43,14 +47,22 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--kmin", type=int, default=14)
     ap.add_argument("--kmax", type=int, default=26)
-    ap.add_argument("--out", default=os.path.join(ROOT, "profiles", "r01_convergence.jsonl"))
+    ap.add_argument("--W", type=int, default=2048)
+    ap.add_argument("--H", type=int, default=1024)
+    ap.add_argument("--out", default=os.path.join(ROOT, "profiles", "r02_convergence.jsonl"))
     a = ap.parse_args()
-    W, H = 2048, 1024
+    W, H = a.W, a.H
     dev = torch.device("cuda", 0)
     img = env_map(W, H)
     p = torch.from_numpy(img.astype(np.float64) / img.astype(np.float64).sum()).to(dev)
     f = rtf.build_2d(torch.from_numpy(img).reshape(H, W).to(dev), W, H)
     assert f.status() == 0
+    import baselines
+    t = torch.from_numpy(img).reshape(H, W).to(dev)
+    K_marg = rtf.build_cdf(torch.from_numpy(f.weights()).to(dev)).cdf.cpu().numpy().view(np.uint64)
+    K_rows = [rtf.build_cdf(t[y].contiguous()).cdf.cpu().numpy().view(np.uint64)
+              if bool((t[y] > 0).any()) else None for y in range(H)]
+    al = rtf.Alias2D(*baselines.alias_2d(K_marg, K_rows), W, H, device=dev)
     rows = []
     for k in range(a.kmin, a.kmax + 1):
         n = 1 << k
@@ -66,6 +78,9 @@ def main():
             pix = f.sample(x1.contiguous(), x2.contiguous(), with_pos=False)
             c = torch.bincount(pix.to(torch.int64), minlength=W * H).to(torch.float64)
             row[f"e_{name}"] = float(((p - c / n) ** 2).sum())
+            pa = al.sample(x1.contiguous(), x2.contiguous())
+            c = torch.bincount(pa.to(torch.int64), minlength=W * H).to(torch.float64)
+            row[f"e_{name}_alias"] = float(((p - c / n) ** 2).sum())
         row["e_mc_expected"] = float((p * (1 - p)).sum() / n)
         rows.append(row)
         print(json.dumps(row), flush=True)
@@ -76,8 +91,12 @@ def main():
         mx, my = sum(xs) / len(xs), sum(ys) / len(ys)
         return sum((x - mx) * (y - my) for x, y in zip(xs, ys)) / sum((x - mx) ** 2 for x in xs)
     summary = {"slope_qmc": round(slope("e_qmc"), 3), "slope_mc": round(slope("e_mc"), 3),
+               "slope_qmc_alias": round(slope("e_qmc_alias"), 3),
+               "slope_mc_alias": round(slope("e_mc_alias"), 3),
                "ratio_mc_over_qmc_at_nmax": round(rows[-1]["e_mc"] / rows[-1]["e_qmc"], 2),
-               "image": "workloads.env_map(2048, 1024), mx = 2048, my = 1024",
+               "ratio_qmc_alias_over_qmc_at_nmax":
+                   round(rows[-1]["e_qmc_alias"] / rows[-1]["e_qmc"], 2),
+               "image": f"workloads.env_map({W}, {H}), mx = {W}, my = {H}",
                "error": "e = sum_i (p_i - c_i / n)^2, p = image / sum(image) (float64)"}
     print(json.dumps(summary), flush=True)
     with open(a.out, "w") as fo:

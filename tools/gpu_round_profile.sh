@@ -10,6 +10,6 @@ timeout 900 python bench.py --workload c4 --steps 3 --warmup 3 > gpurun_out/benc
 timeout 900 python bench.py --impl reference --steps 3 --warmup 1 > gpurun_out/bench_ref_$TAG.json 2> gpurun_out/bench_ref_$TAG.err; echo ref rc=$?
 timeout 900 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none --csv \
   --log-file gpurun_out/${TAG}_launches.csv python bench.py --steps 3 --warmup 3 --no-e2e --no-cpu-baseline > gpurun_out/ncu_launch_$TAG.log 2>&1; echo ncu_launch rc=$?
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:"k_build|k_sample|k_bsearch|k_sample_cutpoint" -s 8 -c 5 \
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:"k_build|k_sample|k_bsearch|k_sample_cutpoint|k_eytzinger|k_fallback" -s 8 -c 5 \
   -o gpurun_out/${TAG}_full python bench.py --steps 1 --warmup 3 --no-e2e --no-cpu-baseline --samples 268435456 > gpurun_out/ncu_full_$TAG.log 2>&1; echo ncu_full rc=$?
 ls gpurun_out
