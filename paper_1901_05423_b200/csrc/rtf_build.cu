@@ -209,19 +209,6 @@ __device__ __forceinline__ uint32_t lam_at(uint32_t lo, uint32_t hi, uint32_t i)
     return __byte_perm(lo, hi, i) & 0xffu;
 }
 
-// Byte masks (top bit per byte) over a thread's 8 packed split levels
-// (glo: bytes 0-3, ghi: bytes 4-7).  Highest marked byte below r / lowest
-// marked byte above r, -1 if none; r in [0, 7].
-__device__ __forceinline__ int byte_below(uint32_t glo, uint32_t ghi, uint32_t r) {
-    const uint32_t ml = r >= 4u ? 0xffffffffu : ((1u << (8u * r)) - 1u);
-    const uint32_t h = r <= 4u ? 0u : (ghi & ((1u << (8u * r - 32u)) - 1u));
-    return h ? 4 + ((31 - __clz(h)) >> 3) : (31 - __clz(glo & ml)) >> 3;
-}
-__device__ __forceinline__ int byte_above(uint32_t glo, uint32_t ghi, uint32_t r) {
-    const uint32_t l = r >= 3u ? 0u : (glo & (0xffffffffu << (8u * r + 8u)));
-    const uint32_t h = r == 7u ? 0u : (r < 4u ? ghi : (ghi & (0xffffffffu << (8u * r - 24u))));
-    return l ? (__ffs(l) - 1) >> 3 : (h ? 4 + ((__ffs(h) - 1) >> 3) : -1);
-}
 // first / last marked byte of a non-empty mask pair
 __device__ __forceinline__ uint32_t byte_first(uint32_t glo, uint32_t ghi) {
     return glo ? (uint32_t)(__ffs(glo) - 1) >> 3 : 4u + ((uint32_t)(__ffs(ghi) - 1) >> 3);
@@ -737,6 +724,10 @@ __global__ void __launch_bounds__(THREADS, MINB)
         glo = (lo + c) & 0x80808080u;
         ghi = (hi + c) & 0x80808080u;
     };
+    // the same flags as 8 bits (bit r: gap r above v)
+    auto mask8 = [](uint32_t glo, uint32_t ghi) -> uint32_t {
+        return ((glo * 0x00204081u) >> 28) | (((ghi * 0x00204081u) >> 28) << 4);
+    };
     // The nearest greater split level of a gap at level v of thread c, to its
     // right / left outside the thread: the first / last gap above v of the
     // nearest thread whose largest level exceeds v (per-warp tables s_B).
@@ -755,7 +746,7 @@ __global__ void __launch_bounds__(THREADS, MINB)
         const unsigned long long lp = s_clp[u];
         uint32_t glo, ghi;
         above((uint32_t)lp, (uint32_t)(lp >> 32), v, glo, ghi);
-        const uint32_t pos = byte_first(glo, ghi);
+        const uint32_t pos = (uint32_t)__ffs(mask8(glo, ghi)) - 1u;
         lev = lam_at((uint32_t)lp, (uint32_t)(lp >> 32), pos);
         gap = s_ccex[u] + pos;
         return true;
@@ -775,7 +766,7 @@ __global__ void __launch_bounds__(THREADS, MINB)
         const unsigned long long lp = s_clp[u];
         uint32_t glo, ghi;
         above((uint32_t)lp, (uint32_t)(lp >> 32), v, glo, ghi);
-        const uint32_t pos = byte_last(glo, ghi);
+        const uint32_t pos = 31u - (uint32_t)__clz(mask8(glo, ghi));
         lev = lam_at((uint32_t)lp, (uint32_t)(lp >> 32), pos);
         gap = s_ccex[u] + pos;
         return true;
@@ -1169,22 +1160,14 @@ __global__ void __launch_bounds__(THREADS, MINB)
                 const uint32_t v = lam_at(lo, hi, r), g = ce + r;
                 uint32_t glo, ghi;
                 above(lo, hi, v, glo, ghi);
-                uint32_t gl = 0, vl = 0, gr = 0, vr = 0;
+                const uint32_t m8 = mask8(glo, ghi);
+                // the in-thread neighbours (garbage on the side a search replaces)
+                const uint32_t nl = 31u - (uint32_t)__clz(m8 & ((1u << r) - 1u));
+                const uint32_t nr = (uint32_t)__ffs(m8 & (0xfeu << r)) - 1u;
+                uint32_t gl = ce + nl, vl = lam_at(lo, hi, nl), gr = ce + nr, vr = lam_at(lo, hi, nr);
                 bool hl = true, hr = true;
-                if (task & 1u) {
-                    hl = search_left(o, v, gl, vl);
-                } else {
-                    const uint32_t nl = (uint32_t)byte_below(glo, ghi, r);
-                    gl = ce + nl;
-                    vl = lam_at(lo, hi, nl);
-                }
-                if (task & 2u) {
-                    hr = search_right(o, v, gr, vr);
-                } else {
-                    const uint32_t nr = (uint32_t)byte_above(glo, ghi, r);
-                    gr = ce + nr;
-                    vr = lam_at(lo, hi, nr);
-                }
+                if (task & 1u) hl = search_left(o, v, gl, vl);
+                if (task & 2u) hr = search_right(o, v, gr, vr);
                 if (hl && hr) {
                     link(g, gl, vl, gr, vr);
                 } else {  // a spine gap of the tile: phase E links it
