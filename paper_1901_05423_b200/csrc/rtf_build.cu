@@ -1114,8 +1114,15 @@ __global__ void __launch_bounds__(THREADS, MINB)
                 const uint32_t slot = (right ? gl : gr) + 1u;
                 sts_u32(a_stage + 16u * stage_pos(slot + sh) + (right ? 12u : 8u), node);
             };
-            // (a) both nearest greater levels inside the thread: link now; the
-            // others (about half) become tasks (thread << 5 | r << 2 | needs)
+            // (a) both nearest greater levels inside the window of this thread
+            // and its two neighbours (24 gaps; a neighbour without leaves has
+            // no gaps): link now; the others become tasks (thread << 5 | r << 2
+            // | 1), about a sixth of the gaps for random split levels
+            const unsigned long long lpl = tid > 0 ? s_clp[tid - 1] : 0ull;
+            const unsigned long long lpr = tid + 1 < (uint32_t)THREADS ? s_clp[tid + 1] : 0ull;
+            const uint32_t llo = (uint32_t)lpl, lhi = (uint32_t)(lpl >> 32);
+            const uint32_t rlo = (uint32_t)lpr, rhi = (uint32_t)(lpr >> 32);
+            const uint32_t cel = tid > 0 ? s_ccex[tid - 1] : 0u, cer = c_ex + tc;
             uint32_t ntask = 0, tasks[VPT];
 #pragma unroll
             for (int r = 0; r < VPT; ++r) {
@@ -1124,17 +1131,38 @@ __global__ void __launch_bounds__(THREADS, MINB)
                 if ((uint32_t)r < tc && v < kLamBoundary) {
                     uint32_t glo, ghi;
                     above(lo32, hi32, v, glo, ghi);
-                    // the 8 byte flags as 8 bits, then the nearest set bit on
-                    // either side of r (-1 if none)
-                    const uint32_t m8 = ((glo * 0x00204081u) >> 28) | (((ghi * 0x00204081u) >> 28) << 4);
-                    const int ngl = r == 0 ? -1 : 31 - __clz(m8 & ((1u << r) - 1u));
-                    const uint32_t up = m8 & (0xffu << (r + 1));
-                    const int ngr = up ? __ffs(up) - 1 : -1;
-                    if (ngl >= 0 && ngr >= 0) {
-                        link(c_ex + r, c_ex + (uint32_t)ngl, lam_at(lo32, hi32, (uint32_t)ngl),
-                             c_ex + (uint32_t)ngr, lam_at(lo32, hi32, (uint32_t)ngr));
+                    const uint32_t m8 = mask8(glo, ghi);
+                    const uint32_t ml = m8 & ((1u << r) - 1u), mr = m8 & (0xfeu << r);
+                    uint32_t gl, vl, gr, vr;
+                    bool ok = true;
+                    if (ml) {
+                        const uint32_t q = 31u - (uint32_t)__clz(ml);
+                        gl = c_ex + q;
+                        vl = lam_at(lo32, hi32, q);
                     } else {
-                        tasks[r] = tid << 5 | (uint32_t)r << 2 | (ngl < 0 ? 1u : 0u) | (ngr < 0 ? 2u : 0u);
+                        above(llo, lhi, v, glo, ghi);
+                        const uint32_t mm = mask8(glo, ghi);
+                        const uint32_t q = 31u - (uint32_t)__clz(mm);
+                        gl = cel + q;
+                        vl = lam_at(llo, lhi, q);
+                        ok = mm != 0u;
+                    }
+                    if (mr) {
+                        const uint32_t q = (uint32_t)__ffs(mr) - 1u;
+                        gr = c_ex + q;
+                        vr = lam_at(lo32, hi32, q);
+                    } else {
+                        above(rlo, rhi, v, glo, ghi);
+                        const uint32_t mm = mask8(glo, ghi);
+                        const uint32_t q = (uint32_t)__ffs(mm) - 1u;
+                        gr = cer + q;
+                        vr = lam_at(rlo, rhi, q);
+                        ok = ok && mm != 0u;
+                    }
+                    if (ok) {
+                        link(c_ex + r, gl, vl, gr, vr);
+                    } else {
+                        tasks[r] = tid << 5 | (uint32_t)r << 2 | 1u;
                         ++ntask;
                     }
                 }
@@ -1161,13 +1189,15 @@ __global__ void __launch_bounds__(THREADS, MINB)
                 uint32_t glo, ghi;
                 above(lo, hi, v, glo, ghi);
                 const uint32_t m8 = mask8(glo, ghi);
-                // the in-thread neighbours (garbage on the side a search replaces)
-                const uint32_t nl = 31u - (uint32_t)__clz(m8 & ((1u << r) - 1u));
-                const uint32_t nr = (uint32_t)__ffs(m8 & (0xfeu << r)) - 1u;
+                // in-thread neighbours, else the search (which finds the
+                // window's neighbour threads first; garbage on a searched side)
+                const uint32_t ml = m8 & ((1u << r) - 1u), mr = m8 & (0xfeu << r);
+                const uint32_t nl = 31u - (uint32_t)__clz(ml);
+                const uint32_t nr = (uint32_t)__ffs(mr) - 1u;
                 uint32_t gl = ce + nl, vl = lam_at(lo, hi, nl), gr = ce + nr, vr = lam_at(lo, hi, nr);
                 bool hl = true, hr = true;
-                if (task & 1u) hl = search_left(o, v, gl, vl);
-                if (task & 2u) hr = search_right(o, v, gr, vr);
+                if (!ml) hl = search_left(o, v, gl, vl);
+                if (!mr) hr = search_right(o, v, gr, vr);
                 if (hl && hr) {
                     link(g, gl, vl, gr, vr);
                 } else {  // a spine gap of the tile: phase E links it
