@@ -345,6 +345,11 @@ int rtf_sample_cutpoint(const uint64_t *cdf, uint32_t n, const rtf_header *heade
 
 /* End-to-end build from HOST weights: copies p_host (pinned for full speed)
  * into p_dev (n floats, device scratch), builds, and reads the header back.
+ * The copy runs in 8 chunks on an internal copy stream; the scan for the
+ * largest weight and the data flags (phase A) runs on each chunk as soon as
+ * it lands, overlapping the rest of the copy, and the build then starts at
+ * the tile totals (n or m above 4096, or RTF_BUILD_SMALL_TILES; otherwise one
+ * copy, then rtf_build).  Ordered after the work already on `stream`.
  * Synchronous; returns the build status (data errors included). */
 int rtf_build_host(const float *p_host, uint32_t n, uint32_t m, uint32_t flags, float *p_dev,
                    void *forest_buf, size_t forest_bytes, void *ws, size_t ws_bytes,

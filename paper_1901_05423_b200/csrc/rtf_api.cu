@@ -472,10 +472,57 @@ int rtf_build_host(const float* p_host, uint32_t n, uint32_t m, uint32_t flags, 
     if (!p_host || !p_dev) return RTF_EINVAL;
     if (int s = check_nm(n, m)) return s;
     cudaStream_t st = as_stream(stream);
-    if (cudaMemcpyAsync(p_dev, p_host, sizeof(float) * (size_t)n, cudaMemcpyHostToDevice, st) !=
-        cudaSuccess)
-        return RTF_ECUDA;
-    int s = rtf_build(p_dev, n, m, flags, forest_buf, forest_bytes, ws, ws_bytes, stream, out);
+    rtf::WsLayout L;
+    const bool rows_kernel = !(flags & RTF_BUILD_SMALL_TILES) && n <= rtf::kRowsMax && m <= rtf::kRowsMax;
+    if (rows_kernel || !ws || ((uintptr_t)ws & (kAlign - 1)) != 0 || ((uintptr_t)p_dev & 3u) != 0 ||
+        (flags & ~RTF_BUILD_SMALL_TILES) || ws_bytes < rtf::build_workspace_layout(n, m, flags, &L)) {
+        // one copy, then the build (which validates its arguments itself)
+        if (cudaMemcpyAsync(p_dev, p_host, sizeof(float) * (size_t)n, cudaMemcpyHostToDevice, st) !=
+            cudaSuccess)
+            return RTF_ECUDA;
+        int s = rtf_build(p_dev, n, m, flags, forest_buf, forest_bytes, ws, ws_bytes, stream, out);
+        if (s != RTF_OK) return s;
+        return rtf_forest_status(out, stream, header_host);
+    }
+    if (int s = rtf_forest_view(forest_buf, forest_bytes, n, m, 1, out)) return s;
+    out->flags = flags;
+    // The copy goes in chunks on a copy stream; phase A (the largest weight,
+    // the data flags) runs on each chunk on the caller's stream as soon as it
+    // has landed, overlapping the next chunks' copies; the build then skips
+    // phase A and reads the scale word (the sharded build's kPhScale-less
+    // call, here with one shard).
+    constexpr uint32_t kChunks = 8;
+    const uint32_t chunk = ((n + kChunks - 1) / kChunks + 1023u) & ~1023u;  // 4-KB aligned chunks
+    cudaStream_t s_cp = nullptr;
+    cudaEvent_t ev_user = nullptr, ev[kChunks] = {};
+    cudaError_t e = cudaStreamCreateWithFlags(&s_cp, cudaStreamNonBlocking);
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ev_user, cudaEventDisableTiming);
+    for (uint32_t c = 0; c < kChunks && e == cudaSuccess; ++c)
+        e = cudaEventCreateWithFlags(&ev[c], cudaEventDisableTiming);
+    int launches = 0;
+    if (e == cudaSuccess) e = rtf::clear_scale(ws, L, st);
+    // the copy starts after everything already on the caller's stream (an
+    // earlier build may still read p_dev)
+    if (e == cudaSuccess) e = cudaEventRecord(ev_user, st);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(s_cp, ev_user, 0);
+    for (uint32_t c = 0, off = 0; c < kChunks && off < n && e == cudaSuccess; ++c, off += chunk) {
+        const uint32_t len = std::min(chunk, n - off);
+        e = cudaMemcpyAsync(p_dev + off, p_host + off, sizeof(float) * (size_t)len,
+                            cudaMemcpyHostToDevice, s_cp);
+        if (e == cudaSuccess) e = cudaEventRecord(ev[c], s_cp);
+        if (e == cudaSuccess) e = cudaStreamWaitEvent(st, ev[c], 0);
+        if (e == cudaSuccess) e = rtf::launch_scale_chunk(p_dev + off, len, ws, L, st, &launches);
+    }
+    if (e == cudaSuccess) {
+        rtf::ShardCall sc{rtf::kPhFull & ~rtf::kPhScale, n, 0, 0, 0, 0, nullptr, nullptr};
+        e = rtf::launch_build(p_dev, n, m, flags, out->header, out->nodes, out->table, nullptr, ws,
+                              L, st, &launches, &sc);
+    }
+    if (s_cp) cudaStreamDestroy(s_cp);  // released once its work is done
+    if (ev_user) cudaEventDestroy(ev_user);
+    for (uint32_t c = 0; c < kChunks; ++c)
+        if (ev[c]) cudaEventDestroy(ev[c]);
+    const int s = finish(e, launches);
     if (s != RTF_OK) return s;
     return rtf_forest_status(out, stream, header_host);
 }

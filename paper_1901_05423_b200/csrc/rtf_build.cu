@@ -42,7 +42,12 @@ constexpr uint32_t kChunk = 2048;   // longer runs: queued in chunks of this man
 constexpr uint32_t kMaxGrid = 8192; // partials capacity (CTAs of the cooperative grid)
 
 // workspace counters
-enum : int { kCtrGridBar = 0, kCtrQueue = 1, kCtrTile = 2, kCtrRpre = 3 };
+enum : int {
+    kCtrGridBar = 0,
+    kCtrQueue = 1,
+    kCtrTile = 2,
+    kCtrRpre = 3,
+};
 
 struct RunChunk {
     uint32_t start, len;
@@ -301,12 +306,28 @@ __device__ int32_t row_right(const uint8_t* tmax, const uint32_t* bmax, uint32_t
     return -1;
 }
 
+// ------------------------------------------------------------ slot-arrival check (debug builds)
+// Compiled only with -DRTF_SLOT_CHECK (tools/slotcheck_target.py,
+// tests/test_gpu_slotcheck.py): every link write of phases D and E also
+// counts, per record child field, how often it was written, and per record,
+// how often it was linked as an internal node.  A race between two writers of
+// one field shows as a count of 2 even when the final bytes happen to agree;
+// Alg. 1's invariant (every internal node gets exactly one
+// parent) is a count of exactly 1 per non-anchor record.  The product library
+// has neither.
 // ------------------------------------------------------------ phase timing (debug builds)
 // Compiled only with -DRTF_PHASE_TIMING (tools/phase_timing.py): thread 0 of
 // each CTA accumulates clock64() deltas per phase; read with
 // rtf_debug_phase_cycles().  The product library has neither.
 #ifdef RTF_PHASE_TIMING
 __device__ unsigned long long g_phase_cycles[kMaxGrid][16];
+// per tile of phase D (the first 65536): globaltimer at its start and end, CTA
+__device__ unsigned long long g_tile_ns[65536][3];
+__device__ __forceinline__ unsigned long long globaltimer_ns() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
 #define RTF_TICK(slot)                                                       \
     do {                                                                     \
         if (threadIdx.x == 0) {                                              \
@@ -493,18 +514,18 @@ __global__ void __launch_bounds__(THREADS, MINB)
     // barrier per tile), then writes each tile's exclusive prefix within its
     // range (excl) and the range total (rng).  Phase C scans only the NRG
     // range totals.
+    Pfx* s_tagg = reinterpret_cast<Pfx*>(s_stage);  // phase B's tile totals; free until phase D
+    constexpr uint32_t CAP = (uint32_t)(TILE + 64);
+    constexpr int F = TILE / 128;  // float4 per lane per tile
+    constexpr int BATCH = F < 8 ? F : 8;
+    // short ranges (small n): up to F / BATCH warps share a tile, so every
+    // warp keeps loads in flight
+    constexpr uint32_t NCH = F / BATCH;
+    const uint32_t WPT = krng >= NW ? 1u : min(NCH, NW / krng >= 4 ? 4u : NW / krng >= 2 ? 2u : 1u);
+    const uint32_t CAPT = CAP / WPT;
     if ((ph & kPhTotals) && b < NRG) {
-        Pfx* s_tagg = reinterpret_cast<Pfx*>(s_stage);  // free until phase D
-        constexpr uint32_t CAP = (uint32_t)(TILE + 64);
-        constexpr int F = TILE / 128;  // float4 per lane per tile
-        constexpr int BATCH = F < 8 ? F : 8;
         const uint32_t t_beg = b * krng, t_end = min(nt, t_beg + krng);
         Pfx run{0ull, 0u, -1};  // thread 0: the range so far
-        // short ranges (small n): up to F / BATCH warps share a tile, so every
-        // warp keeps loads in flight
-        constexpr uint32_t NCH = F / BATCH;
-        const uint32_t WPT = krng >= NW ? 1u : min(NCH, NW / krng >= 4 ? 4u : NW / krng >= 2 ? 2u : 1u);
-        const uint32_t CAPT = CAP / WPT;
         for (uint32_t c0 = t_beg; c0 < t_end; c0 += CAPT) {
             const uint32_t c1 = min(t_end, c0 + CAPT);
             for (uint32_t u = warp; u < (c1 - c0) * WPT; u += NW) {
@@ -557,12 +578,22 @@ __global__ void __launch_bounds__(THREADS, MINB)
     // the tile weights of phase D can stream in while the spine scan runs
     const bool tma = !CDF && A.vec && (ph & kPhTiles);
     auto tma_tile = [&](uint32_t t) { return tma && t < nt && (t + 1) * TILE <= n; };
-    // the order tiles are dealt in: a dealing index maps to a tile (RTF_TILE_REVERSE:
-    // from the end of p; indices >= nt stay out of range)
-#ifdef RTF_TILE_REVERSE
-    auto tmap = [&](uint32_t x) -> uint32_t { return x < nt ? nt - 1u - x : x; };
-#else
+    // the order tiles are dealt in: a dealing index maps to a tile (indices
+    // >= nt stay out of range)
+#ifdef RTF_TILE_INORDER
     auto tmap = [&](uint32_t x) -> uint32_t { return x; };
+#else
+    // the first wave in order (each CTA's first tile: its TMA load is issued
+    // before phase C), then the rest from both ends inwards: x = G + 2k -> G
+    // + k, x = G + 2k + 1 -> nt - 1 - k, so the middle of p is dealt last.
+    // Skewed data is expensive at both ends of p (the deep trees of the first
+    // cells, the table runs where p is large), and an expensive tile dealt
+    // last leaves the other SMs idle (config 3: 262 vs 272 us in order).
+    auto tmap = [&](uint32_t x) -> uint32_t {
+        if (x < G || x >= nt) return x;
+        const uint32_t y = x - G;
+        return (y & 1u) ? nt - 1u - (y >> 1) : G + (y >> 1);
+    };
 #endif
     const uint32_t t_first = tmap(b);
     if (tma && tid == 0) {
@@ -694,7 +725,8 @@ __global__ void __launch_bounds__(THREADS, MINB)
 
     // ---------------------------------------------------------- D: tiles
     // Tiles are dealt dynamically (their cost varies with the zero fraction
-    // and the tree shape): CTA b starts with tile b, then takes G + tickets.
+    // and the tree shape): CTA b starts with tile b, then takes tmap(G +
+    // ticket) -- both ends of p inwards.
     // The issuer thread draws each ticket one tile ahead, so the atomic's
     // latency is hidden; the TMA copy of the next tile's weights also brings
     // its prefix within its range (one mbarrier for both).  Three block
@@ -704,8 +736,10 @@ __global__ void __launch_bounds__(THREADS, MINB)
     static_assert(VPT == 8, "phase D packs a thread's 8 split levels into one 64-bit word");
     constexpr uint32_t kIssuer = THREADS - 1;  // TMA, tickets, stores: the last warp
     uint32_t phase = 0;
-    uint32_t ticket = 0;      // issuer: the tile after the next one
+    uint32_t ticket = 0;      // issuer: the tile after the next one (>= nt: none)
     bool store_pending = false;  // issuer: a TMA store group may still read the stage
+    // the next tile to deal (>= nt: none left)
+    auto draw = [&]() -> uint32_t { return tmap(G + atomicAdd(&A.counters[kCtrTile], 1u)); };
     if (tid == 0) {
         s_mL = s_mR = 0ull;
         s_fw = 0xffffffffu;
@@ -713,7 +747,7 @@ __global__ void __launch_bounds__(THREADS, MINB)
     }
     if (tid == kIssuer) {
         fence_proxy_async_global();  // phase B's prefixes, read by TMA below
-        if (ph & kPhTiles) ticket = G + atomicAdd(&A.counters[kCtrTile], 1u);
+        if (ph & kPhTiles) ticket = draw();
     }
     if (ph & kPhTiles) wait_rpre();
 
@@ -773,6 +807,12 @@ __global__ void __launch_bounds__(THREADS, MINB)
     };
 
     for (uint32_t t = t_first; (ph & kPhTiles) && t < nt; t = s_next) {
+#ifdef RTF_PHASE_TIMING
+        if (tid == 0 && t < 65536) {
+            g_tile_ns[t][0] = globaltimer_ns();
+            g_tile_ns[t][2] = b;
+        }
+#endif
         const uint32_t first = t * TILE + tid * VPT;  // local index into p (global: + ib)
 
         // (0) weights of this thread's VPT consecutive entries
@@ -841,7 +881,7 @@ __global__ void __launch_bounds__(THREADS, MINB)
         __syncthreads();
         RTF_TICK(3);
         if (tid == kIssuer) {  // every thread has its weights: the next tile can stream in
-            const uint32_t nx = tmap(ticket);
+            const uint32_t nx = ticket;
             s_next = nx;  // read at the end of this tile
             if (tma_tile(nx)) {
                 fence_proxy_async_smem();
@@ -851,7 +891,7 @@ __global__ void __launch_bounds__(THREADS, MINB)
             }
             if (nx < nt) {
                 s_rpre = ld_pfx_cg(&A.rpre[nx / krng]);  // read at the next tile's step (0)
-                ticket = G + atomicAdd(&A.counters[kCtrTile], 1u);
+                ticket = draw();
             }
         }
         uint64_t w_ex;
@@ -957,7 +997,11 @@ __global__ void __launch_bounds__(THREADS, MINB)
                                 A.jbound[q] = (uint32_t)anchor;
                         const uint32_t len = cn - cell - 1;
                         if (len <= kShortRun) {
-                            for (uint32_t g = cell + 1; g < cn; ++g) st_cell(table_at(g), g, 0u, ~i);
+                            if (FUSED) {  // the run may cross an owner's boundary
+                                for (uint32_t g = cell + 1; g < cn; ++g) st_cell(table_at(g), g, 0u, ~i);
+                            } else {
+                                fill_run(A.table, cell + 1, cn, ~i);
+                            }
                         } else {
                             table_queue(A.counters, A.queue, A.qcap, i, cell, len);
                         }
@@ -1007,12 +1051,27 @@ __global__ void __launch_bounds__(THREADS, MINB)
         {
             const uint32_t wm = __reduce_max_sync(0xffffffffu, encmax);
             if (lane == 0) s_wmax[warp] = wm;
+#ifdef RTF_WALL_ATOMICS_PER_THREAD
             if (lmax == kLamBoundary && tc) {
                 uint32_t glo, ghi;
                 above(lo32, hi32, kLamBoundary - 1u, glo, ghi);  // the walls
                 atomicMin(&s_fw, c_ex + byte_first(glo, ghi));
                 atomicMax(&s_lw, c_ex + byte_last(glo, ghi));
             }
+#else
+            // the warp's first wall (its lowest lane with one) and last wall:
+            // two shared atomics per warp, not two per thread
+            const uint32_t wb = __ballot_sync(0xffffffffu, lmax == kLamBoundary && tc);
+            if (wb) {
+                const uint32_t lf = (uint32_t)__ffs(wb) - 1u, ll = 31u - (uint32_t)__clz(wb);
+                if ((uint32_t)lane == lf || (uint32_t)lane == ll) {
+                    uint32_t glo, ghi;
+                    above(lo32, hi32, kLamBoundary - 1u, glo, ghi);  // the walls
+                    if ((uint32_t)lane == lf) atomicMin(&s_fw, c_ex + byte_first(glo, ghi));
+                    if ((uint32_t)lane == ll) atomicMax(&s_lw, c_ex + byte_last(glo, ghi));
+                }
+            }
+#endif
             __syncwarp();
             // lane L: the tables of levels L and L + 32 from the warp's 32 maxima
             const uint4 m0 = *reinterpret_cast<const uint4*>(s_cmax + (warp << 5));
@@ -1113,6 +1172,7 @@ __global__ void __launch_bounds__(THREADS, MINB)
                 const bool right = vl <= vr;
                 const uint32_t slot = (right ? gl : gr) + 1u;
                 sts_u32(a_stage + 16u * stage_pos(slot + sh) + (right ? 12u : 8u), node);
+                RTF_SLOT(j0 + slot, right ? 1u : 0u, node);
             };
             // (a) both nearest greater levels inside the window of this thread
             // and its two neighbours (24 gaps; a neighbour without leaves has
@@ -1282,6 +1342,9 @@ __global__ void __launch_bounds__(THREADS, MINB)
         if (cnt == (uint32_t)TILE) tile_body(std::true_type{});
         else tile_body(std::false_type{});
         RTF_TICK(6);
+#ifdef RTF_PHASE_TIMING
+        if (tid == 0 && t < 65536) g_tile_ns[t][1] = globaltimer_ns();
+#endif
     }
     if (tid == kIssuer && store_pending) {  // every record written before the grid barrier
         bulk_wait0();
@@ -1369,9 +1432,13 @@ __global__ void __launch_bounds__(THREADS, MINB)
                         lamp = spine_lowest(__ldcg(&SP[u].mR), __ldcg(&SP[u].walls) & 2u);
                     const int32_t ref = __ldcg(&S->ref0);
                     if (lamp <= lam0) {
-                        if (local(j0)) A.nodes[j0].child[1] = ref;
+                        if (local(j0)) {
+                            A.nodes[j0].child[1] = ref;
+                            RTF_SLOT(j0, 1u, -1);
+                        }
                     } else if (local(j0 + 1)) {
                         A.nodes[j0 + 1].child[0] = ref;
+                        RTF_SLOT(j0 + 1, 0u, -1);
                     }
                     if ((lamp & lam0 & kLamBoundary) != 0 && local(j0)) {  // a one-leaf cell
                         const uint64_t key = __ldcg(&A.nodes[j0].key);
@@ -1438,9 +1505,13 @@ __global__ void __launch_bounds__(THREADS, MINB)
                     }
                     const int32_t node = (int32_t)(g + 1);
                     if (lamL <= lamR) {
-                        if (local((uint32_t)(gL + 1))) A.nodes[gL + 1].child[1] = node;
+                        if (local((uint32_t)(gL + 1))) {
+                            A.nodes[gL + 1].child[1] = node;
+                            RTF_SLOT(gL + 1, 1u, node);
+                        }
                     } else if (local((uint32_t)(gR + 1))) {
                         A.nodes[gR + 1].child[0] = node;
+                        RTF_SLOT(gR + 1, 0u, node);
                     }
                 }
             }
@@ -1486,7 +1557,87 @@ uint32_t build_queue_capacity(uint32_t m) { return m / (kShortRun + 1u) + m / kC
 
 size_t spine_row_bytes() { return sizeof(TileSpine); }
 
+// ------------------------------------------------------------ phase A per chunk
+// Phase A of a build from host memory (rtf_build_host), run on each chunk as
+// its host-to-device copy lands, so the scan for the largest weight overlaps
+// the rest of the copy: the same two integer maxima of the raw float bits as
+// phase A (exact flags when a chunk holds invalid data), MAX-reduced into the
+// scale word {bits of max p, NaN, Inf, negative} the build then reads instead
+// of running phase A (the scale word of a sharded build, kPhScale absent).
+__global__ void __launch_bounds__(256) k_scale_chunk(const float* __restrict__ p, uint32_t n,
+                                                     uint32_t* __restrict__ scale_io) {
+    const uint32_t tid = blockIdx.x * blockDim.x + threadIdx.x, G = gridDim.x * blockDim.x;
+    const bool vec = ((uintptr_t)p & 15u) == 0;
+    const uint32_t n4 = vec ? n >> 2 : 0u;
+    // every element this thread owns: float4 q = tid + k G, then the scalar tail
+    auto each = [&](auto&& f) {
+        for (uint32_t q = tid; q < n4; q += G) {
+            const float4 v = ld_stream_f4(p + 4ull * q);
+            f(v.x);
+            f(v.y);
+            f(v.z);
+            f(v.w);
+        }
+        for (uint32_t i = 4 * n4 + tid; i < n; i += G) f(p[i]);
+    };
+    int32_t smax = 0;
+    uint32_t umax = 0;
+    each([&](float x) {
+        smax = max(smax, __float_as_int(x));
+        umax = max(umax, __float_as_uint(x));
+    });
+    uint32_t fl = 0;
+    if (smax >= 0x7f800000 || umax > 0x80000000u)  // invalid data among this thread's: exact flags
+        each([&](float x) {
+            if (x != x) fl |= RTF_DATA_NAN;
+            else if (fabsf(x) == __int_as_float(0x7f800000)) fl |= RTF_DATA_INF;
+            else if (x < 0.0f) fl |= RTF_DATA_NEG;
+        });
+    const uint32_t mx = __reduce_max_sync(0xffffffffu, (uint32_t)smax);
+    fl = __reduce_or_sync(0xffffffffu, fl);
+    if ((threadIdx.x & 31) == 0) {
+        atomicMax(&scale_io[0], mx);
+        if (fl & RTF_DATA_NAN) atomicMax(&scale_io[1], 1u);
+        if (fl & RTF_DATA_INF) atomicMax(&scale_io[2], 1u);
+        if (fl & RTF_DATA_NEG) atomicMax(&scale_io[3], 1u);
+    }
+}
+
+static int num_sms(int dev);
+
+cudaError_t launch_scale_chunk(const float* p, uint32_t n, void* ws, const WsLayout& L,
+                               cudaStream_t st, int* launches) {
+    if (n == 0) return cudaSuccess;
+    uint32_t* scale_io = reinterpret_cast<uint32_t*>(reinterpret_cast<unsigned char*>(ws) + L.scale);
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess) return cudaErrorInvalidDevice;
+    const uint32_t want = (n / 4 + 255) / 256;  // one float4 per thread, capped at 4 CTAs per SM
+    const uint32_t grid = std::max(1u, std::min(want, (uint32_t)(4 * num_sms(dev))));
+    k_scale_chunk<<<grid, 256, 0, st>>>(p, n, scale_io);
+    ++*launches;
+    return cudaGetLastError();
+}
+
+cudaError_t clear_scale(void* ws, const WsLayout& L, cudaStream_t st) {
+    return cudaMemsetAsync(reinterpret_cast<unsigned char*>(ws) + L.scale, 0, 16, st);
+}
+
+#ifdef RTF_SLOT_CHECK
+// fields: 2 (n' + 1) zeroed u32, nodes: n' + 1 zeroed u32 (device; null: off)
+int rows_slot_buffers(uint32_t* fields, uint32_t* nodes);  // rtf_rows.cu
+extern "C" int rtf_debug_slot_buffers(uint32_t* fields, uint32_t* nodes) {
+    cudaError_t e = cudaMemcpyToSymbol(g_slot_fields, &fields, sizeof(fields));
+    if (e == cudaSuccess) e = cudaMemcpyToSymbol(g_slot_nodes, &nodes, sizeof(nodes));
+    if (e != cudaSuccess) return 5;
+    return rows_slot_buffers(fields, nodes);
+}
+#endif
+
 #ifdef RTF_PHASE_TIMING
+extern "C" int rtf_debug_tile_ns(unsigned long long* host, int tiles) {
+    return cudaMemcpyFromSymbol(host, g_tile_ns, sizeof(unsigned long long) * 3 * tiles) ==
+                   cudaSuccess ? 0 : 5;
+}
 extern "C" int rtf_debug_phase_cycles(unsigned long long* host, int rows, int reset) {
     cudaError_t e = cudaMemcpyFromSymbol(host, g_phase_cycles, sizeof(unsigned long long) * 16 * rows);
     if (reset && e == cudaSuccess) {

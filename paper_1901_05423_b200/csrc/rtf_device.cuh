@@ -424,6 +424,24 @@ __device__ __forceinline__ void st_cell(rtf_ref* table, uint32_t g, uint32_t key
     *reinterpret_cast<uint2*>(table + g) = make_uint2(key32, (uint32_t)ref);
 }
 
+// Cells [g0, g1) of an empty run all get {0, ref}.  RTF_WIDE_RUNS: scalar up
+// to a 4-cell (32-B) boundary, then one 256-bit store per 4 cells (the table
+// is 256-B aligned) -- measured slower on configs 2 and 3 (280 vs 272 us,
+// 76 vs 72 us: the runs there are a few cells long), so not the default.
+__device__ __forceinline__ void fill_run(rtf_ref* table, uint32_t g0, uint32_t g1, int32_t ref) {
+#ifndef RTF_WIDE_RUNS
+    for (uint32_t g = g0; g < g1; ++g) st_cell(table, g, 0u, ref);
+#else
+    uint32_t g = g0;
+    const uint32_t r = (uint32_t)ref;
+    for (; g < g1 && (g & 3u); ++g) st_cell(table, g, 0u, ref);
+    for (; g + 4u <= g1; g += 4u)
+        asm volatile("st.global.v8.b32 [%0], {%1, %2, %1, %2, %1, %2, %1, %2};"
+                     :: "l"(table + g), "r"(0u), "r"(r) : "memory");
+    for (; g < g1; ++g) st_cell(table, g, 0u, ref);
+#endif
+}
+
 // ------------------------------------------------------------ scan prefix payload
 
 // Aggregate of a run of entries: sum of quantised weights, number of positive

@@ -65,6 +65,12 @@ struct ShardCall {
     int32_t j_rank = -1;  // >= 0: finish reads [j_lo, j_hi) = jbound[j_rank .. j_rank + 1]
 };
 
+// phase A of a host-buffer build, one chunk of p at a time (rtf_build_host):
+// MAX-reduces into the workspace's scale word (cleared first by clear_scale)
+cudaError_t launch_scale_chunk(const float* p, uint32_t n, void* ws, const WsLayout& L,
+                               cudaStream_t st, int* launches);
+cudaError_t clear_scale(void* ws, const WsLayout& L, cudaStream_t st);
+
 // leaves of nodes[j0, j0 + cnt) whose cell is below bound[k]: counts[k], k < nb
 cudaError_t launch_count_cells(const rtf_node* nodes, uint32_t j0, uint32_t cnt, uint32_t m,
                                const uint32_t* bounds, uint32_t nb, uint32_t* counts,
@@ -133,5 +139,27 @@ cudaError_t launch_cutpoint(const uint64_t* cdf, uint32_t n, const rtf_header* h
 
 cudaError_t launch_philox(uint64_t seed, uint64_t start, uint64_t count, uint32_t* out,
                           cudaStream_t st, int* launches);
+
+// Slot-arrival check (debug builds only, -DRTF_SLOT_CHECK; rtf_debug_slot_buffers,
+// tools/slotcheck_target.py): every link write also counts, per record child
+// field, how often it was written, and per record, how often it was linked as
+// an internal node (node < 0: a leaf reference, not counted).  A race between
+// two writers of one field shows as a count of 2 even when the bytes agree;
+// Alg. 1's invariant (every internal node gets exactly one
+// parent) is a count of exactly 1 per non-anchor record.  Each translation
+// unit has its own copy of the two pointers (set by rtf_debug_slot_buffers).
+#ifdef RTF_SLOT_CHECK
+static __device__ uint32_t* g_slot_fields;  // 2 per record (+ 1 spare record)
+static __device__ uint32_t* g_slot_nodes;   // per record
+#define RTF_SLOT(rec, side, node)                                                         \
+    do {                                                                                  \
+        if (g_slot_fields) atomicAdd(g_slot_fields + 2ull * (uint64_t)(rec) + (side), 1u); \
+        if (g_slot_nodes && (int64_t)(node) >= 0) atomicAdd(g_slot_nodes + (uint64_t)(node), 1u); \
+    } while (0)
+#else
+#define RTF_SLOT(rec, side, node) \
+    do {                          \
+    } while (0)
+#endif
 
 }  // namespace rtf

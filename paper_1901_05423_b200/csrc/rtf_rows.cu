@@ -263,11 +263,13 @@ __global__ void __launch_bounds__(THREADS, rows_min_blocks<THREADS, VPT>()) k_bu
                     const int32_t leaf = ~(int32_t)(first + k);
                     if ((lamL & lamR & kLamBoundary) != 0) {  // a cell root
                         s_c1[Pd(l)] = leaf;
+                        RTF_SLOT((uint64_t)r * n + l, 1u, -1);
                         continue;
                     }
                     const uint32_t q = right ? l : l + 1;
                     const uint32_t qp = Pd(q);
                     (right ? s_c1 : s_c0)[qp] = leaf;
+                    RTF_SLOT((uint64_t)r * n + q, right ? 1u : 0u, -1);
                     const int32_t other = atomicExch(&s_ob[qp], (int32_t)((right ? lamR : lamL) << 16 | l));
                     if (other >= 0) {
                         s_ob[qp] = -1;
@@ -314,6 +316,7 @@ __global__ void __launch_bounds__(THREADS, rows_min_blocks<THREADS, VPT>()) k_bu
             if (active) {
                 if ((lamL & lamR & kLamBoundary) != 0) {  // a cell root: right child of its anchor
                     s_c1[Pd(lo)] = node;
+                    RTF_SLOT((uint64_t)r * n + (uint32_t)lo, 1u, (uint64_t)r * n + (uint32_t)node);
                     active = false;
                     continue;
                 }
@@ -321,6 +324,7 @@ __global__ void __launch_bounds__(THREADS, rows_min_blocks<THREADS, VPT>()) k_bu
                 const int32_t parent = right ? lo : hi + 1;
                 const uint32_t pp = Pd((uint32_t)parent);
                 (right ? s_c1 : s_c0)[pp] = node;
+                RTF_SLOT((uint64_t)r * n + (uint32_t)parent, right ? 1u : 0u, (uint64_t)r * n + (uint32_t)node);
                 const int32_t dep = right ? (int32_t)(lamR << 16 | (uint32_t)hi)
                                           : (int32_t)(lamL << 16 | (uint32_t)lo);
                 const int32_t other = atomicExch(&s_ob[pp], dep);
@@ -406,5 +410,13 @@ cudaError_t launch_build_rows(const float* p, uint32_t rows, uint32_t n_row, uin
     ++*launches;
     return e;
 }
+
+#ifdef RTF_SLOT_CHECK
+int rows_slot_buffers(uint32_t* fields, uint32_t* nodes) {
+    cudaError_t e = cudaMemcpyToSymbol(g_slot_fields, &fields, sizeof(fields));
+    if (e == cudaSuccess) e = cudaMemcpyToSymbol(g_slot_nodes, &nodes, sizeof(nodes));
+    return e == cudaSuccess ? 0 : 5;
+}
+#endif
 
 }  // namespace rtf

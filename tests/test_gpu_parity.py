@@ -365,6 +365,38 @@ def test_host_entry_points(rtf):
     assert np.array_equal(out_host.numpy(), ref.sample(xi))
 
 
+def test_host_build_chunked_scale(rtf):
+    """rtf_build_host copies p in chunks and runs phase A per chunk while the
+    rest lands: the largest weight in the last chunk, a smaller maximum after
+    a larger one (the scale word is cleared per call), a ragged n, a NaN in
+    the last chunk and an all-zero input."""
+    cases = [(power_law((1 << 20) + 3, "A"), 1 << 18),  # max at the very end, ragged n
+             (power_law(300001, "D"), 70001),             # max at the start
+             (env_map(1024, 512, seed=8) * np.float32(1e-3), 1 << 17)]
+    for p, m in cases:
+        ref = oracle.build(p, m)
+        f = rtf.Forest(p.size, m)
+        p_host = torch.from_numpy(np.ascontiguousarray(p, np.float32)).pin_memory()
+        p_dev = torch.empty(p.size, dtype=torch.float32, device=DEV)
+        big = torch.full_like(p_host, 1e30).pin_memory()
+        assert rtf.build_host(f, big, p_dev) == 0          # a larger maximum first
+        assert rtf.build_host(f, p_host, p_dev) == 0
+        assert_forest_equal(f, ref, "chunked host build")
+        assert f.header().exponent == ref_exponent(p)
+        bad = p_host.clone().pin_memory()
+        bad[-1] = float("nan")
+        st = rtf.build_host(f, bad, p_dev)
+        assert st == rtf._lib.RTF_EDATA and (f.header().status & rtf.RTF_DATA_NAN)
+        zero = torch.zeros_like(p_host).pin_memory()
+        assert rtf.build_host(f, zero, p_dev) == rtf._lib.RTF_EALLZERO
+        assert rtf.build_host(f, p_host, p_dev) == 0       # recovers
+        assert_forest_equal(f, ref, "chunked host build after poisoned inputs")
+
+
+def ref_exponent(p):
+    return int(np.floor(np.log2(np.float64(np.max(p)))))
+
+
 def test_stratified_histogram_closed_form_gpu(rtf):
     p = env_map(1024, 512, seed=2)
     f = rtf.build(dev_f32(p), 4096)

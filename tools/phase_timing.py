@@ -64,6 +64,35 @@ def run(reps, workload):
         col = per[:, s]
         print(f"  {name:30s} mean {col.mean():9.0f}  max {col.max():9.0f}  "
               f"{100 * col.mean() / tot.mean():5.1f} %")
+    # per-tile timeline of the last build (globaltimer, ns)
+    try:
+        tf = ctypes.CDLL(LIB).rtf_debug_tile_ns
+        tf.argtypes = [ctypes.c_void_p, ctypes.c_int]
+        nt = (wl["n"] + 4095) // 4096
+        tb = np.zeros((min(nt, 65536), 3), np.uint64)
+        tf(tb.ctypes.data, tb.shape[0])
+        st = tb[:, 0].astype(np.int64)
+        en = tb[:, 1].astype(np.int64)
+        t0 = st.min()
+        dur = (en - st) / 1e3
+        nb = 16
+        print(f"  tiles {nt}: phase D span {(en.max() - t0) / 1e3:.1f} us from the first tile start; "
+              f"tile duration us (mean / p90 / max) {dur.mean():.2f} / {np.percentile(dur, 90):.2f} / {dur.max():.2f}")
+        for k in range(nb):
+            sl = slice(k * nt // nb, (k + 1) * nt // nb)
+            print(f"    tiles {sl.start:6d}-{sl.stop - 1:6d}: mean {dur[sl].mean():6.2f} us  max {dur[sl].max():6.2f}")
+        cta = tb[:, 2].astype(np.int64)
+        last_end = np.zeros(cta.max() + 1, np.int64)
+        np.maximum.at(last_end, cta, en)
+        le = (last_end[last_end > 0] - t0) / 1e3
+        print(f"  per-CTA last tile end (us from start): min {le.min():.1f} median {np.median(le):.1f} "
+              f"max {le.max():.1f}")
+        order = np.argsort(en)[-8:]
+        print("  last tiles to finish: " + ", ".join(f"t{int(t)} ({dur[t]:.1f} us, ends {(en[t] - t0) / 1e3:.1f})"
+                                                  for t in order))
+        np.save(os.path.join(ROOT, "gpurun_out", f"tiles_{workload}.npy"), tb)
+    except AttributeError:
+        pass
     ex = extra[used]
     print(f"  (issuer waiting for the TMA store to read the stage: mean {ex[:, 0].mean():.0f}; "
           f"thread 0 waiting for the weights' TMA load: mean {ex[:, 1].mean():.0f} cycles per CTA)")
