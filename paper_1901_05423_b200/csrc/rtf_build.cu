@@ -328,6 +328,29 @@ __device__ __forceinline__ unsigned long long globaltimer_ns() {
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
     return t;
 }
+// per block barrier of phase D: the spread of the warps' arrival times
+// (last minus first, clock64 of lane 0 of each warp), accumulated in slots
+// 11-13 of the CTA's row
+__shared__ unsigned long long s_arr_lo[3], s_arr_hi[3];
+__device__ unsigned long long g_last_warp[3][32];  // per barrier: how often warp w arrived last
+#define RTF_ARRIVE(k)                                                        \
+    do {                                                                     \
+        if ((threadIdx.x & 31) == 0) {                                       \
+            const unsigned long long c_ = (unsigned long long)clock64();     \
+            atomicMin(&s_arr_lo[k], c_);                                     \
+            atomicMax(&s_arr_hi[k], (c_ << 5) | (threadIdx.x >> 5));         \
+        }                                                                    \
+    } while (0)
+#define RTF_SPREAD(k)                                                        \
+    do {                                                                     \
+        __syncthreads();                                                     \
+        if (threadIdx.x == 0) {                                              \
+            g_phase_cycles[blockIdx.x][11 + (k)] += (s_arr_hi[k] >> 5) - s_arr_lo[k]; \
+            atomicAdd(&g_last_warp[k][s_arr_hi[k] & 31u], 1ull);            \
+            s_arr_lo[k] = ~0ull;                                             \
+            s_arr_hi[k] = 0ull;                                              \
+        }                                                                    \
+    } while (0)
 #define RTF_TICK(slot)                                                       \
     do {                                                                     \
         if (threadIdx.x == 0) {                                              \
@@ -339,6 +362,12 @@ __device__ __forceinline__ unsigned long long globaltimer_ns() {
 #else
 #define RTF_TICK(slot) \
     do {               \
+    } while (0)
+#define RTF_ARRIVE(k) \
+    do {              \
+    } while (0)
+#define RTF_SPREAD(k) \
+    do {              \
     } while (0)
 #endif
 
@@ -369,7 +398,7 @@ __global__ void __launch_bounds__(THREADS, MINB)
     __shared__ uint32_t s_wmax[NW];  // per warp: max of its threads' 1 + max split level
     __shared__ uint32_t s_B[NW * 64];  // per warp and level v: its threads with a level > v
     __shared__ uint16_t s_task[NW * 256];  // per warp: its spine gaps (thread << 3 | gap)
-    __shared__ __align__(16) Pfx s_rpre;  // the next tile's range prefix (issuer thread)
+    __shared__ __align__(16) Pfx s_rpre;  // TMA target: the next tile's range prefix
     __shared__ Pfx s_tot;
     __shared__ uint32_t s_next;
     __shared__ __align__(16) Pfx s_pin;  // TMA target: the next tile's prefix within its range
@@ -397,6 +426,10 @@ __global__ void __launch_bounds__(THREADS, MINB)
     const int32_t ib = (int32_t)A.index_base;  // original indices are global
 #ifdef RTF_PHASE_TIMING
     long long t_tick_ = clock64();
+    if (tid < 3) {
+        s_arr_lo[tid] = ~0ull;
+        s_arr_hi[tid] = 0ull;
+    }
 #endif
     const bool sharded = A.shard_count > 0;
 
@@ -736,10 +769,12 @@ __global__ void __launch_bounds__(THREADS, MINB)
     static_assert(VPT == 8, "phase D packs a thread's 8 split levels into one 64-bit word");
     constexpr uint32_t kIssuer = THREADS - 1;  // TMA, tickets, stores: the last warp
     uint32_t phase = 0;
-    uint32_t ticket = 0;      // issuer: the tile after the next one (>= nt: none)
+    // issuer: the dispenser's count for the tile after the next one; the
+    // atomic's result is first used one tile later (tmap(G + ticket)), so its
+    // latency hides behind a tile's work
+    uint32_t ticket = 0;
     bool store_pending = false;  // issuer: a TMA store group may still read the stage
-    // the next tile to deal (>= nt: none left)
-    auto draw = [&]() -> uint32_t { return tmap(G + atomicAdd(&A.counters[kCtrTile], 1u)); };
+    auto draw = [&]() -> uint32_t { return atomicAdd(&A.counters[kCtrTile], 1u); };
     if (tid == 0) {
         s_mL = s_mR = 0ull;
         s_fw = 0xffffffffu;
@@ -750,6 +785,7 @@ __global__ void __launch_bounds__(THREADS, MINB)
         if (ph & kPhTiles) ticket = draw();
     }
     if (ph & kPhTiles) wait_rpre();
+    if (tid == kIssuer) fence_proxy_async_global();  // the range prefixes, read by TMA below
 
     // Gaps above level v in a thread's packed split levels: byte + 127 - v
     // reaches bit 7 exactly when byte > v (bytes <= 64, so no carries).
@@ -868,31 +904,31 @@ __global__ void __launch_bounds__(THREADS, MINB)
             s_w[warp] = wi;
             s_c[warp] = ci;
         }
-        if (tid == kIssuer && store_pending) {  // the previous tile's records have left the stage
+        if (store_pending) {  // the previous tile's records have left the stage
 #ifdef RTF_PHASE_TIMING
             const long long tw0_ = clock64();
             bulk_wait_read0();
-            g_phase_cycles[blockIdx.x][9] += (unsigned long long)(clock64() - tw0_);
+            if (tid == 0) g_phase_cycles[blockIdx.x][9] += (unsigned long long)(clock64() - tw0_);
 #else
             bulk_wait_read0();
 #endif
             store_pending = false;
         }
+        RTF_ARRIVE(0);
         __syncthreads();
+        RTF_SPREAD(0);
         RTF_TICK(3);
         if (tid == kIssuer) {  // every thread has its weights: the next tile can stream in
-            const uint32_t nx = ticket;
+            const uint32_t nx = tmap(G + ticket);
             s_next = nx;  // read at the end of this tile
-            if (tma_tile(nx)) {
+            if (tma_tile(nx)) {  // the weights, the prefix within the range and the range's prefix
                 fence_proxy_async_smem();
-                mbar_arrive_expect_tx(&s_bar, TILE * 4 + (uint32_t)sizeof(Pfx));
+                mbar_arrive_expect_tx(&s_bar, TILE * 4 + 2u * (uint32_t)sizeof(Pfx));
                 tma_load_1d(s_p, A.p + (size_t)nx * TILE, TILE * 4, &s_bar);
                 tma_load_1d(&s_pin, A.excl + nx, (uint32_t)sizeof(Pfx), &s_bar);
+                tma_load_1d(&s_rpre, A.rpre + nx / krng, (uint32_t)sizeof(Pfx), &s_bar);
             }
-            if (nx < nt) {
-                s_rpre = ld_pfx_cg(&A.rpre[nx / krng]);  // read at the next tile's step (0)
-                ticket = draw();
-            }
+            if (nx < nt) ticket = draw();
         }
         uint64_t w_ex;
         uint32_t c_ex_in, cnt;
@@ -1088,7 +1124,9 @@ __global__ void __launch_bounds__(THREADS, MINB)
                 s_B[warp * 64 + v] = bits;
             }
         }
+        RTF_ARRIVE(1);
         __syncthreads();
+        RTF_SPREAD(1);
         RTF_TICK(4);
 
         // (5b) cells holding exactly two leaves a, a+1 (reading R20) with
@@ -1273,7 +1311,9 @@ __global__ void __launch_bounds__(THREADS, MINB)
             }
         }
         fence_proxy_async_smem();  // the staged records are read by the TMA store below
+        RTF_ARRIVE(2);
         __syncthreads();
+        RTF_SPREAD(2);
         RTF_TICK(5);
 
         // (7) records out: whole 64-record blocks (1024-B aligned in the stage)
@@ -1346,7 +1386,7 @@ __global__ void __launch_bounds__(THREADS, MINB)
         if (tid == 0 && t < 65536) g_tile_ns[t][1] = globaltimer_ns();
 #endif
     }
-    if (tid == kIssuer && store_pending) {  // every record written before the grid barrier
+    if (store_pending) {  // every record written before the grid barrier
         bulk_wait0();
         fence_proxy_async_global();
     }
@@ -1634,6 +1674,9 @@ extern "C" int rtf_debug_slot_buffers(uint32_t* fields, uint32_t* nodes) {
 #endif
 
 #ifdef RTF_PHASE_TIMING
+extern "C" int rtf_debug_last_warp(unsigned long long* host) {
+    return cudaMemcpyFromSymbol(host, g_last_warp, sizeof(g_last_warp)) == cudaSuccess ? 0 : 5;
+}
 extern "C" int rtf_debug_tile_ns(unsigned long long* host, int tiles) {
     return cudaMemcpyFromSymbol(host, g_tile_ns, sizeof(unsigned long long) * 3 * tiles) ==
                    cudaSuccess ? 0 : 5;

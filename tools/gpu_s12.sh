@@ -1,0 +1,2 @@
+timeout 300 python tools/phase_timing.py --reps 20 2>&1 | grep -v "^    tiles"
+timeout 300 python tools/phase_timing.py --reps 20 --workload c2 2>&1 | grep -v "^    tiles"

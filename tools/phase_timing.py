@@ -94,6 +94,19 @@ def run(reps, workload):
     except AttributeError:
         pass
     ex = extra[used]
+    spread = buf[used, 11:14].astype(np.float64) / reps
+    print("  warp arrival spread at phase D's block barriers (last - first, cycles per CTA per build): "
+          + ", ".join(f"barrier {k + 1} {spread[:, k].mean():.0f}" for k in range(3)))
+    try:
+        lw = np.zeros((3, 32), np.uint64)
+        ctypes.CDLL(LIB).rtf_debug_last_warp(ctypes.c_void_p(lw.ctypes.data))
+        for k in range(3):
+            tot_k = max(1, int(lw[k].sum()))
+            top = np.argsort(lw[k])[::-1][:4]
+            print(f"  barrier {k + 1}: last to arrive " + ", ".join(
+                f"warp {int(w)} {100 * int(lw[k][w]) / tot_k:.0f}%" for w in top))
+    except AttributeError:
+        pass
     print(f"  (issuer waiting for the TMA store to read the stage: mean {ex[:, 0].mean():.0f}; "
           f"thread 0 waiting for the weights' TMA load: mean {ex[:, 1].mean():.0f} cycles per CTA)")
 
