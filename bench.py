@@ -340,7 +340,6 @@ def run_gpu(args):
     # ------------------------------------------------ baseline: the alias method (Sec.2.6)
     # host-built table over the same xi grid (baselines/alias.c); every item
     # receives exactly its inverse-CDF xi count (checked here), not the same xi
-    import numpy as np
     import baselines
     K_host = cdf.cdf.cpu().numpy().view(np.uint64)
     prob, alias, ak = baselines.alias_table(K_host)
