@@ -77,6 +77,13 @@ struct TileSpine {
 static_assert(sizeof(TileSpine) % 16 == 0, "TileSpine rows stay 16-B aligned");
 constexpr int32_t kNoLink = INT32_MIN;
 
+// phase D's record stores: tensor maps of the node array with boxes of
+// 64 << k records (k = 0..5)
+constexpr int kNodeMaps = 6;
+struct NodeMaps {
+    CUtensorMap m[kNodeMaps];
+};
+
 struct BuildArgs {
     const float* p;
     uint32_t n, m, nt;
@@ -375,8 +382,7 @@ __device__ unsigned long long g_last_warp[3][32];  // per barrier: how often war
 
 template <int THREADS, int VPT, bool CDF, int MINB = 2, bool POW2 = false, bool FUSED = false>
 __global__ void __launch_bounds__(THREADS, MINB)
-    k_build(BuildArgs A, const __grid_constant__ CUtensorMap tm_big,
-            const __grid_constant__ CUtensorMap tm_small, const __grid_constant__ CUtensorMap tm_huge) {
+    k_build(BuildArgs A, const __grid_constant__ NodeMaps tm) {
     constexpr int TILE = THREADS * VPT;
     constexpr int NW = THREADS / 32;
     extern __shared__ __align__(1024) unsigned char smem_raw[];
@@ -908,7 +914,7 @@ __global__ void __launch_bounds__(THREADS, MINB)
 #ifdef RTF_PHASE_TIMING
             const long long tw0_ = clock64();
             bulk_wait_read0();
-            if (tid == 0) g_phase_cycles[blockIdx.x][9] += (unsigned long long)(clock64() - tw0_);
+            if (tid == kIssuer) g_phase_cycles[blockIdx.x][9] += (unsigned long long)(clock64() - tw0_);
 #else
             bulk_wait_read0();
 #endif
@@ -1324,18 +1330,13 @@ __global__ void __launch_bounds__(THREADS, MINB)
             if (!A.tma_store || FUSED || a1 <= a0) a0 = a1 = e1;  // every record by the threads
             if (tid == kIssuer && a1 > a0) {
                 const uint32_t base = j0 & ~63u;
+                // the largest power-of-two box (2048 .. 64 records) that fits:
+                // at most 6 store instructions for the aligned middle
                 for (uint32_t a = a0; a < a1;) {
-                    const unsigned char* src = s_stage + 16u * (a - base);
-                    if (a1 - a >= 2048u) {
-                        tma_store_2d(&tm_huge, 0, (int)(a >> 3), src);
-                        a += 2048u;
-                    } else if (a1 - a >= 256u) {
-                        tma_store_2d(&tm_big, 0, (int)(a >> 3), src);
-                        a += 256u;
-                    } else {
-                        tma_store_2d(&tm_small, 0, (int)(a >> 3), src);
-                        a += 64u;
-                    }
+                    const uint32_t left = (a1 - a) >> 6;  // whole 64-record blocks
+                    const int k = min(5, 31 - __clz((int)left));
+                    tma_store_2d(&tm.m[k], 0, (int)(a >> 3), s_stage + 16u * (a - base));
+                    a += 64u << k;
                 }
                 bulk_commit();
                 store_pending = true;
@@ -1741,11 +1742,9 @@ static int num_sms(int dev) {
 }
 
 // the node array as rows of 8 records (128 B) for the TMA tensor stores of
-// phase D: boxes of 256 rows (2048 records), 32 rows (256 records) and 8 rows
-// (64 records), 128-B swizzle (the stage layout, stage_pos).  false: no
-// tensor stores.
-static bool node_tensor_maps(rtf_node* nodes, uint64_t records, CUtensorMap* big,
-                             CUtensorMap* small, CUtensorMap* huge) {
+// phase D: boxes of 8 << k rows (64 << k records, k = 0..5), 128-B swizzle
+// (the stage layout, stage_pos).  false: no tensor stores.
+static bool node_tensor_maps(rtf_node* nodes, uint64_t records, NodeMaps* tm) {
     static std::atomic<PFN_cuTensorMapEncodeTiled_v12000> s_enc{nullptr};
     static std::atomic<int> s_tried{0};
     PFN_cuTensorMapEncodeTiled_v12000 enc = s_enc.load();
@@ -1763,21 +1762,18 @@ static bool node_tensor_maps(rtf_node* nodes, uint64_t records, CUtensorMap* big
     cuuint64_t dims[2] = {32, rows};
     cuuint64_t strides[1] = {128};
     cuuint32_t es[2] = {1, 1};
-    cuuint32_t bb[2] = {32, 32}, bs[2] = {32, 8}, bh[2] = {32, 256};
-    return enc(huge, CU_TENSOR_MAP_DATA_TYPE_UINT32, 2, nodes, dims, strides, bh, es,
-               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
-               CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS &&
-           enc(big, CU_TENSOR_MAP_DATA_TYPE_UINT32, 2, nodes, dims, strides, bb, es,
-               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
-               CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS &&
-           enc(small, CU_TENSOR_MAP_DATA_TYPE_UINT32, 2, nodes, dims, strides, bs, es,
-               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
-               CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+    for (int k = 0; k < kNodeMaps; ++k) {
+        cuuint32_t box[2] = {32, 8u << k};
+        if (enc(&tm->m[k], CU_TENSOR_MAP_DATA_TYPE_UINT32, 2, nodes, dims, strides, box, es,
+                CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+            return false;
+    }
+    return true;
 }
 
 template <int THREADS, int VPT, bool CDF, int MINB = 2, bool POW2 = false, bool FUSED = false>
-static cudaError_t launch_fused(BuildArgs& A, const CUtensorMap* tmb, const CUtensorMap* tms,
-                                const CUtensorMap* tmh,
+static cudaError_t launch_fused(BuildArgs& A, const NodeMaps* tm,
                                 cudaStream_t st, int* launches) {
     auto kern = k_build<THREADS, VPT, CDF, MINB, POW2, FUSED>;
     const size_t smem = build_smem_bytes<THREADS, VPT>();  // phase B stages tile totals there
@@ -1801,8 +1797,7 @@ static cudaError_t launch_fused(BuildArgs& A, const CUtensorMap* tmb, const CUte
         max_grid_dev[dev].store(max_grid, std::memory_order_relaxed);
     }
     const uint32_t grid = std::max<uint32_t>(1u, std::min<uint32_t>(A.nt, (uint32_t)max_grid));
-    void* args[] = {&A, const_cast<CUtensorMap*>(tmb), const_cast<CUtensorMap*>(tms),
-                    const_cast<CUtensorMap*>(tmh)};
+    void* args[] = {&A, const_cast<NodeMaps*>(tm)};
     const cudaError_t e =
         cudaLaunchCooperativeKernel((const void*)kern, dim3(grid), dim3(THREADS), args, smem, st);
     ++*launches;
@@ -1858,10 +1853,8 @@ cudaError_t launch_build(const float* p, uint32_t n, uint32_t m, uint32_t flags,
     A.vec = ((uintptr_t)p & 15u) == 0;
     // phase D's record stores: tensor maps over the caller's node array
     // (sharded calls address the whole forest with global leaf indices)
-    alignas(64) CUtensorMap tmb, tms, tmh;
-    std::memset(&tmb, 0, sizeof(tmb));
-    std::memset(&tms, 0, sizeof(tms));
-    std::memset(&tmh, 0, sizeof(tmh));
+    NodeMaps tm;
+    std::memset(&tm, 0, sizeof(tm));
     A.mshift = 63u - (uint32_t)ceil_log2_u32(m);
 #ifdef RTF_NO_PACK2
     A.pack2 = false;
@@ -1869,23 +1862,23 @@ cudaError_t launch_build(const float* p, uint32_t n, uint32_t m, uint32_t flags,
     A.pack2 = !cdf && pack2_possible(m);
 #endif
     A.tma_store = !cdf && (A.phases & kPhTiles) &&
-                  node_tensor_maps(nodes, sc ? sc->n_global : n, &tmb, &tms, &tmh);
+                  node_tensor_maps(nodes, sc ? sc->n_global : n, &tm);
     const bool small = flags & RTF_BUILD_SMALL_TILES;
     if (cdf)
-        return small ? launch_fused<64, 4, true>(A, &tmb, &tms, &tmh, st, launches)
-                     : launch_fused<kTT, 8, true, kTB>(A, &tmb, &tms, &tmh, st, launches);
+        return small ? launch_fused<64, 4, true>(A, &tm, st, launches)
+                     : launch_fused<kTT, 8, true, kTB>(A, &tm, st, launches);
     // 512 x 8 at 2 CTAs/SM (4096-entry tiles); RTF_BUILD_SMALL_TILES: 32 x 8
     // (256-entry tiles, most links cross tiles: a test schedule)
     const bool pow2 = (m & (m - 1)) == 0;
     A.mshift = 63u - (uint32_t)ceil_log2_u32(m);
     if (A.npeer)  // fused ranged sharding (rtf_shard_build_peers)
-        return small ? launch_fused<32, 8, false, 2, false, true>(A, &tmb, &tms, &tmh, st, launches)
-                     : launch_fused<kTT, 8, false, kTB, false, true>(A, &tmb, &tms, &tmh, st, launches);
+        return small ? launch_fused<32, 8, false, 2, false, true>(A, &tm, st, launches)
+                     : launch_fused<kTT, 8, false, kTB, false, true>(A, &tm, st, launches);
     if (small)
-        return pow2 ? launch_fused<32, 8, false, 2, true>(A, &tmb, &tms, &tmh, st, launches)
-                    : launch_fused<32, 8, false>(A, &tmb, &tms, &tmh, st, launches);
-    return pow2 ? launch_fused<kTT, 8, false, kTB, true>(A, &tmb, &tms, &tmh, st, launches)
-                : launch_fused<kTT, 8, false, kTB>(A, &tmb, &tms, &tmh, st, launches);
+        return pow2 ? launch_fused<32, 8, false, 2, true>(A, &tm, st, launches)
+                    : launch_fused<32, 8, false>(A, &tm, st, launches);
+    return pow2 ? launch_fused<kTT, 8, false, kTB, true>(A, &tm, st, launches)
+                : launch_fused<kTT, 8, false, kTB>(A, &tm, st, launches);
 }
 
 }  // namespace rtf

@@ -72,7 +72,7 @@ with open(os.path.join(P, f"{R}_ncu_full.csv"), "w", newline="") as f:
         name = r[h.index("Kernel Name")].replace("void ", "").replace("rtf::", "")
         rd = float(r[h.index("dram__bytes_read.sum")].replace(",", "")) * scale.get(units[h.index("dram__bytes_read.sum")], 1)
         wr = float(r[h.index("dram__bytes_write.sum")].replace(",", "")) * scale.get(units[h.index("dram__bytes_write.sum")], 1)
-        if name.startswith("k_sample<0, 0>") or name.startswith("k_sample<0>"):
+        if name.startswith("k_sample<0, 0") or name.startswith("k_sample<0>"):
             # the profiled launch is 2^28 config-3 samples (tools/gpu_ncu_main.sh)
             tr.setdefault("k_sample_per_sample", round((rd + wr) / 2**28, 3))
             continue
