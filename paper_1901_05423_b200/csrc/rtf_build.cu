@@ -1356,11 +1356,14 @@ __global__ void __launch_bounds__(THREADS, MINB)
         // (8) the tile's spine row for phase E
         {
             TileSpine* row = A.spine + t;
-            for (uint32_t u = tid; u < 64; u += THREADS) {
+            // by the middle warps: warp 0 starts the next tile's bookkeeping
+            // and warp 15 holds the issuer
+            constexpr uint32_t kRowT = THREADS >= 512 ? 256u : 0u;
+            for (uint32_t u = tid - kRowT; u < 64; u += THREADS) {
                 row->iL[u] = s_iL[u];
                 row->iR[u] = s_iR[u];
             }
-            if (tid == 0) {
+            if (tid == kRowT) {
                 const uint32_t walls = s_fw != 0xffffffffu ? 3u : 0u;
                 row->mL = s_mL;
                 row->mR = s_mR;
