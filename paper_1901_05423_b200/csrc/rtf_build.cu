@@ -40,6 +40,11 @@ namespace rtf {
 constexpr uint32_t kShortRun = RTF_SHORT_RUN;  // empty-cell runs up to this length: written in place
 constexpr uint32_t kChunk = 2048;   // longer runs: queued in chunks of this many cells
 constexpr uint32_t kMaxGrid = 8192; // partials capacity (CTAs of the cooperative grid)
+#ifndef RTF_LOADS
+#define RTF_LOADS 8  // phases A and B: 16-B loads in flight per thread
+#endif
+static_assert(RTF_LOADS == 4 || RTF_LOADS == 8 || RTF_LOADS == 16,
+              "phase B's batches must divide a tile's 32 float4 per lane");
 
 // workspace counters
 enum : int {
@@ -480,12 +485,13 @@ __global__ void __launch_bounds__(THREADS, MINB)
         if (A.vec) {
             const uint32_t lo4 = a_lo >> 2, hi4 = a_hi >> 2;  // a_lo is a multiple of TILE
             uint32_t q = lo4 + tid;
-            for (; q + 7 * THREADS < hi4; q += 8 * THREADS) {  // 8 independent 16-B loads in flight
-                float4 v[8];
+            // RTF_LOADS independent 16-B loads in flight per thread
+            for (; q + (RTF_LOADS - 1) * THREADS < hi4; q += RTF_LOADS * THREADS) {
+                float4 v[RTF_LOADS];
 #pragma unroll
-                for (int u = 0; u < 8; ++u) v[u] = ld_stream_f4(A.p + 4ull * (q + u * THREADS));
+                for (int u = 0; u < RTF_LOADS; ++u) v[u] = ld_stream_f4(A.p + 4ull * (q + u * THREADS));
 #pragma unroll
-                for (int u = 0; u < 8; ++u) {
+                for (int u = 0; u < RTF_LOADS; ++u) {
                     visit(v[u].x);
                     visit(v[u].y);
                     visit(v[u].z);
@@ -556,7 +562,7 @@ __global__ void __launch_bounds__(THREADS, MINB)
     Pfx* s_tagg = reinterpret_cast<Pfx*>(s_stage);  // phase B's tile totals; free until phase D
     constexpr uint32_t CAP = (uint32_t)(TILE + 64);
     constexpr int F = TILE / 128;  // float4 per lane per tile
-    constexpr int BATCH = F < 8 ? F : 8;
+    constexpr int BATCH = F < RTF_LOADS ? F : RTF_LOADS;
     // short ranges (small n): up to F / BATCH warps share a tile, so every
     // warp keeps loads in flight
     constexpr uint32_t NCH = F / BATCH;
