@@ -544,9 +544,10 @@ def run_gpu(args):
                            "bytes_definition": "SURVEY.md 8(d): 4 p + 16 record + 4 m/n table "
                                                "per entry",
                            "implementation_bytes_per_launch": bytes_build_impl,
-                           "limiter": "issue latency: ~290 thread-instructions per entry at "
-                                      "IPC 2.2, 32 warps/SM, block-barrier stalls; DRAM far "
-                                      "below peak (profiles/, DESIGN.md 5.2)",
+                           "limiter": "issue and block barriers: ~231 thread-instructions per "
+                                      "entry, issue active 53 %, 32 warps/SM, barrier the largest "
+                                      "stall; DRAM far below peak (profiles/r02c_summary.md, "
+                                      "DESIGN.md 5.2)",
                            "peak_source": peak_src},
         "gpu_launches": launches,
         "clocks": sampler.summary(),
