@@ -298,9 +298,19 @@ __device__ int32_t row_left(const uint8_t* tmax, const uint32_t* bmax, uint32_t 
     const uint32_t bb = t >> 6;
     const unsigned long long mk = block_rows_above(tmax, bb, thr) & ((1ull << (t & 63)) - 1);
     if (mk) return (int32_t)(64 * bb + 63 - __clzll((long long)mk));
-    for (int32_t c = (int32_t)bb - 1; c >= 0; --c)
-        if (__ldcg(bmax + c) > thr)
-            return 64 * c + 63 - __clzll((long long)block_rows_above(tmax, (uint32_t)c, thr));
+    // the block maxima 8 at a time (independent loads, one L2 round trip per
+    // 8 blocks instead of one per block)
+    for (int32_t c0 = (int32_t)bb - 1; c0 >= 0; c0 -= 8) {
+        uint32_t v[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) v[u] = c0 - u >= 0 ? __ldcg(bmax + c0 - u) : 0u;
+#pragma unroll
+        for (int u = 0; u < 8; ++u)
+            if (v[u] > thr) {
+                const int32_t c = c0 - u;
+                return 64 * c + 63 - __clzll((long long)block_rows_above(tmax, (uint32_t)c, thr));
+            }
+    }
     return -1;
 }
 
@@ -312,9 +322,17 @@ __device__ int32_t row_right(const uint8_t* tmax, const uint32_t* bmax, uint32_t
     const unsigned long long mk = sh >= 64 ? 0ull : (block_rows_above(tmax, bb, thr) & (~0ull << sh));
     if (mk) return (int32_t)(64 * bb + __ffsll((long long)mk) - 1);
     const uint32_t nb = (nrows + 63) / 64;
-    for (uint32_t c = bb + 1; c < nb; ++c)
-        if (__ldcg(bmax + c) > thr)
-            return (int32_t)(64 * c + __ffsll((long long)block_rows_above(tmax, c, thr)) - 1);
+    for (uint32_t c0 = bb + 1; c0 < nb; c0 += 8) {  // 8 block maxima per round trip
+        uint32_t v[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) v[u] = c0 + u < nb ? __ldcg(bmax + c0 + u) : 0u;
+#pragma unroll
+        for (int u = 0; u < 8; ++u)
+            if (v[u] > thr) {
+                const uint32_t c = c0 + u;
+                return (int32_t)(64 * c + __ffsll((long long)block_rows_above(tmax, c, thr)) - 1);
+            }
+    }
     return -1;
 }
 
@@ -1570,6 +1588,7 @@ __global__ void __launch_bounds__(THREADS, MINB)
             }
         }
     }
+    RTF_TICK(14);
     // long empty-cell runs of the guide table: one warp per chunk
     const uint32_t nq = (ph & kPhRuns) ? min(__ldcg(&A.counters[kCtrQueue]), A.qcap) : 0u;
     for (uint32_t q = b * NW + warp; q < nq; q += G * NW) {

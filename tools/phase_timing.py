@@ -55,6 +55,9 @@ def run(reps, workload):
     print(f"{workload}: {start.elapsed_time(stop) / reps * 1e3:.1f} us per build ({reps} builds)")
     fn(buf.ctypes.data, rows, 0)
     extra = buf[:, 9:11].astype(np.float64) / reps
+    # slot 14: phase E's cross-tile links (slot 8 then holds the long runs only)
+    buf[:, 8] += buf[:, 14]
+    e1 = buf[:, 14].astype(np.float64) / reps
     used = buf[:, :9].sum(axis=1) > 0
     per = buf[used, :9].astype(np.float64) / reps
     tot = per.sum(axis=1)
@@ -94,6 +97,9 @@ def run(reps, workload):
     except AttributeError:
         pass
     ex = extra[used]
+    if e1[used].max() > 0:
+        print(f"  E split: cross-tile links mean {e1[used].mean():.0f} max {e1[used].max():.0f}; "
+              f"long runs mean {per[:, 8].mean() - e1[used].mean():.0f} cycles per CTA")
     spread = buf[used, 11:14].astype(np.float64) / reps
     print("  warp arrival spread at phase D's block barriers (last - first, cycles per CTA per build): "
           + ", ".join(f"barrier {k + 1} {spread[:, k].mean():.0f}" for k in range(3)))
