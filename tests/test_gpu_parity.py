@@ -391,6 +391,16 @@ def test_host_build_chunked_scale(rtf):
         assert rtf.build_host(f, zero, p_dev) == rtf._lib.RTF_EALLZERO
         assert rtf.build_host(f, p_host, p_dev) == 0       # recovers
         assert_forest_equal(f, ref, "chunked host build after poisoned inputs")
+    # the 256-entry-tile configuration through the chunked path, and a small
+    # build (the row kernel: one copy, no chunks)
+    for p, m, flags in ((power_law(70001, "B"), 9001, rtf.RTF_BUILD_SMALL_TILES),
+                        (power_law(3001, "A"), 1000, rtf.RTF_BUILD_DEFAULT)):
+        ref = oracle.build(p, m)
+        f = rtf.Forest(p.size, m, flags)
+        p_host = torch.from_numpy(np.ascontiguousarray(p, np.float32)).pin_memory()
+        p_dev = torch.empty(p.size, dtype=torch.float32, device=DEV)
+        assert rtf.build_host(f, p_host, p_dev) == 0
+        assert_forest_equal(f, ref, f"host build flags={flags} n={p.size}")
 
 
 def ref_exponent(p):
