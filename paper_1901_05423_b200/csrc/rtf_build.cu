@@ -607,13 +607,16 @@ __global__ void __launch_bounds__(THREADS, MINB)
                         for (int u = 0; u < BATCH; ++u) {
                             const int32_t e0 = (int32_t)(base + 4 * ((c + u) * 32 + lane)) + ib;
                             const float xs[4] = {v[u].x, v[u].y, v[u].z, v[u].w};
+                            // positives as a 4-bit mask (w > 0 exactly when x > 0:
+                            // the data is validated), counted once per float4
+                            uint32_t pm = 0;
 #pragma unroll
                             for (int q = 0; q < 4; ++q) {
-                                const uint64_t w = quantize(xs[q], scale);
-                                acc.W += w;
-                                acc.cnt += w != 0;
-                                if (w) acc.last = e0 + q;
+                                acc.W += quantize(xs[q], scale);
+                                pm |= (xs[q] > 0.0f ? 1u : 0u) << q;
                             }
+                            acc.cnt += __popc(pm);
+                            if (pm) acc.last = e0 + 31 - __clz((int)pm);
                         }
                     }
                 } else if (part == 0) {
@@ -915,7 +918,7 @@ __global__ void __launch_bounds__(THREADS, MINB)
         for (int k = 0; k < VPT; ++k) {
             w[k] = quantize(x[k], scale);
             tw += w[k];
-            posmask_in |= (w[k] != 0ull ? 1u : 0u) << k;
+            posmask_in |= (x[k] > 0.0f ? 1u : 0u) << k;  // w > 0 exactly when x > 0
         }
         const uint32_t tc_in = __popc(posmask_in);
         s_clast[tid] = posmask_in ? 31 - __clz((int)posmask_in) : -1;
